@@ -1,0 +1,107 @@
+// tc_internal.h — libtc internals shared by the runtime (.cpp) and the kernels (.cu).
+// Product code only; nothing here is shared with oracle/ (DESIGN.md §2 independence).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/tc.h"
+
+namespace tc {
+
+constexpr uint32_t kHdrBytes = 64;
+constexpr uint64_t kMaxChunkWords = 2147483647ull;  // 2^31-1 (PAPER.md:203 chunk + rebase)
+
+// Encode block ("scan unit") sizes: one CTA stages ref+cur of one block in 32 KB of smem.
+constexpr uint32_t kEncThreads = 256;
+constexpr uint32_t kEncBlockWords4 = 4096;  // 4-byte words
+constexpr uint32_t kEncBlockWords2 = 8192;  // 2-byte words
+// Fold unit: 256 threads x one mask word = 8192 state words per sub-step.
+constexpr uint32_t kFoldThreads = 256;
+constexpr uint32_t kFoldWords = 8192;
+
+__host__ __device__ inline uint64_t pad16(uint64_t x) { return (x + 15) & ~uint64_t(15); }
+__host__ __device__ inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline uint64_t record_fixed_bytes(uint64_t m, uint32_t T) {
+    return kHdrBytes + pad16(4 * cdiv(m, 32)) + pad16(4 * (cdiv(m, T) + 1));
+}
+__host__ __device__ inline uint64_t record_bytes(uint64_t m, uint32_t T, uint32_t w, uint64_t count) {
+    return record_fixed_bytes(m, T) + pad16(uint64_t(w) * count);
+}
+
+// ---- per-segment launch description of one encode (kernel parameter, no table) ----
+struct EncSeg {
+    uint8_t* ref;
+    const uint8_t* cur;
+    uint64_t n;             // words
+    uint64_t first_block;   // global block index of the segment's first block
+    uint64_t first_chunk;   // global chunk index of the segment's first chunk
+    uint64_t blocks_per_chunk;  // blocks of a full chunk (>= 1)
+    uint64_t n_chunks;      // >= 1 (an empty segment is one empty chunk)
+    uint32_t w;
+    uint32_t block_words;   // B
+};
+
+struct EncParams {
+    EncSeg seg[TC_MAX_SEGMENTS];
+    int nseg;
+    uint32_t T;
+    uint64_t C;
+    uint64_t total_blocks;
+    uint64_t total_chunks;
+    uint64_t version, ref_version;
+    uint8_t* out;
+    uint64_t* out_bytes;
+    unsigned long long* ticket;
+    unsigned long long* status;  // [total_blocks]
+    unsigned long long* rstart;  // [total_chunks + 1], value = start | 1 once published
+    unsigned int* err;           // sticky error word
+    int advance_ref;
+};
+
+// ---- fold descriptors ----
+struct FoldRec {           // one record of one diff, as located by the walker
+    const uint8_t* mask;
+    const uint8_t* toff;
+    const uint8_t* values;
+    uint64_t chunk_off;
+    uint64_t count;
+    uint32_t m;
+    uint32_t T;
+    uint32_t seg;
+    uint32_t w;
+};
+
+struct FoldParams {
+    uint8_t* state[TC_MAX_SEGMENTS];
+    uint64_t n[TC_MAX_SEGMENTS];
+    uint32_t w[TC_MAX_SEGMENTS];
+    const uint8_t* rec[TC_MAX_FOLD];
+    uint64_t rec_bytes[TC_MAX_FOLD];
+    int nseg;
+    int nrec;               // diffs folded
+    uint32_t cap;           // descriptor capacity per diff
+    uint64_t state_version;
+    FoldRec* desc;          // [nrec][cap]
+    uint64_t* unit_first;   // [cap + 1]
+    unsigned long long* info;  // [0] = records per diff, [1] = total units
+    unsigned int* err;
+};
+
+// launchers (tc_encode.cu / tc_apply.cu / tc_synth.cu); return cudaError_t
+cudaError_t launch_encode(const EncParams& p, cudaStream_t s);
+cudaError_t launch_fold(const FoldParams& p, cudaStream_t s, int num_sms, uint64_t* launches);
+
+// thread-local detail string
+void set_error(const std::string& msg);
+
+}  // namespace tc
+
+// device-side sticky error: first error wins
+#ifdef __CUDACC__
+__device__ __forceinline__ void tc_set_err(unsigned int* err, unsigned int code) {
+    atomicCAS(err, 0u, code);
+}
+#endif

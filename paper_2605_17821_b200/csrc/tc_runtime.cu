@@ -1,0 +1,328 @@
+// tc_runtime.cu — libtc host runtime: contexts, argument validation, scratch management,
+// encode / apply launch plumbing, Tier-1 staging.  Every compute step runs in the kernels
+// of tc_encode.cu / tc_apply.cu; this file only marshals and validates.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "tc_internal.h"
+
+struct tc_ctx {
+    int device = 0;
+    int num_sms = 148;
+    // encode scratch: [ticket u64 | pad | rstart (chunks+1) u64 | status (blocks) u64]
+    void* enc = nullptr;
+    size_t enc_bytes = 0;
+    // fold scratch: desc [nrec*cap] | unit_first [cap+1] | info [2]
+    void* fold = nullptr;
+    size_t fold_bytes = 0;
+    unsigned int* err = nullptr;  // sticky device error word
+    uint64_t launches = 0;
+};
+
+namespace tc {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+static tc_status fail(tc_status s, const std::string& msg) {
+    set_error(msg);
+    return s;
+}
+
+static tc_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(TC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+static bool is_pow2(uint64_t x) { return x && !(x & (x - 1)); }
+
+static void default_opts(const tc_encode_opts* in, tc_encode_opts* out) {
+    if (in) {
+        *out = *in;
+    } else {
+        out->tile_words = 4096;
+        out->advance_ref = 1;
+        out->chunk_words = 1ull << 28;
+    }
+}
+
+static tc_status check_opts(const tc_encode_opts& o) {
+    if (!is_pow2(o.tile_words) || o.tile_words < 32 || o.tile_words > 65536)
+        return fail(TC_ERR_INVALID, "tile_words must be a power of two in [32, 65536]");
+    if (o.chunk_words == 0 || o.chunk_words % o.tile_words != 0 || o.chunk_words > kMaxChunkWords)
+        return fail(TC_ERR_INVALID, "chunk_words must be a positive multiple of tile_words and <= 2^31-1");
+    return TC_OK;
+}
+
+static tc_status check_segs(const tc_segment* segs, int nseg, bool need_ptrs) {
+    if (!segs || nseg < 1 || nseg > TC_MAX_SEGMENTS)
+        return fail(TC_ERR_INVALID, "nseg must be in [1, TC_MAX_SEGMENTS]");
+    for (int s = 0; s < nseg; ++s) {
+        const tc_segment& g = segs[s];
+        if (g.word_bytes != 2 && g.word_bytes != 4) return fail(TC_ERR_INVALID, "word_bytes must be 2 or 4");
+        if (g.reserved != 0) return fail(TC_ERR_INVALID, "tc_segment.reserved must be 0");
+        if (need_ptrs && g.n_words) {
+            if (!g.ref || !g.cur) return fail(TC_ERR_INVALID, "segment pointer is NULL");
+            if (!aligned16(g.ref) || !aligned16(g.cur)) return fail(TC_ERR_INVALID, "segment pointers must be 16-byte aligned");
+        }
+    }
+    return TC_OK;
+}
+
+// grow a stream-ordered scratch allocation
+static tc_status ensure(void** p, size_t* have, size_t need, cudaStream_t s) {
+    if (*have >= need) return TC_OK;
+    size_t want = need + need / 4;
+    if (*p) {
+        cudaError_t e = cudaFreeAsync(*p, s);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
+        *p = nullptr;
+        *have = 0;
+    }
+    cudaError_t e = cudaMallocAsync(p, want, s);
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        return fail(TC_ERR_NOMEM, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+    }
+    *have = want;
+    return TC_OK;
+}
+
+}  // namespace tc
+
+using namespace tc;
+
+extern "C" {
+
+const char* tc_status_string(tc_status s) {
+    switch (s) {
+        case TC_OK: return "TC_OK";
+        case TC_ERR_INVALID: return "TC_ERR_INVALID";
+        case TC_ERR_NOMEM: return "TC_ERR_NOMEM";
+        case TC_ERR_CUDA: return "TC_ERR_CUDA";
+        case TC_ERR_NCCL: return "TC_ERR_NCCL";
+        case TC_ERR_CORRUPT: return "TC_ERR_CORRUPT";
+        case TC_ERR_PROTOCOL: return "TC_ERR_PROTOCOL";
+        case TC_ERR_UNAVAILABLE: return "TC_ERR_UNAVAILABLE";
+        case TC_ERR_CAPACITY: return "TC_ERR_CAPACITY";
+        case TC_ERR_INTERNAL: return "TC_ERR_INTERNAL";
+    }
+    return "TC_ERR_UNKNOWN";
+}
+
+const char* tc_last_error(void) { return g_last_error.c_str(); }
+
+int tc_abi_version(void) { return TC_ABI_VERSION; }
+
+tc_status tc_ctx_create(int device, tc_ctx** out) {
+    if (!out) return fail(TC_ERR_INVALID, "out is NULL");
+    *out = nullptr;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    tc_ctx* c = new (std::nothrow) tc_ctx();
+    if (!c) return fail(TC_ERR_NOMEM, "host allocation failed");
+    c->device = device;
+    e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "cudaDeviceGetAttribute");
+    }
+    e = cudaMalloc(reinterpret_cast<void**>(&c->err), 16);
+    if (e == cudaSuccess) e = cudaMemset(c->err, 0, 16);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "cudaMalloc(err)");
+    }
+    *out = c;
+    return TC_OK;
+}
+
+tc_status tc_ctx_destroy(tc_ctx* c) {
+    if (!c) return TC_OK;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    if (c->enc) cudaFree(c->enc);
+    if (c->fold) cudaFree(c->fold);
+    if (c->err) cudaFree(c->err);
+    delete c;
+    return TC_OK;
+}
+
+tc_status tc_ctx_check(tc_ctx* c, tc_stream stream) {
+    if (!c) return fail(TC_ERR_INVALID, "ctx is NULL");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    unsigned int code = 0;
+    e = cudaMemcpy(&code, c->err, sizeof(code), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(err)");
+    if (code) {
+        e = cudaMemset(c->err, 0, sizeof(code));
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(err)");
+        return fail(static_cast<tc_status>(code), std::string("device reported ") + tc_status_string(static_cast<tc_status>(code)));
+    }
+    return TC_OK;
+}
+
+uint64_t tc_ctx_launches(const tc_ctx* c) { return c ? c->launches : 0; }
+
+tc_status tc_diff_bound(const tc_segment* segs, int nseg, const tc_encode_opts* opts, uint64_t* max_bytes) {
+    if (!max_bytes) return fail(TC_ERR_INVALID, "max_bytes is NULL");
+    tc_encode_opts o;
+    default_opts(opts, &o);
+    tc_status st = check_opts(o);
+    if (st != TC_OK) return st;
+    st = check_segs(segs, nseg, false);
+    if (st != TC_OK) return st;
+    uint64_t tot = 0;
+    for (int s = 0; s < nseg; ++s) {
+        const uint64_t n = segs[s].n_words, w = segs[s].word_bytes;
+        uint64_t off = 0;
+        do {
+            const uint64_t m = n - off < o.chunk_words ? n - off : o.chunk_words;
+            tot += record_bytes(m, o.tile_words, static_cast<uint32_t>(w), m);
+            off += m;
+        } while (off < n);
+    }
+    *max_bytes = tot;
+    return TC_OK;
+}
+
+tc_status tc_diff_encode(tc_ctx* ctx, const tc_segment* segs, int nseg, const tc_encode_opts* opts,
+                         uint64_t version, uint64_t ref_version, void* out, uint64_t out_cap,
+                         uint64_t* out_bytes, tc_stream stream) {
+    if (!ctx) return fail(TC_ERR_INVALID, "ctx is NULL");
+    tc_encode_opts o;
+    default_opts(opts, &o);
+    tc_status st = check_opts(o);
+    if (st != TC_OK) return st;
+    st = check_segs(segs, nseg, true);
+    if (st != TC_OK) return st;
+    if (!out || !aligned16(out)) return fail(TC_ERR_INVALID, "out must be a 16-byte aligned device pointer");
+    if (!out_bytes) return fail(TC_ERR_INVALID, "out_bytes is NULL");
+    uint64_t bound = 0;
+    st = tc_diff_bound(segs, nseg, &o, &bound);
+    if (st != TC_OK) return st;
+    if (out_cap < bound) return fail(TC_ERR_CAPACITY, "out_cap < tc_diff_bound()");
+
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaSetDevice(ctx->device);
+    EncParams P;
+    memset(&P, 0, sizeof(P));
+    uint64_t blocks = 0, chunks = 0;
+    for (int i = 0; i < nseg; ++i) {
+        const tc_segment& g = segs[i];
+        EncSeg& E = P.seg[i];
+        E.ref = static_cast<uint8_t*>(g.ref);
+        E.cur = static_cast<const uint8_t*>(g.cur);
+        E.n = g.n_words;
+        E.w = g.word_bytes;
+        E.block_words = g.word_bytes == 4 ? kEncBlockWords4 : kEncBlockWords2;
+        E.first_block = blocks;
+        E.first_chunk = chunks;
+        E.n_chunks = g.n_words ? cdiv(g.n_words, o.chunk_words) : 1;
+        const uint64_t full = g.n_words < o.chunk_words ? g.n_words : o.chunk_words;
+        E.blocks_per_chunk = full ? cdiv(full, E.block_words) : 1;
+        const uint64_t m_last = g.n_words ? g.n_words - (E.n_chunks - 1) * o.chunk_words : 0;
+        const uint64_t last_blocks = m_last ? cdiv(m_last, E.block_words) : 1;
+        blocks += (E.n_chunks - 1) * E.blocks_per_chunk + last_blocks;
+        chunks += E.n_chunks;
+    }
+    P.nseg = nseg;
+    P.T = o.tile_words;
+    P.C = o.chunk_words;
+    P.total_blocks = blocks;
+    P.total_chunks = chunks;
+    P.version = version;
+    P.ref_version = ref_version;
+    P.out = static_cast<uint8_t*>(out);
+    P.out_bytes = out_bytes;
+    P.advance_ref = o.advance_ref ? 1 : 0;
+    P.err = ctx->err;
+
+    const size_t need = 16 + 8 * (chunks + 1) + 8 * blocks;
+    st = ensure(&ctx->enc, &ctx->enc_bytes, need, s);
+    if (st != TC_OK) return st;
+    uint8_t* base = static_cast<uint8_t*>(ctx->enc);
+    P.ticket = reinterpret_cast<unsigned long long*>(base);
+    P.rstart = reinterpret_cast<unsigned long long*>(base + 16);
+    P.status = reinterpret_cast<unsigned long long*>(base + 16 + 8 * (chunks + 1));
+    cudaError_t e = cudaMemsetAsync(base, 0, need, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(scratch)");
+    e = launch_encode(P, s);
+    if (e != cudaSuccess) return cuda_fail(e, "encode launch");
+    ctx->launches += 1;
+    return TC_OK;
+}
+
+tc_status tc_diff_apply(tc_ctx* ctx, void* const* state, const uint64_t* n_words, const uint32_t* word_bytes,
+                        int nseg, uint64_t state_version, const void* const* records,
+                        const uint64_t* record_bytes_, int n_records, tc_stream stream) {
+    if (!ctx) return fail(TC_ERR_INVALID, "ctx is NULL");
+    if (!state || !n_words || !word_bytes || nseg < 1 || nseg > TC_MAX_SEGMENTS)
+        return fail(TC_ERR_INVALID, "bad state description (1 <= nseg <= TC_MAX_SEGMENTS)");
+    if (!records || !record_bytes_ || n_records < 1 || n_records > TC_MAX_FOLD)
+        return fail(TC_ERR_INVALID, "n_records must be in [1, TC_MAX_FOLD]");
+    FoldParams P;
+    memset(&P, 0, sizeof(P));
+    uint64_t cap = 0;
+    for (int s = 0; s < nseg; ++s) {
+        if (word_bytes[s] != 2 && word_bytes[s] != 4) return fail(TC_ERR_INVALID, "word_bytes must be 2 or 4");
+        if (n_words[s] && (!state[s] || !aligned16(state[s])))
+            return fail(TC_ERR_INVALID, "state pointers must be 16-byte aligned device pointers");
+        P.state[s] = static_cast<uint8_t*>(state[s]);
+        P.n[s] = n_words[s];
+        P.w[s] = word_bytes[s];
+        // records per segment <= ceil(n/32) (chunk_words >= tile_words >= 32), at least 1
+        cap += n_words[s] ? cdiv(n_words[s], 32) : 1;
+    }
+    if (cap > TC_MAX_RECORDS_PER_DIFF) cap = TC_MAX_RECORDS_PER_DIFF;
+    for (int j = 0; j < n_records; ++j) {
+        if (!records[j] || !aligned16(records[j]))
+            return fail(TC_ERR_INVALID, "record pointers must be 16-byte aligned device pointers");
+        P.rec[j] = static_cast<const uint8_t*>(records[j]);
+        P.rec_bytes[j] = record_bytes_[j];
+    }
+    P.nseg = nseg;
+    P.nrec = n_records;
+    P.cap = static_cast<uint32_t>(cap);
+    P.state_version = state_version;
+    P.err = ctx->err;
+
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaSetDevice(ctx->device);
+    const size_t desc_bytes = sizeof(FoldRec) * cap * n_records;
+    const size_t need = desc_bytes + 8 * (cap + 1) + 16;
+    tc_status st = ensure(&ctx->fold, &ctx->fold_bytes, need, s);
+    if (st != TC_OK) return st;
+    uint8_t* base = static_cast<uint8_t*>(ctx->fold);
+    P.desc = reinterpret_cast<FoldRec*>(base);
+    P.unit_first = reinterpret_cast<uint64_t*>(base + desc_bytes);
+    P.info = reinterpret_cast<unsigned long long*>(base + desc_bytes + 8 * (cap + 1));
+    cudaError_t e = launch_fold(P, s, ctx->num_sms, &ctx->launches);
+    if (e != cudaSuccess) return cuda_fail(e, "fold launch");
+    return TC_OK;
+}
+
+tc_status tc_stage_host(void* dst, const void* src, uint64_t bytes, int dir, tc_stream copy_stream) {
+    if (bytes == 0) return TC_OK;
+    if (!dst || !src) return fail(TC_ERR_INVALID, "NULL buffer");
+    if (dir != TC_D2H && dir != TC_H2D) return fail(TC_ERR_INVALID, "dir must be TC_D2H or TC_H2D");
+    const void* host = dir == TC_D2H ? dst : src;
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, host);
+    if (e != cudaSuccess || a.type != cudaMemoryTypeHost) {
+        cudaGetLastError();
+        return fail(TC_ERR_INVALID, "host side of tc_stage_host must be pinned (cudaHostAlloc/cudaHostRegister)");
+    }
+    e = cudaMemcpyAsync(dst, src, bytes, dir == TC_D2H ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice,
+                        static_cast<cudaStream_t>(copy_stream));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync");
+    return TC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,251 @@
+"""Thin ctypes binding of libtc (include/tc.h, include/tc_synth.h).
+
+Argument marshalling only: torch tensors provide device / pinned memory (``data_ptr()``) and
+torch streams provide ``cudaStream_t`` handles; every step of the codec runs in libtc's CUDA
+kernels.  There is NO fallback: if libtc.so is missing or fails to load, importing this
+module raises, and no function here ever computes a result on the host.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import torch
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libtc.so")
+INCLUDE = os.path.join(os.path.dirname(PKG), "include")
+
+OK, ERR_INVALID, ERR_NOMEM, ERR_CUDA, ERR_NCCL = 0, 1, 2, 3, 4
+ERR_CORRUPT, ERR_PROTOCOL, ERR_UNAVAILABLE, ERR_CAPACITY, ERR_INTERNAL = 5, 6, 7, 8, 9
+D2H, H2D = 0, 1
+TO_NEXT, TO_PREV = 0, 1
+MAX_SEGMENTS, MAX_FOLD = 16, 64
+
+u64, u32, vp, cint = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_int
+
+
+class Segment(ctypes.Structure):
+    _fields_ = [("ref", vp), ("cur", vp), ("n_words", u64), ("word_bytes", u32), ("reserved", u32)]
+
+
+class EncodeOpts(ctypes.Structure):
+    _fields_ = [("tile_words", u32), ("advance_ref", u32), ("chunk_words", u64)]
+
+
+class TcError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str = ""):
+        self.status = status
+        super().__init__(f"{where}: {_status_string(status)} ({detail})")
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"libtc.so not found at {LIB_PATH}; build it with `python -m paper_2605_17821_b200.build` "
+            "(there is no CPU fallback)"
+        )
+    L = ctypes.CDLL(LIB_PATH)
+    L.tc_status_string.restype = ctypes.c_char_p
+    L.tc_status_string.argtypes = [cint]
+    L.tc_last_error.restype = ctypes.c_char_p
+    L.tc_last_error.argtypes = []
+    L.tc_abi_version.restype = cint
+    L.tc_ctx_create.argtypes = [cint, ctypes.POINTER(vp)]
+    L.tc_ctx_destroy.argtypes = [vp]
+    L.tc_ctx_check.argtypes = [vp, vp]
+    L.tc_ctx_launches.restype = u64
+    L.tc_ctx_launches.argtypes = [vp]
+    L.tc_diff_bound.argtypes = [ctypes.POINTER(Segment), cint, ctypes.POINTER(EncodeOpts),
+                                ctypes.POINTER(u64)]
+    L.tc_diff_encode.argtypes = [vp, ctypes.POINTER(Segment), cint, ctypes.POINTER(EncodeOpts), u64, u64,
+                                 vp, u64, vp, vp]
+    L.tc_stage_host.argtypes = [vp, vp, u64, cint, vp]
+    L.tc_comm_get_unique_id.argtypes = [ctypes.c_char_p]
+    L.tc_comm_init.argtypes = [cint, cint, cint, ctypes.c_char_p, ctypes.POINTER(vp)]
+    L.tc_comm_destroy.argtypes = [vp]
+    L.tc_replicate_peer.argtypes = [vp, vp, vp, vp, u64, ctypes.POINTER(u64), cint, vp]
+    L.tc_diff_apply.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(u64), ctypes.POINTER(u32), cint, u64,
+                                ctypes.POINTER(vp), ctypes.POINTER(u64), cint, vp]
+    L.tc_synth_base.argtypes = [vp, u64, u32, u64, u32, u64, vp]
+    L.tc_synth_step.argtypes = [vp, u64, u32, u64, u32, u64, u64, cint, u64, vp]
+    for name in ("tc_ctx_create", "tc_ctx_destroy", "tc_ctx_check", "tc_diff_bound", "tc_diff_encode",
+                 "tc_stage_host", "tc_comm_get_unique_id", "tc_comm_init", "tc_comm_destroy",
+                 "tc_replicate_peer", "tc_diff_apply", "tc_synth_base", "tc_synth_step"):
+        getattr(L, name).restype = cint
+    return L
+
+
+LIB = _load()
+
+
+def _status_string(s: int) -> str:
+    return LIB.tc_status_string(s).decode()
+
+
+def _check(rc: int, where: str):
+    if rc != OK:
+        raise TcError(rc, where, LIB.tc_last_error().decode())
+
+
+def header_symbols():
+    """Every function the public headers declare (for the ABI export test)."""
+    names = []
+    for h in ("tc.h", "tc_synth.h"):
+        with open(os.path.join(INCLUDE, h)) as fh:
+            txt = fh.read()
+        names += re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(tc_\w+)\s*\(", txt, re.M)
+    return sorted(set(names))
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, torch.cuda.Stream):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def _opts(tile_words=4096, chunk_words=1 << 28, advance_ref=True) -> EncodeOpts:
+    return EncodeOpts(tile_words, 1 if advance_ref else 0, chunk_words)
+
+
+def _wb(t: torch.Tensor) -> int:
+    wb = t.element_size()
+    if wb not in (2, 4):
+        raise TcError(ERR_INVALID, "segment", f"element size {wb} not in (2, 4)")
+    return wb
+
+
+def segments(ref, cur):
+    if len(ref) != len(cur):
+        raise TcError(ERR_INVALID, "segments", "ref/cur length mismatch")
+    arr = (Segment * len(ref))()
+    for i, (r, c) in enumerate(zip(ref, cur)):
+        if r.numel() != c.numel() or r.element_size() != c.element_size():
+            raise TcError(ERR_INVALID, "segments", f"segment {i} shape mismatch")
+        arr[i] = Segment(r.data_ptr() if r.numel() else None, c.data_ptr() if c.numel() else None,
+                         r.numel(), _wb(r), 0)
+    return arr
+
+
+def layout_segments(sizes, word_bytes):
+    arr = (Segment * len(sizes))()
+    for i, (n, w) in enumerate(zip(sizes, word_bytes)):
+        arr[i] = Segment(None, None, int(n), int(w), 0)
+    return arr
+
+
+def diff_bound(sizes, word_bytes, tile_words=4096, chunk_words=1 << 28) -> int:
+    segs = layout_segments(sizes, word_bytes)
+    o = _opts(tile_words, chunk_words)
+    out = u64(0)
+    _check(LIB.tc_diff_bound(segs, len(sizes), ctypes.byref(o), ctypes.byref(out)), "tc_diff_bound")
+    return out.value
+
+
+class Ctx:
+    """tc_ctx: per-device scratch + sticky device error."""
+
+    def __init__(self, device: int | None = None):
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = device
+        h = vp()
+        _check(LIB.tc_ctx_create(device, ctypes.byref(h)), "tc_ctx_create")
+        self.h = h
+
+    def check(self, stream=None):
+        _check(LIB.tc_ctx_check(self.h, _stream(stream)), "tc_ctx_check")
+
+    def check_status(self, stream=None) -> int:
+        return LIB.tc_ctx_check(self.h, _stream(stream))
+
+    @property
+    def launches(self) -> int:
+        return int(LIB.tc_ctx_launches(self.h))
+
+    def close(self):
+        if self.h:
+            LIB.tc_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def diff_encode(ctx: Ctx, ref, cur, out: torch.Tensor, out_bytes: torch.Tensor, version: int, ref_version: int,
+                tile_words=4096, chunk_words=1 << 28, advance_ref=True, stream=None):
+    """Enqueue tc_diff_encode.  ``out`` uint8 CUDA tensor, ``out_bytes`` int64 CUDA tensor [1]."""
+    segs = segments(ref, cur)
+    o = _opts(tile_words, chunk_words, advance_ref)
+    _check(LIB.tc_diff_encode(ctx.h, segs, len(ref), ctypes.byref(o), version, ref_version, out.data_ptr(),
+                              out.numel() * out.element_size(), out_bytes.data_ptr(), _stream(stream)),
+           "tc_diff_encode")
+
+
+def diff_apply(ctx: Ctx, state, state_version: int, records, record_bytes, stream=None):
+    """Enqueue tc_diff_apply: fold ``records`` (oldest first) onto ``state`` in place."""
+    n = len(state)
+    sp = (vp * n)(*[s.data_ptr() if s.numel() else None for s in state])
+    nw = (u64 * n)(*[s.numel() for s in state])
+    wb = (u32 * n)(*[_wb(s) for s in state])
+    k = len(records)
+    rp = (vp * k)(*[r.data_ptr() for r in records])
+    rb = (u64 * k)(*[int(b) for b in record_bytes])
+    _check(LIB.tc_diff_apply(ctx.h, sp, nw, wb, n, state_version, rp, rb, k, _stream(stream)), "tc_diff_apply")
+
+
+def stage_host(dst: torch.Tensor, src: torch.Tensor, nbytes: int, direction: int, stream=None):
+    _check(LIB.tc_stage_host(dst.data_ptr(), src.data_ptr(), int(nbytes), direction, _stream(stream)),
+           "tc_stage_host")
+
+
+class Comm:
+    """tc_comm: libtc's own NCCL communicator for the Tier-2 ring ("isolated
+    communication groups").  The unique id is broadcast over a torch.distributed group."""
+
+    def __init__(self, rank: int, world: int, device: int, group=None):
+        import torch.distributed as dist
+
+        buf = ctypes.create_string_buffer(128)
+        if rank == 0:
+            _check(LIB.tc_comm_get_unique_id(buf), "tc_comm_get_unique_id")
+        if world > 1:
+            t = torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8).clone()
+            if dist.get_backend(group) == "nccl":
+                t = t.cuda(device)
+            dist.broadcast(t, src=0, group=group)
+            buf = ctypes.create_string_buffer(bytes(t.cpu().tolist()), 128)
+        h = vp()
+        _check(LIB.tc_comm_init(world, rank, device, buf, ctypes.byref(h)), "tc_comm_init")
+        self.h = h
+        self.rank, self.world = rank, world
+
+    def replicate_peer(self, send: torch.Tensor, send_bytes: torch.Tensor, recv: torch.Tensor,
+                       direction: int = TO_NEXT, stream=None) -> int:
+        got = u64(0)
+        _check(LIB.tc_replicate_peer(self.h, send.data_ptr(), send_bytes.data_ptr(), recv.data_ptr(),
+                                     recv.numel() * recv.element_size(), ctypes.byref(got), direction,
+                                     _stream(stream)), "tc_replicate_peer")
+        return got.value
+
+    def close(self):
+        if self.h:
+            LIB.tc_comm_destroy(self.h)
+            self.h = None
+
+
+def synth_base(dst: torch.Tensor, seed: int, seg: int, start: int = 0, stream=None):
+    _check(LIB.tc_synth_base(dst.data_ptr(), dst.numel(), _wb(dst), seed, seg, start, _stream(stream)),
+           "tc_synth_base")
+
+
+def synth_step(words: torch.Tensor, seed: int, seg: int, t: int, p53: int, structure: int = 0, start: int = 0,
+               stream=None):
+    _check(LIB.tc_synth_step(words.data_ptr(), words.numel(), _wb(words), seed, seg, t, p53, structure, start,
+                             _stream(stream)), "tc_synth_step")

@@ -1,0 +1,241 @@
+"""GPU parity: libtc's CUDA encoder / fold vs the oracle, element by element (byte-exact
+records, bit-exact states), on seeded inputs that span several scan blocks, ragged tails,
+chunk boundaries inside and across blocks, and the edge cases of the format."""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+from paper_2605_17821_b200 import tc  # noqa: E402
+from tests.gpu_util import gpu_encode, gpu_fold  # noqa: E402
+
+RNG = np.random.default_rng(7)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = tc.Ctx(0)
+    yield c
+    c.close()
+
+
+def rand_pair(n, w, f, rng=RNG):
+    dt = np.uint16 if w == 2 else np.uint32
+    ref = rng.integers(0, 1 << (8 * w), size=n, dtype=np.uint64).astype(dt)
+    ch = rng.random(n) < f
+    cur = ref.copy()
+    cur[ch] ^= rng.integers(1, 1 << (8 * w), size=int(ch.sum()), dtype=np.uint64).astype(dt)
+    return ref, cur
+
+
+CASES = [
+    # sizes, widths, f, T, C
+    ([6], [4], 0.5, 4096, 1 << 28),
+    ([3], [2], 0.7, 4096, 1 << 28),
+    ([0], [4], 0.0, 4096, 1 << 28),
+    ([1], [2], 1.0, 32, 32),
+    ([7], [2], 1.0, 32, 64),
+    ([4097], [4], 0.3, 4096, 1 << 28),
+    ([8193], [2], 0.3, 4096, 1 << 28),
+    ([100003], [4], 0.01, 4096, 1 << 28),
+    ([100003], [2], 0.01, 4096, 1 << 28),
+    ([50000], [4], 1.0, 4096, 1 << 28),
+    ([50000], [2], 1.0, 4096, 1 << 28),
+    ([50000], [4], 0.0, 4096, 1 << 28),
+    ([20000], [4], 0.2, 32, 32),          # one block per 32-word chunk
+    ([20000], [2], 0.2, 64, 192),         # chunks of 3 tiles, not a block multiple
+    ([70000], [4], 0.1, 8192, 16384),     # T > block words (4096)
+    ([70000], [2], 0.1, 65536, 65536),    # T = max
+    ([30001], [4], 0.05, 128, 4096 * 3),  # chunk = 3 blocks, ragged tail chunk
+    ([777, 1000, 0, 2049], [2, 4, 4, 4], 0.3, 32, 512),
+    ([123457, 123457, 123457, 123457], [2, 4, 4, 4], 0.01, 4096, 1 << 16),
+]
+
+
+@pytest.mark.parametrize("sizes,wb,f,T,C", CASES)
+@pytest.mark.parametrize("advance", [True, False])
+def test_encode_matches_oracle_bytes(ctx, tco, sizes, wb, f, T, C, advance):
+    pairs = [rand_pair(n, w, f) for n, w in zip(sizes, wb)]
+    ref = [p[0] for p in pairs]
+    cur = [p[1] for p in pairs]
+    ref_o = [r.copy() for r in ref]
+    rc, exp = tco.encode(ref_o, cur, tile_words=T, chunk_words=C, advance_ref=advance, version=9, ref_version=8)
+    assert rc == 0
+    got, ref_after, nbytes = gpu_encode(ctx, ref, cur, T, C, advance, 9, 8)
+    assert nbytes == exp.size
+    assert np.array_equal(got, exp), "record bytes differ from the oracle"
+    for a, b in zip(ref_after, ref_o):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("f", [0.0, 0.001, 0.01, 0.1, 0.5, 1.0])
+def test_encode_synth_cfg1_shape(ctx, tco, f):
+    """cfg1 (BASELINE.json configs[0]): 1M fp32 params + Adam m/v, one base and one step."""
+    sizes, wb = [1 << 20] * 3, [4, 4, 4]
+    base = synth.state(sizes, wb, synth.SEED0, 0, f)
+    cur = synth.state(sizes, wb, synth.SEED0, 1, f)
+    ref_o = [a.copy() for a in base]
+    rc, exp = tco.encode(ref_o, cur)
+    got, ref_after, _ = gpu_encode(ctx, base, cur)
+    assert np.array_equal(got, exp)
+    assert all(np.array_equal(a, b) for a, b in zip(ref_after, cur))
+
+
+def test_encode_is_deterministic(ctx):
+    ref, cur = rand_pair(300000, 4, 0.2)
+    a, _, _ = gpu_encode(ctx, [ref], [cur], 256, 4096 * 8)
+    b, _, _ = gpu_encode(ctx, [ref], [cur], 256, 4096 * 8)
+    assert np.array_equal(a, b)
+
+
+def test_encode_capacity_error(ctx):
+    ref = torch.zeros(1000, dtype=torch.int32, device="cuda")
+    out = torch.zeros(100, dtype=torch.uint8, device="cuda")
+    ob = torch.zeros(1, dtype=torch.int64, device="cuda")
+    with pytest.raises(tc.TcError) as e:
+        tc.diff_encode(ctx, [ref], [ref.clone()], out, ob, 1, 0)
+    assert e.value.status == tc.ERR_CAPACITY
+
+
+# ------------------------------------------------------------------ fold -------------
+def make_chain(tco, sizes, wb, N, f, T, C, seed=5, structure=synth.S1_IID):
+    states = [synth.state(sizes, wb, seed, v, f, structure) for v in range(N + 1)]
+    ref = [a.copy() for a in states[0]]
+    diffs = []
+    for v in range(1, N + 1):
+        rc, d = tco.encode(ref, states[v], tile_words=T, chunk_words=C, version=v, ref_version=v - 1)
+        assert rc == 0
+        diffs.append(d)
+    return states, diffs
+
+
+@pytest.mark.parametrize("N", [1, 2, 5, 8, 10])
+@pytest.mark.parametrize("layout", [
+    ([30011, 30011, 30011, 30011], [2, 4, 4, 4], 4096, 1 << 28),
+    ([20000, 9000], [4, 2], 64, 1024),
+    ([40000], [4], 16384, 32768),
+])
+def test_fold_matches_oracle(ctx, tco, N, layout):
+    sizes, wb, T, C = layout
+    states, diffs = make_chain(tco, sizes, wb, N, 0.05, T, C)
+    st_o = [a.copy() for a in states[0]]
+    rc, ver = tco.fold(st_o, 0, diffs)
+    assert rc == 0 and ver == N
+    rc, st_g = gpu_fold(ctx, states[0], 0, diffs)
+    assert rc == tc.OK
+    for a, b, c in zip(st_g, st_o, states[N]):
+        assert np.array_equal(a, b) and np.array_equal(a, c)
+
+
+@pytest.mark.parametrize("f", [0.0, 0.01, 1.0])
+def test_fold_dense_and_empty(ctx, tco, f):
+    states, diffs = make_chain(tco, [50000, 50000], [2, 4], 3, f, 4096, 1 << 28, seed=9)
+    rc, st_g = gpu_fold(ctx, states[0], 0, diffs)
+    assert rc == tc.OK
+    assert all(np.array_equal(a, b) for a, b in zip(st_g, states[3]))
+
+
+def test_fold_s2_runs(ctx, tco):
+    states, diffs = make_chain(tco, [100000, 100000], [2, 4], 5, 0.2, 4096, 1 << 28, seed=2,
+                               structure=synth.S2_RUNS)
+    rc, st_g = gpu_fold(ctx, states[0], 0, diffs)
+    assert rc == tc.OK
+    assert all(np.array_equal(a, b) for a, b in zip(st_g, states[5]))
+
+
+def test_fold_of_gpu_encoded_chain(ctx, tco):
+    """GPU encode (incremental, fused ref advance) -> GPU fold reproduces the final state."""
+    sizes, wb = [60000, 60000, 60000, 60000], [2, 4, 4, 4]
+    N = 8
+    states = [synth.state(sizes, wb, 77, v, 0.02) for v in range(N + 1)]
+    ref = [a.copy() for a in states[0]]
+    diffs = []
+    for v in range(1, N + 1):
+        d, ref, _ = gpu_encode(ctx, ref, states[v], version=v, ref_version=v - 1)
+        diffs.append(d)
+    rc, st_g = gpu_fold(ctx, states[0], 0, diffs)
+    assert rc == tc.OK
+    assert all(np.array_equal(a, b) for a, b in zip(st_g, states[N]))
+
+
+# ------------------------------------------------------------- tampering -------------
+def _chain1(tco, n=20000, w=4, T=256):
+    states, diffs = make_chain(tco, [n], [w], 1, 0.2, T, 1 << 28, seed=3)
+    return states, diffs[0]
+
+
+def test_tamper_mask_bit_corrupt(ctx, tco):
+    states, d = _chain1(tco)
+    bad = d.copy()
+    bad[64 + 4 * 17] ^= 0x10
+    rc, _ = gpu_fold(ctx, states[0], 0, [bad])
+    assert rc == tc.ERR_CORRUPT == tco.fold([a.copy() for a in states[0]], 0, [bad])[0]
+
+
+def test_tamper_tile_off_corrupt(ctx, tco):
+    states, d = _chain1(tco)
+    bad = d.copy()
+    m = 20000
+    toff = 64 + ((4 * -(-m // 32) + 15) // 16) * 16
+    bad[toff + 4 * 5] ^= 1
+    rc, _ = gpu_fold(ctx, states[0], 0, [bad])
+    assert rc == tc.ERR_CORRUPT == tco.fold([a.copy() for a in states[0]], 0, [bad])[0]
+
+
+@pytest.mark.parametrize("byte,val", [(0, ord("X")), (4, 2), (6, 8), (7, 3), (8, 33), (12, 1)])
+def test_tamper_header_corrupt_state_untouched(ctx, tco, byte, val):
+    states, d = _chain1(tco)
+    bad = d.copy()
+    bad[byte] = val
+    rc, st = gpu_fold(ctx, states[0], 0, [bad])
+    assert rc == tc.ERR_CORRUPT
+    assert np.array_equal(st[0], states[0][0])
+
+
+def test_truncated_corrupt(ctx, tco):
+    states, d = _chain1(tco)
+    rc, st = gpu_fold(ctx, states[0], 0, [d[:-16]])
+    assert rc == tc.ERR_CORRUPT and np.array_equal(st[0], states[0][0])
+
+
+def test_chain_gap_protocol(ctx, tco):
+    states, diffs = make_chain(tco, [5000], [4], 3, 0.1, 64, 1 << 28)
+    rc, st = gpu_fold(ctx, states[0], 0, [diffs[0], diffs[2]])
+    assert rc == tc.ERR_PROTOCOL and np.array_equal(st[0], states[0][0])
+    rc, st = gpu_fold(ctx, states[0], 1, [diffs[0]])
+    assert rc == tc.ERR_PROTOCOL
+    # the context is clean again after check
+    rc, st = gpu_fold(ctx, states[0], 0, diffs)
+    assert rc == tc.OK and np.array_equal(st[0], states[3][0])
+
+
+def test_layout_mismatch_invalid(ctx, tco):
+    sizes, wb = [5000], [4]
+    s = [synth.state(sizes, wb, 1, v, 0.1) for v in range(3)]
+    ref = [a.copy() for a in s[0]]
+    _, d1 = tco.encode(ref, s[1], tile_words=64, version=1, ref_version=0)
+    _, d2 = tco.encode(ref, s[2], tile_words=128, version=2, ref_version=1)
+    rc, _ = gpu_fold(ctx, s[0], 0, [d1, d2])
+    assert rc == tc.ERR_INVALID
+    # applied one at a time they restore
+    rc, st = gpu_fold(ctx, s[0], 0, [d1])
+    assert rc == tc.OK
+    rc, st = gpu_fold(ctx, st, 1, [d2])
+    assert rc == tc.OK and np.array_equal(st[0], s[2][0])
+
+
+def test_launch_counter(ctx):
+    before = ctx.launches
+    ref = torch.zeros(5000, dtype=torch.int32, device="cuda")
+    out = torch.zeros(tc.diff_bound([5000], [4]), dtype=torch.uint8, device="cuda")
+    ob = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tc.diff_encode(ctx, [ref], [ref.clone()], out, ob, 1, 0)
+    tc.diff_apply(ctx, [ref], 0, [out], [int(ob.item())])
+    ctx.check()
+    assert ctx.launches == before + 3  # encode + walker + fold
