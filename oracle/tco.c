@@ -80,14 +80,17 @@ static int encode_chunk(void* ref, const void* cur, uint64_t chunk_off, uint64_t
             if (advance_ref) store_word(ref, chunk_off + i, w, b);
         }
     }
-    /* 5. tile_off[t] = number of changed words in [0, t*T), t = 0..n_tiles. */
-    for (uint64_t t = 0; t <= n_tiles; t++) {
-        uint64_t c = 0;
-        uint64_t end = t * T < m ? t * T : m;
-        for (uint64_t i = 0; i < end; i++)
-            if ((get_u32(mask_p + 4 * (i / 32)) >> (i % 32)) & 1u) c++;
+    /* 5. tile_off[t] = number of changed words in [0, t*T), t = 0..n_tiles, as a running
+     *    count of the mask bits (the count of [0, t*T) is the count of [0, (t-1)*T) plus
+     *    the bits of tile t-1). */
+    uint64_t c = 0;
+    for (uint64_t t = 0; t < n_tiles; t++) {
         put_u32(toff_p + 4 * t, (uint32_t)c);
+        uint64_t end = (t + 1) * T < m ? (t + 1) * T : m;
+        for (uint64_t i = t * T; i < end; i++)
+            if ((get_u32(mask_p + 4 * (i / 32)) >> (i % 32)) & 1u) c++;
     }
+    put_u32(toff_p + 4 * n_tiles, (uint32_t)c);
     /* 6. header. */
     out[0] = 'T'; out[1] = 'C'; out[2] = 'D'; out[3] = '1';
     put_u16(out + 4, 1);
