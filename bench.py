@@ -1,0 +1,576 @@
+#!/usr/bin/env python
+"""bench.py — TierCheck differential-checkpoint hot path on B200 (BASELINE.json metric:
+"diff encode & restore GB/s per GPU vs HBM peak; peer-replicate GB/s vs NVLink").
+
+One STEP = one pass of the whole hot path for one checkpoint version
+of each rank's shard:
+    a2-a4  tc_diff_encode   ref(version k) vs cur(version k+1), fused ref advance -> record
+    a5     tc_stage_host    record -> pinned host ring (Tier-1, copy stream)
+    a6     tc_replicate_peer record -> ring neighbour over NCCL (Tier-2, comm stream; N > 1)
+    a7     tc_diff_apply    fold the record onto the restore replica (version k -> k+1)
+    a8     versions chained k -> k+1; every record links to the previous one.
+The current state alternates between two synthetic versions X (v0) and Y (v1 = X + f changes),
+so every step encodes a genuine incremental diff of change fraction f (X->Y->X->...).
+
+value = state bytes of all ranks / step time (GB/s of state), inputs resident in HBM.
+e2e   = the same through the C ABI with HOST buffers: every step copies the new state version
+        from pinned host memory (H2D) and reads the record back (D2H), inside the timed region.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2] [--f 0.01]
+       python bench.py --impl reference ...   (the oracle on host cores, bounded sample)
+Multi-GPU: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "diff encode & restore GB/s per GPU vs HBM peak; peer-replicate GB/s vs NVLink"
+WORKLOADS = {
+    "cfg1": "cfg1: 1M fp32 params + Adam m/v (3 fp32 segments of 2^20 words), one step",
+    "cfg2": "cfg2: GPT-2 1.5B-shaped (h1600 L48) bf16 weights + fp32 master/m/v, 1 GPU",
+    "cfg3": "cfg3: GPT 7B-shaped (h4096 L32) ZeRO shard r of 8 per rank + Tier-2 ring replication",
+    "cfg4": "cfg4: GPT 13B-shaped (h5120 L40) ZeRO shard r of 8 per rank",
+}
+NVLINK_GBS = 900.0          # nominal per direction per GPU
+NVLINK_MEASURED_GBS = 770.0  # B200_PROFILING.md measured peer copy per direction
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ helpers -------------
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def record_counts(host_u8: np.ndarray, nbytes: int):
+    """Parse the record headers of a staged diff (host copy) -> per-record (seg, m, w, T, count)."""
+    out = []
+    pos = 0
+    while pos < nbytes:
+        h = host_u8[pos: pos + 64]
+        w = int(h[6])
+        T = int(h[8:12].view("<u4")[0])
+        seg = int(h[12:16].view("<u4")[0])
+        m = int(h[24:32].view("<u8")[0])
+        count = int(h[32:40].view("<u8")[0])
+        total = int(h[56:64].view("<u8")[0])
+        out.append((seg, m, w, T, count, total))
+        pos += total
+    return out
+
+
+def algorithmic_bytes(recs, sector=False):
+    """encode reads ref+cur (2W), writes mask + tile_off + header + values, and
+    (advance_ref) the changed ref words.  Fold (N=1): reads mask + tile_off + header + values,
+    writes the changed state words.  Word-granular unless sector=True (32-byte sectors)."""
+    enc = fold = 0
+    for seg, m, w, T, count, total in recs:
+        W = m * w
+        meta = 64 + 4 * -(-m // 32) + 4 * (-(-m // T) + 1)
+        vals = w * count
+        if sector and m:
+            f = count / m
+            scat = W * (1 - (1 - f) ** (32 // w))
+        else:
+            scat = vals
+        enc += 2 * W + meta + vals + scat
+        fold += meta + vals + scat
+    return enc, fold
+
+
+class Clocks:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.p = None
+        self.path = os.path.join("/tmp", f"tc_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.fh.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------- the GPU arm --------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_17821_b200 import tc
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    workload = args.workload or ("cfg2" if world == 1 else "cfg3")
+    shard = rank % 8 if workload in ("cfg3", "cfg4", "cfg5") else 0
+    sizes, wb = synth.shard_layout(workload, shard)
+    W = sum(n * w for n, w in zip(sizes, wb))
+    seed = synth.SEED0 + shard
+    p53 = synth.p53_of(args.f)
+    T, C = args.tile_words, args.chunk_words
+
+    def alloc(n, w):
+        return torch.empty(n, dtype=torch.int16 if w == 2 else torch.int32, device=dev)
+
+    s_comp = torch.cuda.Stream(device=dev)
+    s_copy = torch.cuda.Stream(device=dev, priority=0)
+    s_comm = torch.cuda.Stream(device=dev)
+    ctx = tc.Ctx(local)
+    comm = tc.Comm(rank, world, local) if world > 1 else None
+
+    # inputs: X = version 0, Y = version 1 (device synth; input preparation, untimed)
+    X = [alloc(n, w) for n, w in zip(sizes, wb)]
+    Y = [alloc(n, w) for n, w in zip(sizes, wb)]
+    A = [alloc(n, w) for n, w in zip(sizes, wb)]  # the advancing reference (chain state)
+    R = [alloc(n, w) for n, w in zip(sizes, wb)]  # the restore replica (fold target)
+    with torch.cuda.stream(s_comp):
+        for s in range(len(sizes)):
+            tc.synth_base(X[s], seed, s, stream=s_comp)
+            Y[s].copy_(X[s])
+            tc.synth_step(Y[s], seed, s, 1, p53, args.structure, stream=s_comp)
+            A[s].copy_(X[s])
+            R[s].copy_(X[s])
+    s_comp.synchronize()
+    cap = tc.diff_bound(sizes, wb, T, C)
+    # records: the bound at f is ~ (f + 0.036) W; allocate the bound only when it fits
+    free = torch.cuda.mem_get_info(dev)[0]
+    est = int(min(cap, (args.f * 1.1 + 0.05) * W + (64 << 20)))
+    rec_cap = cap if 3 * cap < free - (2 << 30) else est
+    recs = [torch.empty(rec_cap, dtype=torch.uint8, device=dev) for _ in range(2)]
+    recv = torch.empty(rec_cap, dtype=torch.uint8, device=dev) if comm else None
+    obytes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(2)]
+    size_host = torch.zeros(2, dtype=torch.int64, pin_memory=True)
+    host_cap = est  # Tier-1 ring slots sized to the expected record, not the state
+    host_ring = [torch.empty(host_cap, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    state = {"ref_version": 0, "rest_version": 0, "content": "X"}  # content of A and R
+    done_ev = [None, None]  # (copy_done, comm_done) for each record slot
+    n_ops = {"encode": [], "fold": [], "stage": [], "replicate": []}
+
+    def step(k, timed):
+        slot = k % 2
+        cur = Y if state["content"] == "X" else X
+        v = state["ref_version"] + 1
+        if done_ev[slot] is not None:
+            for e in done_ev[slot]:
+                s_comp.wait_event(e)
+        e0, e1 = ev(), ev()
+        e0.record(s_comp)
+        tc.diff_encode(ctx, A, cur, recs[slot], obytes[slot], v, v - 1, T, C, True, stream=s_comp)
+        e1.record(s_comp)
+        with torch.cuda.stream(s_comp):
+            size_host[slot].copy_(obytes[slot][0], non_blocking=True)
+        sz_ev = torch.cuda.Event()
+        sz_ev.record(s_comp)
+        sz_ev.synchronize()
+        nbytes = int(size_host[slot].item())
+        if nbytes > min(rec_cap, host_cap):
+            raise RuntimeError("record exceeds the staging buffers")
+        # Tier-1: D2H into the pinned ring on the copy stream
+        s_copy.wait_event(e1)
+        c0, c1 = ev(), ev()
+        c0.record(s_copy)
+        tc.stage_host(host_ring[slot], recs[slot], nbytes, tc.D2H, stream=s_copy)
+        c1.record(s_copy)
+        # Tier-2: ring-neighbour replication
+        r0 = r1 = None
+        if comm is not None:
+            s_comm.wait_event(e1)
+            r0, r1 = ev(), ev()
+            r0.record(s_comm)
+            comm.replicate_peer(recs[slot], obytes[slot], recv, tc.TO_NEXT, stream=s_comm)
+            r1.record(s_comm)
+        # restore: fold the record onto the replica
+        f0, f1 = ev(), ev()
+        f0.record(s_comp)
+        tc.diff_apply(ctx, R, state["rest_version"], [recs[slot]], [nbytes], stream=s_comp)
+        f1.record(s_comp)
+        state["rest_version"] = v
+        state["ref_version"] = v
+        state["content"] = "Y" if state["content"] == "X" else "X"
+        done_ev[slot] = [c1] + ([r1] if r1 is not None else [])
+        if timed:
+            n_ops["encode"].append((e0, e1))
+            n_ops["fold"].append((f0, f1))
+            n_ops["stage"].append((c0, c1))
+            if r0 is not None:
+                n_ops["replicate"].append((r0, r1, nbytes))
+        return nbytes
+
+    def sync_all():
+        for s in (s_comp, s_copy, s_comm):
+            s.synchronize()
+
+    for k in range(args.warmup):
+        step(k, False)
+    sync_all()
+    ctx.check(s_comp)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = ctx.launches
+    t_start, t_end = ev(), ev()
+    t_start.record(s_comp)
+    sizes_seen = []
+    for k in range(args.warmup, args.warmup + args.steps):
+        sizes_seen.append(step(k, True))
+    for s in (s_copy, s_comm):
+        e = torch.cuda.Event()
+        e.record(s)
+        s_comp.wait_event(e)
+    t_end.record(s_comp)
+    sync_all()
+    torch.cuda.synchronize()
+    launches = ctx.launches - launches0
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ctx.check(s_comp)
+    ms = t_start.elapsed_time(t_end)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+
+    def avg(pairs):
+        return sum(a.elapsed_time(b) for a, b, *_ in pairs) / max(1, len(pairs))
+
+    enc_ms, fold_ms, stage_ms = avg(n_ops["encode"]), avg(n_ops["fold"]), avg(n_ops["stage"])
+    rep_ms = avg(n_ops["replicate"]) if n_ops["replicate"] else None
+    # verify the chain: the restore replica equals the reference (both at the last version)
+    ok = all(torch.equal(a, r) for a, r in zip(A, R))
+    last_cur = Y if state["content"] == "Y" else X
+    ok = ok and all(torch.equal(a, c) for a, c in zip(A, last_cur))
+    host_last = host_ring[(args.warmup + args.steps - 1) % 2].numpy()
+    recs_info = record_counts(host_last, sizes_seen[-1])
+    enc_b, fold_b = algorithmic_bytes(recs_info)
+    enc_bs, fold_bs = algorithmic_bytes(recs_info, sector=True)
+    peak, peak_src = peaks()
+    rec_bytes = sizes_seen[-1]
+    changed = sum(r[4] for r in recs_info)
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, tc, ctx, dev, sizes, wb, X, Y, A, R, recs, obytes, host_ring, rec_cap, T, C,
+                      state, world, s_comp, s_copy)
+    traffic = load_traffic(workload, args.f)
+
+    if rank == 0:
+        res = {
+            "metric": METRIC,
+            "value": round(world * W / (ms_step * 1e-3) / 1e9, 2),
+            "unit": "GB/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "u16+u32 (bitwise)",
+            "data": "synthetic (seeded splitmix64 state shards, DESIGN.md §6)",
+            "config": {
+                "workload": WORKLOADS.get(workload, workload),
+                "shard_of_8": shard if workload != "cfg2" else None,
+                "phi": synth.CONFIGS[workload][0],
+                "segments": [[n, w] for n, w in zip(sizes, wb)],
+                "state_bytes_per_rank": W,
+                "f": args.f,
+                "structure": "S1 iid" if args.structure == 0 else "S2 runs",
+                "tile_words": T,
+                "chunk_words": C,
+                "fold_records_per_step": 1,
+                "l2": f"no flush: every step streams {W / 1e9:.1f} GB of state per rank (> 126 MB L2)",
+                "step": "encode(advance_ref) + D2H stage + " + ("NCCL ring replicate + " if world > 1 else "")
+                        + "fold onto restore replica",
+                "parallelism": f"dp{world} (independent ZeRO shards; Tier-2 ring r->r+1)" if world > 1 else "1 GPU",
+            },
+            "roofline": {
+                "kernel": "encode_kernel (tc_diff_encode)",
+                "bound": "hbm",
+                "achieved": round(enc_b / (enc_ms * 1e-3) / 1e9, 1),
+                "peak": peak,
+                "unit": "GB/s",
+                "frac": round(enc_b / (enc_ms * 1e-3) / 1e9 / peak, 4),
+                "traffic": traffic.get("encode"),
+                "algorithmic_bytes": enc_b,
+                "algorithmic_bytes_sector": int(enc_bs),
+                "peak_source": peak_src,
+                "per_launch_ms": round(enc_ms, 4),
+            },
+            "breakdown": {
+                "encode": {"ms": round(enc_ms, 4), "state_gbs": round(W / enc_ms / 1e6, 1),
+                           "hbm_gbs": round(enc_b / enc_ms / 1e6, 1), "frac_hbm": round(enc_b / enc_ms / 1e6 / peak, 4)},
+                "fold": {"ms": round(fold_ms, 4), "state_gbs": round(W / fold_ms / 1e6, 1),
+                         "hbm_gbs_word": round(fold_b / fold_ms / 1e6, 1),
+                         "hbm_gbs_sector": round(fold_bs / fold_ms / 1e6, 1),
+                         "frac_hbm_sector": round(fold_bs / fold_ms / 1e6 / peak, 4),
+                         "traffic": traffic.get("fold")},
+                "stage_d2h": {"ms": round(stage_ms, 4), "gbs": round(rec_bytes / stage_ms / 1e6, 2)},
+                "replicate": None if rep_ms is None else {
+                    "ms": round(rep_ms, 4), "gbs_per_direction": round(rec_bytes / rep_ms / 1e6, 1),
+                    "frac_nvlink_nominal": round(rec_bytes / rep_ms / 1e6 / NVLINK_GBS, 4),
+                    "frac_nvlink_measured": round(rec_bytes / rep_ms / 1e6 / NVLINK_MEASURED_GBS, 4)},
+                "record_bytes": rec_bytes,
+                "changed_words": changed,
+                "restore_equals_state": bool(ok),
+            },
+            "gpu_launches": launches,
+            "clocks": clk,
+            "e2e": e2e,
+        }
+        if args.cpu_baseline and world == 1:
+            res["cpu_baseline"] = cpu_baseline(workload, args)
+        print(json.dumps(res), flush=True)
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if not ok:
+        sys.exit(1)
+
+
+def run_e2e(args, tc, ctx, dev, sizes, wb, X, Y, A, R, recs, obytes, host_ring, rec_cap, T, C, state, world,
+            s_comp, s_copy):
+    """e2e through the C ABI with host buffers: per step H2D of the new state version from pinned
+    host memory, encode, D2H of the record (the result), fold onto the replica."""
+    import torch
+    import torch.distributed as dist
+
+    steps = min(args.steps, args.e2e_steps)
+    hX = [torch.empty(x.numel(), dtype=x.dtype, pin_memory=True) for x in X]
+    hY = [torch.empty(y.numel(), dtype=y.dtype, pin_memory=True) for y in Y]
+    for h, d in zip(hX + hY, X + Y):
+        h.copy_(d)
+    torch.cuda.synchronize()
+    if min(h.numel() for h in host_ring) < 1:
+        return None
+    CUR = Y  # device landing buffers: reuse Y/X storage as the H2D destination
+    size_host = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    h2d = d2h = 0
+
+    def one(k):
+        nonlocal h2d, d2h
+        src = hY if state["content"] == "X" else hX
+        dst = CUR
+        for hs, ds in zip(src, dst):
+            tc.stage_host(ds, hs, hs.numel() * hs.element_size(), tc.H2D, stream=s_comp)
+            h2d += hs.numel() * hs.element_size()
+        v = state["ref_version"] + 1
+        tc.diff_encode(ctx, A, dst, recs[0], obytes[0], v, v - 1, T, C, True, stream=s_comp)
+        with torch.cuda.stream(s_comp):
+            size_host[0].copy_(obytes[0][0], non_blocking=True)
+        e = torch.cuda.Event()
+        e.record(s_comp)
+        e.synchronize()
+        n = int(size_host.item())
+        if n > host_ring[0].numel():
+            raise RuntimeError("record exceeds the host ring slot")
+        tc.stage_host(host_ring[0], recs[0], n, tc.D2H, stream=s_comp)
+        d2h += n + 8
+        tc.diff_apply(ctx, R, state["rest_version"], [recs[0]], [n], stream=s_comp)
+        state["ref_version"] = v
+        state["rest_version"] = v
+        state["content"] = "Y" if state["content"] == "X" else "X"
+
+    one(0)  # warm (the first H2D of each pinned buffer)
+    s_comp.synchronize()
+    if world > 1:
+        dist.barrier()
+    h2d = d2h = 0
+    t0, t1 = ev(), ev()
+    t0.record(s_comp)
+    for k in range(1, steps + 1):
+        one(k)
+    t1.record(s_comp)
+    s_comp.synchronize()
+    ctx.check(s_comp)
+    ms = t0.elapsed_time(t1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / steps
+    W = sum(n * w for n, w in zip(sizes, wb))
+    del hX, hY
+    return {"value": round(world * W / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "steps": steps,
+            "ms_per_step": round(ms, 3), "h2d_bytes_per_step": h2d // steps, "d2h_bytes_per_step": d2h // steps,
+            "note": "H2D of the new state version from pinned host + encode + D2H record + fold, one stream"}
+
+
+def load_traffic(workload, f):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return {}
+    with open(p) as fh:
+        d = json.load(fh)
+    key = f"{workload}_f{f}"
+    return d.get(key, {})
+
+
+# ------------------------------------------------------------- the oracle arm -----------
+def oracle_sample(workload, f, sample_words):
+    """A bounded sample of the workload: words [0, sample_words) of every segment of shard 0."""
+    sizes, wb = synth.shard_layout(workload, 0)
+    sizes = [min(n, sample_words) for n in sizes]
+    seed = synth.SEED0
+    X = synth.state(sizes, wb, seed, 0, f)
+    Y = synth.state(sizes, wb, seed, 1, f)
+    return sizes, wb, X, Y
+
+
+def time_oracle(workload, f, sample_words, steps):
+    import oracle
+
+    sizes, wb, X, Y = oracle_sample(workload, f, sample_words)
+    W = sum(n * w for n, w in zip(sizes, wb))
+    ref = [a.copy() for a in X]
+    rest = [a.copy() for a in X]
+    times = []
+    ver = 0
+    for k in range(steps):
+        cur = Y if k % 2 == 0 else X
+        t0 = time.perf_counter()
+        rc, rec = oracle.encode(ref, cur, version=ver + 1, ref_version=ver)
+        rc2, _ = oracle.apply(rest, ver, rec)
+        times.append(time.perf_counter() - t0)
+        assert rc == 0 and rc2 == 0
+        ver += 1
+    return W, times, sizes
+
+
+def cpu_baseline(workload, args):
+    W, times, sizes = time_oracle(workload, args.f, args.sample_words, args.oracle_steps)
+    t = statistics.median(times)
+    return {"value": round(W / t / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"words [0, {sizes[0]}) of each of {len(sizes)} segments of the {workload} shard "
+                      f"({W / 1e6:.0f} MB of state); encode + restore per step; median of {len(times)}",
+            "host": host_desc()}
+
+
+def host_desc():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            model = next((ln.split(":", 1)[1].strip() for ln in fh if ln.startswith("model name")), "?")
+    except Exception:
+        model = "?"
+    return {"nproc": os.cpu_count(), "cpu": model}
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    workload = args.workload or ("cfg2" if world == 1 else "cfg3")
+    W, times, sizes = time_oracle(workload, args.f, args.sample_words, args.warmup + args.steps)
+    times = times[args.warmup:]
+    ms = 1e3 * sum(times) / len(times)
+    v = round(W / (ms * 1e-3) / 1e9, 4)
+    res = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u16+u32 (bitwise)", "data": "synthetic",
+        "config": {"workload": WORKLOADS.get(workload, workload), "f": args.f,
+                   "sample": f"words [0, {sizes[0]}) of each segment ({W / 1e6:.0f} MB of state) per step"},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": f"words [0, {sizes[0]}) of each of {len(sizes)} segments; encode + restore",
+                         "host": host_desc()},
+        "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(res), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=None, choices=[None, "cfg1", "cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--f", type=float, default=0.01)
+    ap.add_argument("--structure", type=int, default=0)
+    ap.add_argument("--tile-words", type=int, default=4096)
+    ap.add_argument("--chunk-words", type=int, default=1 << 28)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-baseline", type=int, default=1)
+    ap.add_argument("--sample-words", type=int, default=1 << 25)
+    ap.add_argument("--oracle-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
