@@ -32,6 +32,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# independent hardware work queues for the compute / copy / comm streams (the default of 8
+# connections can alias two streams onto one queue and serialize them)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 import numpy as np  # noqa: E402
 
@@ -199,15 +202,19 @@ def run_ours(args):
     rec_cap = cap if 3 * cap < free - (2 << 30) else est
     recs = [torch.empty(rec_cap, dtype=torch.uint8, device=dev) for _ in range(2)]
     recv = torch.empty(rec_cap, dtype=torch.uint8, device=dev) if comm else None
-    obytes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(2)]
-    size_host = torch.zeros(2, dtype=torch.int64, pin_memory=True)
+    # the encode kernel writes each record's length straight into mapped pinned memory, so the
+    # host learns it without a copy-engine round trip
+    ob_host = tc.HostBuffer(64)
+    ob_view = ob_host.view(torch.int64)
+    obytes = [ob_view[i: i + 1] for i in range(2)]
     host_cap = est  # Tier-1 ring slots sized to the expected record, not the state
-    host_ring = [torch.empty(host_cap, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    host_ring = [tc.HostBuffer(host_cap) for _ in range(2)]  # libtc-pinned Tier-1 ring
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     state = {"ref_version": 0, "rest_version": 0, "content": "X"}  # content of A and R
     done_ev = [None, None]  # (copy_done, comm_done) for each record slot
     n_ops = {"encode": [], "fold": [], "stage": [], "replicate": []}
+    host_t = {"stage": [], "fold": []}
 
     def step(k, timed):
         slot = k % 2
@@ -220,19 +227,17 @@ def run_ours(args):
         e0.record(s_comp)
         tc.diff_encode(ctx, A, cur, recs[slot], obytes[slot], v, v - 1, T, C, True, stream=s_comp)
         e1.record(s_comp)
-        with torch.cuda.stream(s_comp):
-            size_host[slot].copy_(obytes[slot][0], non_blocking=True)
-        sz_ev = torch.cuda.Event()
-        sz_ev.record(s_comp)
-        sz_ev.synchronize()
-        nbytes = int(size_host[slot].item())
+        e1.synchronize()
+        nbytes = int(ob_view[slot].item())
         if nbytes > min(rec_cap, host_cap):
             raise RuntimeError("record exceeds the staging buffers")
         # Tier-1: D2H into the pinned ring on the copy stream
         s_copy.wait_event(e1)
         c0, c1 = ev(), ev()
         c0.record(s_copy)
+        th0 = time.perf_counter()
         tc.stage_host(host_ring[slot], recs[slot], nbytes, tc.D2H, stream=s_copy)
+        host_t["stage"].append(time.perf_counter() - th0)
         c1.record(s_copy)
         # Tier-2: ring-neighbour replication
         r0 = r1 = None
@@ -244,9 +249,11 @@ def run_ours(args):
             r1.record(s_comm)
         # restore: fold the record onto the replica
         f0, f1 = ev(), ev()
+        th0 = time.perf_counter()
         f0.record(s_comp)
         tc.diff_apply(ctx, R, state["rest_version"], [recs[slot]], [nbytes], stream=s_comp)
         f1.record(s_comp)
+        host_t["fold"].append(time.perf_counter() - th0)
         state["rest_version"] = v
         state["ref_version"] = v
         state["content"] = "Y" if state["content"] == "X" else "X"
@@ -302,6 +309,12 @@ def run_ours(args):
         return sum(a.elapsed_time(b) for a, b, *_ in pairs) / max(1, len(pairs))
 
     enc_ms, fold_ms, stage_ms = avg(n_ops["encode"]), avg(n_ops["fold"]), avg(n_ops["stage"])
+    if args.timeline and rank == 0:
+        print("host call ms:", {k: [round(x * 1e3, 3) for x in v] for k, v in host_t.items()}, file=sys.stderr)
+        for name, pairs in n_ops.items():
+            for pr in pairs:
+                print(f"timeline {name:9s} start {t_start.elapsed_time(pr[0]):9.3f} end {t_start.elapsed_time(pr[1]):9.3f}",
+                      file=sys.stderr)
     rep_ms = avg(n_ops["replicate"]) if n_ops["replicate"] else None
     # verify the chain: the restore replica equals the reference (both at the last version)
     ok = all(torch.equal(a, r) for a, r in zip(A, R))
@@ -405,15 +418,16 @@ def run_e2e(args, tc, ctx, dev, sizes, wb, X, Y, A, R, recs, obytes, host_ring, 
     import torch.distributed as dist
 
     steps = min(args.steps, args.e2e_steps)
-    hX = [torch.empty(x.numel(), dtype=x.dtype, pin_memory=True) for x in X]
-    hY = [torch.empty(y.numel(), dtype=y.dtype, pin_memory=True) for y in Y]
+    bX = [tc.HostBuffer(x.numel() * x.element_size()) for x in X]
+    bY = [tc.HostBuffer(y.numel() * y.element_size()) for y in Y]
+    hX = [b.view(x.dtype) for b, x in zip(bX, X)]
+    hY = [b.view(y.dtype) for b, y in zip(bY, Y)]
     for h, d in zip(hX + hY, X + Y):
         h.copy_(d)
     torch.cuda.synchronize()
     if min(h.numel() for h in host_ring) < 1:
         return None
     CUR = Y  # device landing buffers: reuse Y/X storage as the H2D destination
-    size_host = torch.zeros(1, dtype=torch.int64, pin_memory=True)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     h2d = d2h = 0
 
@@ -426,13 +440,11 @@ def run_e2e(args, tc, ctx, dev, sizes, wb, X, Y, A, R, recs, obytes, host_ring, 
             h2d += hs.numel() * hs.element_size()
         v = state["ref_version"] + 1
         tc.diff_encode(ctx, A, dst, recs[0], obytes[0], v, v - 1, T, C, True, stream=s_comp)
-        with torch.cuda.stream(s_comp):
-            size_host[0].copy_(obytes[0][0], non_blocking=True)
         e = torch.cuda.Event()
         e.record(s_comp)
         e.synchronize()
-        n = int(size_host.item())
-        if n > host_ring[0].numel():
+        n = int(obytes[0].item())
+        if n > host_ring[0].nbytes:
             raise RuntimeError("record exceeds the host ring slot")
         tc.stage_host(host_ring[0], recs[0], n, tc.D2H, stream=s_comp)
         d2h += n + 8
@@ -460,6 +472,8 @@ def run_e2e(args, tc, ctx, dev, sizes, wb, X, Y, A, R, recs, obytes, host_ring, 
     ms = float(t.item()) / steps
     W = sum(n * w for n, w in zip(sizes, wb))
     del hX, hY
+    for b in bX + bY:
+        b.free()
     return {"value": round(world * W / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "steps": steps,
             "ms_per_step": round(ms, 3), "h2d_bytes_per_step": h2d // steps, "d2h_bytes_per_step": d2h // steps,
             "note": "H2D of the new state version from pinned host + encode + D2H record + fold, one stream"}
@@ -559,6 +573,7 @@ def main():
     ap.add_argument("--tile-words", type=int, default=4096)
     ap.add_argument("--chunk-words", type=int, default=1 << 28)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--timeline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--sample-words", type=int, default=1 << 25)

@@ -143,6 +143,10 @@ tc_status tc_diff_encode(tc_ctx* ctx, const tc_segment* segs, int nseg,
  * pageable copy would silently stall the caller). */
 tc_status tc_stage_host(void* dst, const void* src, uint64_t bytes, int dir,
                         tc_stream copy_stream);
+/* Page-locked host buffer for the Tier-1 ring (cudaHostAlloc, portable + mapped), owned by the
+ * caller until tc_host_free.  Copies between it and the device never block the caller. */
+tc_status tc_host_alloc(uint64_t bytes, void** out);
+tc_status tc_host_free(void* p);
 
 /* Tier-2 (§3.1 ring peer mapping; §3.2 "Peer ranks first
  * exchange their serialized payload sizes").  Collective over the

@@ -16,11 +16,19 @@
 struct tc_comm {
     ncclComm_t nccl = nullptr;
     int nranks = 0, rank = 0, device = 0;
-    uint64_t* dev_sizes = nullptr;   // device [0] peer size, [1] dst's cap, [2] my cap
-    uint64_t* host_sizes = nullptr;  // pinned [0] mine, [1] peer size, [2] dst cap, [3] my cap
+    uint64_t* dev_sizes = nullptr;   // device [0] peer size, [1] dst's cap, [2] my cap, [3] my size
+    uint64_t* host_sizes = nullptr;  // pinned mirror of dev_sizes
 };
 
 namespace {
+
+// Stage the size-exchange words on the comm stream: dev[2] = my receive capacity, dev[3] = my
+// payload size read from `send_bytes` (device memory or mapped pinned host memory, as written
+// by tc_diff_encode) — a kernel, so no copy engine sits on the replication path.
+__global__ void stage_sizes_kernel(uint64_t* dev, const uint64_t* send_bytes, uint64_t cap) {
+    dev[2] = cap;
+    dev[3] = *reinterpret_cast<const volatile uint64_t*>(send_bytes);
+}
 
 tc_status nccl_fail(ncclResult_t r, const char* what) {
     tc::set_error(std::string(what) + ": " + ncclGetErrorString(r));
@@ -113,13 +121,14 @@ tc_status tc_replicate_peer(tc_comm* c, const void* send, const uint64_t* send_b
     const int src = direction == TC_TO_NEXT ? prev : next;
     *recv_bytes = 0;
     if (P == 1) {  // the ring of one: the replica is the local record itself
-        cudaError_t e = cudaMemcpyAsync(c->host_sizes, send_bytes, 8, cudaMemcpyDeviceToHost, s);
+        stage_sizes_kernel<<<1, 1, 0, s>>>(c->dev_sizes, send_bytes, recv_cap);
+        cudaError_t e = cudaMemcpyAsync(c->host_sizes, c->dev_sizes, 32, cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) {
             tc::set_error(std::string("size read: ") + cudaGetErrorString(e));
             return TC_ERR_CUDA;
         }
-        const uint64_t n = c->host_sizes[0];
+        const uint64_t n = c->host_sizes[3];
         if (n > recv_cap) {
             tc::set_error("payload larger than recv_cap");
             return TC_ERR_CAPACITY;
@@ -130,22 +139,21 @@ tc_status tc_replicate_peer(tc_comm* c, const void* send, const uint64_t* send_b
     }
     // 1) size exchange: my payload size goes to dst, my receive capacity goes
     //    to src, so sender and receiver take the same send/skip decision (no orphan send).
-    c->host_sizes[3] = recv_cap;
-    cudaError_t e = cudaMemcpyAsync(c->dev_sizes + 2, c->host_sizes + 3, 8, cudaMemcpyHostToDevice, s);
+    stage_sizes_kernel<<<1, 1, 0, s>>>(c->dev_sizes, send_bytes, recv_cap);
+    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
-        tc::set_error(std::string("cap stage: ") + cudaGetErrorString(e));
+        tc::set_error(std::string("size stage: ") + cudaGetErrorString(e));
         return TC_ERR_CUDA;
     }
     ncclResult_t r = ncclGroupStart();
-    if (r == ncclSuccess) r = ncclSend(send_bytes, 8, ncclUint8, dst, c->nccl, s);
+    if (r == ncclSuccess) r = ncclSend(c->dev_sizes + 3, 8, ncclUint8, dst, c->nccl, s);
     if (r == ncclSuccess) r = ncclSend(c->dev_sizes + 2, 8, ncclUint8, src, c->nccl, s);
     if (r == ncclSuccess) r = ncclRecv(c->dev_sizes, 8, ncclUint8, src, c->nccl, s);
     if (r == ncclSuccess) r = ncclRecv(c->dev_sizes + 1, 8, ncclUint8, dst, c->nccl, s);
     ncclResult_t r2 = ncclGroupEnd();
     if (r != ncclSuccess) return nccl_fail(r, "size exchange");
     if (r2 != ncclSuccess) return nccl_fail(r2, "size exchange (group end)");
-    e = cudaMemcpyAsync(c->host_sizes, send_bytes, 8, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(c->host_sizes + 1, c->dev_sizes, 16, cudaMemcpyDeviceToHost, s);
+    e = cudaMemcpyAsync(c->host_sizes, c->dev_sizes, 32, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {
         tc_status st = check_async(c);
@@ -153,7 +161,8 @@ tc_status tc_replicate_peer(tc_comm* c, const void* send, const uint64_t* send_b
         tc::set_error(std::string("size exchange sync: ") + cudaGetErrorString(e));
         return TC_ERR_CUDA;
     }
-    const uint64_t mine = c->host_sizes[0], theirs = c->host_sizes[1], dst_cap = c->host_sizes[2];
+    // host_sizes now mirrors dev: [0] peer size, [1] dst's cap, [2] my cap, [3] my size
+    const uint64_t mine = c->host_sizes[3], theirs = c->host_sizes[0], dst_cap = c->host_sizes[1];
     const bool do_send = mine <= dst_cap, do_recv = theirs <= recv_cap;
     // 2) payload
     r = ncclGroupStart();

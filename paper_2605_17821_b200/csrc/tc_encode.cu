@@ -88,36 +88,7 @@ struct Word<2> {
     static constexpr uint32_t kBlock = kEncBlockWords2;
 };
 
-// Warp-cooperative decoupled look-back within one chunk.  Block b's predecessors in the
-// same chunk are b-1 ... first (the chunk's first block, which always publishes INCLUSIVE).
-__device__ __forceinline__ uint32_t lookback(const EncParams& P, uint64_t b, uint64_t first, int lane) {
-    uint32_t excl = 0;
-    int64_t j = static_cast<int64_t>(b) - 1;
-    uint32_t spins = 0;
-    while (true) {
-        const int64_t idx = j - lane;
-        const unsigned long long sv = idx >= static_cast<int64_t>(first) ? ld_relaxed(&P.status[idx]) : kFlagInc;
-        const uint32_t flag = static_cast<uint32_t>(sv >> 62);
-        const uint32_t incl = __ballot_sync(0xffffffffu, flag == 2);
-        const uint32_t empty = __ballot_sync(0xffffffffu, flag == 0);
-        const uint32_t upto = incl ? (((incl & (0u - incl)) << 1) - 1u) : 0xffffffffu;
-        if (empty & upto) {
-            if (++spins > kSpinLimit) {
-                if (lane == 0) tc_set_err(P.err, TC_ERR_INTERNAL);
-                return excl;
-            }
-            __nanosleep(20);
-            continue;
-        }
-        uint32_t v = ((upto >> lane) & 1u) ? static_cast<uint32_t>(sv) : 0u;
-#pragma unroll
-        for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-        excl += v;
-        if (incl) return excl;
-        j -= 32;
-    }
-}
-
+// Record start of chunk c (published by the last block of chunk c-1 as value | 1).
 __device__ __forceinline__ unsigned long long wait_rstart(const EncParams& P, uint64_t c) {
     if (c == 0) return 0;
     uint32_t spins = 0;
@@ -132,188 +103,269 @@ __device__ __forceinline__ unsigned long long wait_rstart(const EncParams& P, ui
     return v & ~1ull;
 }
 
+__device__ __forceinline__ void bar_sync(uint32_t id, uint32_t n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint32_t id, uint32_t n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+constexpr uint32_t kComputeWarps = kEncThreads / 32;   // 8 warps compare/compact
+constexpr uint32_t kCtaThreads = kEncThreads + 32;     // + 1 scan warp (look-back)
+constexpr uint32_t kBarCompute = 1;                    // named barrier: compute warps only
+constexpr uint32_t kBarPrefix = 2;                     // scan warp -> compute warps
+
 struct BlockInfo {
-    uint64_t b;          // global block index (= ticket)
-    uint64_t first;      // global index of the chunk's first block
-    uint64_t chunk;      // global chunk index
-    uint64_t chunk_off;  // word offset of the chunk in its segment
-    uint32_t m;          // words in the chunk
-    uint32_t k;          // block index within the chunk
-    uint32_t p0;         // chunk-relative first word of the block
-    uint32_t nb;         // words in this block
+    unsigned long long b;          // global block index (= ticket)
+    unsigned long long first;      // global index of the chunk's first block
+    unsigned long long chunk;      // global chunk index
+    unsigned long long chunk_off;  // word offset of the chunk in its segment
+    uint32_t m;                    // words in the chunk
+    uint32_t k;                    // block index within the chunk
+    uint32_t p0;                   // chunk-relative first word of the block
+    uint32_t nb;                   // words in this block
     uint32_t seg;
-    bool last;           // last block of its chunk
+    uint32_t w;
+    uint32_t last;                 // last block of its chunk
 };
 
+struct EncSmem {
+    BlockInfo I;
+    uint64_t bar;
+    uint32_t bal[kEncBlockWords2 / 32];  // mask words of the block
+    uint32_t warp_cnt[kComputeWarps];
+    uint32_t warp_off[kComputeWarps];
+    uint32_t total;
+    uint32_t ready;   // counts published to the scan warp (polled)
+    uint32_t excl;    // in-chunk exclusive count of the block
+    unsigned long long rs;  // byte offset of the block's record
+};
+
+// Scan warp: decoupled look-back over the in-chunk status words.  The exclusive prefix of
+// block b does not depend on b's own data, so the look-back starts as soon as the ticket is
+// claimed, overlapping the TMA load and pass 1; b's AGGREGATE is published from inside the
+// polling loop the moment the compute warps report the block count.
+__device__ __forceinline__ void scan_warp(const EncParams& P, EncSmem& sm, int lane) {
+    const BlockInfo& I = sm.I;
+    volatile uint32_t* ready = &sm.ready;
+    uint32_t excl = 0;
+    bool published = false;
+    uint32_t spins = 0;
+    if (I.k != 0) {
+        long long j = static_cast<long long>(I.b) - 1;
+        while (true) {
+            if (!published && __any_sync(0xffffffffu, *ready != 0)) {
+                if (lane == 0) st_relaxed(&P.status[I.b], kFlagAgg | sm.total);
+                published = true;
+            }
+            const long long idx = j - lane;
+            const unsigned long long sv =
+                idx >= static_cast<long long>(I.first) ? ld_relaxed(&P.status[idx]) : kFlagInc;
+            const uint32_t flag = static_cast<uint32_t>(sv >> 62);
+            const uint32_t incl = __ballot_sync(0xffffffffu, flag == 2);
+            const uint32_t empty = __ballot_sync(0xffffffffu, flag == 0);
+            const uint32_t upto = incl ? (((incl & (0u - incl)) << 1) - 1u) : 0xffffffffu;
+            if (empty & upto) {
+                if (++spins > kSpinLimit) {
+                    if (lane == 0) tc_set_err(P.err, TC_ERR_INTERNAL);
+                    break;
+                }
+                __nanosleep(32);
+                continue;
+            }
+            uint32_t v = ((upto >> lane) & 1u) ? static_cast<uint32_t>(sv) : 0u;
+#pragma unroll
+            for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+            excl += v;
+            if (incl) break;
+            j -= 32;
+        }
+    }
+    while (!*ready) __nanosleep(20);
+    const uint32_t total = sm.total;
+    if (lane == 0) {
+        st_relaxed(&P.status[I.b], kFlagInc | static_cast<unsigned long long>(excl + total));
+        const unsigned long long rs = wait_rstart(P, I.chunk);
+        if (I.last) {
+            const uint64_t W = I.w;
+            const uint64_t count = static_cast<uint64_t>(excl) + total;
+            const uint64_t n_mask = cdiv(I.m, 32);
+            const uint64_t n_tiles = cdiv(I.m, P.T);
+            const uint64_t rec_total = record_bytes(I.m, P.T, I.w, count);
+            uint8_t* rec = P.out + rs;
+            uint64_t* h = reinterpret_cast<uint64_t*>(rec);
+            h[0] = 0x31444354ull /* "TCD1" */ | (1ull << 32) | (W << 48) | (1ull << 56);
+            h[1] = static_cast<uint64_t>(P.T) | (static_cast<uint64_t>(I.seg) << 32);
+            h[2] = I.chunk_off;
+            h[3] = I.m;
+            h[4] = count;
+            h[5] = P.version;
+            h[6] = P.ref_version;
+            h[7] = rec_total;
+            uint32_t* gmask = reinterpret_cast<uint32_t*>(rec + kHdrBytes);
+            for (uint64_t x = n_mask; x < pad16(4 * n_mask) / 4; ++x) gmask[x] = 0;
+            uint32_t* gtoff = reinterpret_cast<uint32_t*>(rec + kHdrBytes + pad16(4 * n_mask));
+            gtoff[n_tiles] = static_cast<uint32_t>(count);
+            for (uint64_t x = n_tiles + 1; x < pad16(4 * (n_tiles + 1)) / 4; ++x) gtoff[x] = 0;
+            uint8_t* gval = rec + record_fixed_bytes(I.m, P.T);
+            for (uint64_t x = W * count; x < pad16(W * count); ++x) gval[x] = 0;
+            const unsigned long long next = rs + rec_total;
+            st_relaxed(&P.rstart[I.chunk + 1], next | 1ull);
+            if (I.chunk + 1 == P.total_chunks) *P.out_bytes = next;
+        }
+        sm.excl = excl;
+        sm.rs = rs;
+    }
+    __syncwarp();
+    bar_arrive(kBarPrefix, kCtaThreads);
+}
+
+// Compute warps (8): stage wait, pass 1 (compare -> ballot = mask word; fused ref advance),
+// counts, then (after the scan warp's prefix) pass 2 (mask words, tile_off, packed values).
 template <int W>
-__device__ __forceinline__ void encode_block(const EncParams& P, const BlockInfo& I, uint8_t* tile,
-                                             uint32_t* s_bal, uint32_t* s_warp, uint64_t* s_bar,
-                                             uint32_t* s_excl, unsigned long long* s_rs) {
+__device__ __forceinline__ void compute_warps(const EncParams& P, EncSmem& sm, uint8_t* tile, int tid) {
     using word_t = typename Word<W>::T;
     constexpr uint32_t B = Word<W>::kBlock;
-    constexpr uint32_t kWarps = kEncThreads / 32;
-    constexpr uint32_t MPW = B / 32 / kWarps;  // mask words per warp (16 | 32)
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    constexpr uint32_t MPW = B / 32 / kComputeWarps;  // mask words per warp (16 | 32)
+    const int lane = tid & 31, wid = tid >> 5;
+    const BlockInfo& I = sm.I;
     const EncSeg& S = P.seg[I.seg];
-
     word_t* sref = reinterpret_cast<word_t*>(tile);
     word_t* scur = sref + B;
     word_t* gref = reinterpret_cast<word_t*>(S.ref) + I.chunk_off + I.p0;
     const word_t* gcur = reinterpret_cast<const word_t*>(S.cur) + I.chunk_off + I.p0;
 
-    // ---- stage ref / cur of the block into shared memory (TMA bulk + tail words) ----
+    // tail words (< 16 bytes) not covered by the bulk copy; pad the rest of a short block with
+    // equal words so pass 1 needs no bounds test
     const uint32_t bytes = I.nb * W;
     const uint32_t bulk = bytes & ~15u;
-    if (tid == 0) {
-        if (bulk) {
-            mbar_arrive_expect_tx(s_bar, 2 * bulk);
-            bulk_g2s(sref, gref, bulk, s_bar);
-            bulk_g2s(scur, gcur, bulk, s_bar);
-        } else {
-            mbar_arrive(s_bar);
+    if (I.nb < B) {
+        for (uint32_t i = bulk / W + tid; i < B; i += kEncThreads) {
+            const bool in = i < I.nb;
+            sref[i] = in ? gref[i] : word_t(0);
+            scur[i] = in ? gcur[i] : word_t(0);
         }
     }
-    const uint32_t tail = (bytes - bulk) / W;
-    if (static_cast<uint32_t>(tid) < tail) {
-        const uint32_t i = bulk / W + tid;
-        sref[i] = gref[i];
-        scur[i] = gcur[i];
-    }
-    mbar_wait_parity(s_bar, 0);
-    __syncthreads();
+    mbar_wait_parity(&sm.bar, 0);
+    if (I.nb < B) bar_sync(kBarCompute, kEncThreads);
 
-    // ---- pass 1: compare, ballot -> mask word, popc; fused ref advance ----
-    uint32_t cnt = 0;
+    // ---- pass 1 ----
     const bool adv = P.advance_ref != 0;
+    const uint32_t mw0 = wid * MPW;
 #pragma unroll 4
     for (uint32_t q = 0; q < MPW; ++q) {
-        const uint32_t mw = wid * MPW + q;
-        const uint32_t i = mw * 32 + lane;
-        const word_t a = sref[i];
+        const uint32_t i = (mw0 + q) * 32 + lane;
         const word_t v = scur[i];
-        const bool ch = (i < I.nb) && (a != v);
+        const bool ch = sref[i] != v;
         const uint32_t bal = __ballot_sync(0xffffffffu, ch);
-        if (lane == 0) s_bal[mw] = bal;
-        if (adv && ch) gref[i] = v;
-        cnt += __popc(bal);
+        if (lane == 0) sm.bal[mw0 + q] = bal;
+        if (adv && bal) {
+            if (ch) gref[i] = v;
+        }
     }
-    if (lane == 0) s_warp[wid] = cnt;
-    __syncthreads();
-
-    // ---- block total, warp offsets, look-back, record start (warp 0) ----
-    if (wid == 0) {
-        const uint32_t wc = lane < static_cast<int>(kWarps) ? s_warp[lane] : 0u;
-        uint32_t inc = wc;
+    __syncwarp();
+    // ---- counts: lane-per-mask-word popcount scan over the warp's range ----
+    uint32_t bal = 0, pre = 0;
+    if (lane < static_cast<int>(MPW)) bal = sm.bal[mw0 + lane];
+    const uint32_t c = __popc(bal);
+    uint32_t inc = c;
 #pragma unroll
-        for (int d = 1; d < static_cast<int>(kWarps); d <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
-            if (lane >= d) inc += t;
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += t;
+    }
+    pre = inc - c;
+    if (lane == 31) sm.warp_cnt[wid] = inc;
+    bar_sync(kBarCompute, kEncThreads);
+    if (wid == 0) {
+        const uint32_t wc = lane < static_cast<int>(kComputeWarps) ? sm.warp_cnt[lane] : 0u;
+        uint32_t x = wc;
+#pragma unroll
+        for (int d = 1; d < static_cast<int>(kComputeWarps); d <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += t;
         }
-        const uint32_t total = __shfl_sync(0xffffffffu, inc, kWarps - 1);
-        if (lane < static_cast<int>(kWarps)) s_warp[kWarps + lane] = inc - wc;  // warp exclusive offsets
-        uint32_t excl = 0;
-        if (I.k == 0) {
-            if (lane == 0) st_relaxed(&P.status[I.b], kFlagInc | total);
-        } else {
-            if (lane == 0) st_relaxed(&P.status[I.b], kFlagAgg | total);
-            excl = lookback(P, I.b, I.first, lane);
-            if (lane == 0) st_relaxed(&P.status[I.b], kFlagInc | static_cast<unsigned long long>(excl + total));
-        }
-        if (lane == 0) {
-            const unsigned long long rs = wait_rstart(P, I.chunk);
-            if (I.last) {
-                const uint64_t count = static_cast<uint64_t>(excl) + total;
-                const uint64_t n_mask = cdiv(I.m, 32);
-                const uint64_t n_tiles = cdiv(I.m, P.T);
-                const uint64_t rec_total = record_bytes(I.m, P.T, W, count);
-                uint8_t* rec = P.out + rs;
-                uint64_t* h = reinterpret_cast<uint64_t*>(rec);
-                h[0] = 0x31444354ull /* "TCD1" */ | (1ull << 32) | (static_cast<uint64_t>(W) << 48) | (1ull << 56);
-                h[1] = static_cast<uint64_t>(P.T) | (static_cast<uint64_t>(I.seg) << 32);
-                h[2] = I.chunk_off;
-                h[3] = I.m;
-                h[4] = count;
-                h[5] = P.version;
-                h[6] = P.ref_version;
-                h[7] = rec_total;
-                uint32_t* gmask = reinterpret_cast<uint32_t*>(rec + kHdrBytes);
-                for (uint64_t x = n_mask; x < pad16(4 * n_mask) / 4; ++x) gmask[x] = 0;
-                uint32_t* gtoff = reinterpret_cast<uint32_t*>(rec + kHdrBytes + pad16(4 * n_mask));
-                gtoff[n_tiles] = static_cast<uint32_t>(count);
-                for (uint64_t x = n_tiles + 1; x < pad16(4 * (n_tiles + 1)) / 4; ++x) gtoff[x] = 0;
-                word_t* gval = reinterpret_cast<word_t*>(rec + record_fixed_bytes(I.m, P.T));
-                for (uint64_t x = count; x < pad16(W * count) / W; ++x) gval[x] = 0;
-                const unsigned long long next = rs + rec_total;
-                st_relaxed(&P.rstart[I.chunk + 1], next | 1ull);
-                if (I.chunk + 1 == P.total_chunks) *P.out_bytes = next;
-            }
-            *s_excl = excl;
-            *s_rs = rs;
+        if (lane < static_cast<int>(kComputeWarps)) sm.warp_off[lane] = x - wc;
+        if (lane == kComputeWarps - 1) {
+            sm.total = x;
+            __threadfence_block();
+            *reinterpret_cast<volatile uint32_t*>(&sm.ready) = 1u;
         }
     }
-    __syncthreads();
+    bar_sync(kBarPrefix, kCtaThreads);  // scan warp has the exclusive prefix + record start
 
-    // ---- pass 2: tile_off entries, compacted values, mask words ----
-    const unsigned long long rs = *s_rs;
-    uint8_t* rec = P.out + rs;
+    // ---- pass 2 ----
+    uint8_t* rec = P.out + sm.rs;
     const uint64_t n_mask = cdiv(I.m, 32);
     uint32_t* gmask = reinterpret_cast<uint32_t*>(rec + kHdrBytes);
     uint32_t* gtoff = reinterpret_cast<uint32_t*>(rec + kHdrBytes + pad16(4 * n_mask));
     word_t* gval = reinterpret_cast<word_t*>(rec + record_fixed_bytes(I.m, P.T));
-    uint32_t running = *s_excl + s_warp[kWarps + wid];
-    const uint32_t lt = (1u << lane) - 1u;
-    for (uint32_t q = 0; q < MPW; ++q) {
-        const uint32_t mw = wid * MPW + q;
-        const uint32_t p = I.p0 + mw * 32;
-        if (p >= I.m) break;
-        const uint32_t bal = s_bal[mw];
-        if (lane == 0 && (p & (P.T - 1)) == 0) gtoff[p / P.T] = running;
-        if (bal) {
-            if ((bal >> lane) & 1u) gval[running + __popc(bal & lt)] = scur[mw * 32 + lane];
-            running += __popc(bal);
-        }
+    const uint32_t base = sm.excl + sm.warp_off[wid];
+    const uint32_t p = I.p0 + (mw0 + lane) * 32;  // chunk-relative first word of this lane's mask word
+    const bool mine = lane < static_cast<int>(MPW) && p < I.m;
+    if (mine) {
+        gmask[(I.p0 >> 5) + mw0 + lane] = bal;
+        if ((p & (P.T - 1)) == 0) gtoff[p / P.T] = base + pre;
     }
-    const uint32_t nmw = static_cast<uint32_t>(cdiv(I.nb, 32));
-    for (uint32_t t = tid; t < nmw; t += kEncThreads) gmask[I.p0 / 32 + t] = s_bal[t];
+    uint32_t nz = __ballot_sync(0xffffffffu, bal != 0);
+    const uint32_t lt = (1u << lane) - 1u;
+    while (nz) {
+        const int src = __ffs(nz) - 1;
+        nz &= nz - 1;
+        const uint32_t b = __shfl_sync(0xffffffffu, bal, src);
+        const uint32_t o = __shfl_sync(0xffffffffu, pre, src);
+        if ((b >> lane) & 1u) gval[base + o + __popc(b & lt)] = scur[(mw0 + src) * 32 + lane];
+    }
 }
 
-__global__ void __launch_bounds__(kEncThreads, 6) encode_kernel(const __grid_constant__ EncParams P) {
+__global__ void __launch_bounds__(kCtaThreads, 6) encode_kernel(const __grid_constant__ EncParams P) {
     extern __shared__ __align__(128) uint8_t tile[];
-    __shared__ uint32_t s_bal[kEncBlockWords2 / 32];
-    __shared__ uint32_t s_warp[2 * (kEncThreads / 32)];
-    __shared__ __align__(8) uint64_t s_bar;
-    __shared__ unsigned long long s_b;
-    __shared__ uint32_t s_excl;
-    __shared__ unsigned long long s_rs;
+    __shared__ EncSmem sm;
+    const int tid = threadIdx.x;
 
-    if (threadIdx.x == 0) {
-        s_b = atomicAdd(P.ticket, 1ull);
-        mbar_init(&s_bar, 1);
+    if (tid == kEncThreads) {
+        // one thread: ticket, decode, barrier init, TMA issue — loads start as early as possible
+        BlockInfo I;
+        I.b = atomicAdd(P.ticket, 1ull);
+        int s = 0;
+        while (s + 1 < P.nseg && I.b >= P.seg[s + 1].first_block) ++s;
+        const EncSeg& S = P.seg[s];
+        const uint32_t lb = static_cast<uint32_t>(I.b - S.first_block);
+        const uint32_t bpc = static_cast<uint32_t>(S.blocks_per_chunk);
+        const uint32_t cl = lb / bpc;
+        I.k = lb - cl * bpc;
+        I.seg = s;
+        I.w = S.w;
+        I.chunk = S.first_chunk + cl;
+        I.chunk_off = static_cast<unsigned long long>(cl) * P.C;
+        I.m = static_cast<uint32_t>(S.n - I.chunk_off < P.C ? S.n - I.chunk_off : P.C);
+        I.first = I.b - I.k;
+        const uint32_t nblk = I.m ? (I.m + S.block_words - 1) / S.block_words : 1u;
+        I.last = (I.k + 1 == nblk);
+        I.p0 = I.k * S.block_words;
+        I.nb = I.m > I.p0 ? (I.m - I.p0 < S.block_words ? I.m - I.p0 : S.block_words) : 0u;
+        sm.I = I;
+        sm.ready = 0;
+        mbar_init(&sm.bar, 1);
+        const uint32_t bulk = (I.nb * S.w) & ~15u;
+        if (bulk) {
+            const uint8_t* gref = S.ref + (I.chunk_off + I.p0) * S.w;
+            const uint8_t* gcur = S.cur + (I.chunk_off + I.p0) * S.w;
+            mbar_arrive_expect_tx(&sm.bar, 2 * bulk);
+            bulk_g2s(tile, gref, bulk, &sm.bar);
+            bulk_g2s(tile + 16384, gcur, bulk, &sm.bar);
+        } else {
+            mbar_arrive(&sm.bar);
+        }
     }
     __syncthreads();
-
-    BlockInfo I;
-    I.b = s_b;
-    int s = 0;
-    while (s + 1 < P.nseg && I.b >= P.seg[s + 1].first_block) ++s;
-    const EncSeg& S = P.seg[s];
-    const uint64_t lb = I.b - S.first_block;
-    const uint64_t cl = lb / S.blocks_per_chunk;
-    I.k = static_cast<uint32_t>(lb - cl * S.blocks_per_chunk);
-    I.seg = s;
-    I.chunk = S.first_chunk + cl;
-    I.chunk_off = cl * P.C;
-    I.m = static_cast<uint32_t>(S.n - I.chunk_off < P.C ? S.n - I.chunk_off : P.C);
-    I.first = I.b - I.k;
-    const uint32_t nblk = I.m ? static_cast<uint32_t>(cdiv(I.m, S.block_words)) : 1u;
-    I.last = (I.k + 1 == nblk);
-    I.p0 = I.k * S.block_words;
-    I.nb = I.m > I.p0 ? (I.m - I.p0 < S.block_words ? I.m - I.p0 : S.block_words) : 0u;
-
-    if (S.w == 4)
-        encode_block<4>(P, I, tile, s_bal, s_warp, &s_bar, &s_excl, &s_rs);
-    else
-        encode_block<2>(P, I, tile, s_bal, s_warp, &s_bar, &s_excl, &s_rs);
+    if (tid >= kEncThreads) {
+        scan_warp(P, sm, tid & 31);
+    } else if (sm.I.w == 4) {
+        compute_warps<4>(P, sm, tile, tid);
+    } else {
+        compute_warps<2>(P, sm, tile, tid);
+    }
 }
 
 }  // namespace
@@ -327,7 +379,7 @@ cudaError_t launch_encode(const EncParams& p, cudaStream_t s) {
         attr_set = true;
     }
     if (p.total_blocks == 0) return cudaSuccess;
-    encode_kernel<<<static_cast<unsigned>(p.total_blocks), kEncThreads, kEncDynSmem, s>>>(p);
+    encode_kernel<<<static_cast<unsigned>(p.total_blocks), kCtaThreads, kEncDynSmem, s>>>(p);
     return cudaGetLastError();
 }
 

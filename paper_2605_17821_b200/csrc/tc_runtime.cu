@@ -325,4 +325,23 @@ tc_status tc_stage_host(void* dst, const void* src, uint64_t bytes, int dir, tc_
     return TC_OK;
 }
 
+tc_status tc_host_alloc(uint64_t bytes, void** out) {
+    if (!out) return fail(TC_ERR_INVALID, "out is NULL");
+    *out = nullptr;
+    if (bytes == 0) return TC_OK;
+    cudaError_t e = cudaHostAlloc(out, bytes, cudaHostAllocPortable | cudaHostAllocMapped);
+    if (e != cudaSuccess) {
+        *out = nullptr;
+        return fail(TC_ERR_NOMEM, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+    }
+    return TC_OK;
+}
+
+tc_status tc_host_free(void* p) {
+    if (!p) return TC_OK;
+    cudaError_t e = cudaFreeHost(p);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFreeHost");
+    return TC_OK;
+}
+
 }  // extern "C"

@@ -62,6 +62,8 @@ def _load():
     L.tc_diff_encode.argtypes = [vp, ctypes.POINTER(Segment), cint, ctypes.POINTER(EncodeOpts), u64, u64,
                                  vp, u64, vp, vp]
     L.tc_stage_host.argtypes = [vp, vp, u64, cint, vp]
+    L.tc_host_alloc.argtypes = [u64, ctypes.POINTER(vp)]
+    L.tc_host_free.argtypes = [vp]
     L.tc_comm_get_unique_id.argtypes = [ctypes.c_char_p]
     L.tc_comm_init.argtypes = [cint, cint, cint, ctypes.c_char_p, ctypes.POINTER(vp)]
     L.tc_comm_destroy.argtypes = [vp]
@@ -71,7 +73,7 @@ def _load():
     L.tc_synth_base.argtypes = [vp, u64, u32, u64, u32, u64, vp]
     L.tc_synth_step.argtypes = [vp, u64, u32, u64, u32, u64, u64, cint, u64, vp]
     for name in ("tc_ctx_create", "tc_ctx_destroy", "tc_ctx_check", "tc_diff_bound", "tc_diff_encode",
-                 "tc_stage_host", "tc_comm_get_unique_id", "tc_comm_init", "tc_comm_destroy",
+                 "tc_stage_host", "tc_host_alloc", "tc_host_free", "tc_comm_get_unique_id", "tc_comm_init", "tc_comm_destroy",
                  "tc_replicate_peer", "tc_diff_apply", "tc_synth_base", "tc_synth_step"):
         getattr(L, name).restype = cint
     return L
@@ -203,6 +205,50 @@ def diff_apply(ctx: Ctx, state, state_version: int, records, record_bytes, strea
 def stage_host(dst: torch.Tensor, src: torch.Tensor, nbytes: int, direction: int, stream=None):
     _check(LIB.tc_stage_host(dst.data_ptr(), src.data_ptr(), int(nbytes), direction, _stream(stream)),
            "tc_stage_host")
+
+
+class HostBuffer:
+    """A page-locked host buffer from tc_host_alloc (the Tier-1 ring slot), viewed as a CPU uint8
+    tensor.  Freed with tc_host_free when this object is collected."""
+
+    def __init__(self, nbytes: int):
+        p = vp()
+        _check(LIB.tc_host_alloc(int(nbytes), ctypes.byref(p)), "tc_host_alloc")
+        self.ptr = p.value
+        self.nbytes = int(nbytes)
+        if nbytes:
+            arr = (ctypes.c_uint8 * self.nbytes).from_address(self.ptr)
+            self.tensor = torch.frombuffer(arr, dtype=torch.uint8)
+        else:
+            self.tensor = torch.empty(0, dtype=torch.uint8)
+
+    def view(self, dtype, n=None):
+        t = self.tensor.view(dtype)
+        return t if n is None else t[:n]
+
+    def data_ptr(self):
+        return self.ptr
+
+    def numel(self):
+        return self.nbytes
+
+    def element_size(self):
+        return 1
+
+    def numpy(self):
+        return self.tensor.numpy()
+
+    def free(self):
+        if self.ptr:
+            self.tensor = None
+            LIB.tc_host_free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 class Comm:

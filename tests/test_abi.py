@@ -13,7 +13,7 @@ def test_every_declared_symbol_is_exported():
     expected = {"tc_status_string", "tc_last_error", "tc_abi_version", "tc_ctx_create", "tc_ctx_destroy",
                 "tc_ctx_check", "tc_ctx_launches", "tc_diff_bound", "tc_diff_encode", "tc_stage_host",
                 "tc_comm_get_unique_id", "tc_comm_init", "tc_comm_destroy", "tc_replicate_peer",
-                "tc_diff_apply", "tc_synth_base", "tc_synth_step"}
+                "tc_diff_apply", "tc_synth_base", "tc_synth_step", "tc_host_alloc", "tc_host_free"}
     assert expected <= set(names), set(names) ^ expected
     for n in names:
         assert getattr(tc.LIB, n) is not None
