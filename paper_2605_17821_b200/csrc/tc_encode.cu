@@ -1,26 +1,31 @@
-// tc_encode.cu — single-pass differential-checkpoint encoder for sm_100a.
+// tc_encode.cu — the differential-checkpoint encoder for sm_100a (tc_diff_encode).
 //
 // What it computes: for every chunk of every segment,
 // the mask of changed words (unsigned bitwise compare, reading R5), the in-chunk exclusive
 // counts at every tile start (tile_off), the packed new words (values) and the record header;
-// optionally ref[i] <- cur[i] for changed words.  The paper's own compaction is "a single
-// fused pass to extract and compact surviving entries" (§3.2) — this kernel is
-// that single pass for the lossless word diff.
+// optionally ref[i] <- cur[i] for the changed words.  The paper extracts and compacts the
+// surviving entries in "a single fused pass" (§3.2) instead of multi-pass Top-K;
+// here the one pass over the 2W bytes of ref+cur is kernel A, and everything else touches only
+// the changed words.
 //
-// B200 design:
-//   * one CTA = one scan block of B words (B = 4096 fp32 / 8192 16-bit words = 16 KB per
-//     operand); a CTA takes a dynamic ticket so blocks are processed in stream order, which
-//     makes the decoupled look-back deadlock-free;
-//   * ref and cur of the block are staged to shared memory with two 1-D TMA bulk copies
-//     (cp.async.bulk ... mbarrier::complete_tx) — no register staging, 6 CTAs/SM keep
-//     ~190 KB of HBM reads in flight per SM;
-//   * lane l of a warp tests word 32*q + l, so __ballot_sync IS the mask word (LSB-first,
-//     reading R6) and __popc gives the counts;
-//   * in-chunk prefix: decoupled look-back over 64-bit status words {2-bit flag | count}
-//     (warp-wide 32-predecessor windows); chunk-level record start: a chain of "record
-//     start" words published by each chunk's last block (value | 1);
-//   * values are written compacted in index order (consecutive lanes -> consecutive
-//     addresses); mask words are written coalesced from shared memory.
+// Three launches, no look-back chain through HBM latency (DESIGN.md §7.1 explains why the
+// decoupled look-back single pass of v1 capped at ~2.5 TB/s):
+//   A  encode_mask_kernel   one CTA per scan block of B words (B = 4096 4-byte / 8192 2-byte
+//                           words; 16 KB per operand).  A dynamic ticket orders the blocks.
+//                           ref+cur are staged by two 1-D TMA bulk copies into shared memory;
+//                           lane l of a warp tests word 32q+l so __ballot_sync IS the mask word;
+//                           __popc + warp scans give counts; ref advance is fused.  A sparse
+//                           block (<= 4 KB of changed words) packs its new words into its spill
+//                           slot; a dense one leaves them for kernel B.  The mask and the
+//                           block-relative tile_off entries go straight to their final place once
+//                           the chunk's record start is known (chunk c waits only for chunk c-1's
+//                           counts, i.e. only at chunk boundaries); the block completing a chunk
+//                           writes its header and publishes the next record start.
+//   P  encode_prefix_kernel (1 CTA) exclusive scans of the per-group and per-chunk counts.
+//   B  encode_emit_kernel   one CTA per 256 blocks: block-wide scan of the block counts -> each
+//                           block's in-chunk prefix; a warp per block adds it to the block's
+//                           tile_off entries and moves the spilled words into place (sparse) or
+//                           re-reads mask + cur and packs them (dense).
 #include <cuda_runtime.h>
 
 #include "tc_internal.h"
@@ -29,8 +34,6 @@ namespace tc {
 
 namespace {
 
-constexpr unsigned long long kFlagAgg = 1ull << 62;
-constexpr unsigned long long kFlagInc = 2ull << 62;
 constexpr uint32_t kSpinLimit = 1u << 26;  // watchdog: a bug must not hang the GPU
 
 __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
@@ -88,8 +91,45 @@ struct Word<2> {
     static constexpr uint32_t kBlock = kEncBlockWords2;
 };
 
-// Record start of chunk c (published by the last block of chunk c-1 as value | 1).
-__device__ __forceinline__ unsigned long long wait_rstart(const EncParams& P, uint64_t c) {
+constexpr uint32_t kWarps = kEncThreads / 32;
+
+// Where block b lives (pure arithmetic on the per-segment launch table).
+struct BlockInfo {
+    unsigned long long b;          // global block index
+    unsigned long long chunk;      // global chunk index
+    unsigned long long chunk_off;  // word offset of the chunk in its segment
+    uint32_t m;                    // words in the chunk
+    uint32_t k;                    // block index within the chunk
+    uint32_t nblk;                 // blocks in the chunk
+    uint32_t p0;                   // chunk-relative first word of the block
+    uint32_t nb;                   // words in this block
+    uint32_t seg;
+    uint32_t w;
+};
+
+__device__ __forceinline__ BlockInfo decode_block(const EncParams& P, unsigned long long b) {
+    BlockInfo I;
+    I.b = b;
+    int s = 0;
+    while (s + 1 < P.nseg && b >= P.seg[s + 1].first_block) ++s;
+    const EncSeg& S = P.seg[s];
+    const uint32_t lb = static_cast<uint32_t>(b - S.first_block);
+    const uint32_t bpc = static_cast<uint32_t>(S.blocks_per_chunk);
+    const uint32_t cl = lb / bpc;
+    I.k = lb - cl * bpc;
+    I.seg = s;
+    I.w = S.w;
+    I.chunk = S.first_chunk + cl;
+    I.chunk_off = static_cast<unsigned long long>(cl) * P.C;
+    I.m = static_cast<uint32_t>(S.n - I.chunk_off < P.C ? S.n - I.chunk_off : P.C);
+    I.nblk = I.m ? (I.m + S.block_words - 1) / S.block_words : 1u;
+    I.p0 = I.k * S.block_words;
+    I.nb = I.m > I.p0 ? (I.m - I.p0 < S.block_words ? I.m - I.p0 : S.block_words) : 0u;
+    return I;
+}
+
+// Record start of chunk c (published by the block completing chunk c-1 as value | 1).
+__device__ __forceinline__ unsigned long long wait_rstart(const EncParams& P, unsigned long long c) {
     if (c == 0) return 0;
     uint32_t spins = 0;
     unsigned long long v;
@@ -98,103 +138,111 @@ __device__ __forceinline__ unsigned long long wait_rstart(const EncParams& P, ui
             tc_set_err(P.err, TC_ERR_INTERNAL);
             return 0;
         }
-        __nanosleep(32);
+        __nanosleep(64);
     }
     return v & ~1ull;
 }
 
-__device__ __forceinline__ void bar_sync(uint32_t id, uint32_t n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void bar_arrive(uint32_t id, uint32_t n) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-constexpr uint32_t kComputeWarps = kEncThreads / 32;   // 8 warps compare/compact
-constexpr uint32_t kCtaThreads = kEncThreads + 32;     // + 1 scan warp (look-back)
-constexpr uint32_t kBarCompute = 1;                    // named barrier: compute warps only
-constexpr uint32_t kBarPrefix = 2;                     // scan warp -> compute warps
-
-struct BlockInfo {
-    unsigned long long b;          // global block index (= ticket)
-    unsigned long long first;      // global index of the chunk's first block
-    unsigned long long chunk;      // global chunk index
-    unsigned long long chunk_off;  // word offset of the chunk in its segment
-    uint32_t m;                    // words in the chunk
-    uint32_t k;                    // block index within the chunk
-    uint32_t p0;                   // chunk-relative first word of the block
-    uint32_t nb;                   // words in this block
-    uint32_t seg;
-    uint32_t w;
-    uint32_t last;                 // last block of its chunk
-};
-
-struct EncSmem {
+struct SmemA {
     BlockInfo I;
     uint64_t bar;
-    uint32_t bal[kEncBlockWords2 / 32];  // mask words of the block
-    uint32_t warp_cnt[kComputeWarps];
-    uint32_t warp_off[kComputeWarps];
-    uint32_t total;
-    uint32_t ready;   // counts published to the scan warp (polled)
-    uint32_t excl;    // in-chunk exclusive count of the block
-    unsigned long long rs;  // byte offset of the block's record
+    uint32_t warp_cnt[kWarps];
+    unsigned long long rs;
 };
 
-// Scan warp: decoupled look-back over the in-chunk status words.  The exclusive prefix of
-// block b does not depend on b's own data, so the look-back starts as soon as the ticket is
-// claimed, overlapping the TMA load and pass 1; b's AGGREGATE is published from inside the
-// polling loop the moment the compute warps report the block count.
-__device__ __forceinline__ void scan_warp(const EncParams& P, EncSmem& sm, int lane) {
-    const BlockInfo& I = sm.I;
-    volatile uint32_t* ready = &sm.ready;
-    uint32_t excl = 0;
-    bool published = false;
-    uint32_t spins = 0;
-    if (I.k != 0) {
-        long long j = static_cast<long long>(I.b) - 1;
-        while (true) {
-            if (!published && __any_sync(0xffffffffu, *ready != 0)) {
-                if (lane == 0) st_relaxed(&P.status[I.b], kFlagAgg | sm.total);
-                published = true;
-            }
-            const long long idx = j - lane;
-            const unsigned long long sv =
-                idx >= static_cast<long long>(I.first) ? ld_relaxed(&P.status[idx]) : kFlagInc;
-            const uint32_t flag = static_cast<uint32_t>(sv >> 62);
-            const uint32_t incl = __ballot_sync(0xffffffffu, flag == 2);
-            const uint32_t empty = __ballot_sync(0xffffffffu, flag == 0);
-            const uint32_t upto = incl ? (((incl & (0u - incl)) << 1) - 1u) : 0xffffffffu;
-            if (empty & upto) {
-                if (++spins > kSpinLimit) {
-                    if (lane == 0) tc_set_err(P.err, TC_ERR_INTERNAL);
-                    break;
-                }
-                __nanosleep(32);
-                continue;
-            }
-            uint32_t v = ((upto >> lane) & 1u) ? static_cast<uint32_t>(sv) : 0u;
-#pragma unroll
-            for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-            excl += v;
-            if (incl) break;
-            j -= 32;
+// ------------------------------------------------------------------ kernel A ------------
+template <int W>
+__device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_t* tile, int tid) {
+    using word_t = typename Word<W>::T;
+    constexpr uint32_t B = Word<W>::kBlock;
+    constexpr uint32_t MPW = B / 32 / kWarps;  // mask words per warp (16 | 32)
+    const int lane = tid & 31, wid = tid >> 5;
+    const BlockInfo I = sm.I;
+    const EncSeg& S = P.seg[I.seg];
+    word_t* sref = reinterpret_cast<word_t*>(tile);
+    word_t* scur = sref + B;
+    word_t* gref = reinterpret_cast<word_t*>(S.ref) + I.chunk_off + I.p0;
+    const word_t* gcur = reinterpret_cast<const word_t*>(S.cur) + I.chunk_off + I.p0;
+
+    // words past the bulk copy: the < 16-byte tail, and equal padding up to B so that pass 1
+    // needs no bounds test
+    if (I.nb < B) {
+        const uint32_t bulk = (I.nb * W) & ~15u;
+        for (uint32_t i = bulk / W + tid; i < B; i += kEncThreads) {
+            const bool in = i < I.nb;
+            sref[i] = in ? gref[i] : word_t(0);
+            scur[i] = in ? gcur[i] : word_t(0);
         }
     }
-    while (!*ready) __nanosleep(20);
-    const uint32_t total = sm.total;
-    if (lane == 0) {
-        st_relaxed(&P.status[I.b], kFlagInc | static_cast<unsigned long long>(excl + total));
+    mbar_wait_parity(&sm.bar, 0);
+    if (I.nb < B) __syncthreads();
+
+    // ---- pass 1: compare -> ballot = mask word; fused ref advance ----
+    const bool adv = P.advance_ref != 0;
+    const uint32_t mw0 = wid * MPW;
+    uint32_t mine = 0;  // lane q keeps mask word mw0 + q
+#pragma unroll 4
+    for (uint32_t q = 0; q < MPW; ++q) {
+        const uint32_t i = (mw0 + q) * 32 + lane;
+        const word_t v = scur[i];
+        const bool ch = sref[i] != v;
+        const uint32_t bal = __ballot_sync(0xffffffffu, ch);
+        if (lane == static_cast<int>(q)) mine = bal;
+        if (adv && bal) {
+            if (ch) gref[i] = v;
+        }
+    }
+    // ---- counts: lane-per-mask-word popcount scan over the warp's range ----
+    const uint32_t c = __popc(mine);
+    uint32_t inc = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += t;
+    }
+    const uint32_t pre = inc - c;  // changed words of the warp range before this mask word
+    if (lane == 31) sm.warp_cnt[wid] = inc;
+    __syncthreads();
+    uint32_t woff = 0, total = 0;
+#pragma unroll
+    for (int k = 0; k < static_cast<int>(kWarps); ++k) {
+        const uint32_t v = sm.warp_cnt[k];
+        woff += k < wid ? v : 0u;
+        total += v;
+    }
+    const bool sparse = total * W <= kSpillBytes;
+
+    // ---- sparse block: pack the new words into the block's spill slot now ----
+    if (sparse && total) {
+        word_t* slot = reinterpret_cast<word_t*>(P.spill + I.b * kSpillBytes) + woff;
+        uint32_t nz = __ballot_sync(0xffffffffu, mine != 0);
+        const uint32_t lt = (1u << lane) - 1u;
+        while (nz) {
+            const int src = __ffs(nz) - 1;
+            nz &= nz - 1;
+            const uint32_t bb = __shfl_sync(0xffffffffu, mine, src);
+            const uint32_t o = __shfl_sync(0xffffffffu, pre, src);
+            if ((bb >> lane) & 1u) slot[o + __popc(bb & lt)] = scur[(mw0 + src) * 32 + lane];
+        }
+    }
+
+    // ---- block / chunk bookkeeping (one thread) ----
+    if (tid == 0) {
+        P.info[I.b] = total | (sparse ? 0u : kDenseFlag);
+        atomicAdd(&P.group_sum[I.b / kEmitGroup], static_cast<unsigned long long>(total));
+        atomicAdd(&P.chunk_total[I.chunk], static_cast<unsigned long long>(total));
+        __threadfence();
+        const unsigned done = atomicAdd(&P.chunk_done[I.chunk], 1u);
         const unsigned long long rs = wait_rstart(P, I.chunk);
-        if (I.last) {
-            const uint64_t W = I.w;
-            const uint64_t count = static_cast<uint64_t>(excl) + total;
+        if (done + 1 == I.nblk) {  // this block completes the chunk: header + next record start
+            __threadfence();
+            const uint64_t count = atomicAdd(&P.chunk_total[I.chunk], 0ull);
             const uint64_t n_mask = cdiv(I.m, 32);
             const uint64_t n_tiles = cdiv(I.m, P.T);
-            const uint64_t rec_total = record_bytes(I.m, P.T, I.w, count);
+            const uint64_t rec_total = record_bytes(I.m, P.T, W, count);
             uint8_t* rec = P.out + rs;
             uint64_t* h = reinterpret_cast<uint64_t*>(rec);
-            h[0] = 0x31444354ull /* "TCD1" */ | (1ull << 32) | (W << 48) | (1ull << 56);
+            h[0] = 0x31444354ull /* "TCD1" */ | (1ull << 32) | (static_cast<uint64_t>(W) << 48) | (1ull << 56);
             h[1] = static_cast<uint64_t>(P.T) | (static_cast<uint64_t>(I.seg) << 32);
             h[2] = I.chunk_off;
             h[3] = I.m;
@@ -213,144 +261,36 @@ __device__ __forceinline__ void scan_warp(const EncParams& P, EncSmem& sm, int l
             st_relaxed(&P.rstart[I.chunk + 1], next | 1ull);
             if (I.chunk + 1 == P.total_chunks) *P.out_bytes = next;
         }
-        sm.excl = excl;
         sm.rs = rs;
     }
-    __syncwarp();
-    bar_arrive(kBarPrefix, kCtaThreads);
-}
+    __syncthreads();
 
-// Compute warps (8): stage wait, pass 1 (compare -> ballot = mask word; fused ref advance),
-// counts, then (after the scan warp's prefix) pass 2 (mask words, tile_off, packed values).
-template <int W>
-__device__ __forceinline__ void compute_warps(const EncParams& P, EncSmem& sm, uint8_t* tile, int tid) {
-    using word_t = typename Word<W>::T;
-    constexpr uint32_t B = Word<W>::kBlock;
-    constexpr uint32_t MPW = B / 32 / kComputeWarps;  // mask words per warp (16 | 32)
-    const int lane = tid & 31, wid = tid >> 5;
-    const BlockInfo& I = sm.I;
-    const EncSeg& S = P.seg[I.seg];
-    word_t* sref = reinterpret_cast<word_t*>(tile);
-    word_t* scur = sref + B;
-    word_t* gref = reinterpret_cast<word_t*>(S.ref) + I.chunk_off + I.p0;
-    const word_t* gcur = reinterpret_cast<const word_t*>(S.cur) + I.chunk_off + I.p0;
-
-    // tail words (< 16 bytes) not covered by the bulk copy; pad the rest of a short block with
-    // equal words so pass 1 needs no bounds test
-    const uint32_t bytes = I.nb * W;
-    const uint32_t bulk = bytes & ~15u;
-    if (I.nb < B) {
-        for (uint32_t i = bulk / W + tid; i < B; i += kEncThreads) {
-            const bool in = i < I.nb;
-            sref[i] = in ? gref[i] : word_t(0);
-            scur[i] = in ? gcur[i] : word_t(0);
-        }
-    }
-    mbar_wait_parity(&sm.bar, 0);
-    if (I.nb < B) bar_sync(kBarCompute, kEncThreads);
-
-    // ---- pass 1 ----
-    const bool adv = P.advance_ref != 0;
-    const uint32_t mw0 = wid * MPW;
-#pragma unroll 4
-    for (uint32_t q = 0; q < MPW; ++q) {
-        const uint32_t i = (mw0 + q) * 32 + lane;
-        const word_t v = scur[i];
-        const bool ch = sref[i] != v;
-        const uint32_t bal = __ballot_sync(0xffffffffu, ch);
-        if (lane == 0) sm.bal[mw0 + q] = bal;
-        if (adv && bal) {
-            if (ch) gref[i] = v;
-        }
-    }
-    __syncwarp();
-    // ---- counts: lane-per-mask-word popcount scan over the warp's range ----
-    uint32_t bal = 0, pre = 0;
-    if (lane < static_cast<int>(MPW)) bal = sm.bal[mw0 + lane];
-    const uint32_t c = __popc(bal);
-    uint32_t inc = c;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += t;
-    }
-    pre = inc - c;
-    if (lane == 31) sm.warp_cnt[wid] = inc;
-    bar_sync(kBarCompute, kEncThreads);
-    if (wid == 0) {
-        const uint32_t wc = lane < static_cast<int>(kComputeWarps) ? sm.warp_cnt[lane] : 0u;
-        uint32_t x = wc;
-#pragma unroll
-        for (int d = 1; d < static_cast<int>(kComputeWarps); d <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, x, d);
-            if (lane >= d) x += t;
-        }
-        if (lane < static_cast<int>(kComputeWarps)) sm.warp_off[lane] = x - wc;
-        if (lane == kComputeWarps - 1) {
-            sm.total = x;
-            __threadfence_block();
-            *reinterpret_cast<volatile uint32_t*>(&sm.ready) = 1u;
-        }
-    }
-    bar_sync(kBarPrefix, kCtaThreads);  // scan warp has the exclusive prefix + record start
-
-    // ---- pass 2 ----
+    // ---- mask words and block-relative tile_off entries, in their final place ----
     uint8_t* rec = P.out + sm.rs;
     const uint64_t n_mask = cdiv(I.m, 32);
     uint32_t* gmask = reinterpret_cast<uint32_t*>(rec + kHdrBytes);
     uint32_t* gtoff = reinterpret_cast<uint32_t*>(rec + kHdrBytes + pad16(4 * n_mask));
-    word_t* gval = reinterpret_cast<word_t*>(rec + record_fixed_bytes(I.m, P.T));
-    const uint32_t base = sm.excl + sm.warp_off[wid];
-    const uint32_t p = I.p0 + (mw0 + lane) * 32;  // chunk-relative first word of this lane's mask word
-    const bool mine = lane < static_cast<int>(MPW) && p < I.m;
-    if (mine) {
-        gmask[(I.p0 >> 5) + mw0 + lane] = bal;
-        if ((p & (P.T - 1)) == 0) gtoff[p / P.T] = base + pre;
-    }
-    uint32_t nz = __ballot_sync(0xffffffffu, bal != 0);
-    const uint32_t lt = (1u << lane) - 1u;
-    while (nz) {
-        const int src = __ffs(nz) - 1;
-        nz &= nz - 1;
-        const uint32_t b = __shfl_sync(0xffffffffu, bal, src);
-        const uint32_t o = __shfl_sync(0xffffffffu, pre, src);
-        if ((b >> lane) & 1u) gval[base + o + __popc(b & lt)] = scur[(mw0 + src) * 32 + lane];
+    const uint32_t p = I.p0 + (mw0 + lane) * 32;
+    if (lane < static_cast<int>(MPW) && p < I.m) {
+        gmask[(I.p0 >> 5) + mw0 + lane] = mine;
+        if ((p & (P.T - 1)) == 0) gtoff[p / P.T] = woff + pre;  // kernel B adds the block prefix
     }
 }
 
-__global__ void __launch_bounds__(kCtaThreads, 6) encode_kernel(const __grid_constant__ EncParams P) {
+__global__ void __launch_bounds__(kEncThreads, 6) encode_mask_kernel(const __grid_constant__ EncParams P) {
     extern __shared__ __align__(128) uint8_t tile[];
-    __shared__ EncSmem sm;
+    __shared__ SmemA sm;
     const int tid = threadIdx.x;
-
-    if (tid == kEncThreads) {
-        // one thread: ticket, decode, barrier init, TMA issue — loads start as early as possible
-        BlockInfo I;
-        I.b = atomicAdd(P.ticket, 1ull);
-        int s = 0;
-        while (s + 1 < P.nseg && I.b >= P.seg[s + 1].first_block) ++s;
-        const EncSeg& S = P.seg[s];
-        const uint32_t lb = static_cast<uint32_t>(I.b - S.first_block);
-        const uint32_t bpc = static_cast<uint32_t>(S.blocks_per_chunk);
-        const uint32_t cl = lb / bpc;
-        I.k = lb - cl * bpc;
-        I.seg = s;
-        I.w = S.w;
-        I.chunk = S.first_chunk + cl;
-        I.chunk_off = static_cast<unsigned long long>(cl) * P.C;
-        I.m = static_cast<uint32_t>(S.n - I.chunk_off < P.C ? S.n - I.chunk_off : P.C);
-        I.first = I.b - I.k;
-        const uint32_t nblk = I.m ? (I.m + S.block_words - 1) / S.block_words : 1u;
-        I.last = (I.k + 1 == nblk);
-        I.p0 = I.k * S.block_words;
-        I.nb = I.m > I.p0 ? (I.m - I.p0 < S.block_words ? I.m - I.p0 : S.block_words) : 0u;
+    if (tid == 0) {
+        // one thread: ticket, decode, barrier init, TMA issue — the loads start at once
+        const BlockInfo I = decode_block(P, atomicAdd(P.ticket, 1ull));
         sm.I = I;
-        sm.ready = 0;
         mbar_init(&sm.bar, 1);
-        const uint32_t bulk = (I.nb * S.w) & ~15u;
+        const uint32_t bulk = (I.nb * I.w) & ~15u;
         if (bulk) {
-            const uint8_t* gref = S.ref + (I.chunk_off + I.p0) * S.w;
-            const uint8_t* gcur = S.cur + (I.chunk_off + I.p0) * S.w;
+            const EncSeg& S = P.seg[I.seg];
+            const uint8_t* gref = S.ref + (I.chunk_off + I.p0) * I.w;
+            const uint8_t* gcur = S.cur + (I.chunk_off + I.p0) * I.w;
             mbar_arrive_expect_tx(&sm.bar, 2 * bulk);
             bulk_g2s(tile, gref, bulk, &sm.bar);
             bulk_g2s(tile + 16384, gcur, bulk, &sm.bar);
@@ -359,12 +299,137 @@ __global__ void __launch_bounds__(kCtaThreads, 6) encode_kernel(const __grid_con
         }
     }
     __syncthreads();
-    if (tid >= kEncThreads) {
-        scan_warp(P, sm, tid & 31);
-    } else if (sm.I.w == 4) {
-        compute_warps<4>(P, sm, tile, tid);
-    } else {
-        compute_warps<2>(P, sm, tile, tid);
+    if (sm.I.w == 4)
+        mask_block<4>(P, sm, tile, tid);
+    else
+        mask_block<2>(P, sm, tile, tid);
+}
+
+// ------------------------------------------------------------------ kernel P ------------
+__global__ void __launch_bounds__(1024) encode_prefix_kernel(const __grid_constant__ EncParams P) {
+    __shared__ unsigned long long s_carry;
+    __shared__ unsigned long long s_warp[32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int pass = 0; pass < 2; ++pass) {
+        const unsigned long long* in = pass == 0 ? P.group_sum : P.chunk_total;
+        unsigned long long* out = pass == 0 ? P.gpre : P.cbase;
+        const uint64_t n = pass == 0 ? P.n_groups : P.total_chunks;
+        if (tid == 0) s_carry = 0;
+        __syncthreads();
+        for (uint64_t base = 0; base < n; base += 1024) {
+            const uint64_t i = base + tid;
+            const unsigned long long v = i < n ? in[i] : 0ull;
+            unsigned long long x = v;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, x, d);
+                if (lane >= d) x += y;
+            }
+            if (lane == 31) s_warp[wid] = x;
+            __syncthreads();
+            unsigned long long wp = 0, tot = 0;
+            for (int k = 0; k < 32; ++k) {
+                const unsigned long long t = s_warp[k];
+                wp += k < wid ? t : 0ull;
+                tot += t;
+            }
+            const unsigned long long carry = s_carry;
+            if (i < n) out[i] = carry + wp + x - v;
+            __syncthreads();
+            if (tid == 0) s_carry = carry + tot;
+            __syncthreads();
+        }
+    }
+}
+
+// ------------------------------------------------------------------ kernel B ------------
+template <int W>
+__device__ __forceinline__ void emit_block(const EncParams& P, const BlockInfo& I, uint32_t info,
+                                           unsigned long long prefix, int lane) {
+    using word_t = typename Word<W>::T;
+    const uint32_t count = info & ~kDenseFlag;
+    const unsigned long long rs = ld_relaxed(&P.rstart[I.chunk]) & ~1ull;
+    uint8_t* rec = P.out + rs;
+    const uint64_t n_mask = cdiv(I.m, 32);
+    uint32_t* gmask = reinterpret_cast<uint32_t*>(rec + kHdrBytes);
+    uint32_t* gtoff = reinterpret_cast<uint32_t*>(rec + kHdrBytes + pad16(4 * n_mask));
+    word_t* gval = reinterpret_cast<word_t*>(rec + record_fixed_bytes(I.m, P.T)) + prefix;
+    const uint32_t pr = static_cast<uint32_t>(prefix);
+    // tile_off entries at tile starts inside the block: kernel A wrote them block-relative
+    if (I.nb) {
+        if (P.T >= Word<W>::kBlock) {
+            if (lane == 0 && (I.p0 & (P.T - 1)) == 0) gtoff[I.p0 / P.T] += pr;
+        } else {
+            const uint32_t n_t = (I.nb + P.T - 1) / P.T;
+            for (uint32_t t = lane; t < n_t; t += 32) gtoff[I.p0 / P.T + t] += pr;
+        }
+    }
+    if (!count) return;
+    if (!(info & kDenseFlag)) {
+        const word_t* slot = reinterpret_cast<const word_t*>(P.spill + I.b * kSpillBytes);
+        for (uint32_t i = lane; i < count; i += 32) gval[i] = slot[i];
+        return;
+    }
+    // dense block: re-read mask (from the record) and cur, pack in index order
+    const EncSeg& S = P.seg[I.seg];
+    const word_t* gcur = reinterpret_cast<const word_t*>(S.cur) + I.chunk_off + I.p0;
+    const uint32_t nmw = (I.nb + 31) / 32;
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t run = 0;
+    for (uint32_t q0 = 0; q0 < nmw; q0 += 32) {
+        const uint32_t bal = q0 + lane < nmw ? gmask[(I.p0 >> 5) + q0 + lane] : 0u;
+        const uint32_t c = __popc(bal);
+        uint32_t inc = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += t;
+        }
+        const uint32_t pre = run + inc - c;
+        run += __shfl_sync(0xffffffffu, inc, 31);
+        uint32_t nz = __ballot_sync(0xffffffffu, bal != 0);
+        while (nz) {
+            const int src = __ffs(nz) - 1;
+            nz &= nz - 1;
+            const uint32_t bb = __shfl_sync(0xffffffffu, bal, src);
+            const uint32_t o = __shfl_sync(0xffffffffu, pre, src);
+            if ((bb >> lane) & 1u) gval[o + __popc(bb & lt)] = gcur[(q0 + src) * 32 + lane];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kEncThreads) encode_emit_kernel(const __grid_constant__ EncParams P) {
+    __shared__ uint32_t s_info[kEmitGroup];
+    __shared__ unsigned long long s_pre[kEmitGroup];
+    __shared__ uint32_t s_warp[kWarps];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const unsigned long long g = blockIdx.x;
+    const unsigned long long b = g * kEmitGroup + tid;
+    const uint32_t info = b < P.total_blocks ? P.info[b] : 0u;
+    const uint32_t c = info & ~kDenseFlag;
+    uint32_t inc = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += t;
+    }
+    if (lane == 31) s_warp[wid] = inc;
+    __syncthreads();
+    uint32_t wp = 0;
+#pragma unroll
+    for (int k = 0; k < static_cast<int>(kWarps); ++k) wp += k < wid ? s_warp[k] : 0u;
+    s_info[tid] = info;
+    s_pre[tid] = P.gpre[g] + wp + inc - c;  // global exclusive prefix of block b
+    __syncthreads();
+    for (uint32_t t = wid; t < kEmitGroup; t += kWarps) {
+        const unsigned long long bb = g * kEmitGroup + t;
+        if (bb >= P.total_blocks) break;
+        const BlockInfo I = decode_block(P, bb);
+        const unsigned long long prefix = s_pre[t] - P.cbase[I.chunk];  // in-chunk exclusive count
+        if (I.w == 4)
+            emit_block<4>(P, I, s_info[t], prefix, lane);
+        else
+            emit_block<2>(P, I, s_info[t], prefix, lane);
     }
 }
 
@@ -375,11 +440,17 @@ constexpr size_t kEncDynSmem = 2 * 16384;
 cudaError_t launch_encode(const EncParams& p, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(encode_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(encode_mask_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr_set = true;
     }
     if (p.total_blocks == 0) return cudaSuccess;
-    encode_kernel<<<static_cast<unsigned>(p.total_blocks), kCtaThreads, kEncDynSmem, s>>>(p);
+    encode_mask_kernel<<<static_cast<unsigned>(p.total_blocks), kEncThreads, kEncDynSmem, s>>>(p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    encode_prefix_kernel<<<1, 1024, 0, s>>>(p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    encode_emit_kernel<<<static_cast<unsigned>(p.n_groups), kEncThreads, 0, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -12,9 +12,13 @@
 struct tc_ctx {
     int device = 0;
     int num_sms = 148;
-    // encode scratch: [ticket u64 | pad | rstart (chunks+1) u64 | status (blocks) u64]
+    // encode scratch: ticket, per-chunk totals / done counts / record starts, per-group sums,
+    // per-block counts, group and chunk prefixes (layout in tc_diff_encode)
     void* enc = nullptr;
     size_t enc_bytes = 0;
+    // encode spill slots: kSpillBytes per scan block (packed new words of sparse blocks)
+    void* spill = nullptr;
+    size_t spill_bytes = 0;
     // fold scratch: desc [nrec*cap] | unit_first [cap+1] | info [2]
     void* fold = nullptr;
     size_t fold_bytes = 0;
@@ -147,6 +151,7 @@ tc_status tc_ctx_destroy(tc_ctx* c) {
     cudaDeviceSynchronize();
     if (c->enc) cudaFree(c->enc);
     if (c->fold) cudaFree(c->fold);
+    if (c->spill) cudaFree(c->spill);
     if (c->err) cudaFree(c->err);
     delete c;
     return TC_OK;
@@ -244,18 +249,37 @@ tc_status tc_diff_encode(tc_ctx* ctx, const tc_segment* segs, int nseg, const tc
     P.advance_ref = o.advance_ref ? 1 : 0;
     P.err = ctx->err;
 
-    const size_t need = 16 + 8 * (chunks + 1) + 8 * blocks;
+    const uint64_t groups = cdiv(blocks, kEmitGroup);
+    P.n_groups = groups;
+    // zeroed region: ticket | chunk_total | chunk_done | rstart | group_sum
+    const size_t z_ticket = 0, z_ctot = 16, z_cdone = z_ctot + 8 * chunks;
+    const size_t z_rstart = z_cdone + ((4 * chunks + 15) & ~size_t(15));
+    const size_t z_gsum = z_rstart + 8 * (chunks + 1);
+    const size_t z_end = z_gsum + 8 * groups;
+    // written-every-call region: info | gpre | cbase
+    const size_t w_info = (z_end + 255) & ~size_t(255);
+    const size_t w_gpre = w_info + ((4 * blocks + 15) & ~size_t(15));
+    const size_t w_cbase = w_gpre + 8 * groups;
+    const size_t need = w_cbase + 8 * chunks;
     st = ensure(&ctx->enc, &ctx->enc_bytes, need, s);
     if (st != TC_OK) return st;
+    st = ensure(&ctx->spill, &ctx->spill_bytes, blocks * static_cast<size_t>(kSpillBytes), s);
+    if (st != TC_OK) return st;
     uint8_t* base = static_cast<uint8_t*>(ctx->enc);
-    P.ticket = reinterpret_cast<unsigned long long*>(base);
-    P.rstart = reinterpret_cast<unsigned long long*>(base + 16);
-    P.status = reinterpret_cast<unsigned long long*>(base + 16 + 8 * (chunks + 1));
-    cudaError_t e = cudaMemsetAsync(base, 0, need, s);
+    P.ticket = reinterpret_cast<unsigned long long*>(base + z_ticket);
+    P.chunk_total = reinterpret_cast<unsigned long long*>(base + z_ctot);
+    P.chunk_done = reinterpret_cast<unsigned int*>(base + z_cdone);
+    P.rstart = reinterpret_cast<unsigned long long*>(base + z_rstart);
+    P.group_sum = reinterpret_cast<unsigned long long*>(base + z_gsum);
+    P.info = reinterpret_cast<uint32_t*>(base + w_info);
+    P.gpre = reinterpret_cast<unsigned long long*>(base + w_gpre);
+    P.cbase = reinterpret_cast<unsigned long long*>(base + w_cbase);
+    P.spill = static_cast<uint8_t*>(ctx->spill);
+    cudaError_t e = cudaMemsetAsync(base, 0, z_end, s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(scratch)");
     e = launch_encode(P, s);
     if (e != cudaSuccess) return cuda_fail(e, "encode launch");
-    ctx->launches += 1;
+    ctx->launches += 3;
     return TC_OK;
 }
 

@@ -238,4 +238,4 @@ def test_launch_counter(ctx):
     tc.diff_encode(ctx, [ref], [ref.clone()], out, ob, 1, 0)
     tc.diff_apply(ctx, [ref], 0, [out], [int(ob.item())])
     ctx.check()
-    assert ctx.launches == before + 3  # encode + walker + fold
+    assert ctx.launches == before + 5  # encode (mask, prefix, emit) + fold (walker, fold)
