@@ -13,14 +13,10 @@
 //                              (-> CORRUPT), the version chain (-> PROTOCOL) and
 //                              the common chunk layout (-> INVALID); builds the descriptor
 //                              table and the per-record unit prefix.
-//   fold_kernel       (persistent, 6 CTAs/SM) per unit of up to 8192 words: one thread per
-//                              mask word; per group of 4 records a packed 4x16-bit block scan
-//                              gives every record's in-unit value offsets; newest-first winner
-//                              masks carried in registers; winning (word, record, value index)
-//                              triples are compacted into a shared-memory list and then
-//                              gathered/scattered by consecutive threads (coalesced-ish reads
-//                              of values, ordered writes of state).  Tile-offset consistency is
-//                              checked on the way (-> CORRUPT).
+//   fold_kernel       (persistent, one warp per unit of max(T, 1024) words; see the fold
+//                              section) newest-first winner masks, popcount warp scans for
+//                              the value offsets, warp-broadcast scatter of the winning
+//                              words; tile_off consistency checked on the way (-> CORRUPT).
 #include <cuda_runtime.h>
 
 #include "tc_internal.h"
@@ -149,7 +145,18 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
 }
 
 // -------------------------------------------------------------------- fold ----------
-constexpr int kWarps = kFoldThreads / 32;
+// One WARP per unit of U = max(T, kFoldWords) chunk words (units never straddle a tile
+// boundary, so each unit starts at a tile_off entry).  A unit is walked in sub-units of up to
+// kSub = 4096 words = 4 groups of 32 mask words, lane l holding mask word 32g + l of group g.
+// For each record, newest first: load its mask words (4 independent loads per lane), popcount
+// warp scans give every mask word's in-chunk value offset, winners = mask & rem (rem = words
+// no newer record covers), and the winners are scattered: for each lane whose mask word has
+// winners, the warp broadcasts (win, mask, offset) and lane b copies word 32*src+b.  No
+// barriers and no shared-memory staging; latency is hidden by 64 resident warps per SM.
+constexpr uint32_t kFoldWarps = kFoldThreads / 32;
+constexpr uint32_t kSubGroups = 4;
+constexpr uint32_t kSub = kSubGroups * 1024;
+constexpr int kBatch = 4;  // gathers in flight per lane in the scatter
 
 template <int W>
 struct Word;
@@ -158,179 +165,123 @@ struct Word<4> { using T = uint32_t; };
 template <>
 struct Word<2> { using T = uint16_t; };
 
-struct FoldSmem {
-    uint32_t list[kFoldWords];                     // packed (off:13 | j:6 | lv:13)
-    unsigned long long wsum[2][kWarps];            // per-warp packed scan totals (double-buffered)
-    uint32_t run[TC_MAX_FOLD];                     // in-chunk count at the current sub-step start
-    uint32_t add[TC_MAX_FOLD];                     // this sub-step's popcount per record
-    uint32_t cnt;                                  // list length
-    uint32_t bad;
-};
-
-template <int W>
-__device__ void fold_unit(const FoldParams& P, FoldSmem& sm, uint64_t r, uint64_t ku) {
-    using word_t = typename Word<W>::T;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int N = P.nrec;
-    const FoldRec& L = P.desc[r];  // layout (shared by every diff)
-    const uint32_t m = L.m, T = L.T;
-    const uint64_t U = T > kFoldWords ? T : kFoldWords;
-    const uint32_t ustart = static_cast<uint32_t>(ku * U);
-    const uint32_t uend = static_cast<uint32_t>(ustart + U < m ? ustart + U : m);
-    word_t* state = reinterpret_cast<word_t*>(P.state[L.seg]) + L.chunk_off;
-
-    if (tid < N) {
-        const FoldRec& R = P.desc[static_cast<size_t>(tid) * P.cap + r];
-        const uint32_t base = reinterpret_cast<const uint32_t*>(R.toff)[ustart / T];
-        sm.run[tid] = base;
-        if (ku == 0 && base != 0) atomicExch(&sm.bad, 1u);
-    }
-    if (tid == 0) sm.cnt = 0;
-    __syncthreads();
-
-    for (uint32_t sub = ustart; sub < uend; sub += kFoldWords) {
-        const uint32_t send = sub + kFoldWords < uend ? sub + kFoldWords : uend;
-        const uint32_t p = sub + 32u * tid;  // first word of this thread's mask word
-        const bool valid = p < send;
-        const uint32_t validbits = !valid ? 0u : (send - p >= 32 ? 0xffffffffu : ((1u << (send - p)) - 1u));
-        uint32_t rem = 0xffffffffu;
-        int gi = 0;
-        for (int g = N - 1; g >= 0; g -= 4, ++gi) {
-            uint32_t mk[4];
-            const FoldRec* Rq[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int j = g - q;
-                mk[q] = 0;
-                Rq[q] = nullptr;
-                if (j >= 0) {
-                    Rq[q] = &P.desc[static_cast<size_t>(j) * P.cap + r];
-                    if (valid) {
-                        const uint32_t raw = reinterpret_cast<const uint32_t*>(Rq[q]->mask)[p >> 5];
-                        if (raw & ~validbits & (p + 32 > m ? 0xffffffffu : 0u)) atomicExch(&sm.bad, 1u);  // tail bits
-                        mk[q] = raw & validbits;
-                    }
-                }
-            }
-            // packed 4 x 16-bit block-wide exclusive scan of the popcounts
-            const unsigned long long pk = static_cast<unsigned long long>(__popc(mk[0])) |
-                                          (static_cast<unsigned long long>(__popc(mk[1])) << 16) |
-                                          (static_cast<unsigned long long>(__popc(mk[2])) << 32) |
-                                          (static_cast<unsigned long long>(__popc(mk[3])) << 48);
-            unsigned long long x = pk;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const unsigned long long y = __shfl_up_sync(0xffffffffu, x, d);
-                if (lane >= d) x += y;
-            }
-            if (lane == 31) sm.wsum[gi & 1][wid] = x;
-            __syncthreads();
-            unsigned long long wpre = 0, tot = 0;
-#pragma unroll
-            for (int k = 0; k < kWarps; ++k) {
-                const unsigned long long v = sm.wsum[gi & 1][k];
-                wpre += k < wid ? v : 0ull;
-                tot += v;
-            }
-            const unsigned long long ex = x - pk + wpre;
-            // tile_off consistency at tile starts inside the sub-step
-            if (valid && (p & (T - 1)) == 0 && p != ustart) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    if (!Rq[q]) continue;
-                    const uint32_t want = sm.run[g - q] + static_cast<uint32_t>((ex >> (16 * q)) & 0xffffu);
-                    if (reinterpret_cast<const uint32_t*>(Rq[q]->toff)[p / T] != want) atomicExch(&sm.bad, 1u);
-                }
-            }
-            if (tid < 4 && g - tid >= 0) sm.add[g - tid] = static_cast<uint32_t>((tot >> (16 * tid)) & 0xffffu);
-            // newest-first winners, compacted into the list
-            uint32_t win[4];
-            uint32_t e = 0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                win[q] = mk[q] & rem;
-                rem &= ~mk[q];
-                e += __popc(win[q]);
-            }
-            uint32_t ei = e;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, ei, d);
-                if (lane >= d) ei += y;
-            }
-            uint32_t wbase = 0;
-            if (lane == 31 && ei) wbase = atomicAdd(&sm.cnt, ei);
-            wbase = __shfl_sync(0xffffffffu, wbase, 31);
-            uint32_t pos = wbase + ei - e;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                uint32_t wq = win[q];
-                const uint32_t exq = static_cast<uint32_t>((ex >> (16 * q)) & 0xffffu);
-                while (wq) {
-                    const uint32_t b = __ffs(wq) - 1;
-                    wq &= wq - 1;
-                    const uint32_t lv = exq + __popc(mk[q] & ((1u << b) - 1u));
-                    sm.list[pos++] = (32u * tid + b) | (static_cast<uint32_t>(g - q) << 13) | (lv << 19);
-                }
-            }
-        }
-        __syncthreads();
-        // gather winning values, scatter into the state (ordered by word within each warp)
-        const uint32_t n = sm.cnt;
-        const bool ok = sm.bad == 0;
-        for (uint32_t e = tid; e < n && ok; e += kFoldThreads) {
-            const uint32_t ent = sm.list[e];
-            const uint32_t off = ent & 0x1fffu;
-            const uint32_t j = (ent >> 13) & 0x3fu;
-            const uint32_t lv = ent >> 19;
-            const FoldRec& R = P.desc[static_cast<size_t>(j) * P.cap + r];
-            const uint64_t idx = static_cast<uint64_t>(sm.run[j]) + lv;
-            if (idx >= R.count) {
-                atomicExch(&sm.bad, 1u);
-                continue;
-            }
-            state[sub + off] = reinterpret_cast<const word_t*>(R.values)[idx];
-        }
-        __syncthreads();
-        if (tid < N) sm.run[tid] += sm.add[tid];
-        if (tid == 0) sm.cnt = 0;
-        __syncthreads();
-    }
-    // end-of-unit check: the entry at uend (next unit's start) or the final entry == count
-    if (tid < N) {
-        const FoldRec& R = P.desc[static_cast<size_t>(tid) * P.cap + r];
-        const uint32_t* toff = reinterpret_cast<const uint32_t*>(R.toff);
-        if (uend < m) {
-            if (toff[uend / T] != sm.run[tid]) atomicExch(&sm.bad, 1u);
-        } else {
-            if (toff[cdiv(m, T)] != sm.run[tid] || R.count != sm.run[tid]) atomicExch(&sm.bad, 1u);
-        }
-    }
-    __syncthreads();
+__device__ __forceinline__ uint32_t ldg_u32(const uint32_t* p) { return __ldg(p); }
+__device__ __forceinline__ uint32_t ldg_word(const uint32_t* p) { return __ldg(p); }
+__device__ __forceinline__ uint16_t ldg_word(const uint16_t* p) {
+    return static_cast<uint16_t>(__ldg(reinterpret_cast<const unsigned short*>(p)));
 }
 
-__global__ void __launch_bounds__(kFoldThreads, 5) fold_kernel(const __grid_constant__ FoldParams P) {
-    __shared__ FoldSmem sm;
+template <int W>
+__device__ void fold_unit(const FoldParams& P, uint64_t r, uint64_t ku, uint32_t* carry, int lane, bool& bad) {
+    using word_t = typename Word<W>::T;
+    const int N = P.nrec;
+    const FoldRec& L = P.desc[r];  // the chunk layout (shared by every diff)
+    const uint32_t m = L.m, T = L.T;
+    const uint32_t U = T > kFoldWords ? T : kFoldWords;
+    const uint32_t ustart = static_cast<uint32_t>(ku) * U;
+    const uint32_t uend = ustart + U < m ? ustart + U : m;
+    word_t* state = reinterpret_cast<word_t*>(P.state[L.seg]) + L.chunk_off;
+    const uint32_t lt = (1u << lane) - 1u;
+
+    for (uint32_t sub = ustart; sub < uend; sub += kSub) {
+        const uint32_t send = sub + kSub < uend ? sub + kSub : uend;
+        uint32_t rem[kSubGroups];
+#pragma unroll
+        for (uint32_t g = 0; g < kSubGroups; ++g) rem[g] = 0xffffffffu;
+        for (int j = N - 1; j >= 0; --j) {
+            const FoldRec& R = P.desc[static_cast<size_t>(j) * P.cap + r];
+            const uint32_t* mask = reinterpret_cast<const uint32_t*>(R.mask);
+            const uint32_t* toff = reinterpret_cast<const uint32_t*>(R.toff);
+            const word_t* vals = reinterpret_cast<const word_t*>(R.values);
+            const uint32_t count = static_cast<uint32_t>(R.count);
+            // all mask words of the sub-unit first (independent read-only loads)
+            uint32_t mk[kSubGroups];
+#pragma unroll
+            for (uint32_t g = 0; g < kSubGroups; ++g) {
+                const uint32_t p = sub + (32 * g + lane) * 32;
+                mk[g] = p < send ? ldg_u32(mask + (p >> 5)) : 0u;
+            }
+            uint32_t run = sub == ustart ? ldg_u32(toff + ustart / T) : carry[j];
+            if (sub == ustart && ku == 0 && run != 0) bad = true;
+#pragma unroll
+            for (uint32_t g = 0; g < kSubGroups; ++g) {
+                const uint32_t p = sub + (32 * g + lane) * 32;
+                if (p + 32 > send && p < send) {  // the chunk's tail word: bits past m must be 0
+                    const uint32_t vb = (1u << (send - p)) - 1u;
+                    if (mk[g] & ~vb) bad = true;
+                    mk[g] &= vb;
+                }
+                const uint32_t c = __popc(mk[g]);
+                uint32_t inc = c;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+                    if (lane >= d) inc += t;
+                }
+                const uint32_t pre = run + inc - c;  // in-chunk offset of this mask word's values
+                run += __shfl_sync(0xffffffffu, inc, 31);
+                if (T < kSub && p < send && p != ustart && (p & (T - 1)) == 0 && ldg_u32(toff + p / T) != pre)
+                    bad = true;
+                const uint32_t win = mk[g] & rem[g];
+                rem[g] &= ~mk[g];
+                uint32_t nz = __ballot_sync(0xffffffffu, win != 0);
+                // batches of kBatch source mask words: the value gathers of a batch are issued
+                // before its stores, so kBatch gathers are in flight per lane
+                while (nz) {
+                    word_t v[kBatch];
+                    uint32_t dst[kBatch];
+#pragma unroll
+                    for (int q = 0; q < kBatch; ++q) {
+                        dst[q] = 0xffffffffu;
+                        if (nz) {  // warp-uniform
+                            const int src = __ffs(nz) - 1;
+                            nz &= nz - 1;
+                            const uint32_t wb = __shfl_sync(0xffffffffu, win, src);
+                            const uint32_t mb = __shfl_sync(0xffffffffu, mk[g], src);
+                            const uint32_t o = __shfl_sync(0xffffffffu, pre, src);
+                            const uint32_t idx = o + __popc(mb & lt);
+                            if (((wb >> lane) & 1u) && idx < count) {  // idx < count keeps a corrupt
+                                v[q] = ldg_word(vals + idx);           // record's reads in bounds
+                                dst[q] = sub + (32 * g + src) * 32 + lane;
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < kBatch; ++q)
+                        if (dst[q] != 0xffffffffu) state[dst[q]] = v[q];
+                }
+            }
+            carry[j] = run;
+            if (send == uend) {  // unit end: the next unit's first entry, or the final entry
+                const uint32_t want = uend < m ? ldg_u32(toff + uend / T) : ldg_u32(toff + (m + T - 1) / T);
+                if (want != run || (uend == m && count != run)) bad = true;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const __grid_constant__ FoldParams P) {
+    __shared__ uint32_t s_carry[kFoldWarps][TC_MAX_FOLD];
     if (*reinterpret_cast<volatile unsigned*>(P.err) != 0) return;  // sticky error pending
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint64_t R = P.info[0];
     const uint64_t total = P.info[1];
-    if (threadIdx.x == 0) sm.bad = 0;
-    __syncthreads();
-    for (uint64_t u = blockIdx.x; u < total; u += gridDim.x) {
+    const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * kFoldWarps;
+    bool bad = false;
+    for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * kFoldWarps + wid; u < total; u += nwarps) {
         // record r: unit_first[r] <= u < unit_first[r+1]
         uint64_t lo = 0, hi = R;
         while (hi - lo > 1) {
             const uint64_t mid = (lo + hi) >> 1;
             if (P.unit_first[mid] <= u) lo = mid; else hi = mid;
         }
-        const uint64_t r = lo;
-        const uint64_t ku = u - P.unit_first[r];
-        if (P.desc[r].w == 4)
-            fold_unit<4>(P, sm, r, ku);
+        const uint64_t ku = u - P.unit_first[lo];
+        if (P.desc[lo].w == 4)
+            fold_unit<4>(P, lo, ku, s_carry[wid], lane, bad);
         else
-            fold_unit<2>(P, sm, r, ku);
-        if (sm.bad) {
-            if (threadIdx.x == 0) tc_set_err(P.err, TC_ERR_CORRUPT);
+            fold_unit<2>(P, lo, ku, s_carry[wid], lane, bad);
+        if (__any_sync(0xffffffffu, bad)) {  // malformed record: state unspecified
+            if (lane == 0) tc_set_err(P.err, TC_ERR_CORRUPT);
             return;
         }
     }
@@ -342,7 +293,12 @@ cudaError_t launch_fold(const FoldParams& p, cudaStream_t s, int num_sms, uint64
     fold_walk_kernel<<<1, TC_MAX_FOLD, 0, s>>>(p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    fold_kernel<<<num_sms * 5, kFoldThreads, 0, s>>>(p);
+    static int occ = 0;
+    if (!occ) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fold_kernel, kFoldThreads, 0) != cudaSuccess || occ < 1)
+            occ = 1;
+    }
+    fold_kernel<<<num_sms * occ, kFoldThreads, 0, s>>>(p);
     *launches += 2;
     return cudaGetLastError();
 }

@@ -18,9 +18,9 @@ constexpr uint64_t kMaxChunkWords = 2147483647ull;  // 2^31-1 (PAPER.md:203 chun
 constexpr uint32_t kEncThreads = 256;
 constexpr uint32_t kEncBlockWords4 = 4096;  // 4-byte words
 constexpr uint32_t kEncBlockWords2 = 8192;  // 2-byte words
-// Fold unit: 256 threads x one mask word = 8192 state words per sub-step.
+// Fold: one warp per unit of max(T, kFoldWords) words.
 constexpr uint32_t kFoldThreads = 256;
-constexpr uint32_t kFoldWords = 8192;
+constexpr uint32_t kFoldWords = 1024;  // minimum fold unit (one warp: 32 mask words)
 
 __host__ __device__ inline uint64_t pad16(uint64_t x) { return (x + 15) & ~uint64_t(15); }
 __host__ __device__ inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
