@@ -177,21 +177,44 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
     mbar_wait_parity(&sm.bar, 0);
     if (I.nb < B) __syncthreads();
 
-    // ---- pass 1: compare -> ballot = mask word; fused ref advance ----
+    // ---- pass 1: 128-bit shared loads, per-lane change bits -> mask words; fused ref advance.
+    //      Lane l of iteration q compares words [VW*(32q'+l), +VW) (VW = 16 / W): its VW change
+    //      bits are OR-shuffled across the VW/... lanes of one 32-word mask word (LSB-first). ----
     const bool adv = P.advance_ref != 0;
     const uint32_t mw0 = wid * MPW;
-    uint32_t mine = 0;  // lane q keeps mask word mw0 + q
-#pragma unroll 4
-    for (uint32_t q = 0; q < MPW; ++q) {
-        const uint32_t i = (mw0 + q) * 32 + lane;
-        const word_t v = scur[i];
-        const bool ch = sref[i] != v;
-        const uint32_t bal = __ballot_sync(0xffffffffu, ch);
-        if (lane == static_cast<int>(q)) mine = bal;
-        if (adv && bal) {
-            if (ch) gref[i] = v;
+    {
+        constexpr uint32_t VW = 16 / W;          // words per 128-bit vector (4 | 8)
+        constexpr uint32_t LPM = 32 / VW;        // lanes per mask word (8 | 4)
+        constexpr uint32_t ITER = MPW * 32 / (32 * VW);  // vectors per lane over the warp range (4)
+        const uint4* r4 = reinterpret_cast<const uint4*>(sref);
+        const uint4* c4 = reinterpret_cast<const uint4*>(scur);
+        uint4* g4 = reinterpret_cast<uint4*>(gref);
+        uint32_t* s_bal = reinterpret_cast<uint32_t*>(tile) + (2 * B * W) / 4;  // after ref|cur
+#pragma unroll
+        for (uint32_t q = 0; q < ITER; ++q) {
+            const uint32_t vi = (wid * ITER + q) * 32 + lane;  // vector index in the block
+            const uint4 a = r4[vi];
+            const uint4 v = c4[vi];
+            uint32_t bits;
+            if (W == 4) {
+                bits = (a.x != v.x ? 1u : 0u) | (a.y != v.y ? 2u : 0u) | (a.z != v.z ? 4u : 0u) | (a.w != v.w ? 8u : 0u);
+            } else {
+                const uint32_t d0 = __vcmpne2(a.x, v.x), d1 = __vcmpne2(a.y, v.y);
+                const uint32_t d2 = __vcmpne2(a.z, v.z), d3 = __vcmpne2(a.w, v.w);
+                bits = (d0 & 1u) | ((d0 >> 15) & 2u) | ((d1 & 1u) << 2) | ((d1 >> 13) & 8u) |
+                       ((d2 & 1u) << 4) | ((d2 >> 11) & 32u) | ((d3 & 1u) << 6) | ((d3 >> 9) & 128u);
+            }
+            if (adv && bits) g4[vi] = v;  // new ref = cur on the whole vector (equal where unchanged)
+            uint32_t x = bits << (VW * (lane & (LPM - 1)));
+#pragma unroll
+            for (uint32_t d = 1; d < LPM; d <<= 1) x |= __shfl_xor_sync(0xffffffffu, x, d);
+            if ((lane & (LPM - 1)) == 0) s_bal[mw0 + q * (32 / LPM) + lane / LPM] = x;
         }
+        __syncwarp();
     }
+    uint32_t mine = 0;  // lane q keeps mask word mw0 + q
+    if (lane < static_cast<int>(MPW))
+        mine = reinterpret_cast<const uint32_t*>(tile)[(2 * B * W) / 4 + mw0 + lane];
     // ---- counts: lane-per-mask-word popcount scan over the warp's range ----
     const uint32_t c = __popc(mine);
     uint32_t inc = c;
@@ -435,7 +458,7 @@ __global__ void __launch_bounds__(kEncThreads) encode_emit_kernel(const __grid_c
 
 }  // namespace
 
-constexpr size_t kEncDynSmem = 2 * 16384;
+constexpr size_t kEncDynSmem = 2 * 16384 + 1024;  // ref | cur | mask words
 
 cudaError_t launch_encode(const EncParams& p, cudaStream_t s) {
     static bool attr_set = false;
