@@ -1,0 +1,87 @@
+"""Host-side logic of the multi-rank path on CPU: world-size-2 gloo process group (consensus MIN,
+ring mapping, unique-id broadcast shape) and the version-chain bookkeeping."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2605_17821_b200.checkpoint import DiffChain, consensus, ring_peers
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # every rank can recover a different newest base / chain end: consensus takes the MIN
+        base = [100, 150][rank]
+        end = [137, 149][rank]
+        got = consensus(base, end)
+        nxt, prv = ring_peers(rank, world)
+        # the ring is a permutation: my next's prev is me
+        peers = [None] * world
+        dist.all_gather_object(peers, (nxt, prv))
+        ring_ok = all(peers[peers[r][0]][1] == r for r in range(world))
+        # the 128-byte NCCL unique id travels over the process group as uint8 (Comm.__init__)
+        uid = torch.arange(128, dtype=torch.uint8) if rank == 0 else torch.zeros(128, dtype=torch.uint8)
+        dist.broadcast(uid, src=0)
+        q.put((rank, got, ring_ok, bool((uid == torch.arange(128, dtype=torch.uint8)).all())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_consensus_and_ring_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, got, ring_ok, uid_ok in res:
+        assert got == (100, 137)
+        assert ring_ok and uid_ok
+
+
+def test_ring_peers():
+    assert ring_peers(0, 1) == (0, 0)
+    assert ring_peers(0, 2) == (1, 1)
+    assert ring_peers(3, 4) == (0, 2)
+    with pytest.raises(ValueError):
+        ring_peers(4, 4)
+
+
+def test_consensus_single_process():
+    assert consensus(7, 9) == (7, 9)
+
+
+def test_diff_chain_links_batches_reclaim():
+    c = DiffChain(base_version=50)
+    for v in range(51, 64):
+        c.append(v, v - 1, 1000 + v, tiers=("t1", "t2") if v < 60 else ("t1",))
+    with pytest.raises(ValueError):
+        c.append(70, 68, 1)  # gap
+    with pytest.raises(ValueError):
+        c.append(63, 63, 1)  # version must advance
+    assert c.head == 63
+    assert c.replay_end() == 63 and c.replay_end("t2") == 59
+    b = c.batches(5)
+    assert [len(x) for x in b] == [5, 5, 3] and b[0][0].version == 51 and b[-1][-1].version == 63
+    assert [len(x) for x in c.batches(5, upto=57)] == [5, 2]
+    gone = c.reclaim(55)
+    assert [e.version for e in gone] == [51, 52, 53, 54, 55]
+    assert c.base_version == 55 and c.entries[0].version == 56
+    with pytest.raises(ValueError):
+        c.reclaim(40)

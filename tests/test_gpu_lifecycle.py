@@ -1,0 +1,114 @@
+"""GPU: the save / retrieve lifecycle (cfg4 scenario, scaled down): a chain of 8 incremental
+records, a simulated GPU failure that wipes the live state and the reference, restore from
+Tier-1 (H2D of the staged records) with one fold of the chain — bit-exact against the state the
+seeded generator defines; plus the full-size (cfg2) parity of the bench launch configuration on
+sampled chunks and a full-size round trip."""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+from paper_2605_17821_b200 import tc  # noqa: E402
+from paper_2605_17821_b200.checkpoint import Checkpointer  # noqa: E402
+from tests.gpu_util import to_dev, to_np  # noqa: E402
+
+
+def _dev_state(sizes, wb, seed, version, f):
+    segs = []
+    for s, (n, w) in enumerate(zip(sizes, wb)):
+        t = torch.empty(n, dtype=torch.int16 if w == 2 else torch.int32, device="cuda")
+        tc.synth_base(t, seed, s)
+        for v in range(1, version + 1):
+            tc.synth_step(t, seed, s, v, synth.p53_of(f))
+        segs.append(t)
+    return segs
+
+
+@pytest.mark.parametrize("source", ["t1", "device"])
+def test_chain_of_8_restore_after_failure(source):
+    sizes, wb, seed, f = [70001, 70001, 70001, 70001], [2, 4, 4, 4], synth.SEED0 + 4, 0.01
+    live = _dev_state(sizes, wb, seed, 0, f)
+    base_host = [to_np(s) for s in live]  # the base checkpoint (version 0)
+    ck = Checkpointer(live, tile_words=4096, chunk_words=1 << 14)
+    for v in range(1, 9):
+        for s, t in enumerate(live):  # one training step changes a fraction f of the words
+            tc.synth_step(t, seed, s, v, synth.p53_of(f))
+        ck.save_step(v)
+    torch.cuda.synchronize()
+    expect = synth.state(sizes, wb, seed, 8, f)
+    assert all(np.array_equal(to_np(a), b) for a, b in zip(live, expect))
+    # simulated GPU failure: the device state and the reference are gone
+    for t in live + ck.ref:
+        t.zero_()
+    restored = [to_dev(b) for b in base_host]  # base fetched back (Tier-1/2/3)
+    ver = ck.restore(restored, source=source, batch=8)
+    assert ver == 8
+    for a, b in zip(restored, expect):
+        assert np.array_equal(to_np(a), b)
+    # restore to an intermediate version with batches of 5 (N = 5)
+    mid = [to_dev(b) for b in base_host]
+    assert ck.restore(mid, upto=6, batch=5) == 6
+    exp6 = synth.state(sizes, wb, seed, 6, f)
+    assert all(np.array_equal(to_np(a), b) for a, b in zip(mid, exp6))
+    ck.reclaim(6)
+    assert ck.chain.base_version == 6 and [e.version for e in ck.chain.entries] == [7, 8]
+
+
+def test_fullsize_cfg2_sampled_parity_and_round_trip(tco):
+    """BASELINE configs[1] (cfg2, 21.8 GB) in the launch configuration bench.py times
+    (T = 4096, C = 2^28): GPU record bytes == oracle bytes on sampled chunks, and the fold of the
+    full record reproduces the current state exactly."""
+    sizes, wb = synth.shard_layout("cfg2")
+    seed, f = synth.SEED0, 0.01
+    free = torch.cuda.mem_get_info()[0]
+    W = sum(n * w for n, w in zip(sizes, wb))
+    if free < 4.5 * W:
+        pytest.skip("not enough device memory for the full-size case")
+    X = _dev_state(sizes, wb, seed, 0, f)
+    Y = [x.clone() for x in X]
+    for s, t in enumerate(Y):
+        tc.synth_step(t, seed, s, 1, synth.p53_of(f))
+    ctx = tc.Ctx(0)
+    cap = tc.diff_bound(sizes, wb)
+    out = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    ob = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tc.diff_encode(ctx, X, Y, out, ob, 1, 0, advance_ref=False)
+    ctx.check()
+    n = int(ob.item())
+    # locate records on the device copy: walk headers (64 B reads)
+    hdrs = []
+    pos = 0
+    while pos < n:
+        h = out[pos: pos + 64].cpu().numpy()
+        seg = int(h[12:16].view("<u4")[0])
+        off = int(h[16:24].view("<u8")[0])
+        m = int(h[24:32].view("<u8")[0])
+        total = int(h[56:64].view("<u8")[0])
+        hdrs.append((seg, off, m, pos, total))
+        pos += total
+    assert pos == n
+    C = 1 << 28
+    picks = [hdrs[0], [h for h in hdrs if h[0] == 3][-1]]  # seg 0 chunk 0 (bf16), seg 3 last chunk
+    for seg, off, m, pos, total in picks:
+        gpu_rec = out[pos: pos + total].cpu().numpy()
+        w = wb[seg]
+        ref_np = synth.base(m, w, seed, seg, start=off)
+        cur_np = synth.step(ref_np, seed, seg, 1, f, start=off)
+        rc, exp = tco.encode([ref_np], [cur_np], tile_words=4096, chunk_words=C, advance_ref=False,
+                             version=1, ref_version=0)
+        assert rc == 0 and exp.size == total
+        # the oracle encoded a one-segment shard: patch segment id and chunk offset, then compare
+        exp = exp.copy()
+        exp[12:16] = np.frombuffer(np.uint32(seg).tobytes(), np.uint8)
+        exp[16:24] = np.frombuffer(np.uint64(off).tobytes(), np.uint8)
+        assert np.array_equal(gpu_rec, exp), f"segment {seg} chunk at {off} differs"
+    # full-size round trip
+    tc.diff_apply(ctx, X, 0, [out], [n])
+    ctx.check()
+    assert all(torch.equal(a, b) for a, b in zip(X, Y))
+    ctx.close()
