@@ -328,6 +328,9 @@ def run_ours(args):
     rec_bytes = sizes_seen[-1]
     changed = sum(r[4] for r in recs_info)
 
+    rep_probe = None
+    if comm is not None:
+        rep_probe = replicate_probe(tc, comm, recs[0], obytes, recv, rec_bytes, dev, s_comm)
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, tc, ctx, dev, sizes, wb, X, Y, A, R, recs, obytes, host_ring, rec_cap, T, C,
@@ -365,7 +368,7 @@ def run_ours(args):
                 "parallelism": f"dp{world} (independent ZeRO shards; Tier-2 ring r->r+1)" if world > 1 else "1 GPU",
             },
             "roofline": {
-                "kernel": "encode_kernel (tc_diff_encode)",
+                "kernel": "tc_diff_encode = encode_mask_kernel + encode_prefix_kernel + encode_emit_kernel",
                 "bound": "hbm",
                 "achieved": round(enc_b / (enc_ms * 1e-3) / 1e9, 1),
                 "peak": peak,
@@ -386,10 +389,11 @@ def run_ours(args):
                          "frac_hbm_sector": round(fold_bs / fold_ms / 1e6 / peak, 4),
                          "traffic": traffic.get("fold")},
                 "stage_d2h": {"ms": round(stage_ms, 4), "gbs": round(rec_bytes / stage_ms / 1e6, 2)},
-                "replicate": None if rep_ms is None else {
+                "replicate_in_step": None if rep_ms is None else {
                     "ms": round(rep_ms, 4), "gbs_per_direction": round(rec_bytes / rep_ms / 1e6, 1),
-                    "frac_nvlink_nominal": round(rec_bytes / rep_ms / 1e6 / NVLINK_GBS, 4),
-                    "frac_nvlink_measured": round(rec_bytes / rep_ms / 1e6 / NVLINK_MEASURED_GBS, 4)},
+                    "note": "inside the pipelined step: shares HBM with encode/fold, PCIe with the "
+                            "Tier-1 D2H, and waits for the slower neighbour's encode"},
+                "replicate": rep_probe,
                 "record_bytes": rec_bytes,
                 "changed_words": changed,
                 "restore_equals_state": bool(ok),
@@ -408,6 +412,47 @@ def run_ours(args):
         dist.destroy_process_group()
     if not ok:
         sys.exit(1)
+
+
+def replicate_probe(tc, comm, rec, obytes, recv, rec_bytes, dev, s_comm):
+    """Tier-2 in isolation: ring shifts of this step's record (size exchange + payload through
+    tc_replicate_peer) and of a fixed 1 GiB payload, CUDA events on the comm stream, max over
+    ranks."""
+    import torch
+    import torch.distributed as dist
+
+    def timed(send, nb, rcv, reps=5):
+        for _ in range(2):
+            comm.replicate_peer(send, nb, rcv, tc.TO_NEXT, stream=s_comm)
+        s_comm.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s_comm)
+        for _ in range(reps):
+            comm.replicate_peer(send, nb, rcv, tc.TO_NEXT, stream=s_comm)
+        e1.record(s_comm)
+        s_comm.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / reps], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    nb_dev = torch.tensor([rec_bytes], dtype=torch.int64, device=dev)
+    ms_rec = timed(rec, nb_dev, recv)
+    G = 1 << 30
+    big = torch.empty(G, dtype=torch.uint8, device=dev)
+    big_r = torch.empty(G, dtype=torch.uint8, device=dev)
+    ms_1g = timed(big, torch.tensor([G], dtype=torch.int64, device=dev), big_r)
+    del big, big_r
+    g_rec = rec_bytes / ms_rec / 1e6
+    g_1g = G / ms_1g / 1e6
+    return {"record_bytes": rec_bytes, "ms": round(ms_rec, 4), "gbs_per_direction": round(g_rec, 1),
+            "frac_nvlink_nominal": round(g_rec / NVLINK_GBS, 4),
+            "frac_nvlink_measured": round(g_rec / NVLINK_MEASURED_GBS, 4),
+            "ring_shift_1GiB": {"ms": round(ms_1g, 4), "gbs_per_direction": round(g_1g, 1),
+                                "frac_nvlink_nominal": round(g_1g / NVLINK_GBS, 4),
+                                "frac_nvlink_measured": round(g_1g / NVLINK_MEASURED_GBS, 4)},
+            "note": "isolated tc_replicate_peer ring shift (size exchange + NCCL send/recv), max over ranks; "
+                    "nominal 900 GB/s, measured peer copy 770 GB/s (B200_PROFILING.md)"}
 
 
 def run_e2e(args, tc, ctx, dev, sizes, wb, X, Y, A, R, recs, obytes, host_ring, rec_cap, T, C, state, world,
