@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
 constexpr uint32_t kFoldWarps = kFoldThreads / 32;
 constexpr uint32_t kSubGroups = 4;
 constexpr uint32_t kSub = kSubGroups * 1024;
-constexpr int kBatch = 4;  // gathers in flight per lane in the scatter
+constexpr int kBatch = 4;  // gathers in flight per lane in the dense scatter
+constexpr uint32_t kLaneSerialMax = 96;  // winners per 1024 words below which lanes scatter alone
 
 template <int W>
 struct Word;
@@ -224,6 +225,32 @@ __device__ void fold_unit(const FoldParams& P, uint64_t r, uint64_t ku, uint32_t
                     bad = true;
                 const uint32_t win = mk[g] & rem[g];
                 rem[g] &= ~mk[g];
+                if (__reduce_add_sync(0xffffffffu, __popc(win)) <= kLaneSerialMax) {
+                    // sparse group: each lane walks the winners of its own mask word (at f = 1 %
+                    // ~1 bit per lane, so the warp needs a few iterations for all 32 mask words);
+                    // two gathers in flight per lane per iteration
+                    uint32_t wv = win;
+                    const uint32_t base_w = sub + (32 * g + lane) * 32;
+                    while (__any_sync(0xffffffffu, wv != 0)) {
+                        word_t v0 = 0, v1 = 0;
+                        uint32_t d0 = 0xffffffffu, d1 = 0xffffffffu;
+                        if (wv) {
+                            const uint32_t b = __ffs(wv) - 1;
+                            wv &= wv - 1;
+                            const uint32_t idx = pre + __popc(mk[g] & ((1u << b) - 1u));
+                            if (idx < count) { v0 = ldg_word(vals + idx); d0 = base_w + b; }
+                        }
+                        if (wv) {
+                            const uint32_t b = __ffs(wv) - 1;
+                            wv &= wv - 1;
+                            const uint32_t idx = pre + __popc(mk[g] & ((1u << b) - 1u));
+                            if (idx < count) { v1 = ldg_word(vals + idx); d1 = base_w + b; }
+                        }
+                        if (d0 != 0xffffffffu) state[d0] = v0;
+                        if (d1 != 0xffffffffu) state[d1] = v1;
+                    }
+                    continue;
+                }
                 uint32_t nz = __ballot_sync(0xffffffffu, win != 0);
                 // batches of kBatch source mask words: the value gathers of a batch are issued
                 // before its stores, so kBatch gathers are in flight per lane

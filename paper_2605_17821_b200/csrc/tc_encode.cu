@@ -238,6 +238,16 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
     // ---- sparse block: pack the new words into the block's spill slot now ----
     if (sparse && total) {
         word_t* slot = reinterpret_cast<word_t*>(P.spill + I.b * kSpillBytes) + woff;
+        if (__shfl_sync(0xffffffffu, inc, 31) <= 96u) {
+            // few changes in this warp's range: each lane packs its own mask word's words
+            uint32_t wv = mine;
+            uint32_t k = pre;
+            while (wv) {
+                const uint32_t b = __ffs(wv) - 1;
+                wv &= wv - 1;
+                slot[k++] = scur[(mw0 + lane) * 32 + b];
+            }
+        } else {
         uint32_t nz = __ballot_sync(0xffffffffu, mine != 0);
         const uint32_t lt = (1u << lane) - 1u;
         while (nz) {
@@ -246,6 +256,7 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
             const uint32_t bb = __shfl_sync(0xffffffffu, mine, src);
             const uint32_t o = __shfl_sync(0xffffffffu, pre, src);
             if ((bb >> lane) & 1u) slot[o + __popc(bb & lt)] = scur[(mw0 + src) * 32 + lane];
+        }
         }
     }
 
