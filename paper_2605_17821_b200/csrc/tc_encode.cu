@@ -23,9 +23,10 @@
 //                           writes its header and publishes the next record start.
 //   P  encode_prefix_kernel (1 CTA) exclusive scans of the per-group and per-chunk counts.
 //   B  encode_emit_kernel   one CTA per 256 blocks: block-wide scan of the block counts -> each
-//                           block's in-chunk prefix; a warp per block adds it to the block's
-//                           tile_off entries and moves the spilled words into place (sparse) or
-//                           re-reads mask + cur and packs them (dense).
+//                           block's in-chunk prefix (a thread per block, which also adds it to
+//                           the block's tile_off entries); each warp then moves its blocks'
+//                           spilled words into place, 4 blocks per batch with all loads in
+//                           flight before the stores, and packs dense blocks from mask + cur.
 #include <cuda_runtime.h>
 
 #include "tc_internal.h"
@@ -377,39 +378,27 @@ __global__ void __launch_bounds__(1024) encode_prefix_kernel(const __grid_consta
 }
 
 // ------------------------------------------------------------------ kernel B ------------
+__device__ __forceinline__ uint32_t ldg_word(const uint32_t* p) { return __ldg(p); }
+__device__ __forceinline__ uint16_t ldg_word(const uint16_t* p) {
+    return static_cast<uint16_t>(__ldg(reinterpret_cast<const unsigned short*>(p)));
+}
+
+// Dense block (more than 4 KB of changed words, not spilled): re-read its mask words from the
+// record and the changed words from cur, pack them in index order (a warp per block).
 template <int W>
-__device__ __forceinline__ void emit_block(const EncParams& P, const BlockInfo& I, uint32_t info,
+__device__ __forceinline__ void emit_dense(const EncParams& P, const BlockInfo& I, uint32_t info,
                                            unsigned long long prefix, int lane) {
     using word_t = typename Word<W>::T;
-    const uint32_t count = info & ~kDenseFlag;
     const unsigned long long rs = ld_relaxed(&P.rstart[I.chunk]) & ~1ull;
     uint8_t* rec = P.out + rs;
-    const uint64_t n_mask = cdiv(I.m, 32);
-    uint32_t* gmask = reinterpret_cast<uint32_t*>(rec + kHdrBytes);
-    uint32_t* gtoff = reinterpret_cast<uint32_t*>(rec + kHdrBytes + pad16(4 * n_mask));
+    const uint32_t* gmask = reinterpret_cast<const uint32_t*>(rec + kHdrBytes);
     word_t* gval = reinterpret_cast<word_t*>(rec + record_fixed_bytes(I.m, P.T)) + prefix;
-    const uint32_t pr = static_cast<uint32_t>(prefix);
-    // tile_off entries at tile starts inside the block: kernel A wrote them block-relative
-    if (I.nb) {
-        if (P.T >= Word<W>::kBlock) {
-            if (lane == 0 && (I.p0 & (P.T - 1)) == 0) gtoff[I.p0 / P.T] += pr;
-        } else {
-            const uint32_t n_t = (I.nb + P.T - 1) / P.T;
-            for (uint32_t t = lane; t < n_t; t += 32) gtoff[I.p0 / P.T + t] += pr;
-        }
-    }
-    if (!count) return;
-    if (!(info & kDenseFlag)) {
-        const word_t* slot = reinterpret_cast<const word_t*>(P.spill + I.b * kSpillBytes);
-        for (uint32_t i = lane; i < count; i += 32) gval[i] = slot[i];
-        return;
-    }
-    // dense block: re-read mask (from the record) and cur, pack in index order
     const EncSeg& S = P.seg[I.seg];
     const word_t* gcur = reinterpret_cast<const word_t*>(S.cur) + I.chunk_off + I.p0;
     const uint32_t nmw = (I.nb + 31) / 32;
     const uint32_t lt = (1u << lane) - 1u;
     uint32_t run = 0;
+    (void)info;
     for (uint32_t q0 = 0; q0 < nmw; q0 += 32) {
         const uint32_t bal = q0 + lane < nmw ? gmask[(I.p0 >> 5) + q0 + lane] : 0u;
         const uint32_t c = __popc(bal);
@@ -422,24 +411,46 @@ __device__ __forceinline__ void emit_block(const EncParams& P, const BlockInfo& 
         const uint32_t pre = run + inc - c;
         run += __shfl_sync(0xffffffffu, inc, 31);
         uint32_t nz = __ballot_sync(0xffffffffu, bal != 0);
-        while (nz) {
-            const int src = __ffs(nz) - 1;
-            nz &= nz - 1;
-            const uint32_t bb = __shfl_sync(0xffffffffu, bal, src);
-            const uint32_t o = __shfl_sync(0xffffffffu, pre, src);
-            if ((bb >> lane) & 1u) gval[o + __popc(bb & lt)] = gcur[(q0 + src) * 32 + lane];
+        while (nz) {  // batches of 8 source mask words: 8 cur loads in flight before the stores
+            word_t v[8];
+            uint32_t d[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                d[q] = 0xffffffffu;
+                if (nz) {
+                    const int src = __ffs(nz) - 1;
+                    nz &= nz - 1;
+                    const uint32_t bb = __shfl_sync(0xffffffffu, bal, src);
+                    const uint32_t o = __shfl_sync(0xffffffffu, pre, src);
+                    if ((bb >> lane) & 1u) {
+                        v[q] = ldg_word(gcur + (q0 + src) * 32 + lane);
+                        d[q] = o + __popc(bb & lt);
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (d[q] != 0xffffffffu) gval[d[q]] = v[q];
         }
     }
 }
 
-__global__ void __launch_bounds__(kEncThreads) encode_emit_kernel(const __grid_constant__ EncParams P) {
-    __shared__ uint32_t s_info[kEmitGroup];
-    __shared__ unsigned long long s_pre[kEmitGroup];
+// Copy one batch of up to 4 spilled blocks (<= 64 words each handled here; the rest of a longer
+// block in the caller's loop): loads of the whole batch are issued before any store.
+__device__ __forceinline__ void copy_words(uint8_t* dst, const uint8_t* src, uint32_t w, uint32_t i) {
+    if (w == 4)
+        reinterpret_cast<uint32_t*>(dst)[i] = __ldg(reinterpret_cast<const uint32_t*>(src) + i);
+    else
+        reinterpret_cast<uint16_t*>(dst)[i] = __ldg(reinterpret_cast<const unsigned short*>(src) + i);
+}
+
+__global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __grid_constant__ EncParams P) {
     __shared__ uint32_t s_warp[kWarps];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const unsigned long long g = blockIdx.x;
     const unsigned long long b = g * kEmitGroup + tid;
-    const uint32_t info = b < P.total_blocks ? P.info[b] : 0u;
+    const bool valid = b < P.total_blocks;
+    const uint32_t info = valid ? P.info[b] : 0u;
     const uint32_t c = info & ~kDenseFlag;
     uint32_t inc = c;
 #pragma unroll
@@ -452,18 +463,94 @@ __global__ void __launch_bounds__(kEncThreads) encode_emit_kernel(const __grid_c
     uint32_t wp = 0;
 #pragma unroll
     for (int k = 0; k < static_cast<int>(kWarps); ++k) wp += k < wid ? s_warp[k] : 0u;
-    s_info[tid] = info;
-    s_pre[tid] = P.gpre[g] + wp + inc - c;  // global exclusive prefix of block b
-    __syncthreads();
-    for (uint32_t t = wid; t < kEmitGroup; t += kWarps) {
-        const unsigned long long bb = g * kEmitGroup + t;
-        if (bb >= P.total_blocks) break;
+
+    // ---- per block (one thread each): in-chunk prefix, tile_off entries, destination ----
+    uint8_t* dst = nullptr;
+    const uint8_t* src = nullptr;
+    uint32_t w = 4;
+    bool dense = false;
+    if (valid) {
+        const BlockInfo I = decode_block(P, b);
+        w = I.w;
+        const unsigned long long prefix = P.gpre[g] + wp + inc - c - P.cbase[I.chunk];
+        const unsigned long long rs = ld_relaxed(&P.rstart[I.chunk]) & ~1ull;
+        uint8_t* rec = P.out + rs;
+        const uint64_t n_mask = cdiv(I.m, 32);
+        uint32_t* gtoff = reinterpret_cast<uint32_t*>(rec + kHdrBytes + pad16(4 * n_mask));
+        const uint32_t pr = static_cast<uint32_t>(prefix);
+        const uint32_t B = I.w == 4 ? kEncBlockWords4 : kEncBlockWords2;
+        if (I.nb) {  // kernel A wrote the tile_off entries of the block block-relative
+            if (P.T >= B) {
+                if ((I.p0 & (P.T - 1)) == 0) gtoff[I.p0 / P.T] += pr;
+            } else {
+                const uint32_t n_t = (I.nb + P.T - 1) / P.T;
+                for (uint32_t t = 0; t < n_t; ++t) gtoff[I.p0 / P.T + t] += pr;
+            }
+        }
+        dst = rec + record_fixed_bytes(I.m, P.T) + prefix * I.w;
+        src = P.spill + b * kSpillBytes;
+        dense = (info & kDenseFlag) != 0 && c != 0;
+    }
+
+    // ---- sparse blocks of this warp: packed words spill slot -> record, 4 blocks per batch ----
+    uint32_t todo = __ballot_sync(0xffffffffu, valid && !dense && c != 0);
+    while (todo) {
+        int bl[4];
+        uint32_t cn[4], wq[4];
+        uint8_t* dq[4];
+        const uint8_t* sq[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            bl[q] = todo ? __ffs(todo) - 1 : -1;
+            if (todo) todo &= todo - 1;
+            const int sl = bl[q] < 0 ? 0 : bl[q];
+            cn[q] = bl[q] < 0 ? 0u : __shfl_sync(0xffffffffu, c, sl);
+            wq[q] = __shfl_sync(0xffffffffu, w, sl);
+            dq[q] = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst), sl));
+            sq[q] = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(src), sl));
+        }
+        uint32_t v[4][2];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const uint32_t i = lane + 32 * k;
+                v[q][k] = 0;
+                if (i < cn[q])
+                    v[q][k] = wq[q] == 4 ? __ldg(reinterpret_cast<const uint32_t*>(sq[q]) + i)
+                                         : __ldg(reinterpret_cast<const unsigned short*>(sq[q]) + i);
+            }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const uint32_t i = lane + 32 * k;
+                if (i < cn[q]) {
+                    if (wq[q] == 4)
+                        reinterpret_cast<uint32_t*>(dq[q])[i] = v[q][k];
+                    else
+                        reinterpret_cast<uint16_t*>(dq[q])[i] = static_cast<uint16_t>(v[q][k]);
+                }
+            }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            for (uint32_t i = 64 + lane; i < cn[q]; i += 32) copy_words(dq[q], sq[q], wq[q], i);
+    }
+
+    // ---- dense blocks: re-read mask + cur, pack in index order (a warp per block) ----
+    uint32_t dn = __ballot_sync(0xffffffffu, dense);
+    while (dn) {
+        const int t = __ffs(dn) - 1;
+        dn &= dn - 1;
+        const unsigned long long bb = g * kEmitGroup + wid * 32 + t;
         const BlockInfo I = decode_block(P, bb);
-        const unsigned long long prefix = s_pre[t] - P.cbase[I.chunk];  // in-chunk exclusive count
+        const unsigned long long prefix =
+            P.gpre[g] + __shfl_sync(0xffffffffu, wp + inc - c, t) - P.cbase[I.chunk];
+        const uint32_t inf = __shfl_sync(0xffffffffu, info, t);
         if (I.w == 4)
-            emit_block<4>(P, I, s_info[t], prefix, lane);
+            emit_dense<4>(P, I, inf, prefix, lane);
         else
-            emit_block<2>(P, I, s_info[t], prefix, lane);
+            emit_dense<2>(P, I, inf, prefix, lane);
     }
 }
 
