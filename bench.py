@@ -328,6 +328,19 @@ def run_ours(args):
     rec_bytes = sizes_seen[-1]
     changed = sum(r[4] for r in recs_info)
 
+    restore = None
+    if args.restore_chain > 0:
+        restore = restore_bench(tc, ctx, X, Y, A, R, recs[0], sizes, wb, seed, p53, T, C, s_comp,
+                                args.restore_chain, args.structure, peak, dev)
+        # put the step buffers back to the X / Y pair (X intact; Y, A, R were reused)
+        with torch.cuda.stream(s_comp):
+            for i in range(len(sizes)):
+                Y[i].copy_(X[i])
+                tc.synth_step(Y[i], seed, i, 1, p53, args.structure, stream=s_comp)
+                A[i].copy_(X[i])
+                R[i].copy_(X[i])
+        s_comp.synchronize()
+        state["content"] = "X"
     rep_probe = None
     if comm is not None:
         rep_probe = replicate_probe(tc, comm, recs[0], obytes, recv, rec_bytes, dev, s_comm)
@@ -394,6 +407,7 @@ def run_ours(args):
                     "note": "inside the pipelined step: shares HBM with encode/fold, PCIe with the "
                             "Tier-1 D2H, and waits for the slower neighbour's encode"},
                 "replicate": rep_probe,
+                "restore_chain": restore,
                 "record_bytes": rec_bytes,
                 "changed_words": changed,
                 "restore_equals_state": bool(ok),
@@ -412,6 +426,83 @@ def run_ours(args):
         dist.destroy_process_group()
     if not ok:
         sys.exit(1)
+
+
+def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nrec, structure, peak, dev):
+    """a7 at N = nrec (SURVEY §8(a), config 4's "chained restore of 8 differentials"): build a real
+    chain of `nrec` incremental records (versions 1..nrec, each a fresh f-change set), then
+    (1) fold all of them onto a base copy in one tc_diff_apply call (records resident in HBM), and
+    (2) restore from Tier-1: H2D of the records from pinned host memory + the same fold.
+    CUDA events on the stream; the restored state is checked against the chain head."""
+    import torch
+
+    with torch.cuda.stream(s):  # Z (chain head) and ref start at the base X
+        for z, r_, x in zip(Z, ref, X):
+            z.copy_(x)
+            r_.copy_(x)
+    ob = torch.zeros(1, dtype=torch.int64, device=dev)
+    recs, lens = [], []
+    with torch.cuda.stream(s):
+        for v in range(1, nrec + 1):
+            for i, z in enumerate(Z):
+                tc.synth_step(z, seed, i, 1000 + v, p53, structure, stream=s)
+            tc.diff_encode(ctx, ref, Z, tmp, ob, v, v - 1, T, C, True, stream=s)
+            s.synchronize()
+            n = int(ob.item())
+            recs.append(tmp[:n].clone())
+            lens.append(n)
+    union = 0
+    with torch.cuda.stream(s):
+        for x, z in zip(X, Z):
+            union += int((x != z).sum().item())
+    hosts = [tc.HostBuffer(n) for n in lens]
+    for h, r, n in zip(hosts, recs, lens):
+        tc.stage_host(h, r, n, tc.D2H, stream=s)
+    s.synchronize()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    fold_ms, t1_ms = [], []
+    for rep in range(3):
+        with torch.cuda.stream(s):
+            for r_, x in zip(R, X):
+                r_.copy_(x)
+        a, b = ev(), ev()
+        a.record(s)
+        tc.diff_apply(ctx, R, 0, recs, lens, stream=s)
+        b.record(s)
+        s.synchronize()
+        fold_ms.append(a.elapsed_time(b))
+        with torch.cuda.stream(s):
+            for r_, x in zip(R, X):
+                r_.copy_(x)
+        staged = [torch.empty(max(n, 16), dtype=torch.uint8, device=dev) for n in lens]
+        a, b = ev(), ev()
+        a.record(s)
+        for d, h, n in zip(staged, hosts, lens):
+            tc.stage_host(d, h, n, tc.H2D, stream=s)
+        tc.diff_apply(ctx, R, 0, staged, lens, stream=s)
+        b.record(s)
+        s.synchronize()
+        t1_ms.append(a.elapsed_time(b))
+        del staged
+    ctx.check(s)
+    ok = all(torch.equal(r_, z) for r_, z in zip(R, Z))
+    # algorithmic bytes of the fold: every record's mask + tile_off + header, the winning values
+    # read and the state words written (word-granular), SURVEY §8(d)
+    meta = 0
+    for n_, w_ in zip(sizes, wb):
+        chunks = max(1, -(-n_ // C))
+        meta += nrec * (4 * -(-n_ // 32) + 4 * (-(-n_ // T) + chunks) + 64 * chunks)
+    wmean = sum(n_ * w_ for n_, w_ in zip(sizes, wb)) / sum(sizes)
+    fold_b = meta + 2 * union * wmean
+    fm = statistics.median(fold_ms)
+    for h in hosts:
+        h.free()
+    W = sum(n_ * w_ for n_, w_ in zip(sizes, wb))
+    return {"records": nrec, "record_bytes_total": sum(lens), "union_changed_words": union,
+            "fold_ms": round(fm, 4), "state_gbs": round(W / fm / 1e6, 1),
+            "hbm_gbs_word": round(fold_b / fm / 1e6, 1), "frac_hbm_word": round(fold_b / fm / 1e6 / peak, 4),
+            "tier1_restore_ms": round(statistics.median(t1_ms), 3),
+            "restored_equals_head": bool(ok)}
 
 
 def replicate_probe(tc, comm, rec, obytes, recv, rec_bytes, dev, s_comm):
@@ -619,6 +710,7 @@ def main():
     ap.add_argument("--chunk-words", type=int, default=1 << 28)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--timeline", action="store_true")
+    ap.add_argument("--restore-chain", type=int, default=8, help="records in the chained-restore probe (0: off)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--sample-words", type=int, default=1 << 25)
