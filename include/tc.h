@@ -136,6 +136,20 @@ tc_status tc_diff_encode(tc_ctx* ctx, const tc_segment* segs, int nseg,
                          const tc_encode_opts* opts, uint64_t version, uint64_t ref_version,
                          void* out, uint64_t out_cap, uint64_t* out_bytes, tc_stream stream);
 
+/* Streaming encode of a contiguous run of whole chunks of ONE segment: writes exactly the bytes
+ * the records of chunks [first_chunk, first_chunk + n_chunks) of segment `segment_id` have in the
+ * full tc_diff_encode output (same header segment_id / chunk_word_offset), so concatenating the
+ * ranges of every segment in order reproduces the full diff.  Used when the full bound does not
+ * fit in HBM next to the state (40B-shaped shards: SURVEY.md §7 build plan step 9).  `seg`
+ * describes the WHOLE segment; out_cap >= tc_diff_bound_range(...) (else TC_ERR_CAPACITY);
+ * *out_bytes (device or mapped pinned) receives the range's length. */
+tc_status tc_diff_bound_range(const tc_segment* seg, const tc_encode_opts* opts, uint64_t first_chunk,
+                              uint64_t n_chunks, uint64_t* max_bytes);
+tc_status tc_diff_encode_range(tc_ctx* ctx, const tc_segment* seg, uint32_t segment_id,
+                               const tc_encode_opts* opts, uint64_t first_chunk, uint64_t n_chunks,
+                               uint64_t version, uint64_t ref_version, void* out, uint64_t out_cap,
+                               uint64_t* out_bytes, tc_stream stream);
+
 /* Tier-1 (§4 "low-priority CUDA streams and pinned host memory buffers";
  * SURVEY.md §8(a) a5): cudaMemcpyAsync of `bytes` between a device buffer and a PINNED
  * host buffer on `copy_stream`.  dir = TC_D2H (save) or TC_H2D (restore fetch).  The host

@@ -278,8 +278,8 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
             uint8_t* rec = P.out + rs;
             uint64_t* h = reinterpret_cast<uint64_t*>(rec);
             h[0] = 0x31444354ull /* "TCD1" */ | (1ull << 32) | (static_cast<uint64_t>(W) << 48) | (1ull << 56);
-            h[1] = static_cast<uint64_t>(P.T) | (static_cast<uint64_t>(I.seg) << 32);
-            h[2] = I.chunk_off;
+            h[1] = static_cast<uint64_t>(P.T) | (static_cast<uint64_t>(P.seg[I.seg].seg_id) << 32);
+            h[2] = P.seg[I.seg].word_base + I.chunk_off;
             h[3] = I.m;
             h[4] = count;
             h[5] = P.version;

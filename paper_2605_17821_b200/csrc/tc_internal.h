@@ -42,6 +42,9 @@ struct EncSeg {
     uint64_t n_chunks;      // >= 1 (an empty segment is one empty chunk)
     uint32_t w;
     uint32_t block_words;   // B
+    uint32_t seg_id;        // segment_id written in the headers
+    uint32_t pad_;
+    uint64_t word_base;     // added to chunk offsets in the headers (range encodes)
 };
 
 struct EncParams {

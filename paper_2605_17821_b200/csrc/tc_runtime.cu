@@ -197,42 +197,41 @@ tc_status tc_diff_bound(const tc_segment* segs, int nseg, const tc_encode_opts* 
     return TC_OK;
 }
 
-tc_status tc_diff_encode(tc_ctx* ctx, const tc_segment* segs, int nseg, const tc_encode_opts* opts,
-                         uint64_t version, uint64_t ref_version, void* out, uint64_t out_cap,
-                         uint64_t* out_bytes, tc_stream stream) {
-    if (!ctx) return fail(TC_ERR_INVALID, "ctx is NULL");
-    tc_encode_opts o;
-    default_opts(opts, &o);
-    tc_status st = check_opts(o);
-    if (st != TC_OK) return st;
-    st = check_segs(segs, nseg, true);
-    if (st != TC_OK) return st;
-    if (!out || !aligned16(out)) return fail(TC_ERR_INVALID, "out must be a 16-byte aligned device pointer");
-    if (!out_bytes) return fail(TC_ERR_INVALID, "out_bytes is NULL");
-    uint64_t bound = 0;
-    st = tc_diff_bound(segs, nseg, &o, &bound);
-    if (st != TC_OK) return st;
-    if (out_cap < bound) return fail(TC_ERR_CAPACITY, "out_cap < tc_diff_bound()");
+namespace {
+struct SegSpec {
+    uint8_t* ref;
+    const uint8_t* cur;
+    uint64_t n;
+    uint32_t w;
+    uint32_t seg_id;
+    uint64_t word_base;
+};
+}  // namespace
 
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
+static tc_status encode_impl(tc_ctx* ctx, const SegSpec* specs, int nseg, const tc_encode_opts& o,
+                             uint64_t version, uint64_t ref_version, void* out, uint64_t* out_bytes,
+                             cudaStream_t s) {
     cudaSetDevice(ctx->device);
+    tc_status st = TC_OK;
     EncParams P;
     memset(&P, 0, sizeof(P));
     uint64_t blocks = 0, chunks = 0;
     for (int i = 0; i < nseg; ++i) {
-        const tc_segment& g = segs[i];
+        const SegSpec& g = specs[i];
         EncSeg& E = P.seg[i];
-        E.ref = static_cast<uint8_t*>(g.ref);
-        E.cur = static_cast<const uint8_t*>(g.cur);
-        E.n = g.n_words;
-        E.w = g.word_bytes;
-        E.block_words = g.word_bytes == 4 ? kEncBlockWords4 : kEncBlockWords2;
+        E.ref = g.ref;
+        E.cur = g.cur;
+        E.n = g.n;
+        E.w = g.w;
+        E.seg_id = g.seg_id;
+        E.word_base = g.word_base;
+        E.block_words = g.w == 4 ? kEncBlockWords4 : kEncBlockWords2;
         E.first_block = blocks;
         E.first_chunk = chunks;
-        E.n_chunks = g.n_words ? cdiv(g.n_words, o.chunk_words) : 1;
-        const uint64_t full = g.n_words < o.chunk_words ? g.n_words : o.chunk_words;
+        E.n_chunks = g.n ? cdiv(g.n, o.chunk_words) : 1;
+        const uint64_t full = g.n < o.chunk_words ? g.n : o.chunk_words;
         E.blocks_per_chunk = full ? cdiv(full, E.block_words) : 1;
-        const uint64_t m_last = g.n_words ? g.n_words - (E.n_chunks - 1) * o.chunk_words : 0;
+        const uint64_t m_last = g.n ? g.n - (E.n_chunks - 1) * o.chunk_words : 0;
         const uint64_t last_blocks = m_last ? cdiv(m_last, E.block_words) : 1;
         blocks += (E.n_chunks - 1) * E.blocks_per_chunk + last_blocks;
         chunks += E.n_chunks;
@@ -281,6 +280,83 @@ tc_status tc_diff_encode(tc_ctx* ctx, const tc_segment* segs, int nseg, const tc
     if (e != cudaSuccess) return cuda_fail(e, "encode launch");
     ctx->launches += 3;
     return TC_OK;
+}
+
+static uint64_t range_bound(uint64_t n, uint32_t w, const tc_encode_opts& o, uint64_t c0, uint64_t nc) {
+    uint64_t tot = 0;
+    const uint64_t total_chunks = n ? cdiv(n, o.chunk_words) : 1;
+    for (uint64_t c = c0; c < c0 + nc && c < total_chunks; ++c) {
+        const uint64_t off = c * o.chunk_words;
+        const uint64_t m = n > off ? (n - off < o.chunk_words ? n - off : o.chunk_words) : 0;
+        tot += record_bytes(m, o.tile_words, w, m);
+    }
+    return tot;
+}
+
+extern "C" tc_status tc_diff_encode(tc_ctx* ctx, const tc_segment* segs, int nseg, const tc_encode_opts* opts,
+                                    uint64_t version, uint64_t ref_version, void* out, uint64_t out_cap,
+                                    uint64_t* out_bytes, tc_stream stream) {
+    if (!ctx) return fail(TC_ERR_INVALID, "ctx is NULL");
+    tc_encode_opts o;
+    default_opts(opts, &o);
+    tc_status st = check_opts(o);
+    if (st != TC_OK) return st;
+    st = check_segs(segs, nseg, true);
+    if (st != TC_OK) return st;
+    if (!out || !aligned16(out)) return fail(TC_ERR_INVALID, "out must be a 16-byte aligned device pointer");
+    if (!out_bytes) return fail(TC_ERR_INVALID, "out_bytes is NULL");
+    uint64_t bound = 0;
+    st = tc_diff_bound(segs, nseg, &o, &bound);
+    if (st != TC_OK) return st;
+    if (out_cap < bound) return fail(TC_ERR_CAPACITY, "out_cap < tc_diff_bound()");
+    SegSpec sp[TC_MAX_SEGMENTS];
+    for (int i = 0; i < nseg; ++i)
+        sp[i] = {static_cast<uint8_t*>(segs[i].ref), static_cast<const uint8_t*>(segs[i].cur), segs[i].n_words,
+                 segs[i].word_bytes, static_cast<uint32_t>(i), 0};
+    return encode_impl(ctx, sp, nseg, o, version, ref_version, out, out_bytes, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" tc_status tc_diff_bound_range(const tc_segment* seg, const tc_encode_opts* opts, uint64_t first_chunk,
+                                         uint64_t n_chunks, uint64_t* max_bytes) {
+    if (!max_bytes) return fail(TC_ERR_INVALID, "max_bytes is NULL");
+    tc_encode_opts o;
+    default_opts(opts, &o);
+    tc_status st = check_opts(o);
+    if (st != TC_OK) return st;
+    st = check_segs(seg, 1, false);
+    if (st != TC_OK) return st;
+    const uint64_t total_chunks = seg->n_words ? cdiv(seg->n_words, o.chunk_words) : 1;
+    if (n_chunks == 0 || first_chunk >= total_chunks)
+        return fail(TC_ERR_INVALID, "chunk range outside the segment");
+    *max_bytes = range_bound(seg->n_words, seg->word_bytes, o, first_chunk, n_chunks);
+    return TC_OK;
+}
+
+extern "C" tc_status tc_diff_encode_range(tc_ctx* ctx, const tc_segment* seg, uint32_t segment_id,
+                                          const tc_encode_opts* opts, uint64_t first_chunk, uint64_t n_chunks,
+                                          uint64_t version, uint64_t ref_version, void* out, uint64_t out_cap,
+                                          uint64_t* out_bytes, tc_stream stream) {
+    if (!ctx) return fail(TC_ERR_INVALID, "ctx is NULL");
+    tc_encode_opts o;
+    default_opts(opts, &o);
+    tc_status st = check_opts(o);
+    if (st != TC_OK) return st;
+    st = check_segs(seg, 1, true);
+    if (st != TC_OK) return st;
+    if (!out || !aligned16(out)) return fail(TC_ERR_INVALID, "out must be a 16-byte aligned device pointer");
+    if (!out_bytes) return fail(TC_ERR_INVALID, "out_bytes is NULL");
+    uint64_t bound = 0;
+    st = tc_diff_bound_range(seg, &o, first_chunk, n_chunks, &bound);
+    if (st != TC_OK) return st;
+    if (out_cap < bound) return fail(TC_ERR_CAPACITY, "out_cap < tc_diff_bound_range()");
+    const uint64_t off = first_chunk * o.chunk_words;
+    const uint64_t n = seg->n_words > off ? seg->n_words - off : 0;
+    const uint64_t len = n < n_chunks * o.chunk_words ? n : n_chunks * o.chunk_words;
+    const uint64_t w = seg->word_bytes;
+    SegSpec sp = {seg->n_words ? static_cast<uint8_t*>(seg->ref) + off * w : nullptr,
+                  seg->n_words ? static_cast<const uint8_t*>(seg->cur) + off * w : nullptr, len,
+                  seg->word_bytes, segment_id, off};
+    return encode_impl(ctx, &sp, 1, o, version, ref_version, out, out_bytes, static_cast<cudaStream_t>(stream));
 }
 
 tc_status tc_diff_apply(tc_ctx* ctx, void* const* state, const uint64_t* n_words, const uint32_t* word_bytes,

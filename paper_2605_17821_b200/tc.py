@@ -62,6 +62,10 @@ def _load():
     L.tc_diff_encode.argtypes = [vp, ctypes.POINTER(Segment), cint, ctypes.POINTER(EncodeOpts), u64, u64,
                                  vp, u64, vp, vp]
     L.tc_stage_host.argtypes = [vp, vp, u64, cint, vp]
+    L.tc_diff_bound_range.argtypes = [ctypes.POINTER(Segment), ctypes.POINTER(EncodeOpts), u64, u64,
+                                      ctypes.POINTER(u64)]
+    L.tc_diff_encode_range.argtypes = [vp, ctypes.POINTER(Segment), u32, ctypes.POINTER(EncodeOpts), u64, u64,
+                                       u64, u64, vp, u64, vp, vp]
     L.tc_host_alloc.argtypes = [u64, ctypes.POINTER(vp)]
     L.tc_host_free.argtypes = [vp]
     L.tc_comm_get_unique_id.argtypes = [ctypes.c_char_p]
@@ -73,7 +77,7 @@ def _load():
     L.tc_synth_base.argtypes = [vp, u64, u32, u64, u32, u64, vp]
     L.tc_synth_step.argtypes = [vp, u64, u32, u64, u32, u64, u64, cint, u64, vp]
     for name in ("tc_ctx_create", "tc_ctx_destroy", "tc_ctx_check", "tc_diff_bound", "tc_diff_encode",
-                 "tc_stage_host", "tc_host_alloc", "tc_host_free", "tc_comm_get_unique_id", "tc_comm_init", "tc_comm_destroy",
+                 "tc_stage_host", "tc_diff_bound_range", "tc_diff_encode_range", "tc_host_alloc", "tc_host_free", "tc_comm_get_unique_id", "tc_comm_init", "tc_comm_destroy",
                  "tc_replicate_peer", "tc_diff_apply", "tc_synth_base", "tc_synth_step"):
         getattr(L, name).restype = cint
     return L
@@ -188,6 +192,28 @@ def diff_encode(ctx: Ctx, ref, cur, out: torch.Tensor, out_bytes: torch.Tensor, 
     _check(LIB.tc_diff_encode(ctx.h, segs, len(ref), ctypes.byref(o), version, ref_version, out.data_ptr(),
                               out.numel() * out.element_size(), out_bytes.data_ptr(), _stream(stream)),
            "tc_diff_encode")
+
+
+def diff_bound_range(n_words: int, word_bytes: int, first_chunk: int, n_chunks: int, tile_words=4096,
+                     chunk_words=1 << 28) -> int:
+    seg = Segment(None, None, int(n_words), int(word_bytes), 0)
+    o = _opts(tile_words, chunk_words)
+    out = u64(0)
+    _check(LIB.tc_diff_bound_range(ctypes.byref(seg), ctypes.byref(o), first_chunk, n_chunks, ctypes.byref(out)),
+           "tc_diff_bound_range")
+    return out.value
+
+
+def diff_encode_range(ctx: Ctx, ref: torch.Tensor, cur: torch.Tensor, segment_id: int, first_chunk: int,
+                      n_chunks: int, out: torch.Tensor, out_bytes: torch.Tensor, version: int, ref_version: int,
+                      tile_words=4096, chunk_words=1 << 28, advance_ref=True, stream=None):
+    """Enqueue tc_diff_encode_range (the records of chunks [first_chunk, first_chunk+n_chunks) of
+    one segment, byte-identical to that part of the full encode)."""
+    seg = segments([ref], [cur])
+    o = _opts(tile_words, chunk_words, advance_ref)
+    _check(LIB.tc_diff_encode_range(ctx.h, seg, segment_id, ctypes.byref(o), first_chunk, n_chunks, version,
+                                    ref_version, out.data_ptr(), out.numel() * out.element_size(),
+                                    out_bytes.data_ptr(), _stream(stream)), "tc_diff_encode_range")
 
 
 def diff_apply(ctx: Ctx, state, state_version: int, records, record_bytes, stream=None):

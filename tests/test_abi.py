@@ -13,7 +13,7 @@ def test_every_declared_symbol_is_exported():
     expected = {"tc_status_string", "tc_last_error", "tc_abi_version", "tc_ctx_create", "tc_ctx_destroy",
                 "tc_ctx_check", "tc_ctx_launches", "tc_diff_bound", "tc_diff_encode", "tc_stage_host",
                 "tc_comm_get_unique_id", "tc_comm_init", "tc_comm_destroy", "tc_replicate_peer",
-                "tc_diff_apply", "tc_synth_base", "tc_synth_step", "tc_host_alloc", "tc_host_free"}
+                "tc_diff_apply", "tc_synth_base", "tc_synth_step", "tc_host_alloc", "tc_host_free", "tc_diff_bound_range", "tc_diff_encode_range"}
     assert expected <= set(names), set(names) ^ expected
     for n in names:
         assert getattr(tc.LIB, n) is not None
@@ -69,3 +69,13 @@ def test_ctx_create_without_gpu_reports_cuda_error():
     h = ctypes.c_void_p()
     rc = tc.LIB.tc_ctx_create(0, ctypes.byref(h))
     assert rc == tc.ERR_CUDA and not h.value
+
+
+def test_bound_range_sums_to_bound(tco):
+    n, w, T, C = 100003, 4, 256, 4096
+    full = tc.diff_bound([n], [w], T, C)
+    nch = -(-n // C)
+    parts = [tc.diff_bound_range(n, w, c, 3, T, C) for c in range(0, nch, 3)]
+    assert sum(parts) == full
+    with pytest.raises(tc.TcError):
+        tc.diff_bound_range(n, w, nch, 1, T, C)

@@ -13,7 +13,7 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs a GPU", allow_module_level=True)
 
 from paper_2605_17821_b200 import tc  # noqa: E402
-from tests.gpu_util import gpu_encode, gpu_fold  # noqa: E402
+from tests.gpu_util import gpu_encode, gpu_fold, to_dev, to_np  # noqa: E402
 
 RNG = np.random.default_rng(7)
 
@@ -239,3 +239,27 @@ def test_launch_counter(ctx):
     tc.diff_apply(ctx, [ref], 0, [out], [int(ob.item())])
     ctx.check()
     assert ctx.launches == before + 5  # encode (mask, prefix, emit) + fold (walker, fold)
+
+
+@pytest.mark.parametrize("advance", [True, False])
+def test_range_encode_concatenates_to_full(ctx, tco, advance):
+    """tc_diff_encode_range over consecutive chunk runs of every segment == tc_diff_encode."""
+    sizes, wb, T, C = [40001, 70003, 0, 33000], [2, 4, 4, 4], 256, 8192
+    pairs = [rand_pair(n, w, 0.05) for n, w in zip(sizes, wb)]
+    full, ref_full, n_full = gpu_encode(ctx, [p[0] for p in pairs], [p[1] for p in pairs], T, C, advance, 3, 2)
+    parts = []
+    refs = [to_dev(p[0]) for p in pairs]
+    curs = [to_dev(p[1]) for p in pairs]
+    for s, (n, w) in enumerate(zip(sizes, wb)):
+        nch = max(1, -(-n // C))
+        for c0 in range(0, nch, 2):
+            cap = tc.diff_bound_range(n, w, c0, 2, T, C)
+            out = torch.full((cap,), 0xCD, dtype=torch.uint8, device="cuda")
+            ob = torch.zeros(1, dtype=torch.int64, device="cuda")
+            tc.diff_encode_range(ctx, refs[s], curs[s], s, c0, 2, out, ob, 3, 2, T, C, advance)
+            ctx.check()
+            parts.append(out[: int(ob.item())].cpu().numpy())
+    got = np.concatenate(parts)
+    assert got.size == n_full and np.array_equal(got, full)
+    for a, b in zip(refs, ref_full):
+        assert np.array_equal(to_np(a), b)
