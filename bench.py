@@ -180,9 +180,14 @@ def run_ours(args):
 
     s_comp = torch.cuda.Stream(device=dev)
     s_copy = torch.cuda.Stream(device=dev, priority=0)
-    s_comm = torch.cuda.Stream(device=dev)
+    s_comm = torch.cuda.Stream(device=dev, priority=-1)  # NCCL CTAs get SM slots ahead of the encode
     ctx = tc.Ctx(local)
     comm = tc.Comm(rank, world, local) if world > 1 else None
+    rep_pool = None
+    if comm is not None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        rep_pool = ThreadPoolExecutor(1, initializer=lambda: torch.cuda.set_device(local))
 
     # inputs: X = version 0, Y = version 1 (device synth; input preparation, untimed)
     X = [alloc(n, w) for n, w in zip(sizes, wb)]
@@ -223,8 +228,14 @@ def run_ours(args):
         cur = Y if state["content"] == "X" else X
         v = state["ref_version"] + 1
         if done_ev[slot] is not None:
-            for e in done_ev[slot]:
+            evs, fut_prev, timed_prev = done_ev[slot]
+            for e in evs:
                 s_comp.wait_event(e)
+            if fut_prev is not None:
+                r0p, r1p, nbp = fut_prev.result()
+                s_comp.wait_event(r1p)
+                if timed_prev:
+                    n_ops["replicate"].append((r0p, r1p, nbp))
         e0, e1 = ev(), ev()
         e0.record(s_comp)
         tc.diff_encode(ctx, A, cur, recs[slot], obytes[slot], v, v - 1, T, C, True, stream=s_comp)
@@ -241,14 +252,18 @@ def run_ours(args):
         tc.stage_host(host_ring[slot], recs[slot], nbytes, tc.D2H, stream=s_copy)
         host_t["stage"].append(time.perf_counter() - th0)
         c1.record(s_copy)
-        # Tier-2: ring-neighbour replication
-        r0 = r1 = None
+        # Tier-2: ring-neighbour replication, issued from a background thread (the size exchange
+        # blocks its caller until both neighbours are ready; the training-side thread must not)
+        fut = None
         if comm is not None:
-            s_comm.wait_event(e1)
-            r0, r1 = ev(), ev()
-            r0.record(s_comm)
-            comm.replicate_peer(recs[slot], obytes[slot], recv, tc.TO_NEXT, stream=s_comm)
-            r1.record(s_comm)
+            def _replicate(slot=slot, e1=e1, nb=nbytes):
+                s_comm.wait_event(e1)
+                r0, r1 = ev(), ev()
+                r0.record(s_comm)
+                comm.replicate_peer(recs[slot], obytes[slot], recv, tc.TO_NEXT, stream=s_comm)
+                r1.record(s_comm)
+                return r0, r1, nb
+            fut = rep_pool.submit(_replicate)
         # restore: fold the record onto the replica
         f0, f1 = ev(), ev()
         th0 = time.perf_counter()
@@ -259,21 +274,28 @@ def run_ours(args):
         state["rest_version"] = v
         state["ref_version"] = v
         state["content"] = "Y" if state["content"] == "X" else "X"
-        done_ev[slot] = [c1] + ([r1] if r1 is not None else [])
+        done_ev[slot] = ([c1], fut, timed)
         if timed:
             n_ops["encode"].append((e0, e1))
             n_ops["fold"].append((f0, f1))
             n_ops["stage"].append((c0, c1))
-            if r0 is not None:
-                n_ops["replicate"].append((r0, r1, nbytes))
         return nbytes
 
     def sync_all():
         for s in (s_comp, s_copy, s_comm):
             s.synchronize()
 
+    def drain():
+        for sl in range(2):  # outstanding replications of the last two steps
+            if done_ev[sl] is not None and done_ev[sl][1] is not None:
+                r0p, r1p, nbp = done_ev[sl][1].result()
+                if done_ev[sl][2]:
+                    n_ops["replicate"].append((r0p, r1p, nbp))
+                done_ev[sl] = (done_ev[sl][0], None, False)
+
     for k in range(args.warmup):
         step(k, False)
+    drain()
     sync_all()
     ctx.check(s_comp)
     if world > 1:
@@ -288,6 +310,7 @@ def run_ours(args):
     sizes_seen = []
     for k in range(args.warmup, args.warmup + args.steps):
         sizes_seen.append(step(k, True))
+    drain()
     for s in (s_copy, s_comm):
         e = torch.cuda.Event()
         e.record(s)

@@ -30,6 +30,13 @@ __global__ void stage_sizes_kernel(uint64_t* dev, const uint64_t* send_bytes, ui
     dev[3] = *reinterpret_cast<const volatile uint64_t*>(send_bytes);
 }
 
+// Export the exchanged words to mapped pinned host memory with a kernel, not a D2H copy: a copy
+// would queue behind multi-GB Tier-1 staging copies on the same copy engine.
+__global__ void export_sizes_kernel(volatile uint64_t* host, const uint64_t* dev) {
+    if (threadIdx.x < 4) host[threadIdx.x] = dev[threadIdx.x];
+    __threadfence_system();
+}
+
 tc_status nccl_fail(ncclResult_t r, const char* what) {
     tc::set_error(std::string(what) + ": " + ncclGetErrorString(r));
     if (r == ncclRemoteError || r == ncclSystemError) return TC_ERR_UNAVAILABLE;
@@ -87,7 +94,7 @@ tc_status tc_comm_init(int nranks, int rank, int device, const uint8_t id[128], 
         return nccl_fail(r, "ncclCommInitRank");
     }
     if (cudaMalloc(reinterpret_cast<void**>(&c->dev_sizes), 32) != cudaSuccess ||
-        cudaHostAlloc(reinterpret_cast<void**>(&c->host_sizes), 32, cudaHostAllocDefault) != cudaSuccess) {
+        cudaHostAlloc(reinterpret_cast<void**>(&c->host_sizes), 32, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
         ncclCommDestroy(c->nccl);
         delete c;
         tc::set_error("allocation of size-exchange buffers failed");
@@ -122,7 +129,8 @@ tc_status tc_replicate_peer(tc_comm* c, const void* send, const uint64_t* send_b
     *recv_bytes = 0;
     if (P == 1) {  // the ring of one: the replica is the local record itself
         stage_sizes_kernel<<<1, 1, 0, s>>>(c->dev_sizes, send_bytes, recv_cap);
-        cudaError_t e = cudaMemcpyAsync(c->host_sizes, c->dev_sizes, 32, cudaMemcpyDeviceToHost, s);
+        export_sizes_kernel<<<1, 32, 0, s>>>(c->host_sizes, c->dev_sizes);
+        cudaError_t e = cudaGetLastError();
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) {
             tc::set_error(std::string("size read: ") + cudaGetErrorString(e));
@@ -153,7 +161,8 @@ tc_status tc_replicate_peer(tc_comm* c, const void* send, const uint64_t* send_b
     ncclResult_t r2 = ncclGroupEnd();
     if (r != ncclSuccess) return nccl_fail(r, "size exchange");
     if (r2 != ncclSuccess) return nccl_fail(r2, "size exchange (group end)");
-    e = cudaMemcpyAsync(c->host_sizes, c->dev_sizes, 32, cudaMemcpyDeviceToHost, s);
+    export_sizes_kernel<<<1, 32, 0, s>>>(c->host_sizes, c->dev_sizes);
+    e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {
         tc_status st = check_async(c);
