@@ -216,7 +216,8 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
     uint32_t mine = 0;  // lane q keeps mask word mw0 + q
     if (lane < static_cast<int>(MPW))
         mine = reinterpret_cast<const uint32_t*>(tile)[(2 * B * W) / 4 + mw0 + lane];
-    // ---- counts: lane-per-mask-word popcount scan over the warp's range ----
+    // ---- counts: lane-per-mask-word popcount scan over the warp's range (the barrier below
+    //      also publishes thread 0's prefetched record start) ----
     const uint32_t c = __popc(mine);
     uint32_t inc = c;
 #pragma unroll
@@ -261,17 +262,40 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
         }
     }
 
-    // ---- block / chunk bookkeeping (one thread) ----
+    // ---- record start of the chunk: prefetched by thread 0 at block start; only the first
+    //      blocks of a chunk can find it unpublished and wait (block-uniform branch) ----
+    unsigned long long rs = sm.rs;
+    if (!(rs & 1ull)) {
+        __syncthreads();  // every thread has read sm.rs before thread 0 rewrites it
+        if (tid == 0) sm.rs = wait_rstart(P, I.chunk) | 1ull;
+        __syncthreads();
+        rs = sm.rs;
+    }
+    rs &= ~1ull;
+
+    // ---- mask words and block-relative tile_off entries, in their final place ----
+    {
+        uint8_t* rec = P.out + rs;
+        const uint64_t n_mask = cdiv(I.m, 32);
+        uint32_t* gmask = reinterpret_cast<uint32_t*>(rec + kHdrBytes);
+        uint32_t* gtoff = reinterpret_cast<uint32_t*>(rec + kHdrBytes + pad16(4 * n_mask));
+        const uint32_t p = I.p0 + (mw0 + lane) * 32;
+        if (lane < static_cast<int>(MPW) && p < I.m) {
+            gmask[(I.p0 >> 5) + mw0 + lane] = mine;
+            if ((p & (P.T - 1)) == 0) gtoff[p / P.T] = woff + pre;  // kernel B adds the block prefix
+        }
+    }
+
+    // ---- block / chunk bookkeeping (thread 0, after its own stores; nobody waits for it):
+    //      one packed atomic {done blocks : 24 | changed words : 40} per chunk tells the block
+    //      that completes the chunk, which writes the header and publishes the next record start ----
     if (tid == 0) {
         P.info[I.b] = total | (sparse ? 0u : kDenseFlag);
         atomicAdd(&P.group_sum[I.b / kEmitGroup], static_cast<unsigned long long>(total));
-        atomicAdd(&P.chunk_total[I.chunk], static_cast<unsigned long long>(total));
-        __threadfence();
-        const unsigned done = atomicAdd(&P.chunk_done[I.chunk], 1u);
-        const unsigned long long rs = wait_rstart(P, I.chunk);
-        if (done + 1 == I.nblk) {  // this block completes the chunk: header + next record start
-            __threadfence();
-            const uint64_t count = atomicAdd(&P.chunk_total[I.chunk], 0ull);
+        const unsigned long long old =
+            atomicAdd(&P.chunk_acc[I.chunk], (1ull << kAccDoneShift) | static_cast<unsigned long long>(total));
+        if ((old >> kAccDoneShift) + 1 == I.nblk) {
+            const uint64_t count = (old & kAccCountMask) + total;
             const uint64_t n_mask = cdiv(I.m, 32);
             const uint64_t n_tiles = cdiv(I.m, P.T);
             const uint64_t rec_total = record_bytes(I.m, P.T, W, count);
@@ -296,19 +320,6 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
             st_relaxed(&P.rstart[I.chunk + 1], next | 1ull);
             if (I.chunk + 1 == P.total_chunks) *P.out_bytes = next;
         }
-        sm.rs = rs;
-    }
-    __syncthreads();
-
-    // ---- mask words and block-relative tile_off entries, in their final place ----
-    uint8_t* rec = P.out + sm.rs;
-    const uint64_t n_mask = cdiv(I.m, 32);
-    uint32_t* gmask = reinterpret_cast<uint32_t*>(rec + kHdrBytes);
-    uint32_t* gtoff = reinterpret_cast<uint32_t*>(rec + kHdrBytes + pad16(4 * n_mask));
-    const uint32_t p = I.p0 + (mw0 + lane) * 32;
-    if (lane < static_cast<int>(MPW) && p < I.m) {
-        gmask[(I.p0 >> 5) + mw0 + lane] = mine;
-        if ((p & (P.T - 1)) == 0) gtoff[p / P.T] = woff + pre;  // kernel B adds the block prefix
     }
 }
 
@@ -321,6 +332,7 @@ __global__ void __launch_bounds__(kEncThreads, 6) encode_mask_kernel(const __gri
         const BlockInfo I = decode_block(P, atomicAdd(P.ticket, 1ull));
         sm.I = I;
         mbar_init(&sm.bar, 1);
+        sm.rs = I.chunk == 0 ? 1ull : 0ull;  // chunk 0 starts at 0; others: prefetched below
         const uint32_t bulk = (I.nb * I.w) & ~15u;
         if (bulk) {
             const EncSeg& S = P.seg[I.seg];
@@ -334,6 +346,7 @@ __global__ void __launch_bounds__(kEncThreads, 6) encode_mask_kernel(const __gri
         }
     }
     __syncthreads();
+    if (tid == 0 && sm.I.chunk != 0) sm.rs = ld_relaxed(&P.rstart[sm.I.chunk]);  // value | 1 once published
     if (sm.I.w == 4)
         mask_block<4>(P, sm, tile, tid);
     else
@@ -346,14 +359,14 @@ __global__ void __launch_bounds__(1024) encode_prefix_kernel(const __grid_consta
     __shared__ unsigned long long s_warp[32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     for (int pass = 0; pass < 2; ++pass) {
-        const unsigned long long* in = pass == 0 ? P.group_sum : P.chunk_total;
+        const unsigned long long* in = pass == 0 ? P.group_sum : P.chunk_acc;
         unsigned long long* out = pass == 0 ? P.gpre : P.cbase;
         const uint64_t n = pass == 0 ? P.n_groups : P.total_chunks;
         if (tid == 0) s_carry = 0;
         __syncthreads();
         for (uint64_t base = 0; base < n; base += 1024) {
             const uint64_t i = base + tid;
-            const unsigned long long v = i < n ? in[i] : 0ull;
+            const unsigned long long v = i < n ? (pass == 0 ? in[i] : in[i] & kAccCountMask) : 0ull;
             unsigned long long x = v;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {

@@ -58,16 +58,15 @@ struct EncParams {
     uint64_t version, ref_version;
     uint8_t* out;
     uint64_t* out_bytes;
-    // scratch (tc_ctx), zeroed per call: ticket | chunk_total | chunk_done | rstart | group_sum
+    // scratch (tc_ctx), zeroed per call: ticket | chunk_acc | rstart | group_sum
     unsigned long long* ticket;
-    unsigned long long* chunk_total;  // [total_chunks] changed words per chunk
-    unsigned int* chunk_done;         // [total_chunks] blocks counted
+    unsigned long long* chunk_acc;    // [total_chunks] {blocks counted : 24 | changed words : 40}
     unsigned long long* rstart;       // [total_chunks + 1] record start | 1 once published
     unsigned long long* group_sum;    // [n_groups] changed words per group of kEmitGroup blocks
     // scratch, fully written each call
     uint32_t* info;                   // [total_blocks] count | kDenseFlag
     unsigned long long* gpre;         // [n_groups] exclusive prefix of group_sum
-    unsigned long long* cbase;        // [total_chunks] exclusive prefix of chunk_total
+    unsigned long long* cbase;        // [total_chunks] exclusive prefix of the chunk counts
     uint8_t* spill;                   // [total_blocks] slots of kSpillBytes: packed values
     unsigned int* err;                // sticky error word
     int advance_ref;
@@ -76,6 +75,8 @@ struct EncParams {
 constexpr uint32_t kEmitGroup = 256;        // blocks per emit CTA / per group sum
 constexpr uint32_t kSpillBytes = 4096;      // per-block spill slot (1/4 of a block's words)
 constexpr uint32_t kDenseFlag = 0x80000000u;
+constexpr int kAccDoneShift = 40;  // chunk_acc: blocks counted above bit 40 (a chunk has <= 2^19 blocks)
+constexpr unsigned long long kAccCountMask = (1ull << kAccDoneShift) - 1;
 
 // ---- fold descriptors ----
 struct FoldRec {           // one record of one diff, as located by the walker

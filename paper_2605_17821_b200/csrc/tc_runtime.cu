@@ -250,9 +250,9 @@ static tc_status encode_impl(tc_ctx* ctx, const SegSpec* specs, int nseg, const 
 
     const uint64_t groups = cdiv(blocks, kEmitGroup);
     P.n_groups = groups;
-    // zeroed region: ticket | chunk_total | chunk_done | rstart | group_sum
-    const size_t z_ticket = 0, z_ctot = 16, z_cdone = z_ctot + 8 * chunks;
-    const size_t z_rstart = z_cdone + ((4 * chunks + 15) & ~size_t(15));
+    // zeroed region: ticket | chunk_acc | rstart | group_sum
+    const size_t z_ticket = 0, z_ctot = 16;
+    const size_t z_rstart = z_ctot + 8 * chunks;
     const size_t z_gsum = z_rstart + 8 * (chunks + 1);
     const size_t z_end = z_gsum + 8 * groups;
     // written-every-call region: info | gpre | cbase
@@ -266,8 +266,7 @@ static tc_status encode_impl(tc_ctx* ctx, const SegSpec* specs, int nseg, const 
     if (st != TC_OK) return st;
     uint8_t* base = static_cast<uint8_t*>(ctx->enc);
     P.ticket = reinterpret_cast<unsigned long long*>(base + z_ticket);
-    P.chunk_total = reinterpret_cast<unsigned long long*>(base + z_ctot);
-    P.chunk_done = reinterpret_cast<unsigned int*>(base + z_cdone);
+    P.chunk_acc = reinterpret_cast<unsigned long long*>(base + z_ctot);
     P.rstart = reinterpret_cast<unsigned long long*>(base + z_rstart);
     P.group_sum = reinterpret_cast<unsigned long long*>(base + z_gsum);
     P.info = reinterpret_cast<uint32_t*>(base + w_info);
