@@ -6,6 +6,7 @@
  */
 #include "tco.h"
 
+#include <stdlib.h>
 #include <string.h>
 
 /* ---- little-endian scalar access (little-endian wire format) ---- */
@@ -46,9 +47,15 @@ uint64_t tco_record_bytes(uint64_t m, uint32_t T, uint32_t w, uint64_t count) {
     return HDR_BYTES + pad16(4 * ceil_div(m, 32)) + pad16(4 * (ceil_div(m, T) + 1)) + pad16((uint64_t)w * count);
 }
 
+/* Index-mode record (flags bit1): 64 + pad16(4*(ceil(m/T)+1)) + pad16(2*count)
+ * + pad16(w*count). */
+uint64_t tco_record_bytes_index(uint64_t m, uint32_t T, uint32_t w, uint64_t count) {
+    return HDR_BYTES + pad16(4 * (ceil_div(m, T) + 1)) + pad16(2 * count) + pad16((uint64_t)w * count);
+}
+
 /* one chunk [chunk_off, chunk_off+m) of one segment. */
 static int encode_chunk(void* ref, const void* cur, uint64_t chunk_off, uint64_t m, uint32_t w,
-                        uint32_t T, uint32_t seg, int advance_ref, uint64_t version,
+                        uint32_t T, uint32_t seg, int advance_ref, int index_mode, uint64_t version,
                         uint64_t ref_version, uint8_t* out, uint64_t cap, uint64_t* written) {
     /* 1. count the changed words: unsigned bitwise compare of each word (reading R5). */
     uint64_t count = 0;
@@ -57,13 +64,29 @@ static int encode_chunk(void* ref, const void* cur, uint64_t chunk_off, uint64_t
 
     uint64_t n_mask = ceil_div(m, 32);
     uint64_t n_tiles = ceil_div(m, T);
-    uint64_t total = tco_record_bytes(m, T, w, count);
+    uint64_t total = index_mode ? tco_record_bytes_index(m, T, w, count) : tco_record_bytes(m, T, w, count);
     if (total > cap) return TCO_ERR_CAPACITY;
     memset(out, 0, total); /* every pad byte is zero (reading R9) */
 
-    uint8_t* mask_p = out + HDR_BYTES;
-    uint8_t* toff_p = mask_p + pad16(4 * n_mask);
-    uint8_t* val_p = toff_p + pad16(4 * (n_tiles + 1));
+    /* mask mode: header | mask | tile_off | values.  index mode: header | tile_off | idx | values;
+     * there the mask is built in a heap buffer, used only to derive tile_off and the indices. */
+    uint8_t* mask_heap = NULL;
+    uint8_t* mask_p;
+    uint8_t* toff_p;
+    uint8_t* idx_p = NULL;
+    uint8_t* val_p;
+    if (!index_mode) {
+        mask_p = out + HDR_BYTES;
+        toff_p = mask_p + pad16(4 * n_mask);
+        val_p = toff_p + pad16(4 * (n_tiles + 1));
+    } else {
+        mask_heap = (uint8_t*)calloc(n_mask ? 4 * n_mask : 4, 1);
+        if (!mask_heap) return TCO_ERR_CAPACITY;
+        mask_p = mask_heap;
+        toff_p = out + HDR_BYTES;
+        idx_p = toff_p + pad16(4 * (n_tiles + 1));
+        val_p = idx_p + pad16(2 * count);
+    }
 
     /* 2-4. mask bit i set iff word i changed; values = changed cur words in index
      *      order; optional ref advance after the compare. */
@@ -91,11 +114,21 @@ static int encode_chunk(void* ref, const void* cur, uint64_t chunk_off, uint64_t
             if ((get_u32(mask_p + 4 * (i / 32)) >> (i % 32)) & 1u) c++;
     }
     put_u32(toff_p + 4 * n_tiles, (uint32_t)c);
+    /* 5b. index mode: idx[k] = in-tile position (i mod T) of the k-th changed word, in index order. */
+    if (index_mode) {
+        uint64_t k2 = 0;
+        for (uint64_t i = 0; i < m; i++)
+            if ((get_u32(mask_p + 4 * (i / 32)) >> (i % 32)) & 1u) {
+                put_u16(idx_p + 2 * k2, (uint16_t)(i % T));
+                k2++;
+            }
+        free(mask_heap);
+    }
     /* 6. header. */
     out[0] = 'T'; out[1] = 'C'; out[2] = 'D'; out[3] = '1';
     put_u16(out + 4, 1);
     out[6] = (uint8_t)w;
-    out[7] = 1; /* REPLACE */
+    out[7] = index_mode ? 3 : 1; /* REPLACE (| INDEX) */
     put_u32(out + 8, T);
     put_u32(out + 12, seg);
     put_u64(out + 16, chunk_off);
@@ -109,7 +142,7 @@ static int encode_chunk(void* ref, const void* cur, uint64_t chunk_off, uint64_t
 }
 
 int tco_encode(void* const* ref, const void* const* cur, const uint64_t* n, const uint32_t* w,
-               int nseg, uint32_t T, uint64_t C, int advance_ref, uint64_t version,
+               int nseg, uint32_t T, uint64_t C, int advance_ref, int index_mode, uint64_t version,
                uint64_t ref_version, uint8_t* out, uint64_t out_cap, uint64_t* out_bytes) {
     *out_bytes = 0;
     if (nseg < 0 || !is_pow2(T) || T < 32 || T > 65536) return TCO_ERR_INVALID;
@@ -123,7 +156,7 @@ int tco_encode(void* const* ref, const void* const* cur, const uint64_t* n, cons
         do {
             uint64_t m = n[s] - off < C ? n[s] - off : C;
             uint64_t written = 0;
-            int rc = encode_chunk(ref[s], cur[s], off, m, w[s], T, (uint32_t)s, advance_ref,
+            int rc = encode_chunk(ref[s], cur[s], off, m, w[s], T, (uint32_t)s, advance_ref, index_mode,
                                   version, ref_version, out + pos, out_cap - pos, &written);
             if (rc != TCO_OK) return rc;
             pos += written;
@@ -137,10 +170,11 @@ int tco_encode(void* const* ref, const void* const* cur, const uint64_t* n, cons
 /* ---------------------------------------------------------------- restore ---- */
 
 typedef struct {
-    uint32_t w, T, seg;
+    uint32_t w, T, seg, index_mode;
     uint64_t chunk_off, m, count, version, ref_version, total;
-    const uint8_t* mask;
+    const uint8_t* mask; /* mask mode */
     const uint8_t* toff;
+    const uint8_t* idx;  /* index mode */
     const uint8_t* values;
 } rec_view;
 
@@ -151,7 +185,8 @@ static int parse_header(const uint8_t* p, uint64_t avail, rec_view* r) {
     if (get_u16(p + 4) != 1) return TCO_ERR_CORRUPT;
     r->w = p[6];
     if (r->w != 2 && r->w != 4) return TCO_ERR_CORRUPT;
-    if (p[7] != 1) return TCO_ERR_CORRUPT;
+    if (p[7] != 1 && p[7] != 3) return TCO_ERR_CORRUPT;
+    r->index_mode = p[7] == 3;
     r->T = get_u32(p + 8);
     if (!is_pow2(r->T) || r->T < 32 || r->T > 65536) return TCO_ERR_CORRUPT;
     r->seg = get_u32(p + 12);
@@ -162,11 +197,21 @@ static int parse_header(const uint8_t* p, uint64_t avail, rec_view* r) {
     r->ref_version = get_u64(p + 48);
     r->total = get_u64(p + 56);
     if (r->m > MAX_CHUNK_WORDS || r->count > r->m) return TCO_ERR_CORRUPT;
-    if (r->total != tco_record_bytes(r->m, r->T, r->w, r->count)) return TCO_ERR_CORRUPT;
+    uint64_t want = r->index_mode ? tco_record_bytes_index(r->m, r->T, r->w, r->count)
+                                   : tco_record_bytes(r->m, r->T, r->w, r->count);
+    if (r->total != want) return TCO_ERR_CORRUPT;
     if (r->total > avail) return TCO_ERR_CORRUPT;
-    r->mask = p + HDR_BYTES;
-    r->toff = r->mask + pad16(4 * ceil_div(r->m, 32));
-    r->values = r->toff + pad16(4 * (ceil_div(r->m, r->T) + 1));
+    if (!r->index_mode) {
+        r->mask = p + HDR_BYTES;
+        r->toff = r->mask + pad16(4 * ceil_div(r->m, 32));
+        r->idx = NULL;
+        r->values = r->toff + pad16(4 * (ceil_div(r->m, r->T) + 1));
+    } else {
+        r->mask = NULL;
+        r->toff = p + HDR_BYTES;
+        r->idx = r->toff + pad16(4 * (ceil_div(r->m, r->T) + 1));
+        r->values = r->idx + pad16(2 * r->count);
+    }
     return TCO_OK;
 }
 
@@ -176,6 +221,22 @@ static int check_body(const rec_view* r) {
     uint64_t n_tiles = ceil_div(r->m, r->T);
     uint64_t n_mask = ceil_div(r->m, 32);
     if (get_u32(r->toff) != 0) return TCO_ERR_CORRUPT;
+    if (r->index_mode) {
+        /* tile_off non-decreasing, ends at count; within each tile the indices are strictly
+         * increasing and inside the tile (so each names a distinct word of the chunk). */
+        for (uint64_t t = 0; t < n_tiles; t++) {
+            uint64_t a = get_u32(r->toff + 4 * t), b = get_u32(r->toff + 4 * (t + 1));
+            uint64_t len = (t + 1) * r->T < r->m ? r->T : r->m - t * r->T;
+            if (b < a || b > r->count) return TCO_ERR_CORRUPT;
+            for (uint64_t k = a; k < b; k++) {
+                uint64_t x = get_u16(r->idx + 2 * k);
+                if (x >= len) return TCO_ERR_CORRUPT;
+                if (k > a && x <= get_u16(r->idx + 2 * (k - 1))) return TCO_ERR_CORRUPT;
+            }
+        }
+        if (get_u32(r->toff + 4 * n_tiles) != r->count) return TCO_ERR_CORRUPT;
+        return TCO_OK;
+    }
     for (uint64_t t = 0; t < n_tiles; t++) {
         uint64_t c = 0;
         uint64_t end = (t + 1) * r->T < r->m ? (t + 1) * r->T : r->m;
@@ -242,11 +303,20 @@ int tco_apply(void* const* state, const uint64_t* n, const uint32_t* w, int nseg
     for (uint64_t k = 0; k < n_rec; k++) {
         rec_view r;
         parse_header(diff + pos, diff_bytes - pos, &r);
-        uint64_t kv = 0;
-        for (uint64_t i = 0; i < r.m; i++) {
-            if ((get_u32(r.mask + 4 * (i / 32)) >> (i % 32)) & 1u) {
-                store_word(state[r.seg], r.chunk_off + i, r.w, load_word(r.values, kv, r.w));
-                kv++;
+        if (r.index_mode) {
+            /* the k-th value goes to word t*T + idx[k] of the chunk, t = the tile holding k */
+            uint64_t n_tiles = ceil_div(r.m, r.T);
+            for (uint64_t t = 0; t < n_tiles; t++)
+                for (uint64_t k = get_u32(r.toff + 4 * t); k < get_u32(r.toff + 4 * (t + 1)); k++)
+                    store_word(state[r.seg], r.chunk_off + t * r.T + get_u16(r.idx + 2 * k), r.w,
+                               load_word(r.values, k, r.w));
+        } else {
+            uint64_t kv = 0;
+            for (uint64_t i = 0; i < r.m; i++) {
+                if ((get_u32(r.mask + 4 * (i / 32)) >> (i % 32)) & 1u) {
+                    store_word(state[r.seg], r.chunk_off + i, r.w, load_word(r.values, kv, r.w));
+                    kv++;
+                }
             }
         }
         pos += r.total;

@@ -5,6 +5,7 @@ Files and what pins them (see README.md in this directory):
   hand1_fp32.bin   SURVEY.md Appendix A hand example 1 (fp32, m=6, T=4096, v7 <- v6)
   hand2_bf16.bin   SURVEY.md Appendix A hand example 2 (bf16, m=3)
   empty_m0.bin     SURVEY.md §8(c) reading c12 (empty segment -> 80-byte record)
+  hand1_fp32_index.bin  hand example 1 as an index-mode record (idx = [1, 3])
   cfg1_small_v1.bin / cfg1_small_v2.bin
                    a two-link chain on a cfg1-shaped (3 fp32 segments) 3000-word shard,
                    f = 1 %, T = 64, chunk_words = 1024, seed 0x7C0DEC (determinism pin)
@@ -44,6 +45,15 @@ def hand2():
     return rec
 
 
+def hand1_index():
+    ref = np.array(HAND1_REF, dtype=np.uint32)
+    cur = np.array(HAND1_CUR, dtype=np.uint32)
+    rc, rec = oracle.encode([ref], [cur], tile_words=4096, advance_ref=False, version=7,
+                            ref_version=6, index_mode=True)
+    assert rc == 0
+    return rec
+
+
 def empty():
     e = np.zeros(0, dtype=np.uint32)
     rc, rec = oracle.encode([e], [e.copy()], tile_words=4096, advance_ref=False, version=1,
@@ -70,6 +80,7 @@ def main():
         "hand1_fp32.bin": hand1(),
         "hand2_bf16.bin": hand2(),
         "empty_m0.bin": empty(),
+        "hand1_fp32_index.bin": hand1_index(),
     }
     r1, r2 = cfg1_small()
     out["cfg1_small_v1.bin"] = r1

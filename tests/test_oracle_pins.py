@@ -378,3 +378,126 @@ def test_multi_segment_order_and_mixed_widths(tco):
     st = [p[0].copy() for p in pairs]
     rc, _ = tco.apply(st, 0, rec)
     assert rc == 0 and all(np.array_equal(a, b) for a, b in zip(st, cur))
+
+
+# ------------------------------------------------------- index-mode records ------
+def _parse_index(rec, pos=0):
+    """Independent parse of an index-mode record: header | tile_off | idx | values."""
+    import struct
+    (magic, fmt, w, flags, T, seg, off, m, count, version, ref_version, total) = recfmt.HDR.unpack(
+        bytes(rec[pos: pos + 64]))
+    n_tiles = -(-m // T)
+    p = pos + 64
+    toff = rec[p: p + 4 * (n_tiles + 1)].view("<u4")
+    p += recfmt.pad16(4 * (n_tiles + 1))
+    idx = rec[p: p + 2 * count].view("<u2")
+    p += recfmt.pad16(2 * count)
+    vals = rec[p: p + w * count].view("<u2" if w == 2 else "<u4")
+    return dict(flags=flags, T=T, m=m, count=count, total=total, toff=toff, idx=idx, values=vals, off=off, seg=seg)
+
+
+def test_hand_example_fp32_index_mode(tco):
+    ref = np.array([0x3F800000, 0, 0x80000000, 0x7FC00000, 0x12345678, 0x7FC00000], np.uint32)
+    cur = np.array([0x3F800000, 0x80000000, 0x80000000, 0x7FC00001, 0x12345678, 0x7FC00000], np.uint32)
+    rc, rec = tco.encode([ref], [cur], tile_words=4096, advance_ref=False, version=7, ref_version=6,
+                         index_mode=True)
+    assert rc == 0 and rec.size == 64 + 16 + 16 + 16
+    r = _parse_index(rec)
+    assert r["flags"] == 3 and list(r["idx"]) == [1, 3] and list(r["toff"]) == [0, 2]
+    assert list(r["values"]) == [0x80000000, 0x7FC00001]
+    assert np.array_equal(rec, gold("hand1_fp32_index.bin"))
+    st = ref.copy()
+    rc, v = tco.apply([st], 6, rec)
+    assert rc == 0 and v == 7 and np.array_equal(st, cur)
+
+
+@pytest.mark.parametrize("n,w,f,T,C", [(1000, 4, 0.01, 64, 256), (70000, 2, 0.003, 4096, 8192),
+                                       (12345, 4, 1.0, 32, 4096), (5000, 2, 0.0, 64, 64),
+                                       (40000, 4, 0.2, 65536, 65536)])
+def test_index_records_equal_library_special_cases(tco, n, w, f, T, C):
+    ref, cur = _rand_pair(n, w, f)
+    changed = ref != cur
+    rc, rec = tco.encode([ref.copy()], [cur], tile_words=T, chunk_words=C, index_mode=True)
+    assert rc == 0
+    pos = 0
+    for k in range(-(-n // C)):
+        r = _parse_index(rec, pos)
+        m = r["m"]
+        ch = changed[r["off"]: r["off"] + m]
+        where = np.nonzero(ch)[0]
+        assert np.array_equal(r["idx"], (where % T).astype(np.uint16))  # in-tile positions
+        assert np.array_equal(r["values"], cur[r["off"]: r["off"] + m][ch])
+        per_tile = np.add.reduceat(ch.astype(np.int64), np.arange(0, m, T)) if m else []
+        assert np.array_equal(r["toff"], np.concatenate([[0], np.cumsum(per_tile)]))
+        assert r["total"] == tco.record_bytes(m, T, w, r["count"], index_mode=True) == (
+            64 + recfmt.pad16(4 * (-(-m // T) + 1)) + recfmt.pad16(2 * r["count"]) + recfmt.pad16(w * r["count"]))
+        pos += r["total"]
+    assert pos == rec.size
+    st = ref.copy()
+    rc, _ = tco.apply([st], 0, rec)
+    assert rc == 0 and np.array_equal(st, cur)
+
+
+@pytest.mark.parametrize("w", [2, 4])
+def test_index_mode_all_change_masks_m12(tco, w):
+    dt = np.uint16 if w == 2 else np.uint32
+    base = RNG.integers(0, 1 << (8 * w), size=12, dtype=np.uint64).astype(dt)
+    for bits in range(0, 1 << 12, 7):
+        ch = np.array([(bits >> i) & 1 for i in range(12)], bool)
+        cur = base.copy()
+        cur[ch] ^= dt(0x3C)
+        rc, rec = tco.encode([base.copy()], [cur], tile_words=32, chunk_words=32, index_mode=True)
+        assert rc == 0
+        assert list(_parse_index(rec)["idx"]) == [i for i in range(12) if ch[i]]
+        st = base.copy()
+        rc, _ = tco.apply([st], 0, rec)
+        assert rc == 0 and np.array_equal(st, cur)
+
+
+def test_mixed_mode_chain_fold(tco):
+    sizes, wb = [3000, 5000], [2, 4]
+    s = [synth.state(sizes, wb, 21, v, 0.05) for v in range(5)]
+    ref = [a.copy() for a in s[0]]
+    ds = []
+    for v in range(1, 5):
+        rc, d = tco.encode(ref, s[v], tile_words=64, chunk_words=1024, version=v, ref_version=v - 1,
+                           index_mode=(v % 2 == 1))
+        assert rc == 0
+        ds.append(d)
+    st = [a.copy() for a in s[0]]
+    rc, ver = tco.fold(st, 0, ds)
+    assert rc == 0 and ver == 4 and all(np.array_equal(a, b) for a, b in zip(st, s[4]))
+
+
+def _index_rec(tco):
+    ref, cur = _rand_pair(300, 4, 0.2)
+    rc, rec = tco.encode([ref.copy()], [cur], tile_words=64, version=5, ref_version=4, index_mode=True)
+    return ref, rec
+
+
+def test_index_tamper_out_of_tile_is_corrupt(tco):
+    base, rec = _index_rec(tco)
+    r = _parse_index(rec)
+    bad = rec.copy()
+    p = 64 + recfmt.pad16(4 * (-(-300 // 64) + 1))
+    bad[p: p + 2] = np.frombuffer(np.uint16(64).tobytes(), np.uint8)  # position 64 is outside a 64-word tile
+    _expect(tco, base, bad, tco.ERR_CORRUPT)
+    assert r["count"] > 1
+
+
+def test_index_tamper_not_increasing_is_corrupt(tco):
+    base, rec = _index_rec(tco)
+    r = _parse_index(rec)
+    bad = rec.copy()
+    p = 64 + recfmt.pad16(4 * (-(-300 // 64) + 1))
+    first = int(r["idx"][0])
+    bad[p + 2: p + 4] = np.frombuffer(np.uint16(first).tobytes(), np.uint8)  # duplicate of idx[0]
+    if int(r["toff"][1]) >= 2:
+        _expect(tco, base, bad, tco.ERR_CORRUPT)
+
+
+def test_index_tamper_flags_is_corrupt(tco):
+    base, rec = _index_rec(tco)
+    bad = rec.copy()
+    bad[7] = 2  # INDEX without REPLACE
+    _expect(tco, base, bad, tco.ERR_CORRUPT)
