@@ -41,6 +41,8 @@
  *   u32 tile_words T, u32 segment_id, u64 chunk_word_offset, u64 n_words m, u64 count,
  *   u64 version, u64 ref_version, u64 total_bytes} || mask u32[ceil(m/32)] ||
  *   tile_off u32[ceil(m/T)+1] || values (word_bytes * count); each section zero-padded to 16 B.
+ *   Index mode (flags = 3): header || tile_off u32[ceil(m/T)+1] || idx u16[count] (in-tile
+ *   position of each changed word, increasing within a tile) || values; each padded to 16 B.
  *   Mask bit (i mod 32) of word i/32 is set iff word i of the chunk changed (unsigned
  *   bitwise compare); values are the new words of the changed positions in index order;
  *   tile_off[t] = changed words in [0, t*T).  A shard diff is the concatenation of its
@@ -96,6 +98,13 @@ typedef struct tc_encode_opts {
                              record is incremental (reading R2); 0: ref untouched             */
     uint64_t chunk_words; /* C: multiple of T, <= 2^31-1; default 2^28 (PAPER.md:203 chunking,
                              reading R8)                                                      */
+    uint32_t index_mode;  /* 0 (default): mask section (4 bytes per 32 words).  1: index mode —
+                             the mask is replaced by u16[count] in-tile positions after tile_off
+                             (flags bit1; 2 bytes per changed word), smaller when f < 1/16: the
+                             lossless analog of the paper's "FP16 values and INT32 indices"
+                             sparse payload (§3.2).  Records of both modes fold
+                             together.  Requires T <= 8192 (restore stages a tile's mask words). */
+    uint32_t reserved;    /* must be 0 */
 } tc_encode_opts;
 
 enum { TC_D2H = 0, TC_H2D = 1 };

@@ -59,19 +59,30 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
                 const uint32_t seg = static_cast<uint32_t>(h1 >> 32);
                 const uint64_t coff = ld_u64(h + 16), m = ld_u64(h + 24), count = ld_u64(h + 32);
                 const uint64_t version = ld_u64(h + 40), ref_version = ld_u64(h + 48), total = ld_u64(h + 56);
-                if (magic != 0x31444354u || fmt != 1 || (w != 2 && w != 4) || flags != 1 ||
+                const bool imode = flags == 3;
+                if (magic != 0x31444354u || fmt != 1 || (w != 2 && w != 4) || (flags != 1 && flags != 3) ||
                     !is_pow2(T) || T < 32 || T > 65536 || seg != static_cast<uint32_t>(s) || w != P.w[s] ||
                     coff != off || coff % T != 0 || m > kMaxChunkWords || count > m ||
-                    (m == 0 && P.n[s] != 0) || off + m > P.n[s] || total != record_bytes(m, T, w, count) ||
+                    (m == 0 && P.n[s] != 0) || off + m > P.n[s] ||
+                    total != (imode ? record_bytes_index(m, T, w, count) : record_bytes(m, T, w, count)) ||
                     total > bytes - pos) {
                     err = TC_ERR_CORRUPT;
                     break;
                 }
                 if (r >= P.cap) { err = TC_ERR_CAPACITY; break; }
+                if (imode && T > kIndexMaxT) { err = TC_ERR_INVALID; break; }  // unsupported here
                 FoldRec R;
-                R.mask = h + kHdrBytes;
-                R.toff = R.mask + pad16(4 * cdiv(m, 32));
-                R.values = h + record_fixed_bytes(m, T);
+                if (imode) {
+                    R.mask = nullptr;
+                    R.toff = h + index_toff_off();
+                    R.idx = h + index_idx_off(m, T);
+                    R.values = h + index_val_off(m, T, count);
+                } else {
+                    R.mask = h + kHdrBytes;
+                    R.idx = nullptr;
+                    R.toff = R.mask + pad16(4 * cdiv(m, 32));
+                    R.values = h + record_fixed_bytes(m, T);
+                }
                 R.chunk_off = coff;
                 R.count = count;
                 R.m = static_cast<uint32_t>(m);
@@ -172,8 +183,59 @@ __device__ __forceinline__ uint16_t ldg_word(const uint16_t* p) {
     return static_cast<uint16_t>(__ldg(reinterpret_cast<const unsigned short*>(p)));
 }
 
+// Index-mode record: set the bits of the changed words of [sub, send) (chunk-relative) in the
+// warp's 128 shared mask words.  Checks each position lies inside its tile and strictly increases
+// within the tile (the oracle's index-mode body check); duplicates merge and are caught by the
+// unit-end popcount check.
+__device__ __forceinline__ void build_mask_from_index(const FoldRec& R, uint32_t sub, uint32_t send, uint32_t* imask,
+                                                      int lane, bool& bad) {
+#pragma unroll
+    for (uint32_t g = 0; g < kSubGroups; ++g) imask[32 * g + lane] = 0;
+    __syncwarp();
+    const uint32_t T = R.T, m = R.m;
+    const uint32_t* toff = reinterpret_cast<const uint32_t*>(R.toff);
+    const uint16_t* idx = reinterpret_cast<const uint16_t*>(R.idx);
+    for (uint32_t t = sub / T; t * T < send; ++t) {
+        const uint32_t ts = t * T;
+        const uint32_t tlen = m - ts < T ? m - ts : T;
+        const uint32_t a = ldg_u32(toff + t), b = ldg_u32(toff + t + 1);
+        if (b < a || b > R.count) {
+            bad = true;
+            break;
+        }
+        uint32_t lo = a, hi = b;
+        if (ts < sub || ts + T > send) {  // the tile is larger than the sub-unit: find its slice
+            const uint32_t want_lo = sub > ts ? sub - ts : 0, want_hi = send - ts;
+            uint32_t l = a, h = b;
+            while (l < h) {
+                const uint32_t mid = (l + h) >> 1;
+                if (__ldg(reinterpret_cast<const unsigned short*>(idx) + mid) < want_lo) l = mid + 1; else h = mid;
+            }
+            lo = l;
+            h = b;
+            while (l < h) {
+                const uint32_t mid = (l + h) >> 1;
+                if (__ldg(reinterpret_cast<const unsigned short*>(idx) + mid) < want_hi) l = mid + 1; else h = mid;
+            }
+            hi = l;
+        }
+        for (uint32_t k = lo + lane; k < hi; k += 32) {
+            const uint32_t x = __ldg(reinterpret_cast<const unsigned short*>(idx) + k);
+            if (x >= tlen) {
+                bad = true;
+                continue;
+            }
+            if (k > a && __ldg(reinterpret_cast<const unsigned short*>(idx) + k - 1) >= x) bad = true;
+            const uint32_t pos = ts + x - sub;
+            atomicOr(&imask[pos >> 5], 1u << (pos & 31));
+        }
+    }
+    __syncwarp();
+}
+
 template <int W>
-__device__ void fold_unit(const FoldParams& P, uint64_t r, uint64_t ku, uint32_t* carry, int lane, bool& bad) {
+__device__ void fold_unit(const FoldParams& P, uint64_t r, uint64_t ku, uint32_t* carry, uint32_t* imask, int lane,
+                          bool& bad) {
     using word_t = typename Word<W>::T;
     const int N = P.nrec;
     const FoldRec& L = P.desc[r];  // the chunk layout (shared by every diff)
@@ -197,10 +259,17 @@ __device__ void fold_unit(const FoldParams& P, uint64_t r, uint64_t ku, uint32_t
             const uint32_t count = static_cast<uint32_t>(R.count);
             // all mask words of the sub-unit first (independent read-only loads)
             uint32_t mk[kSubGroups];
+            if (R.idx) {
+                // index-mode record: build this sub-unit's mask words from the in-tile positions
+                build_mask_from_index(R, sub, send, imask, lane, bad);
 #pragma unroll
-            for (uint32_t g = 0; g < kSubGroups; ++g) {
-                const uint32_t p = sub + (32 * g + lane) * 32;
-                mk[g] = p < send ? ldg_u32(mask + (p >> 5)) : 0u;
+                for (uint32_t g = 0; g < kSubGroups; ++g) mk[g] = imask[32 * g + lane];
+            } else {
+#pragma unroll
+                for (uint32_t g = 0; g < kSubGroups; ++g) {
+                    const uint32_t p = sub + (32 * g + lane) * 32;
+                    mk[g] = p < send ? ldg_u32(mask + (p >> 5)) : 0u;
+                }
             }
             uint32_t run = sub == ustart ? ldg_u32(toff + ustart / T) : carry[j];
             if (sub == ustart && ku == 0 && run != 0) bad = true;
@@ -289,6 +358,7 @@ __device__ void fold_unit(const FoldParams& P, uint64_t r, uint64_t ku, uint32_t
 
 __global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const __grid_constant__ FoldParams P) {
     __shared__ uint32_t s_carry[kFoldWarps][TC_MAX_FOLD];
+    __shared__ uint32_t s_imask[kFoldWarps][kSubGroups * 32];  // index-mode records: built mask words
     if (*reinterpret_cast<volatile unsigned*>(P.err) != 0) return;  // sticky error pending
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint64_t R = P.info[0];
@@ -304,9 +374,9 @@ __global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const __grid_cons
         }
         const uint64_t ku = u - P.unit_first[lo];
         if (P.desc[lo].w == 4)
-            fold_unit<4>(P, lo, ku, s_carry[wid], lane, bad);
+            fold_unit<4>(P, lo, ku, s_carry[wid], s_imask[wid], lane, bad);
         else
-            fold_unit<2>(P, lo, ku, s_carry[wid], lane, bad);
+            fold_unit<2>(P, lo, ku, s_carry[wid], s_imask[wid], lane, bad);
         if (__any_sync(0xffffffffu, bad)) {  // malformed record: state unspecified
             if (lane == 0) tc_set_err(P.err, TC_ERR_CORRUPT);
             return;

@@ -237,30 +237,45 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
     }
     const bool sparse = total * W <= kSpillBytes;
 
-    // ---- sparse block: pack the new words into the block's spill slot now ----
+    // ---- sparse block: pack the new words into the block's spill slot now (index mode: and
+    //      their u16 in-tile positions in the second half of the slot) ----
+    const bool imode = P.index_mode != 0;
+    const size_t slot_bytes = imode ? 2 * kSpillBytes : kSpillBytes;
     if (sparse && total) {
-        word_t* slot = reinterpret_cast<word_t*>(P.spill + I.b * kSpillBytes) + woff;
+        word_t* slot = reinterpret_cast<word_t*>(P.spill + I.b * slot_bytes) + woff;
+        uint16_t* islot = reinterpret_cast<uint16_t*>(P.spill + I.b * slot_bytes + kSpillBytes) + woff;
+        const uint32_t tmask = P.T - 1;
         if (__shfl_sync(0xffffffffu, inc, 31) <= 96u) {
             // few changes in this warp's range: each lane packs its own mask word's words
             uint32_t wv = mine;
             uint32_t k = pre;
+            const uint32_t q0 = (mw0 + lane) * 32;
             while (wv) {
                 const uint32_t b = __ffs(wv) - 1;
                 wv &= wv - 1;
-                slot[k++] = scur[(mw0 + lane) * 32 + b];
+                slot[k] = scur[q0 + b];
+                if (imode) islot[k] = static_cast<uint16_t>((I.p0 + q0 + b) & tmask);
+                ++k;
             }
         } else {
-        uint32_t nz = __ballot_sync(0xffffffffu, mine != 0);
-        const uint32_t lt = (1u << lane) - 1u;
-        while (nz) {
-            const int src = __ffs(nz) - 1;
-            nz &= nz - 1;
-            const uint32_t bb = __shfl_sync(0xffffffffu, mine, src);
-            const uint32_t o = __shfl_sync(0xffffffffu, pre, src);
-            if ((bb >> lane) & 1u) slot[o + __popc(bb & lt)] = scur[(mw0 + src) * 32 + lane];
-        }
+            uint32_t nz = __ballot_sync(0xffffffffu, mine != 0);
+            const uint32_t lt = (1u << lane) - 1u;
+            while (nz) {
+                const int src = __ffs(nz) - 1;
+                nz &= nz - 1;
+                const uint32_t bb = __shfl_sync(0xffffffffu, mine, src);
+                const uint32_t o = __shfl_sync(0xffffffffu, pre, src);
+                if ((bb >> lane) & 1u) {
+                    const uint32_t q = (mw0 + src) * 32 + lane;
+                    slot[o + __popc(bb & lt)] = scur[q];
+                    if (imode) islot[o + __popc(bb & lt)] = static_cast<uint16_t>((I.p0 + q) & tmask);
+                }
+            }
         }
     }
+    // index mode, dense block: its mask words go to the staging area (kernel B packs from them)
+    if (imode && !sparse && lane < static_cast<int>(MPW))
+        P.mstage[I.b * kMaskStageWords + mw0 + lane] = mine;
 
     // ---- record start of the chunk: prefetched by thread 0 at block start; only the first
     //      blocks of a chunk can find it unpublished and wait (block-uniform branch) ----
@@ -273,15 +288,15 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
     }
     rs &= ~1ull;
 
-    // ---- mask words and block-relative tile_off entries, in their final place ----
+    // ---- mask words (mask mode) and block-relative tile_off entries, in their final place ----
     {
         uint8_t* rec = P.out + rs;
         const uint64_t n_mask = cdiv(I.m, 32);
         uint32_t* gmask = reinterpret_cast<uint32_t*>(rec + kHdrBytes);
-        uint32_t* gtoff = reinterpret_cast<uint32_t*>(rec + kHdrBytes + pad16(4 * n_mask));
+        uint32_t* gtoff = reinterpret_cast<uint32_t*>(rec + (imode ? index_toff_off() : kHdrBytes + pad16(4 * n_mask)));
         const uint32_t p = I.p0 + (mw0 + lane) * 32;
         if (lane < static_cast<int>(MPW) && p < I.m) {
-            gmask[(I.p0 >> 5) + mw0 + lane] = mine;
+            if (!imode) gmask[(I.p0 >> 5) + mw0 + lane] = mine;
             if ((p & (P.T - 1)) == 0) gtoff[p / P.T] = woff + pre;  // kernel B adds the block prefix
         }
     }
@@ -298,10 +313,11 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
             const uint64_t count = (old & kAccCountMask) + total;
             const uint64_t n_mask = cdiv(I.m, 32);
             const uint64_t n_tiles = cdiv(I.m, P.T);
-            const uint64_t rec_total = record_bytes(I.m, P.T, W, count);
+            const uint64_t rec_total = imode ? record_bytes_index(I.m, P.T, W, count) : record_bytes(I.m, P.T, W, count);
             uint8_t* rec = P.out + rs;
             uint64_t* h = reinterpret_cast<uint64_t*>(rec);
-            h[0] = 0x31444354ull /* "TCD1" */ | (1ull << 32) | (static_cast<uint64_t>(W) << 48) | (1ull << 56);
+            h[0] = 0x31444354ull /* "TCD1" */ | (1ull << 32) | (static_cast<uint64_t>(W) << 48) |
+                   ((imode ? 3ull : 1ull) << 56);
             h[1] = static_cast<uint64_t>(P.T) | (static_cast<uint64_t>(P.seg[I.seg].seg_id) << 32);
             h[2] = P.seg[I.seg].word_base + I.chunk_off;
             h[3] = I.m;
@@ -309,12 +325,21 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
             h[5] = P.version;
             h[6] = P.ref_version;
             h[7] = rec_total;
-            uint32_t* gmask = reinterpret_cast<uint32_t*>(rec + kHdrBytes);
-            for (uint64_t x = n_mask; x < pad16(4 * n_mask) / 4; ++x) gmask[x] = 0;
-            uint32_t* gtoff = reinterpret_cast<uint32_t*>(rec + kHdrBytes + pad16(4 * n_mask));
+            uint32_t* gtoff;
+            uint8_t* gval;
+            if (imode) {
+                gtoff = reinterpret_cast<uint32_t*>(rec + index_toff_off());
+                uint8_t* gidx = rec + index_idx_off(I.m, P.T);
+                for (uint64_t x = 2 * count; x < pad16(2 * count); ++x) gidx[x] = 0;
+                gval = rec + index_val_off(I.m, P.T, count);
+            } else {
+                uint32_t* gmask = reinterpret_cast<uint32_t*>(rec + kHdrBytes);
+                for (uint64_t x = n_mask; x < pad16(4 * n_mask) / 4; ++x) gmask[x] = 0;
+                gtoff = reinterpret_cast<uint32_t*>(rec + kHdrBytes + pad16(4 * n_mask));
+                gval = rec + record_fixed_bytes(I.m, P.T);
+            }
             gtoff[n_tiles] = static_cast<uint32_t>(count);
             for (uint64_t x = n_tiles + 1; x < pad16(4 * (n_tiles + 1)) / 4; ++x) gtoff[x] = 0;
-            uint8_t* gval = rec + record_fixed_bytes(I.m, P.T);
             for (uint64_t x = W * count; x < pad16(W * count); ++x) gval[x] = 0;
             const unsigned long long next = rs + rec_total;
             st_relaxed(&P.rstart[I.chunk + 1], next | 1ull);
@@ -402,10 +427,17 @@ template <int W>
 __device__ __forceinline__ void emit_dense(const EncParams& P, const BlockInfo& I, uint32_t info,
                                            unsigned long long prefix, int lane) {
     using word_t = typename Word<W>::T;
+    const bool imode = P.index_mode != 0;
     const unsigned long long rs = ld_relaxed(&P.rstart[I.chunk]) & ~1ull;
     uint8_t* rec = P.out + rs;
-    const uint32_t* gmask = reinterpret_cast<const uint32_t*>(rec + kHdrBytes);
-    word_t* gval = reinterpret_cast<word_t*>(rec + record_fixed_bytes(I.m, P.T)) + prefix;
+    // mask words: from the record (mask mode) or the staging area (index mode, block-relative)
+    const uint32_t* gmask = imode ? P.mstage + I.b * kMaskStageWords - (I.p0 >> 5)
+                                  : reinterpret_cast<const uint32_t*>(rec + kHdrBytes);
+    const uint64_t ccount = P.chunk_acc[I.chunk] & kAccCountMask;
+    word_t* gval = reinterpret_cast<word_t*>(rec + (imode ? index_val_off(I.m, P.T, ccount)
+                                                          : record_fixed_bytes(I.m, P.T))) + prefix;
+    uint16_t* gidx = reinterpret_cast<uint16_t*>(rec + index_idx_off(I.m, P.T)) + prefix;
+    const uint32_t tmask = P.T - 1;
     const EncSeg& S = P.seg[I.seg];
     const word_t* gcur = reinterpret_cast<const word_t*>(S.cur) + I.chunk_off + I.p0;
     const uint32_t nmw = (I.nb + 31) / 32;
@@ -438,6 +470,7 @@ __device__ __forceinline__ void emit_dense(const EncParams& P, const BlockInfo& 
                     if ((bb >> lane) & 1u) {
                         v[q] = ldg_word(gcur + (q0 + src) * 32 + lane);
                         d[q] = o + __popc(bb & lt);
+                        if (imode) gidx[d[q]] = static_cast<uint16_t>((I.p0 + (q0 + src) * 32 + lane) & tmask);
                     }
                 }
             }
@@ -478,7 +511,9 @@ __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __gri
     for (int k = 0; k < static_cast<int>(kWarps); ++k) wp += k < wid ? s_warp[k] : 0u;
 
     // ---- per block (one thread each): in-chunk prefix, tile_off entries, destination ----
+    const bool imode = P.index_mode != 0;
     uint8_t* dst = nullptr;
+    uint8_t* idst = nullptr;
     const uint8_t* src = nullptr;
     uint32_t w = 4;
     bool dense = false;
@@ -489,7 +524,7 @@ __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __gri
         const unsigned long long rs = ld_relaxed(&P.rstart[I.chunk]) & ~1ull;
         uint8_t* rec = P.out + rs;
         const uint64_t n_mask = cdiv(I.m, 32);
-        uint32_t* gtoff = reinterpret_cast<uint32_t*>(rec + kHdrBytes + pad16(4 * n_mask));
+        uint32_t* gtoff = reinterpret_cast<uint32_t*>(rec + (imode ? index_toff_off() : kHdrBytes + pad16(4 * n_mask)));
         const uint32_t pr = static_cast<uint32_t>(prefix);
         const uint32_t B = I.w == 4 ? kEncBlockWords4 : kEncBlockWords2;
         if (I.nb) {  // kernel A wrote the tile_off entries of the block block-relative
@@ -500,8 +535,15 @@ __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __gri
                 for (uint32_t t = 0; t < n_t; ++t) gtoff[I.p0 / P.T + t] += pr;
             }
         }
-        dst = rec + record_fixed_bytes(I.m, P.T) + prefix * I.w;
-        src = P.spill + b * kSpillBytes;
+        if (imode) {
+            const uint64_t ccount = P.chunk_acc[I.chunk] & kAccCountMask;
+            dst = rec + index_val_off(I.m, P.T, ccount) + prefix * I.w;
+            idst = rec + index_idx_off(I.m, P.T) + prefix * 2;
+            src = P.spill + b * (2 * kSpillBytes);
+        } else {
+            dst = rec + record_fixed_bytes(I.m, P.T) + prefix * I.w;
+            src = P.spill + b * kSpillBytes;
+        }
         dense = (info & kDenseFlag) != 0 && c != 0;
     }
 
@@ -548,6 +590,30 @@ __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __gri
 #pragma unroll
         for (int q = 0; q < 4; ++q)
             for (uint32_t i = 64 + lane; i < cn[q]; i += 32) copy_words(dq[q], sq[q], wq[q], i);
+        if (imode) {  // the u16 in-tile positions, same batching
+            uint16_t iv[4][2];
+            uint8_t* iq[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int sl = bl[q] < 0 ? 0 : bl[q];
+                iq[q] = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(idst), sl));
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const uint32_t i = lane + 32 * k;
+                    iv[q][k] = i < cn[q] ? static_cast<uint16_t>(__ldg(reinterpret_cast<const unsigned short*>(sq[q] + kSpillBytes) + i)) : 0;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const uint32_t i = lane + 32 * k;
+                    if (i < cn[q]) reinterpret_cast<uint16_t*>(iq[q])[i] = iv[q][k];
+                }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                for (uint32_t i = 64 + lane; i < cn[q]; i += 32) copy_words(iq[q], sq[q] + kSpillBytes, 2, i);
+        }
     }
 
     // ---- dense blocks: re-read mask + cur, pack in index order (a warp per block) ----

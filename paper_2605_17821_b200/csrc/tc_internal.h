@@ -30,6 +30,16 @@ __host__ __device__ inline uint64_t record_fixed_bytes(uint64_t m, uint32_t T) {
 __host__ __device__ inline uint64_t record_bytes(uint64_t m, uint32_t T, uint32_t w, uint64_t count) {
     return record_fixed_bytes(m, T) + pad16(uint64_t(w) * count);
 }
+// index mode (flags bit1): header | tile_off | idx u16[count] | values
+__host__ __device__ inline uint64_t index_toff_off() { return kHdrBytes; }
+__host__ __device__ inline uint64_t index_idx_off(uint64_t m, uint32_t T) { return kHdrBytes + pad16(4 * (cdiv(m, T) + 1)); }
+__host__ __device__ inline uint64_t index_val_off(uint64_t m, uint32_t T, uint64_t count) {
+    return index_idx_off(m, T) + pad16(2 * count);
+}
+__host__ __device__ inline uint64_t record_bytes_index(uint64_t m, uint32_t T, uint32_t w, uint64_t count) {
+    return index_val_off(m, T, count) + pad16(uint64_t(w) * count);
+}
+constexpr uint32_t kIndexMaxT = 8192;
 
 // ---- per-segment launch description of one encode (kernel parameter, no table) ----
 struct EncSeg {
@@ -69,8 +79,12 @@ struct EncParams {
     unsigned long long* cbase;        // [total_chunks] exclusive prefix of the chunk counts
     uint8_t* spill;                   // [total_blocks] slots of kSpillBytes: packed values
     unsigned int* err;                // sticky error word
+    uint32_t* mstage;                 // index mode: [total_blocks][kMaskStageWords] mask words
     int advance_ref;
+    int index_mode;
 };
+
+constexpr uint32_t kMaskStageWords = 256;  // mask words of one block (8192 16-bit words max)
 
 constexpr uint32_t kEmitGroup = 256;        // blocks per emit CTA / per group sum
 constexpr uint32_t kSpillBytes = 4096;      // per-block spill slot (1/4 of a block's words)
@@ -80,7 +94,8 @@ constexpr unsigned long long kAccCountMask = (1ull << kAccDoneShift) - 1;
 
 // ---- fold descriptors ----
 struct FoldRec {           // one record of one diff, as located by the walker
-    const uint8_t* mask;
+    const uint8_t* mask;   // mask mode (nullptr in index mode)
+    const uint8_t* idx;    // index mode: u16 in-tile positions (nullptr in mask mode)
     const uint8_t* toff;
     const uint8_t* values;
     uint64_t chunk_off;

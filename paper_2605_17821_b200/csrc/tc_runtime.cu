@@ -19,6 +19,9 @@ struct tc_ctx {
     // encode spill slots: kSpillBytes per scan block (packed new words of sparse blocks)
     void* spill = nullptr;
     size_t spill_bytes = 0;
+    // index-mode mask staging: kMaskStageWords per scan block
+    void* mstage = nullptr;
+    size_t mstage_bytes = 0;
     // fold scratch: desc [nrec*cap] | unit_first [cap+1] | info [2]
     void* fold = nullptr;
     size_t fold_bytes = 0;
@@ -51,6 +54,8 @@ static void default_opts(const tc_encode_opts* in, tc_encode_opts* out) {
         out->tile_words = 4096;
         out->advance_ref = 1;
         out->chunk_words = 1ull << 28;
+        out->index_mode = 0;
+        out->reserved = 0;
     }
 }
 
@@ -59,6 +64,8 @@ static tc_status check_opts(const tc_encode_opts& o) {
         return fail(TC_ERR_INVALID, "tile_words must be a power of two in [32, 65536]");
     if (o.chunk_words == 0 || o.chunk_words % o.tile_words != 0 || o.chunk_words > kMaxChunkWords)
         return fail(TC_ERR_INVALID, "chunk_words must be a positive multiple of tile_words and <= 2^31-1");
+    if (o.index_mode > 1 || o.reserved != 0) return fail(TC_ERR_INVALID, "index_mode must be 0 or 1, reserved 0");
+    if (o.index_mode && o.tile_words > kIndexMaxT) return fail(TC_ERR_INVALID, "index mode requires tile_words <= 8192");
     return TC_OK;
 }
 
@@ -152,6 +159,7 @@ tc_status tc_ctx_destroy(tc_ctx* c) {
     if (c->enc) cudaFree(c->enc);
     if (c->fold) cudaFree(c->fold);
     if (c->spill) cudaFree(c->spill);
+    if (c->mstage) cudaFree(c->mstage);
     if (c->err) cudaFree(c->err);
     delete c;
     return TC_OK;
@@ -189,7 +197,8 @@ tc_status tc_diff_bound(const tc_segment* segs, int nseg, const tc_encode_opts* 
         uint64_t off = 0;
         do {
             const uint64_t m = n - off < o.chunk_words ? n - off : o.chunk_words;
-            tot += record_bytes(m, o.tile_words, static_cast<uint32_t>(w), m);
+            tot += o.index_mode ? record_bytes_index(m, o.tile_words, static_cast<uint32_t>(w), m)
+                                : record_bytes(m, o.tile_words, static_cast<uint32_t>(w), m);
             off += m;
         } while (off < n);
     }
@@ -246,6 +255,7 @@ static tc_status encode_impl(tc_ctx* ctx, const SegSpec* specs, int nseg, const 
     P.out = static_cast<uint8_t*>(out);
     P.out_bytes = out_bytes;
     P.advance_ref = o.advance_ref ? 1 : 0;
+    P.index_mode = o.index_mode ? 1 : 0;
     P.err = ctx->err;
 
     const uint64_t groups = cdiv(blocks, kEmitGroup);
@@ -262,8 +272,13 @@ static tc_status encode_impl(tc_ctx* ctx, const SegSpec* specs, int nseg, const 
     const size_t need = w_cbase + 8 * chunks;
     st = ensure(&ctx->enc, &ctx->enc_bytes, need, s);
     if (st != TC_OK) return st;
-    st = ensure(&ctx->spill, &ctx->spill_bytes, blocks * static_cast<size_t>(kSpillBytes), s);
+    st = ensure(&ctx->spill, &ctx->spill_bytes, blocks * static_cast<size_t>(kSpillBytes) * (o.index_mode ? 2 : 1), s);
     if (st != TC_OK) return st;
+    if (o.index_mode) {
+        st = ensure(&ctx->mstage, &ctx->mstage_bytes, blocks * static_cast<size_t>(kMaskStageWords) * 4, s);
+        if (st != TC_OK) return st;
+        P.mstage = static_cast<uint32_t*>(ctx->mstage);
+    }
     uint8_t* base = static_cast<uint8_t*>(ctx->enc);
     P.ticket = reinterpret_cast<unsigned long long*>(base + z_ticket);
     P.chunk_acc = reinterpret_cast<unsigned long long*>(base + z_ctot);
@@ -287,7 +302,7 @@ static uint64_t range_bound(uint64_t n, uint32_t w, const tc_encode_opts& o, uin
     for (uint64_t c = c0; c < c0 + nc && c < total_chunks; ++c) {
         const uint64_t off = c * o.chunk_words;
         const uint64_t m = n > off ? (n - off < o.chunk_words ? n - off : o.chunk_words) : 0;
-        tot += record_bytes(m, o.tile_words, w, m);
+        tot += o.index_mode ? record_bytes_index(m, o.tile_words, w, m) : record_bytes(m, o.tile_words, w, m);
     }
     return tot;
 }

@@ -31,7 +31,8 @@ class Segment(ctypes.Structure):
 
 
 class EncodeOpts(ctypes.Structure):
-    _fields_ = [("tile_words", u32), ("advance_ref", u32), ("chunk_words", u64)]
+    _fields_ = [("tile_words", u32), ("advance_ref", u32), ("chunk_words", u64), ("index_mode", u32),
+                ("reserved", u32)]
 
 
 class TcError(RuntimeError):
@@ -113,8 +114,8 @@ def _stream(stream) -> int | None:
     return int(stream)
 
 
-def _opts(tile_words=4096, chunk_words=1 << 28, advance_ref=True) -> EncodeOpts:
-    return EncodeOpts(tile_words, 1 if advance_ref else 0, chunk_words)
+def _opts(tile_words=4096, chunk_words=1 << 28, advance_ref=True, index_mode=False) -> EncodeOpts:
+    return EncodeOpts(tile_words, 1 if advance_ref else 0, chunk_words, 1 if index_mode else 0, 0)
 
 
 def _wb(t: torch.Tensor) -> int:
@@ -143,9 +144,9 @@ def layout_segments(sizes, word_bytes):
     return arr
 
 
-def diff_bound(sizes, word_bytes, tile_words=4096, chunk_words=1 << 28) -> int:
+def diff_bound(sizes, word_bytes, tile_words=4096, chunk_words=1 << 28, index_mode=False) -> int:
     segs = layout_segments(sizes, word_bytes)
-    o = _opts(tile_words, chunk_words)
+    o = _opts(tile_words, chunk_words, True, index_mode)
     out = u64(0)
     _check(LIB.tc_diff_bound(segs, len(sizes), ctypes.byref(o), ctypes.byref(out)), "tc_diff_bound")
     return out.value
@@ -185,19 +186,19 @@ class Ctx:
 
 
 def diff_encode(ctx: Ctx, ref, cur, out: torch.Tensor, out_bytes: torch.Tensor, version: int, ref_version: int,
-                tile_words=4096, chunk_words=1 << 28, advance_ref=True, stream=None):
+                tile_words=4096, chunk_words=1 << 28, advance_ref=True, stream=None, index_mode=False):
     """Enqueue tc_diff_encode.  ``out`` uint8 CUDA tensor, ``out_bytes`` int64 CUDA tensor [1]."""
     segs = segments(ref, cur)
-    o = _opts(tile_words, chunk_words, advance_ref)
+    o = _opts(tile_words, chunk_words, advance_ref, index_mode)
     _check(LIB.tc_diff_encode(ctx.h, segs, len(ref), ctypes.byref(o), version, ref_version, out.data_ptr(),
                               out.numel() * out.element_size(), out_bytes.data_ptr(), _stream(stream)),
            "tc_diff_encode")
 
 
 def diff_bound_range(n_words: int, word_bytes: int, first_chunk: int, n_chunks: int, tile_words=4096,
-                     chunk_words=1 << 28) -> int:
+                     chunk_words=1 << 28, index_mode=False) -> int:
     seg = Segment(None, None, int(n_words), int(word_bytes), 0)
-    o = _opts(tile_words, chunk_words)
+    o = _opts(tile_words, chunk_words, True, index_mode)
     out = u64(0)
     _check(LIB.tc_diff_bound_range(ctypes.byref(seg), ctypes.byref(o), first_chunk, n_chunks, ctypes.byref(out)),
            "tc_diff_bound_range")
@@ -206,11 +207,11 @@ def diff_bound_range(n_words: int, word_bytes: int, first_chunk: int, n_chunks: 
 
 def diff_encode_range(ctx: Ctx, ref: torch.Tensor, cur: torch.Tensor, segment_id: int, first_chunk: int,
                       n_chunks: int, out: torch.Tensor, out_bytes: torch.Tensor, version: int, ref_version: int,
-                      tile_words=4096, chunk_words=1 << 28, advance_ref=True, stream=None):
+                      tile_words=4096, chunk_words=1 << 28, advance_ref=True, stream=None, index_mode=False):
     """Enqueue tc_diff_encode_range (the records of chunks [first_chunk, first_chunk+n_chunks) of
     one segment, byte-identical to that part of the full encode)."""
     seg = segments([ref], [cur])
-    o = _opts(tile_words, chunk_words, advance_ref)
+    o = _opts(tile_words, chunk_words, advance_ref, index_mode)
     _check(LIB.tc_diff_encode_range(ctx.h, seg, segment_id, ctypes.byref(o), first_chunk, n_chunks, version,
                                     ref_version, out.data_ptr(), out.numel() * out.element_size(),
                                     out_bytes.data_ptr(), _stream(stream)), "tc_diff_encode_range")

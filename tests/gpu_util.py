@@ -21,14 +21,15 @@ def to_np(t: torch.Tensor) -> np.ndarray:
 
 
 def gpu_encode(ctx, ref_np, cur_np, tile_words=4096, chunk_words=1 << 28, advance_ref=True, version=1,
-               ref_version=0):
+               ref_version=0, index_mode=False):
     """Returns (record bytes as numpy uint8, ref-after numpy list, out_bytes)."""
     ref = [to_dev(a) for a in ref_np]
     cur = [to_dev(a) for a in cur_np]
-    cap = tc.diff_bound([a.size for a in ref_np], [a.itemsize for a in ref_np], tile_words, chunk_words)
+    cap = tc.diff_bound([a.size for a in ref_np], [a.itemsize for a in ref_np], tile_words, chunk_words, index_mode)
     out = torch.full((cap + 64,), 0xAB, dtype=torch.uint8, device="cuda")  # poison: pads must be written
     ob = torch.zeros(1, dtype=torch.int64, device="cuda")
-    tc.diff_encode(ctx, ref, cur, out, ob, version, ref_version, tile_words, chunk_words, advance_ref)
+    tc.diff_encode(ctx, ref, cur, out, ob, version, ref_version, tile_words, chunk_words, advance_ref,
+                   index_mode=index_mode)
     ctx.check()
     n = int(ob.item())
     return out[:n].cpu().numpy(), [to_np(r) for r in ref], n

@@ -263,3 +263,91 @@ def test_range_encode_concatenates_to_full(ctx, tco, advance):
     assert got.size == n_full and np.array_equal(got, full)
     for a, b in zip(refs, ref_full):
         assert np.array_equal(to_np(a), b)
+
+
+# ------------------------------------------------------------ index mode -------------
+IDX_CASES = [c for c in CASES if c[3] <= 8192]
+
+
+@pytest.mark.parametrize("sizes,wb,f,T,C", IDX_CASES)
+def test_index_mode_encode_matches_oracle_bytes(ctx, tco, sizes, wb, f, T, C):
+    pairs = [rand_pair(n, w, f) for n, w in zip(sizes, wb)]
+    ref = [p[0] for p in pairs]
+    cur = [p[1] for p in pairs]
+    ref_o = [r.copy() for r in ref]
+    rc, exp = tco.encode(ref_o, cur, tile_words=T, chunk_words=C, version=9, ref_version=8, index_mode=True)
+    assert rc == 0
+    got, ref_after, nbytes = gpu_encode(ctx, ref, cur, T, C, True, 9, 8, index_mode=True)
+    assert nbytes == exp.size and np.array_equal(got, exp), "index-mode record bytes differ from the oracle"
+    assert all(np.array_equal(a, b) for a, b in zip(ref_after, ref_o))
+
+
+@pytest.mark.parametrize("N", [1, 3, 8, 10])
+@pytest.mark.parametrize("layout", [
+    ([30011, 30011, 30011, 30011], [2, 4, 4, 4], 4096, 1 << 28),
+    ([20000, 9000], [4, 2], 64, 1024),
+    ([40000], [4], 8192, 16384),
+])
+def test_index_and_mixed_mode_fold_matches_oracle(ctx, tco, N, layout):
+    sizes, wb, T, C = layout
+    states = [synth.state(sizes, wb, 13, v, 0.03) for v in range(N + 1)]
+    ref = [a.copy() for a in states[0]]
+    diffs = []
+    for v in range(1, N + 1):
+        rc, d = tco.encode(ref, states[v], tile_words=T, chunk_words=C, version=v, ref_version=v - 1,
+                           index_mode=(v % 3 != 0))
+        assert rc == 0
+        diffs.append(d)
+    st_o = [a.copy() for a in states[0]]
+    rc, ver = tco.fold(st_o, 0, diffs)
+    assert rc == 0
+    rc, st_g = gpu_fold(ctx, states[0], 0, diffs)
+    assert rc == tc.OK
+    for a, b, c in zip(st_g, st_o, states[N]):
+        assert np.array_equal(a, b) and np.array_equal(a, c)
+
+
+def test_index_mode_gpu_chain_dense_and_sparse(ctx, tco):
+    """GPU index-mode encode over sparse and dense blocks, folded on the GPU."""
+    sizes, wb = [50000, 50000], [2, 4]
+    for f in (0.005, 0.7):
+        states = [synth.state(sizes, wb, 31, v, f) for v in range(4)]
+        ref = [a.copy() for a in states[0]]
+        diffs = []
+        for v in range(1, 4):
+            d, ref, _ = gpu_encode(ctx, ref, states[v], version=v, ref_version=v - 1, index_mode=True)
+            diffs.append(d)
+        rc, st_g = gpu_fold(ctx, states[0], 0, diffs)
+        assert rc == tc.OK and all(np.array_equal(a, b) for a, b in zip(st_g, states[3]))
+
+
+def test_index_tamper_gpu(ctx, tco):
+    ref, cur = rand_pair(20000, 4, 0.1)
+    rc, rec = tco.encode([ref.copy()], [cur], tile_words=256, version=1, ref_version=0, index_mode=True)
+    nt = -(-20000 // 256)
+    p = 64 + ((4 * (nt + 1) + 15) // 16) * 16
+    bad = rec.copy()
+    bad[p: p + 2] = np.frombuffer(np.uint16(300).tobytes(), np.uint8)  # outside a 256-word tile
+    rc, _ = gpu_fold(ctx, [ref], 0, [bad])
+    assert rc == tc.ERR_CORRUPT == tco.fold([ref.copy()], 0, [bad])[0]
+    bad = rec.copy()
+    bad[7] = 2
+    rc, st = gpu_fold(ctx, [ref], 0, [bad])
+    assert rc == tc.ERR_CORRUPT and np.array_equal(st[0], ref)
+
+
+def test_index_mode_range_encode(ctx, tco):
+    sizes, wb, T, C = [40001, 70003], [2, 4], 256, 8192
+    pairs = [rand_pair(n, w, 0.02) for n, w in zip(sizes, wb)]
+    full, _, n_full = gpu_encode(ctx, [p[0] for p in pairs], [p[1] for p in pairs], T, C, False, 3, 2, index_mode=True)
+    parts = []
+    for s, (n, w) in enumerate(zip(sizes, wb)):
+        ref_d, cur_d = to_dev(pairs[s][0]), to_dev(pairs[s][1])
+        for c0 in range(0, -(-n // C), 3):
+            cap = tc.diff_bound_range(n, w, c0, 3, T, C, index_mode=True)
+            out = torch.empty(cap, dtype=torch.uint8, device="cuda")
+            ob = torch.zeros(1, dtype=torch.int64, device="cuda")
+            tc.diff_encode_range(ctx, ref_d, cur_d, s, c0, 3, out, ob, 3, 2, T, C, False, index_mode=True)
+            ctx.check()
+            parts.append(out[: int(ob.item())].cpu().numpy())
+    assert np.array_equal(np.concatenate(parts), full)
