@@ -75,12 +75,13 @@ def record_counts(host_u8: np.ndarray, nbytes: int):
     while pos < nbytes:
         h = host_u8[pos: pos + 64]
         w = int(h[6])
+        flags = int(h[7])
         T = int(h[8:12].view("<u4")[0])
         seg = int(h[12:16].view("<u4")[0])
         m = int(h[24:32].view("<u8")[0])
         count = int(h[32:40].view("<u8")[0])
         total = int(h[56:64].view("<u8")[0])
-        out.append((seg, m, w, T, count, total))
+        out.append((seg, m, w, T, count, total, flags))
         pos += total
     return out
 
@@ -90,9 +91,12 @@ def algorithmic_bytes(recs, sector=False):
     (advance_ref) the changed ref words.  Fold (N=1): reads mask + tile_off + header + values,
     writes the changed state words.  Word-granular unless sector=True (32-byte sectors)."""
     enc = fold = 0
-    for seg, m, w, T, count, total in recs:
+    for seg, m, w, T, count, total, flags in recs:
         W = m * w
-        meta = 64 + 4 * -(-m // 32) + 4 * (-(-m // T) + 1)
+        if flags & 2:  # index mode: tile_off + u16 position per changed word instead of the mask
+            meta = 64 + 4 * (-(-m // T) + 1) + 2 * count
+        else:
+            meta = 64 + 4 * -(-m // 32) + 4 * (-(-m // T) + 1)
         vals = w * count
         if sector and m:
             f = count / m
@@ -203,10 +207,16 @@ def run_ours(args):
             R[s].copy_(X[s])
     s_comp.synchronize()
     cap = tc.diff_bound(sizes, wb, T, C)
+    cap_idx = tc.diff_bound(sizes, wb, T, C, index_mode=True)
+    allow_index = args.format in ("index", "adaptive") and T <= 8192
+    if allow_index:
+        cap = max(cap, cap_idx)
+    fixed_mask = tc.diff_bound(sizes, [w for w in wb], T, C) - sum(n * w for n, w in zip(sizes, wb))
     # records: the bound at f is ~ (f + 0.036) W; allocate the bound only when it fits
     free = torch.cuda.mem_get_info(dev)[0]
     est = int(min(cap, (args.f * 1.1 + 0.05) * W + (64 << 20)))
-    rec_cap = cap if 3 * cap < free - (2 << 30) else est
+    spill_need = (sum(sizes) // 4096 + 1) * (8192 + 1024)  # encode scratch (index mode: 8 KB spill + mask stage)
+    rec_cap = cap if 2 * cap + spill_need + (8 << 30) < free else est
     recs = [torch.empty(rec_cap, dtype=torch.uint8, device=dev) for _ in range(2)]
     recv = torch.empty(rec_cap, dtype=torch.uint8, device=dev) if comm else None
     # the encode kernel writes each record's length straight into mapped pinned memory, so the
@@ -218,7 +228,22 @@ def run_ours(args):
     host_ring = [tc.HostBuffer(host_cap) for _ in range(2)]  # libtc-pinned Tier-1 ring
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-    state = {"ref_version": 0, "rest_version": 0, "content": "X"}  # content of A and R
+    state = {"ref_version": 0, "rest_version": 0, "content": "X",  # content of A and R
+             "index": args.format == "index" and allow_index, "modes": []}
+    total_words = sum(sizes)
+    w_avg = W / total_words
+
+    def next_mode(nbytes, was_index):
+        """Adaptive record format (the paper adapts its payload format per tensor; here per
+        checkpoint from the last record's density): index mode iff 2 B per changed word beats
+        the 4 B per 32 words of the mask, i.e. fewer than 1/16 of the words changed."""
+        if args.format != "adaptive" or not allow_index:
+            return state["index"]
+        if was_index:
+            count = max(0.0, nbytes - (cap_idx - (2 + w_avg) * total_words)) / (2 + w_avg)
+        else:
+            count = max(0.0, nbytes - fixed_mask) / w_avg
+        return count * 16 < total_words
     done_ev = [None, None]  # (copy_done, comm_done) for each record slot
     n_ops = {"encode": [], "fold": [], "stage": [], "replicate": []}
     host_t = {"stage": [], "fold": []}
@@ -238,12 +263,17 @@ def run_ours(args):
                     n_ops["replicate"].append((r0p, r1p, nbp))
         e0, e1 = ev(), ev()
         e0.record(s_comp)
-        tc.diff_encode(ctx, A, cur, recs[slot], obytes[slot], v, v - 1, T, C, True, stream=s_comp)
+        use_index = state["index"]
+        tc.diff_encode(ctx, A, cur, recs[slot], obytes[slot], v, v - 1, T, C, True, stream=s_comp,
+                       index_mode=use_index)
         e1.record(s_comp)
         e1.synchronize()
         nbytes = int(ob_view[slot].item())
         if nbytes > min(rec_cap, host_cap):
             raise RuntimeError("record exceeds the staging buffers")
+        state["index"] = next_mode(nbytes, use_index)
+        if timed:
+            state["modes"].append("index" if use_index else "mask")
         # Tier-1: D2H into the pinned ring on the copy stream
         s_copy.wait_event(e1)
         c0, c1 = ev(), ev()
@@ -400,6 +430,8 @@ def run_ours(args):
                 "tile_words": T,
                 "chunk_words": C,
                 "fold_records_per_step": 1,
+                "record_format": args.format,
+                "record_modes_timed": sorted(set(state["modes"])),
                 "l2": f"no flush: every step streams {W / 1e9:.1f} GB of state per rank (> 126 MB L2)",
                 "step": "encode(advance_ref) + D2H stage + " + ("NCCL ring replicate + " if world > 1 else "")
                         + "fold onto restore replica",
@@ -494,7 +526,15 @@ def run_streaming(args, rank, world, local, dev):
         nch = max(1, -(-n // C))
         for c0 in range(0, nch, K):
             runs.append((i, c0, min(K, nch - c0)))
-    slot_cap = max(tc.diff_bound_range(sizes[i], wb[i], c0, k, T, C) for i, c0, k in runs)
+    allow_index = args.format in ("index", "adaptive") and T <= 8192
+    slot_cap = max(max(tc.diff_bound_range(sizes[i], wb[i], c0, k, T, C),
+                       tc.diff_bound_range(sizes[i], wb[i], c0, k, T, C, index_mode=True) if allow_index else 0)
+                   for i, c0, k in runs)
+    total_words = sum(sizes)
+    w_avg = W / total_words
+    fixed_mask = tc.diff_bound(sizes, wb, T, C) - W
+    fixed_idx = tc.diff_bound(sizes, wb, T, C, index_mode=True) - (2 + w_avg) * total_words
+    mode = {"index": args.format == "index" and allow_index}
     slots = [torch.empty(slot_cap, dtype=torch.uint8, device=dev) for _ in range(2)]
     rslots = [torch.empty(slot_cap, dtype=torch.uint8, device=dev) for _ in range(2)] if comm else None
     lens_h = tc.HostBuffer(8 * max(2, len(runs)))
@@ -512,7 +552,7 @@ def run_streaming(args, rank, world, local, dev):
             e0, e1 = ev(), ev()
             e0.record(s_comp)
             tc.diff_encode_range(ctx, X[i], Y[i], i, c0, k, slots[sl], lens[r_i: r_i + 1], 1, 0, T, C, False,
-                                 stream=s_comp)
+                                 stream=s_comp, index_mode=mode["index"])
             e1.record(s_comp)
             e1.synchronize()
             n = int(lens[r_i].item())
@@ -532,6 +572,12 @@ def run_streaming(args, rank, world, local, dev):
             pos += n
             if times is not None:
                 times.append((e0, e1))
+        if args.format == "adaptive" and allow_index:  # density of this checkpoint picks the next format
+            if mode["index"]:
+                count = max(0.0, pos - fixed_idx) / (2 + w_avg)
+            else:
+                count = max(0.0, pos - fixed_mask) / w_avg
+            mode["index"] = count * 16 < total_words
         return pos
 
     for _ in range(args.warmup):
@@ -581,6 +627,7 @@ def run_streaming(args, rank, world, local, dev):
                        "phi": synth.CONFIGS["cfg5"][0], "segments": [[n, w] for n, w in zip(sizes, wb)],
                        "state_bytes_per_rank": W, "f": args.f, "tile_words": T, "chunk_words": C,
                        "chunks_per_run": K, "runs": len(runs), "advance_ref": 0,
+                       "record_format": args.format, "record_mode_timed": "index" if mode["index"] else "mask",
                        "l2": f"no flush: {W / 1e9:.1f} GB of state per rank per step",
                        "parallelism": f"dp{world} shards of the 8-way split" if world > 1 else "1 GPU (shard 0 of 8)"},
             "end_to_end_checkpoint_s": round(ms_step / 1e3, 4),
@@ -629,7 +676,8 @@ def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nre
     union = 0
     with torch.cuda.stream(s):
         for x, z in zip(X, Z):
-            union += int((x != z).sum().item())
+            for a in range(0, x.numel(), 1 << 27):  # slices: no full-size temporaries
+                union += int((x[a: a + (1 << 27)] != z[a: a + (1 << 27)]).sum().item())
     hosts = [tc.HostBuffer(n) for n in lens]
     for h, r, n in zip(hosts, recs, lens):
         tc.stage_host(h, r, n, tc.D2H, stream=s)
@@ -750,7 +798,8 @@ def run_e2e(args, tc, ctx, dev, sizes, wb, X, Y, A, R, recs, obytes, host_ring, 
             tc.stage_host(ds, hs, hs.numel() * hs.element_size(), tc.H2D, stream=s_comp)
             h2d += hs.numel() * hs.element_size()
         v = state["ref_version"] + 1
-        tc.diff_encode(ctx, A, dst, recs[0], obytes[0], v, v - 1, T, C, True, stream=s_comp)
+        tc.diff_encode(ctx, A, dst, recs[0], obytes[0], v, v - 1, T, C, True, stream=s_comp,
+                       index_mode=state["index"])
         e = torch.cuda.Event()
         e.record(s_comp)
         e.synchronize()
@@ -886,6 +935,8 @@ def main():
     ap.add_argument("--chunk-words", type=int, default=1 << 28)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--timeline", action="store_true")
+    ap.add_argument("--format", default="adaptive", choices=["mask", "index", "adaptive"],
+                    help="record format: mask, index (u16 positions), or adaptive per step from density")
     ap.add_argument("--restore-chain", type=int, default=8, help="records in the chained-restore probe (0: off)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-baseline", type=int, default=1)
