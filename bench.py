@@ -386,7 +386,7 @@ def run_ours(args):
     restore = None
     if args.restore_chain > 0:
         restore = restore_bench(tc, ctx, X, Y, A, R, recs[0], sizes, wb, seed, p53, T, C, s_comp,
-                                args.restore_chain, args.structure, peak, dev)
+                                args.restore_chain, args.structure, peak, dev, state["index"])
         # put the step buffers back to the X / Y pair (X intact; Y, A, R were reused)
         with torch.cuda.stream(s_comp):
             for i in range(len(sizes)):
@@ -650,7 +650,8 @@ def run_streaming(args, rank, world, local, dev):
         dist.destroy_process_group()
 
 
-def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nrec, structure, peak, dev):
+def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nrec, structure, peak, dev,
+                  index_mode=False):
     """a7 at N = nrec (SURVEY §8(a), config 4's "chained restore of 8 differentials"): build a real
     chain of `nrec` incremental records (versions 1..nrec, each a fresh f-change set), then
     (1) fold all of them onto a base copy in one tc_diff_apply call (records resident in HBM), and
@@ -663,12 +664,17 @@ def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nre
             z.copy_(x)
             r_.copy_(x)
     ob = torch.zeros(1, dtype=torch.int64, device=dev)
-    recs, lens = [], []
+    recs, lens, counts = [], [], []
     with torch.cuda.stream(s):
         for v in range(1, nrec + 1):
             for i, z in enumerate(Z):
                 tc.synth_step(z, seed, i, 1000 + v, p53, structure, stream=s)
-            tc.diff_encode(ctx, ref, Z, tmp, ob, v, v - 1, T, C, True, stream=s)
+            cnt = 0
+            for r_, z in zip(ref, Z):
+                for a in range(0, z.numel(), 1 << 27):
+                    cnt += int((r_[a: a + (1 << 27)] != z[a: a + (1 << 27)]).sum().item())
+            counts.append(cnt)
+            tc.diff_encode(ctx, ref, Z, tmp, ob, v, v - 1, T, C, True, stream=s, index_mode=index_mode)
             s.synchronize()
             n = int(ob.item())
             recs.append(tmp[:n].clone())
@@ -714,14 +720,17 @@ def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nre
     meta = 0
     for n_, w_ in zip(sizes, wb):
         chunks = max(1, -(-n_ // C))
-        meta += nrec * (4 * -(-n_ // 32) + 4 * (-(-n_ // T) + chunks) + 64 * chunks)
+        meta += nrec * ((0 if index_mode else 4 * -(-n_ // 32)) + 4 * (-(-n_ // T) + chunks) + 64 * chunks)
+    if index_mode:  # every record's u16 positions: 2 bytes per changed word of each record
+        meta += 2 * sum(counts)
     wmean = sum(n_ * w_ for n_, w_ in zip(sizes, wb)) / sum(sizes)
     fold_b = meta + 2 * union * wmean
     fm = statistics.median(fold_ms)
     for h in hosts:
         h.free()
     W = sum(n_ * w_ for n_, w_ in zip(sizes, wb))
-    return {"records": nrec, "record_bytes_total": sum(lens), "union_changed_words": union,
+    return {"records": nrec, "record_format": "index" if index_mode else "mask",
+            "record_bytes_total": sum(lens), "union_changed_words": union,
             "fold_ms": round(fm, 4), "state_gbs": round(W / fm / 1e6, 1),
             "hbm_gbs_word": round(fold_b / fm / 1e6, 1), "frac_hbm_word": round(fold_b / fm / 1e6 / peak, 4),
             "tier1_restore_ms": round(statistics.median(t1_ms), 3),
