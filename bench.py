@@ -186,6 +186,8 @@ def run_ours(args):
     s_copy = torch.cuda.Stream(device=dev, priority=0)
     s_comm = torch.cuda.Stream(device=dev, priority=-1)  # NCCL CTAs get SM slots ahead of the encode
     ctx = tc.Ctx(local)
+    if args.fold_dense_permille is not None:
+        ctx.set_fold_dense_permille(args.fold_dense_permille)
     comm = tc.Comm(rank, world, local) if world > 1 else None
     rep_pool = None
     if comm is not None:
@@ -512,6 +514,8 @@ def run_streaming(args, rank, world, local, dev):
     s_copy = torch.cuda.Stream(device=dev)
     s_comm = torch.cuda.Stream(device=dev)
     ctx = tc.Ctx(local)
+    if args.fold_dense_permille is not None:
+        ctx.set_fold_dense_permille(args.fold_dense_permille)
     comm = tc.Comm(rank, world, local) if world > 1 else None
     X = [torch.empty(n, dtype=torch.int16 if w == 2 else torch.int32, device=dev) for n, w in zip(sizes, wb)]
     Y = [torch.empty(n, dtype=torch.int16 if w == 2 else torch.int32, device=dev) for n, w in zip(sizes, wb)]
@@ -948,6 +952,8 @@ def main():
                     help="record format: mask, index (u16 positions), or adaptive per step from density")
     ap.add_argument("--restore-chain", type=int, default=8, help="records in the chained-restore probe (0: off)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--fold-dense-permille", type=int, default=None,
+                    help="restore strategy threshold (tc_ctx_set_fold_dense_permille); default: libtc's")
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--sample-words", type=int, default=1 << 25)
     ap.add_argument("--oracle-steps", type=int, default=3)

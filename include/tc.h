@@ -123,6 +123,12 @@ tc_status tc_ctx_destroy(tc_ctx* ctx);
 tc_status tc_ctx_check(tc_ctx* ctx, tc_stream stream);
 /* Number of kernel launches libtc has enqueued through this ctx since creation. */
 uint64_t tc_ctx_launches(const tc_ctx* ctx);
+/* Restore strategy threshold: tc_diff_apply folds a chunk by streaming it
+ * through shared memory (full-line writes) when the N records together change more than
+ * permille/1000 of its words, and by scattering the winning words otherwise.  Both produce
+ * identical state.  Default 30 (3 %); 0 = always stream; UINT32_MAX = always scatter.
+ * Takes effect for later tc_diff_apply calls.  Errors: TC_ERR_INVALID (NULL ctx). */
+tc_status tc_ctx_set_fold_dense_permille(tc_ctx* ctx, uint32_t permille);
 
 /* ----------------------------------------------------------------------- SAVE ---- */
 /* Worst-case diff bytes for this shard layout (every word changed); host only.

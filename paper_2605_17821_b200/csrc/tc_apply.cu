@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include "tc_internal.h"
+#include "tc_ptx.cuh"
 
 namespace tc {
 
@@ -144,9 +145,14 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
             uint64_t u = 0;
             for (unsigned r = 0; r < R; ++r) {
                 P.unit_first[r] = u;
-                const FoldRec& a = P.desc[r];
+                FoldRec& a = P.desc[r];
                 const uint64_t U = a.T > kFoldWords ? a.T : kFoldWords;
                 u += a.m ? cdiv(a.m, U) : 0;
+                // dense chunk: the changed words of the N records cover enough sectors that
+                // streaming the whole chunk through shared memory beats scattered writes
+                uint64_t sum = 0;
+                for (int k = 0; k < P.nrec; ++k) sum += P.desc[static_cast<size_t>(k) * P.cap + r].count;
+                a.dense = sum * 1000ull > static_cast<uint64_t>(a.m) * P.dense_permille ? 1u : 0u;
             }
             P.unit_first[R] = u;
             P.info[0] = R;
@@ -372,6 +378,11 @@ __global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const __grid_cons
             const uint64_t mid = (lo + hi) >> 1;
             if (P.unit_first[mid] <= u) lo = mid; else hi = mid;
         }
+        if (P.desc[lo].dense) {  // folded by fold_dense_kernel: jump past the chunk
+            const uint64_t nxt = P.unit_first[lo + 1];
+            u += (nxt - u + nwarps - 1) / nwarps * nwarps - nwarps;
+            continue;
+        }
         const uint64_t ku = u - P.unit_first[lo];
         if (P.desc[lo].w == 4)
             fold_unit<4>(P, lo, ku, s_carry[wid], s_imask[wid], lane, bad);
@@ -382,6 +393,418 @@ __global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const __grid_cons
             return;
         }
     }
+}
+
+// ------------------------------------------------------------- dense fold ----------
+// Chunks whose N records together change more than dense_permille of the words (the walker's
+// `dense` flag) are folded by streaming: at union densities of a few percent most 32-byte
+// sectors hold a changed word, and scattered partial-sector writes cost a DRAM read-modify-
+// write each (the scatter fold of the cfg2 N = 8 chain: 16-17 ms).
+// One warp per CTA; per sub-unit of kDSub words (lane l owns mask words kMW*l .. kMW*l+kMW-1):
+//   1. one TMA bulk copy brings the sub-unit's state into a shared tile (mbarrier);
+//   2. for a batch of up to kDBatch records, all in flight together: the mask words (index
+//      mode: a 64-entry window of positions) and a kWin-byte window of the value run, which
+//      starts at the record's running value count (known before the mask arrives);
+//   3. popcount-scan the masks to value offsets, check tile_off;
+//   4. expand each record's values into the tile oldest -> newest (newest wins) from the
+//      staged window, or - when the run is longer than the window - straight from the record;
+//   5. each lane writes its touched 32-word lines back with TMA bulk stores (whole lines: no
+//      partial-sector writes); they drain while the next sub-unit loads.
+constexpr uint32_t kDenseThreads = 32;
+constexpr uint32_t kDSub = 4096;
+constexpr uint32_t kMW = kDSub / 1024;  // mask words per lane
+constexpr uint32_t kDenseBlocksPerSM = 9;
+constexpr int kDBatch = 8;
+constexpr uint32_t kWin = 512;
+static_assert(kFoldWords % kDSub == 0, "fold units are whole dense sub-units");
+static_assert(kWin >= 4 * kLaneSerialMax + 32, "a lane-serial run always fits its window");
+
+struct DenseRec {                 // per record of the current chunk, in shared memory
+    const uint8_t* body;          // mask words, or (index mode) u16 positions
+    const uint8_t* values;
+    const uint32_t* toff;
+    uint32_t count;
+    uint32_t is_idx;
+};
+
+struct DenseSmem {
+    uint4 tile[kDSub * 4 / 16];           // the sub-unit's state (16 KB for fp32)
+    uint4 stage[kDBatch * kWin / 16];     // value windows
+    DenseRec rec[TC_MAX_FOLD];
+    uint32_t carry[TC_MAX_FOLD];          // running value count (= first entry) per record
+    uint32_t tend[TC_MAX_FOLD];           // tile end entry (T >= kDSub)
+    uint32_t want[TC_MAX_FOLD];           // tile_off entry at the unit end
+    uint32_t imask[kDSub / 32];           // index-mode positions -> mask words
+    uint64_t bar;                         // tile load barrier
+};
+
+__device__ __forceinline__ uint32_t ldg_u16(const uint8_t* base, uint32_t k) {
+    return __ldg(reinterpret_cast<const unsigned short*>(base) + k);
+}
+
+// the 16-byte-aligned cover of value run [rb, rb + tot), in bytes
+template <int W>
+__device__ __forceinline__ uint32_t run_bytes(uint32_t rb, uint32_t tot) {
+    const uint64_t a0 = (static_cast<uint64_t>(rb) * W) & ~uint64_t(15);
+    const uint64_t a1 = (static_cast<uint64_t>(rb + tot) * W + 15) & ~uint64_t(15);
+    return static_cast<uint32_t>(a1 - a0);
+}
+// the speculative window from the run start: at most kWin bytes, inside the padded values section
+template <int W>
+__device__ __forceinline__ uint32_t window_bytes(uint32_t count, uint32_t rb) {
+    const uint64_t a0 = (static_cast<uint64_t>(rb) * W) & ~uint64_t(15);
+    const uint64_t vend = pad16(static_cast<uint64_t>(count) * W);
+    return a0 >= vend ? 0u : static_cast<uint32_t>(vend - a0 < kWin ? vend - a0 : kWin);
+}
+
+// Index-mode record: its positions inside [sub, send) -> the warp's shared mask words.
+// Entries are consumed from rb on (the running count = the first entry of this sub-unit).
+// T >= kDSub: the sub-unit lies in one tile ending at entry `e`; xa / xb = entries rb + lane and
+// rb + 32 + lane, loaded with the batch.  T < kDSub: the sub-unit holds whole tiles.
+__device__ __forceinline__ void dense_index_build(const DenseRec& D, uint32_t T, uint32_t m, uint32_t sub,
+                                                  uint32_t send, uint32_t rb, uint32_t e, uint32_t xa, uint32_t xb,
+                                                  uint32_t* imask, int lane, bool& bad) {
+#pragma unroll
+    for (uint32_t q = 0; q < kMW; ++q) imask[32 * q + lane] = 0u;
+    __syncwarp();
+    if (T >= kDSub) {
+        const uint32_t ts = sub / T * T;
+        const uint32_t tend = ts + T < m ? ts + T : m;
+        const uint32_t lim = (send < tend ? send : tend) - ts, lo_rel = sub - ts;
+        uint32_t k = rb, lastx = 0;
+        for (int round = 0;; ++round) {
+            const uint32_t x = round == 0 ? xa : round == 1 ? xb
+                                                           : (k + lane < e ? ldg_u16(D.body, k + lane) : 0xffffffffu);
+            const bool in = k + lane < e && x < lim;
+            const unsigned bal = __ballot_sync(0xffffffffu, in);
+            const uint32_t prev = __shfl_up_sync(0xffffffffu, x, 1);
+            if (bal & (bal + 1u)) bad = true;  // the in-range entries must be a prefix (sorted)
+            if (in) {
+                if (x < lo_rel || (lane > 0 && prev >= x) || (lane == 0 && k > rb && lastx >= x)) bad = true;
+                else {
+                    const uint32_t pos = ts + x - sub;
+                    atomicOr(&imask[pos >> 5], 1u << (pos & 31));
+                }
+            }
+            lastx = __shfl_sync(0xffffffffu, x, 31);
+            const uint32_t n = __popc(bal);
+            k += n;
+            if (n < 32 || __any_sync(0xffffffffu, bad)) break;
+        }
+    } else {
+        uint32_t k = rb;
+        for (uint32_t t = sub / T; t * T < send; ++t) {
+            const uint32_t ts = t * T;
+            const uint32_t tl = m - ts < T ? m - ts : T;
+            const uint32_t et = ldg_u32(D.toff + t + 1);
+            if (et < k || et > D.count) {
+                bad = true;
+                break;
+            }
+            for (uint32_t b = k; b < et; b += 32) {
+                const uint32_t kk = b + lane;
+                if (kk < et) {
+                    const uint32_t x = ldg_u16(D.body, kk);
+                    if (x >= tl || (kk > k && ldg_u16(D.body, kk - 1) >= x)) bad = true;
+                    else {
+                        const uint32_t pos = ts + x - sub;
+                        atomicOr(&imask[pos >> 5], 1u << (pos & 31));
+                    }
+                }
+            }
+            k = et;
+        }
+    }
+    __syncwarp();
+}
+
+// Write one record's values into the tile at its mask bits; value k of the run is sv[k].
+// kGlobal: sv points into the record (run longer than its window) -> batched gathers.
+template <typename word_t, bool kGlobal>
+__device__ __forceinline__ void expand_run(word_t* tw, const word_t* sv, const uint32_t (&mk)[kMW], uint32_t pre,
+                                           uint32_t tot, int lane, uint32_t lt) {
+    if (!kGlobal && tot <= kLaneSerialMax) {
+        uint32_t k = pre;
+#pragma unroll
+        for (uint32_t q = 0; q < kMW; ++q) {
+            uint32_t wv = mk[q];
+            while (wv) {
+                const uint32_t b = __ffs(wv) - 1;
+                wv &= wv - 1;
+                tw[32 * (kMW * lane + q) + b] = sv[k++];
+            }
+        }
+        return;
+    }
+    uint32_t pk = pre;
+#pragma unroll
+    for (uint32_t q = 0; q < kMW; ++q) {
+        uint32_t nz = __ballot_sync(0xffffffffu, mk[q] != 0);
+        while (nz) {
+            word_t v[4];
+            uint32_t d[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                d[i] = 0xffffffffu;
+                if (nz) {  // warp-uniform
+                    const int src = __ffs(nz) - 1;
+                    nz &= nz - 1;
+                    const uint32_t mb = __shfl_sync(0xffffffffu, mk[q], src);
+                    const uint32_t o = __shfl_sync(0xffffffffu, pk, src);
+                    if ((mb >> lane) & 1u) {
+                        v[i] = kGlobal ? ldg_word(sv + o + __popc(mb & lt)) : sv[o + __popc(mb & lt)];
+                        d[i] = 32 * (kMW * src + q) + lane;
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (d[i] != 0xffffffffu) tw[d[i]] = v[i];
+        }
+        pk += __popc(mk[q]);
+    }
+}
+
+template <int W>
+__device__ void fold_dense_unit(const FoldParams& P, uint64_t r, uint64_t ku, DenseSmem& S, int lane,
+                                uint32_t& phase, bool& bad) {
+    using word_t = typename Word<W>::T;
+    const int N = P.nrec;
+    const FoldRec& L = P.desc[r];
+    const uint32_t m = L.m, T = L.T;
+    const uint32_t U = T > kFoldWords ? T : kFoldWords;
+    const uint32_t ustart = static_cast<uint32_t>(ku) * U;
+    const uint32_t uend = ustart + U < m ? ustart + U : m;
+    word_t* state = reinterpret_cast<word_t*>(P.state[L.seg]) + L.chunk_off;
+    word_t* tw = reinterpret_cast<word_t*>(S.tile);
+    uint8_t* sb = reinterpret_cast<uint8_t*>(S.stage);
+    const uint32_t lt = (1u << lane) - 1u;
+
+    for (int j = lane; j < N; j += 32) {  // running counts at the unit start, tile end, unit end
+        const uint32_t* toff = S.rec[j].toff;
+        S.carry[j] = ldg_u32(toff + ustart / T);
+        S.tend[j] = ldg_u32(toff + ustart / T + 1);
+        S.want[j] = uend < m ? ldg_u32(toff + uend / T) : ldg_u32(toff + (m + T - 1) / T);
+    }
+
+    for (uint32_t sub = ustart; sub < uend; sub += kDSub) {
+        const uint32_t send = sub + kDSub < uend ? sub + kDSub : uend;
+        const uint32_t nw = send - sub;
+        const uint32_t bulk = nw * W & ~15u;  // 16-byte part of the sub-unit
+        // 1. state -> tile: the previous sub-unit's bulk stores must have read the tile first
+        bulk_wait_read();
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive_expect_tx(&S.bar, bulk);
+            if (bulk) bulk_g2s(S.tile, state + sub, bulk, &S.bar);
+            for (uint32_t i = bulk / W; i < nw; ++i) tw[i] = state[sub + i];
+        }
+        uint32_t uni[kMW];
+#pragma unroll
+        for (uint32_t q = 0; q < kMW; ++q) uni[q] = 0u;
+        const uint32_t p0 = sub + 32 * kMW * lane;  // first word of this lane's mask words
+        bool tile_ready = false;
+
+        for (int j0 = 0; j0 < N; j0 += kDBatch) {
+            const int nb = N - j0 < kDBatch ? N - j0 : kDBatch;
+            uint32_t mk[kDBatch][kMW], pre[kDBatch], tot[kDBatch], rb[kDBatch], xa[kDBatch], xb[kDBatch];
+            __syncwarp();  // carry / tend / want of this unit are written
+            // 2. masks / position windows and value windows of the batch, all in flight together
+#pragma unroll
+            for (int jj = 0; jj < kDBatch; ++jj) {
+#pragma unroll
+                for (uint32_t q = 0; q < kMW; ++q) mk[jj][q] = 0u;
+                xa[jj] = xb[jj] = 0xffffffffu;
+                rb[jj] = 0;
+                if (jj < nb) {
+                    const DenseRec& D = S.rec[j0 + jj];
+                    rb[jj] = S.carry[j0 + jj];
+                    const uint32_t wb = window_bytes<W>(D.count, rb[jj]);
+                    if (16u * lane < wb)
+                        cp_async16(sb + jj * kWin + 16 * lane,
+                                   D.values + ((static_cast<uint64_t>(rb[jj]) * W) & ~uint64_t(15)) + 16 * lane);
+                    if (!D.is_idx) {
+                        if (p0 < send) {
+                            if constexpr (kMW == 4) {
+                                const uint4 v = __ldg(reinterpret_cast<const uint4*>(D.body) + (p0 >> 7));
+                                mk[jj][0] = v.x;
+                                mk[jj][1] = v.y;
+                                mk[jj][2] = v.z;
+                                mk[jj][3] = v.w;
+                            } else {
+                                const uint2 v = __ldg(reinterpret_cast<const uint2*>(D.body) + (p0 >> 6));
+                                mk[jj][0] = v.x;
+                                mk[jj][1] = v.y;
+                            }
+                        }
+                    } else if (T >= kDSub) {
+                        const uint32_t e = S.tend[j0 + jj];
+                        if (rb[jj] + lane < e) xa[jj] = ldg_u16(D.body, rb[jj] + lane);
+                        if (rb[jj] + 32 + lane < e) xb[jj] = ldg_u16(D.body, rb[jj] + 32 + lane);
+                    }
+                }
+            }
+#pragma unroll
+            for (int jj = 0; jj < kDBatch; ++jj) {
+                if (jj < nb && S.rec[j0 + jj].is_idx) {
+                    dense_index_build(S.rec[j0 + jj], T, m, sub, send, rb[jj], S.tend[j0 + jj], xa[jj], xb[jj],
+                                      S.imask, lane, bad);
+#pragma unroll
+                    for (uint32_t q = 0; q < kMW; ++q) mk[jj][q] = S.imask[kMW * lane + q];
+                    __syncwarp();
+                }
+            }
+            // 3. value offsets; tile_off and bounds checks
+#pragma unroll
+            for (int jj = 0; jj < kDBatch; ++jj) {
+                tot[jj] = 0;
+                pre[jj] = 0;
+                if (jj < nb) {
+                    const DenseRec& D = S.rec[j0 + jj];
+                    if (sub == ustart && ku == 0 && rb[jj] != 0) bad = true;
+                    uint32_t c[kMW], ls = 0;
+#pragma unroll
+                    for (uint32_t q = 0; q < kMW; ++q) {
+                        const uint32_t p = p0 + 32 * q;
+                        if (p >= send) {
+                            mk[jj][q] = 0u;  // past the chunk: mask padding
+                        } else if (p + 32 > send) {  // the chunk's tail word: bits past m must be 0
+                            const uint32_t vb = (1u << (send - p)) - 1u;
+                            if (mk[jj][q] & ~vb) bad = true;
+                            mk[jj][q] &= vb;
+                        }
+                        c[q] = __popc(mk[jj][q]);
+                        ls += c[q];
+                    }
+                    uint32_t inc = ls;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+                        if (lane >= d) inc += t;
+                    }
+                    pre[jj] = inc - ls;
+                    tot[jj] = __shfl_sync(0xffffffffu, inc, 31);
+                    if (T < kDSub) {
+                        uint32_t q0 = pre[jj];
+#pragma unroll
+                        for (uint32_t q = 0; q < kMW; ++q) {
+                            const uint32_t p = p0 + 32 * q;
+                            if (p < send && p != ustart && (p & (T - 1)) == 0 && ldg_u32(D.toff + p / T) != rb[jj] + q0)
+                                bad = true;
+                            q0 += c[q];
+                        }
+                    }
+                    const uint32_t run = rb[jj] + tot[jj];
+                    if (run > D.count) {  // values past the record: corrupt, read nothing
+                        bad = true;
+                        tot[jj] = 0;
+                    }
+                    if (send == uend && (S.want[j0 + jj] != run || (uend == m && D.count != run)))
+                        bad = true;  // unit end: the next unit's first entry, or the final entry
+#pragma unroll
+                    for (uint32_t q = 0; q < kMW; ++q) uni[q] |= mk[jj][q];
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int jj = 0; jj < kDBatch; ++jj)
+                if (jj < nb && lane == jj) S.carry[j0 + jj] = rb[jj] + tot[jj];
+            // 4. expand oldest -> newest
+            cp_async_wait_all();  // value windows
+            if (!tile_ready) {
+                mbar_wait_parity(&S.bar, phase);
+                phase ^= 1u;
+                tile_ready = true;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int jj = 0; jj < kDBatch; ++jj) {
+                if (jj < nb && tot[jj]) {
+                    const DenseRec& D = S.rec[j0 + jj];
+                    if (run_bytes<W>(rb[jj], tot[jj]) <= window_bytes<W>(D.count, rb[jj]))
+                        expand_run<word_t, false>(
+                            tw, reinterpret_cast<const word_t*>(sb + jj * kWin + ((rb[jj] * W) & 15u)), mk[jj], pre[jj],
+                            tot[jj], lane, lt);
+                    else
+                        expand_run<word_t, true>(tw, reinterpret_cast<const word_t*>(D.values) + rb[jj], mk[jj],
+                                                 pre[jj], tot[jj], lane, lt);
+                }
+                __syncwarp();
+            }
+        }
+        // 5. write back this lane's touched lines: runs of consecutive touched lines, bulk stores
+        fence_proxy_async_smem();  // the tile writes of every lane -> async proxy
+        __syncwarp();
+        const uint32_t lw0 = 32 * kMW * lane;  // this lane's first word in the sub-unit
+        uint32_t q = 0;
+        while (q < kMW) {
+            if (!uni[q] || lw0 + 32 * q >= nw) {
+                ++q;
+                continue;
+            }
+            uint32_t qe = q + 1;
+            while (qe < kMW && uni[qe] && lw0 + 32 * qe < nw) ++qe;
+            const uint32_t w0 = lw0 + 32 * q;
+            const uint32_t w1 = lw0 + 32 * qe < nw ? lw0 + 32 * qe : nw;
+            const uint32_t bytes = (w1 - w0) * W;
+            const uint32_t bb = bytes & ~15u;
+            if (bb) bulk_s2g(state + sub + w0, tw + w0, bb);
+            for (uint32_t i = w0 + bb / W; i < w1; ++i) state[sub + i] = tw[i];  // ragged chunk end
+            q = qe;
+        }
+        bulk_commit();
+    }
+}
+
+__global__ void __launch_bounds__(kDenseThreads, kDenseBlocksPerSM) fold_dense_kernel(const __grid_constant__ FoldParams P) {
+    __shared__ DenseSmem S;
+    if (*reinterpret_cast<volatile unsigned*>(P.err) != 0) return;  // sticky error pending
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) mbar_init(&S.bar, 1);
+    __syncwarp();
+    const uint64_t R = P.info[0];
+    const uint64_t total = P.info[1];
+    const uint64_t nwarps = gridDim.x;
+    bool bad = false;
+    uint32_t phase = 0;
+    uint64_t cur = ~uint64_t(0);  // chunk whose record table is in S.rec
+    for (uint64_t u = blockIdx.x; u < total; u += nwarps) {
+        uint64_t lo = 0, hi = R;
+        while (hi - lo > 1) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (P.unit_first[mid] <= u) lo = mid; else hi = mid;
+        }
+        if (!P.desc[lo].dense) {  // folded by fold_kernel: jump past the chunk
+            const uint64_t nxt = P.unit_first[lo + 1];
+            u += (nxt - u + nwarps - 1) / nwarps * nwarps - nwarps;
+            continue;
+        }
+        if (lo != cur) {
+            __syncwarp();
+            for (int j = lane; j < P.nrec; j += 32) {
+                const FoldRec& F = P.desc[static_cast<size_t>(j) * P.cap + lo];
+                DenseRec D;
+                D.body = F.idx ? F.idx : F.mask;
+                D.values = F.values;
+                D.toff = reinterpret_cast<const uint32_t*>(F.toff);
+                D.count = static_cast<uint32_t>(F.count);
+                D.is_idx = F.idx != nullptr;
+                S.rec[j] = D;
+            }
+            __syncwarp();
+            cur = lo;
+        }
+        const uint64_t ku = u - P.unit_first[lo];
+        if (P.desc[lo].w == 4)
+            fold_dense_unit<4>(P, lo, ku, S, lane, phase, bad);
+        else
+            fold_dense_unit<2>(P, lo, ku, S, lane, phase, bad);
+        if (__any_sync(0xffffffffu, bad)) {
+            if (lane == 0) tc_set_err(P.err, TC_ERR_CORRUPT);
+            break;
+        }
+    }
+    bulk_wait_all();  // the bulk stores are done before the CTA's shared memory goes away
 }
 
 }  // namespace
@@ -396,7 +819,16 @@ cudaError_t launch_fold(const FoldParams& p, cudaStream_t s, int num_sms, uint64
             occ = 1;
     }
     fold_kernel<<<num_sms * occ, kFoldThreads, 0, s>>>(p);
-    *launches += 2;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    static int occ_d = 0;
+    if (!occ_d) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, fold_dense_kernel, kDenseThreads, 0) != cudaSuccess ||
+            occ_d < 1)
+            occ_d = 1;
+    }
+    fold_dense_kernel<<<num_sms * occ_d, kDenseThreads, 0, s>>>(p);
+    *launches += 3;
     return cudaGetLastError();
 }
 

@@ -20,7 +20,7 @@ constexpr uint32_t kEncBlockWords4 = 4096;  // 4-byte words
 constexpr uint32_t kEncBlockWords2 = 8192;  // 2-byte words
 // Fold: one warp per unit of max(T, kFoldWords) words.
 constexpr uint32_t kFoldThreads = 256;
-constexpr uint32_t kFoldWords = 1024;  // minimum fold unit (one warp: 32 mask words)
+constexpr uint32_t kFoldWords = 4096;  // minimum fold unit (one warp: 128 mask words)
 
 __host__ __device__ inline uint64_t pad16(uint64_t x) { return (x + 15) & ~uint64_t(15); }
 __host__ __device__ inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
@@ -104,6 +104,8 @@ struct FoldRec {           // one record of one diff, as located by the walker
     uint32_t T;
     uint32_t seg;
     uint32_t w;
+    uint32_t dense;        // desc[r] of diff 0 only: chunk r is folded by the dense kernel
+    uint32_t pad_;
 };
 
 struct FoldParams {
@@ -116,6 +118,7 @@ struct FoldParams {
     int nrec;               // diffs folded
     uint32_t cap;           // descriptor capacity per diff
     uint64_t state_version;
+    uint32_t dense_permille;  // chunk r is dense when sum_j count_j * 1000 > m * dense_permille
     FoldRec* desc;          // [nrec][cap]
     uint64_t* unit_first;   // [cap + 1]
     unsigned long long* info;  // [0] = records per diff, [1] = total units

@@ -27,6 +27,7 @@ struct tc_ctx {
     size_t fold_bytes = 0;
     unsigned int* err = nullptr;  // sticky device error word
     uint64_t launches = 0;
+    uint32_t fold_dense_permille = 30;  // tc_ctx_set_fold_dense_permille
 };
 
 namespace tc {
@@ -149,6 +150,12 @@ tc_status tc_ctx_create(int device, tc_ctx** out) {
         return cuda_fail(e, "cudaMalloc(err)");
     }
     *out = c;
+    return TC_OK;
+}
+
+tc_status tc_ctx_set_fold_dense_permille(tc_ctx* c, uint32_t permille) {
+    if (!c) return fail(TC_ERR_INVALID, "ctx is NULL");
+    c->fold_dense_permille = permille;
     return TC_OK;
 }
 
@@ -405,6 +412,7 @@ tc_status tc_diff_apply(tc_ctx* ctx, void* const* state, const uint64_t* n_words
     P.nrec = n_records;
     P.cap = static_cast<uint32_t>(cap);
     P.state_version = state_version;
+    P.dense_permille = ctx->fold_dense_permille;
     P.err = ctx->err;
 
     cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -25,6 +25,20 @@ def ctx():
     c.close()
 
 
+# restore strategies (include/tc.h tc_ctx_set_fold_dense_permille): the default threshold, every
+# chunk streamed through shared memory (fold_dense_kernel), every chunk scattered (fold_kernel)
+FOLD_STRATEGIES = {"auto": None, "stream": 0, "scatter": 0xFFFFFFFF}
+
+
+@pytest.fixture(scope="module", params=list(FOLD_STRATEGIES))
+def fctx(request):
+    c = tc.Ctx(0)
+    if FOLD_STRATEGIES[request.param] is not None:
+        c.set_fold_dense_permille(FOLD_STRATEGIES[request.param])
+    yield c
+    c.close()
+
+
 def rand_pair(n, w, f, rng=RNG):
     dt = np.uint16 if w == 2 else np.uint32
     ref = rng.integers(0, 1 << (8 * w), size=n, dtype=np.uint64).astype(dt)
@@ -121,35 +135,64 @@ def make_chain(tco, sizes, wb, N, f, T, C, seed=5, structure=synth.S1_IID):
     ([20000, 9000], [4, 2], 64, 1024),
     ([40000], [4], 16384, 32768),
 ])
-def test_fold_matches_oracle(ctx, tco, N, layout):
+def test_fold_matches_oracle(fctx, tco, N, layout):
     sizes, wb, T, C = layout
     states, diffs = make_chain(tco, sizes, wb, N, 0.05, T, C)
     st_o = [a.copy() for a in states[0]]
     rc, ver = tco.fold(st_o, 0, diffs)
     assert rc == 0 and ver == N
-    rc, st_g = gpu_fold(ctx, states[0], 0, diffs)
+    rc, st_g = gpu_fold(fctx, states[0], 0, diffs)
     assert rc == tc.OK
     for a, b, c in zip(st_g, st_o, states[N]):
         assert np.array_equal(a, b) and np.array_equal(a, c)
 
 
+def test_fold_max_chain(fctx, tco):
+    """TC_MAX_FOLD records: 8 batches of kDBatch records in the streaming fold."""
+    N = tc.MAX_FOLD
+    states, diffs = make_chain(tco, [9000, 7001], [4, 2], N, 0.01, 1024, 1 << 28, seed=21)
+    rc, st_g = gpu_fold(fctx, states[0], 0, diffs)
+    assert rc == tc.OK
+    assert all(np.array_equal(a, b) for a, b in zip(st_g, states[N]))
+
+
+@pytest.mark.parametrize("sizes,wb,T,C,f", [
+    ([1027, 3], [4, 4], 32, 64, 0.6),        # T < 1024 (sub-unit of many tiles), ragged words
+    ([5000, 5001], [2, 2], 2048, 4096, 0.9),  # index windows longer than 32 entries
+    ([33000], [4], 8192, 8192, 0.3),          # T > 1024: carried positions across sub-units
+])
+def test_index_fold_strategies(fctx, tco, sizes, wb, T, C, f):
+    N = 4
+    states = [synth.state(sizes, wb, 17, v, f) for v in range(N + 1)]
+    ref = [a.copy() for a in states[0]]
+    diffs = []
+    for v in range(1, N + 1):
+        rc, d = tco.encode(ref, states[v], tile_words=T, chunk_words=C, version=v, ref_version=v - 1,
+                           index_mode=True)
+        assert rc == 0
+        diffs.append(d)
+    rc, st_g = gpu_fold(fctx, states[0], 0, diffs)
+    assert rc == tc.OK
+    assert all(np.array_equal(a, b) for a, b in zip(st_g, states[N]))
+
+
 @pytest.mark.parametrize("f", [0.0, 0.01, 1.0])
-def test_fold_dense_and_empty(ctx, tco, f):
+def test_fold_dense_and_empty(fctx, tco, f):
     states, diffs = make_chain(tco, [50000, 50000], [2, 4], 3, f, 4096, 1 << 28, seed=9)
-    rc, st_g = gpu_fold(ctx, states[0], 0, diffs)
+    rc, st_g = gpu_fold(fctx, states[0], 0, diffs)
     assert rc == tc.OK
     assert all(np.array_equal(a, b) for a, b in zip(st_g, states[3]))
 
 
-def test_fold_s2_runs(ctx, tco):
+def test_fold_s2_runs(fctx, tco):
     states, diffs = make_chain(tco, [100000, 100000], [2, 4], 5, 0.2, 4096, 1 << 28, seed=2,
                                structure=synth.S2_RUNS)
-    rc, st_g = gpu_fold(ctx, states[0], 0, diffs)
+    rc, st_g = gpu_fold(fctx, states[0], 0, diffs)
     assert rc == tc.OK
     assert all(np.array_equal(a, b) for a, b in zip(st_g, states[5]))
 
 
-def test_fold_of_gpu_encoded_chain(ctx, tco):
+def test_fold_of_gpu_encoded_chain(fctx, tco):
     """GPU encode (incremental, fused ref advance) -> GPU fold reproduces the final state."""
     sizes, wb = [60000, 60000, 60000, 60000], [2, 4, 4, 4]
     N = 8
@@ -157,9 +200,9 @@ def test_fold_of_gpu_encoded_chain(ctx, tco):
     ref = [a.copy() for a in states[0]]
     diffs = []
     for v in range(1, N + 1):
-        d, ref, _ = gpu_encode(ctx, ref, states[v], version=v, ref_version=v - 1)
+        d, ref, _ = gpu_encode(fctx, ref, states[v], version=v, ref_version=v - 1)
         diffs.append(d)
-    rc, st_g = gpu_fold(ctx, states[0], 0, diffs)
+    rc, st_g = gpu_fold(fctx, states[0], 0, diffs)
     assert rc == tc.OK
     assert all(np.array_equal(a, b) for a, b in zip(st_g, states[N]))
 
@@ -170,63 +213,63 @@ def _chain1(tco, n=20000, w=4, T=256):
     return states, diffs[0]
 
 
-def test_tamper_mask_bit_corrupt(ctx, tco):
+def test_tamper_mask_bit_corrupt(fctx, tco):
     states, d = _chain1(tco)
     bad = d.copy()
     bad[64 + 4 * 17] ^= 0x10
-    rc, _ = gpu_fold(ctx, states[0], 0, [bad])
+    rc, _ = gpu_fold(fctx, states[0], 0, [bad])
     assert rc == tc.ERR_CORRUPT == tco.fold([a.copy() for a in states[0]], 0, [bad])[0]
 
 
-def test_tamper_tile_off_corrupt(ctx, tco):
+def test_tamper_tile_off_corrupt(fctx, tco):
     states, d = _chain1(tco)
     bad = d.copy()
     m = 20000
     toff = 64 + ((4 * -(-m // 32) + 15) // 16) * 16
     bad[toff + 4 * 5] ^= 1
-    rc, _ = gpu_fold(ctx, states[0], 0, [bad])
+    rc, _ = gpu_fold(fctx, states[0], 0, [bad])
     assert rc == tc.ERR_CORRUPT == tco.fold([a.copy() for a in states[0]], 0, [bad])[0]
 
 
 @pytest.mark.parametrize("byte,val", [(0, ord("X")), (4, 2), (6, 8), (7, 3), (8, 33), (12, 1)])
-def test_tamper_header_corrupt_state_untouched(ctx, tco, byte, val):
+def test_tamper_header_corrupt_state_untouched(fctx, tco, byte, val):
     states, d = _chain1(tco)
     bad = d.copy()
     bad[byte] = val
-    rc, st = gpu_fold(ctx, states[0], 0, [bad])
+    rc, st = gpu_fold(fctx, states[0], 0, [bad])
     assert rc == tc.ERR_CORRUPT
     assert np.array_equal(st[0], states[0][0])
 
 
-def test_truncated_corrupt(ctx, tco):
+def test_truncated_corrupt(fctx, tco):
     states, d = _chain1(tco)
-    rc, st = gpu_fold(ctx, states[0], 0, [d[:-16]])
+    rc, st = gpu_fold(fctx, states[0], 0, [d[:-16]])
     assert rc == tc.ERR_CORRUPT and np.array_equal(st[0], states[0][0])
 
 
-def test_chain_gap_protocol(ctx, tco):
+def test_chain_gap_protocol(fctx, tco):
     states, diffs = make_chain(tco, [5000], [4], 3, 0.1, 64, 1 << 28)
-    rc, st = gpu_fold(ctx, states[0], 0, [diffs[0], diffs[2]])
+    rc, st = gpu_fold(fctx, states[0], 0, [diffs[0], diffs[2]])
     assert rc == tc.ERR_PROTOCOL and np.array_equal(st[0], states[0][0])
-    rc, st = gpu_fold(ctx, states[0], 1, [diffs[0]])
+    rc, st = gpu_fold(fctx, states[0], 1, [diffs[0]])
     assert rc == tc.ERR_PROTOCOL
     # the context is clean again after check
-    rc, st = gpu_fold(ctx, states[0], 0, diffs)
+    rc, st = gpu_fold(fctx, states[0], 0, diffs)
     assert rc == tc.OK and np.array_equal(st[0], states[3][0])
 
 
-def test_layout_mismatch_invalid(ctx, tco):
+def test_layout_mismatch_invalid(fctx, tco):
     sizes, wb = [5000], [4]
     s = [synth.state(sizes, wb, 1, v, 0.1) for v in range(3)]
     ref = [a.copy() for a in s[0]]
     _, d1 = tco.encode(ref, s[1], tile_words=64, version=1, ref_version=0)
     _, d2 = tco.encode(ref, s[2], tile_words=128, version=2, ref_version=1)
-    rc, _ = gpu_fold(ctx, s[0], 0, [d1, d2])
+    rc, _ = gpu_fold(fctx, s[0], 0, [d1, d2])
     assert rc == tc.ERR_INVALID
     # applied one at a time they restore
-    rc, st = gpu_fold(ctx, s[0], 0, [d1])
+    rc, st = gpu_fold(fctx, s[0], 0, [d1])
     assert rc == tc.OK
-    rc, st = gpu_fold(ctx, st, 1, [d2])
+    rc, st = gpu_fold(fctx, st, 1, [d2])
     assert rc == tc.OK and np.array_equal(st[0], s[2][0])
 
 
@@ -238,7 +281,7 @@ def test_launch_counter(ctx):
     tc.diff_encode(ctx, [ref], [ref.clone()], out, ob, 1, 0)
     tc.diff_apply(ctx, [ref], 0, [out], [int(ob.item())])
     ctx.check()
-    assert ctx.launches == before + 5  # encode (mask, prefix, emit) + fold (walker, fold)
+    assert ctx.launches == before + 6  # encode (mask, prefix, emit) + fold (walker, scatter, stream)
 
 
 @pytest.mark.parametrize("advance", [True, False])
@@ -288,7 +331,7 @@ def test_index_mode_encode_matches_oracle_bytes(ctx, tco, sizes, wb, f, T, C):
     ([20000, 9000], [4, 2], 64, 1024),
     ([40000], [4], 8192, 16384),
 ])
-def test_index_and_mixed_mode_fold_matches_oracle(ctx, tco, N, layout):
+def test_index_and_mixed_mode_fold_matches_oracle(fctx, tco, N, layout):
     sizes, wb, T, C = layout
     states = [synth.state(sizes, wb, 13, v, 0.03) for v in range(N + 1)]
     ref = [a.copy() for a in states[0]]
@@ -301,13 +344,13 @@ def test_index_and_mixed_mode_fold_matches_oracle(ctx, tco, N, layout):
     st_o = [a.copy() for a in states[0]]
     rc, ver = tco.fold(st_o, 0, diffs)
     assert rc == 0
-    rc, st_g = gpu_fold(ctx, states[0], 0, diffs)
+    rc, st_g = gpu_fold(fctx, states[0], 0, diffs)
     assert rc == tc.OK
     for a, b, c in zip(st_g, st_o, states[N]):
         assert np.array_equal(a, b) and np.array_equal(a, c)
 
 
-def test_index_mode_gpu_chain_dense_and_sparse(ctx, tco):
+def test_index_mode_gpu_chain_dense_and_sparse(fctx, tco):
     """GPU index-mode encode over sparse and dense blocks, folded on the GPU."""
     sizes, wb = [50000, 50000], [2, 4]
     for f in (0.005, 0.7):
@@ -315,24 +358,24 @@ def test_index_mode_gpu_chain_dense_and_sparse(ctx, tco):
         ref = [a.copy() for a in states[0]]
         diffs = []
         for v in range(1, 4):
-            d, ref, _ = gpu_encode(ctx, ref, states[v], version=v, ref_version=v - 1, index_mode=True)
+            d, ref, _ = gpu_encode(fctx, ref, states[v], version=v, ref_version=v - 1, index_mode=True)
             diffs.append(d)
-        rc, st_g = gpu_fold(ctx, states[0], 0, diffs)
+        rc, st_g = gpu_fold(fctx, states[0], 0, diffs)
         assert rc == tc.OK and all(np.array_equal(a, b) for a, b in zip(st_g, states[3]))
 
 
-def test_index_tamper_gpu(ctx, tco):
+def test_index_tamper_gpu(fctx, tco):
     ref, cur = rand_pair(20000, 4, 0.1)
     rc, rec = tco.encode([ref.copy()], [cur], tile_words=256, version=1, ref_version=0, index_mode=True)
     nt = -(-20000 // 256)
     p = 64 + ((4 * (nt + 1) + 15) // 16) * 16
     bad = rec.copy()
     bad[p: p + 2] = np.frombuffer(np.uint16(300).tobytes(), np.uint8)  # outside a 256-word tile
-    rc, _ = gpu_fold(ctx, [ref], 0, [bad])
+    rc, _ = gpu_fold(fctx, [ref], 0, [bad])
     assert rc == tc.ERR_CORRUPT == tco.fold([ref.copy()], 0, [bad])[0]
     bad = rec.copy()
     bad[7] = 2
-    rc, st = gpu_fold(ctx, [ref], 0, [bad])
+    rc, st = gpu_fold(fctx, [ref], 0, [bad])
     assert rc == tc.ERR_CORRUPT and np.array_equal(st[0], ref)
 
 
