@@ -434,8 +434,9 @@ struct DenseSmem {
     uint32_t carry[TC_MAX_FOLD];          // running value count (= first entry) per record
     uint32_t tend[TC_MAX_FOLD];           // tile end entry (T >= kDSub)
     uint32_t want[TC_MAX_FOLD];           // tile_off entry at the unit end
-    uint32_t imask[kDSub / 32];           // index-mode positions -> mask words
+    uint32_t imask[kDSub / 32];           // index-mode positions -> mask words / touched lines
     uint64_t bar;                         // tile load barrier
+    uint32_t list;                        // every record is index mode with T == kDSub
 };
 
 __device__ __forceinline__ uint32_t ldg_u16(const uint8_t* base, uint32_t k) {
@@ -565,6 +566,108 @@ __device__ __forceinline__ void expand_run(word_t* tw, const word_t* sv, const u
     }
 }
 
+// "List" sub-unit: every record is an index-mode record whose tile is exactly this sub-unit
+// (T == kDSub), so record j's entries for it are [carry_j, tend_j): positions and values are
+// contiguous runs, staged with coalesced 16-byte copies and scattered into the tile oldest
+// record first, with no mask arithmetic.  Rounds fill the stage with whole records; a record
+// larger than the stage goes through it in pieces.
+template <int W>
+__device__ __forceinline__ uint32_t list_run_bytes(uint32_t a, uint32_t b, uint32_t& pb) {
+    if (b <= a) {
+        pb = 0;
+        return 0u;
+    }
+    pb = ((2u * b + 15u) & ~15u) - ((2u * a) & ~15u);
+    return pb + static_cast<uint32_t>(((static_cast<uint64_t>(b) * W + 15) & ~uint64_t(15)) -
+                                      (static_cast<uint64_t>(a) * W & ~uint64_t(15)));
+}
+
+template <int W>
+__device__ __forceinline__ void dense_list_sub(int N, uint32_t nw, DenseSmem& S, uint32_t& phase, int lane, bool& bad) {
+    using word_t = typename Word<W>::T;
+    constexpr uint32_t kStage = kDBatch * kWin;
+    constexpr uint32_t kPiece = ((kStage - 64) / (2 + W)) & ~7u;  // entries of a piece
+    word_t* tw = reinterpret_cast<word_t*>(S.tile);
+    uint8_t* sb = reinterpret_cast<uint8_t*>(S.stage);
+    uint32_t* touched = S.imask;  // per 32-word line: written
+#pragma unroll
+    for (uint32_t q = 0; q < kMW; ++q) touched[32 * q + lane] = 0u;
+    bool tile_ready = false;
+    int r = 0;
+    uint32_t a = S.carry[0], lastx = 0;
+    while (r < N) {
+        // the round's items, walked twice with the same logic: copies, then scatter
+        int r_end = r;
+        uint32_t a_end = a;
+        for (int pass = 0; pass < 2; ++pass) {
+            int rr = r;
+            uint32_t aa = a, used = 0, pb;
+            while (rr < N) {
+                const uint32_t k1 = S.tend[rr];
+                uint32_t bb = k1;
+                uint32_t sz = list_run_bytes<W>(aa, bb, pb);
+                if (used + sz > kStage) {
+                    if (used) break;
+                    bb = aa + kPiece;  // a piece of a record larger than the stage
+                    sz = list_run_bytes<W>(aa, bb, pb);
+                }
+                const DenseRec& D = S.rec[rr];
+                if (pass == 0) {
+                    if (sz) {
+                        const uint8_t* ps = D.body + ((2u * aa) & ~15u);
+                        const uint8_t* vs = D.values + (static_cast<uint64_t>(aa) * W & ~uint64_t(15));
+                        for (uint32_t o = 16 * lane; o < pb; o += 512) cp_async16(sb + used + o, ps + o);
+                        for (uint32_t o = 16 * lane; o < sz - pb; o += 512) cp_async16(sb + used + pb + o, vs + o);
+                    }
+                } else {
+                    const uint16_t* px = reinterpret_cast<const uint16_t*>(sb + used + ((2u * aa) & 15u));
+                    const word_t* pv = reinterpret_cast<const word_t*>(sb + used + pb + ((aa * W) & 15u));
+                    const uint32_t k0 = S.carry[rr];  // the record's first entry of this tile
+                    for (uint32_t k = lane; k < bb - aa; k += 32) {
+                        const uint32_t x = px[k];
+                        const bool has_prev = aa + k > k0;
+                        const uint32_t prev = k > 0 ? px[k - 1] : lastx;
+                        if (x >= nw || (has_prev && prev >= x)) {
+                            bad = true;
+                            continue;
+                        }
+                        tw[x] = pv[k];
+                        touched[x >> 5] = 1u;
+                    }
+                    if (bb > aa) lastx = px[bb - aa - 1];
+                    __syncwarp();
+                }
+                used += sz;
+                if (bb < k1) {  // piece: the round ends inside record rr
+                    aa = bb;
+                    break;
+                }
+                ++rr;
+                if (rr < N) aa = S.carry[rr];
+            }
+            if (pass == 0) {
+                r_end = rr;
+                a_end = aa;
+                cp_async_wait_all();
+                if (!tile_ready) {
+                    mbar_wait_parity(&S.bar, phase);
+                    phase ^= 1u;
+                    tile_ready = true;
+                }
+                __syncwarp();
+            }
+        }
+        if (r_end == r && a_end == a) break;  // no progress: cannot happen (a piece always fits)
+        r = r_end;
+        a = a_end;
+    }
+    if (!tile_ready) {
+        mbar_wait_parity(&S.bar, phase);
+        phase ^= 1u;
+    }
+    __syncwarp();
+}
+
 template <int W>
 __device__ void fold_dense_unit(const FoldParams& P, uint64_t r, uint64_t ku, DenseSmem& S, int lane,
                                 uint32_t& phase, bool& bad) {
@@ -605,7 +708,23 @@ __device__ void fold_dense_unit(const FoldParams& P, uint64_t r, uint64_t ku, De
         const uint32_t p0 = sub + 32 * kMW * lane;  // first word of this lane's mask words
         bool tile_ready = false;
 
-        for (int j0 = 0; j0 < N; j0 += kDBatch) {
+        if (S.list) {
+            __syncwarp();  // carry / tend of this unit are written
+            for (int j = lane; j < N; j += 32) {
+                const uint32_t k0 = S.carry[j], k1 = S.tend[j];
+                if (k1 < k0 || k1 > S.rec[j].count || (ku == 0 && k0 != 0) || (uend == m && k1 != S.rec[j].count))
+                    bad = true;
+            }
+            if (__any_sync(0xffffffffu, bad)) {  // drain the tile load, write nothing
+                mbar_wait_parity(&S.bar, phase);
+                phase ^= 1u;
+                return;
+            }
+            dense_list_sub<W>(N, nw, S, phase, lane, bad);
+#pragma unroll
+            for (uint32_t q = 0; q < kMW; ++q) uni[q] = S.imask[kMW * lane + q];
+        }
+        for (int j0 = 0; j0 < (S.list ? 0 : N); j0 += kDBatch) {
             const int nb = N - j0 < kDBatch ? N - j0 : kDBatch;
             uint32_t mk[kDBatch][kMW], pre[kDBatch], tot[kDBatch], rb[kDBatch], xa[kDBatch], xb[kDBatch];
             __syncwarp();  // carry / tend / want of this unit are written
@@ -791,6 +910,10 @@ __global__ void __launch_bounds__(kDenseThreads, kDenseBlocksPerSM) fold_dense_k
                 D.is_idx = F.idx != nullptr;
                 S.rec[j] = D;
             }
+            bool list = P.desc[lo].T == kDSub;
+            for (int j = lane; j < P.nrec; j += 32) list = list && P.desc[static_cast<size_t>(j) * P.cap + lo].idx != nullptr;
+            list = __all_sync(0xffffffffu, list);
+            if (lane == 0) S.list = list;
             __syncwarp();
             cur = lo;
         }

@@ -379,6 +379,44 @@ def test_index_tamper_gpu(fctx, tco):
     assert rc == tc.ERR_CORRUPT and np.array_equal(st[0], ref)
 
 
+@pytest.mark.parametrize("f", [0.01, 0.3])
+def test_index_list_fold_t4096(fctx, tco, f):
+    """All-index chains at T = 4096 (the streaming fold's list path): ragged chunk ends, records
+    larger than the stage (f = 0.3), chunk boundaries inside a segment."""
+    sizes, wb, T, C = [70001, 9000, 4096], [4, 2, 4], 4096, 4096 * 5
+    N = 6
+    states = [synth.state(sizes, wb, 41, v, f) for v in range(N + 1)]
+    ref = [a.copy() for a in states[0]]
+    diffs = []
+    for v in range(1, N + 1):
+        rc, d = tco.encode(ref, states[v], tile_words=T, chunk_words=C, version=v, ref_version=v - 1,
+                           index_mode=True)
+        assert rc == 0
+        diffs.append(d)
+    rc, st_g = gpu_fold(fctx, states[0], 0, diffs)
+    assert rc == tc.OK
+    assert all(np.array_equal(a, b) for a, b in zip(st_g, states[N]))
+
+
+def test_index_list_tamper(fctx, tco):
+    ref, cur = rand_pair(9000, 4, 0.05)
+    rc, rec = tco.encode([ref.copy()], [cur], tile_words=4096, version=1, ref_version=0, index_mode=True)
+    nt = -(-9000 // 4096)
+    p = 64 + ((4 * (nt + 1) + 15) // 16) * 16
+    bad = rec.copy()
+    bad[p: p + 4] = bad[[p + 2, p + 3, p, p + 1]]  # two positions out of order
+    assert tco.fold([ref.copy()], 0, [bad])[0] == tc.ERR_CORRUPT
+    rc, _ = gpu_fold(fctx, [ref], 0, [bad])
+    assert rc == tc.ERR_CORRUPT
+    bad = rec.copy()
+    toff1 = 64 + 4
+    v = int(np.frombuffer(bad[toff1:toff1 + 4].tobytes(), np.uint32)[0])
+    bad[toff1:toff1 + 4] = np.frombuffer(np.uint32(v + 1).tobytes(), np.uint8)  # tile 0 claims one more entry
+    assert tco.fold([ref.copy()], 0, [bad])[0] == tc.ERR_CORRUPT
+    rc, _ = gpu_fold(fctx, [ref], 0, [bad])
+    assert rc == tc.ERR_CORRUPT
+
+
 def test_index_mode_range_encode(ctx, tco):
     sizes, wb, T, C = [40001, 70003], [2, 4], 256, 8192
     pairs = [rand_pair(n, w, 0.02) for n, w in zip(sizes, wb)]
