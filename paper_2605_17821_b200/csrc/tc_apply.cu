@@ -414,6 +414,7 @@ constexpr uint32_t kDenseThreads = 32;
 constexpr uint32_t kDSub = 4096;
 constexpr uint32_t kMW = kDSub / 1024;  // mask words per lane
 constexpr uint32_t kDenseBlocksPerSM = 9;
+constexpr uint64_t kDenseRun = 16;  // consecutive units per CTA visit (running counts carry over)
 constexpr int kDBatch = 8;
 constexpr uint32_t kWin = 512;
 static_assert(kFoldWords % kDSub == 0, "fold units are whole dense sub-units");
@@ -670,7 +671,7 @@ __device__ __forceinline__ void dense_list_sub(int N, uint32_t nw, DenseSmem& S,
 
 template <int W>
 __device__ void fold_dense_unit(const FoldParams& P, uint64_t r, uint64_t ku, DenseSmem& S, int lane,
-                                uint32_t& phase, bool& bad) {
+                                uint32_t& phase, bool preloaded, bool& bad) {
     using word_t = typename Word<W>::T;
     const int N = P.nrec;
     const FoldRec& L = P.desc[r];
@@ -683,11 +684,13 @@ __device__ void fold_dense_unit(const FoldParams& P, uint64_t r, uint64_t ku, De
     uint8_t* sb = reinterpret_cast<uint8_t*>(S.stage);
     const uint32_t lt = (1u << lane) - 1u;
 
-    for (int j = lane; j < N; j += 32) {  // running counts at the unit start, tile end, unit end
-        const uint32_t* toff = S.rec[j].toff;
-        S.carry[j] = ldg_u32(toff + ustart / T);
-        S.tend[j] = ldg_u32(toff + ustart / T + 1);
-        S.want[j] = uend < m ? ldg_u32(toff + uend / T) : ldg_u32(toff + (m + T - 1) / T);
+    if (!preloaded) {
+        for (int j = lane; j < N; j += 32) {  // running counts at the unit start, tile end, unit end
+            const uint32_t* toff = S.rec[j].toff;
+            S.carry[j] = ldg_u32(toff + ustart / T);
+            S.tend[j] = ldg_u32(toff + ustart / T + 1);
+            S.want[j] = uend < m ? ldg_u32(toff + uend / T) : ldg_u32(toff + (m + T - 1) / T);
+        }
     }
 
     for (uint32_t sub = ustart; sub < uend; sub += kDSub) {
@@ -875,32 +878,48 @@ __device__ void fold_dense_unit(const FoldParams& P, uint64_t r, uint64_t ku, De
     }
 }
 
+// Persistent: each CTA (= one warp) folds runs of kDenseRun consecutive units, the runs grid-
+// strided over the CTAs.  In list chunks the running counts carry from unit to unit and the next
+// unit's tile end is loaded while the current unit is folded.
 __global__ void __launch_bounds__(kDenseThreads, kDenseBlocksPerSM) fold_dense_kernel(const __grid_constant__ FoldParams P) {
     __shared__ DenseSmem S;
     if (*reinterpret_cast<volatile unsigned*>(P.err) != 0) return;  // sticky error pending
     const int lane = threadIdx.x & 31;
-    if (lane == 0) mbar_init(&S.bar, 1);
-    __syncwarp();
+    const int N = P.nrec;
     const uint64_t R = P.info[0];
     const uint64_t total = P.info[1];
-    const uint64_t nwarps = gridDim.x;
+    if (blockIdx.x * kDenseRun >= total) return;
+    if (lane == 0) mbar_init(&S.bar, 1);
+    __syncwarp();
     bool bad = false;
     uint32_t phase = 0;
     uint64_t cur = ~uint64_t(0);  // chunk whose record table is in S.rec
-    for (uint64_t u = blockIdx.x; u < total; u += nwarps) {
-        uint64_t lo = 0, hi = R;
-        while (hi - lo > 1) {
-            const uint64_t mid = (lo + hi) >> 1;
-            if (P.unit_first[mid] <= u) lo = mid; else hi = mid;
+    uint32_t te[2] = {0u, 0u};     // list chunks: tile end entries of unit u (lane j: records j, j + 32)
+    bool te_valid = false;
+    uint64_t lo = 0, u1 = 0;
+    for (uint64_t u = 0;; ++u) {
+        if (u >= u1) {  // the next run of consecutive units
+            const uint64_t run = u1 == 0 ? blockIdx.x : u1 / kDenseRun + gridDim.x - 1;
+            if (run * kDenseRun >= total) break;
+            u = run * kDenseRun;
+            u1 = u + kDenseRun < total ? u + kDenseRun : total;
+            uint64_t hi = R;
+            lo = 0;
+            while (hi - lo > 1) {
+                const uint64_t mid = (lo + hi) >> 1;
+                if (P.unit_first[mid] <= u) lo = mid; else hi = mid;
+            }
+            te_valid = false;
         }
-        if (!P.desc[lo].dense) {  // folded by fold_kernel: jump past the chunk
-            const uint64_t nxt = P.unit_first[lo + 1];
-            u += (nxt - u + nwarps - 1) / nwarps * nwarps - nwarps;
+        while (u >= P.unit_first[lo + 1]) ++lo;
+        if (!P.desc[lo].dense) {  // folded by fold_kernel: skip the chunk
+            u = (P.unit_first[lo + 1] < u1 ? P.unit_first[lo + 1] : u1) - 1;
+            te_valid = false;
             continue;
         }
         if (lo != cur) {
             __syncwarp();
-            for (int j = lane; j < P.nrec; j += 32) {
+            for (int j = lane; j < N; j += 32) {
                 const FoldRec& F = P.desc[static_cast<size_t>(j) * P.cap + lo];
                 DenseRec D;
                 D.body = F.idx ? F.idx : F.mask;
@@ -911,17 +930,44 @@ __global__ void __launch_bounds__(kDenseThreads, kDenseBlocksPerSM) fold_dense_k
                 S.rec[j] = D;
             }
             bool list = P.desc[lo].T == kDSub;
-            for (int j = lane; j < P.nrec; j += 32) list = list && P.desc[static_cast<size_t>(j) * P.cap + lo].idx != nullptr;
+            for (int j = lane; j < N; j += 32) list = list && P.desc[static_cast<size_t>(j) * P.cap + lo].idx != nullptr;
             list = __all_sync(0xffffffffu, list);
             if (lane == 0) S.list = list;
             __syncwarp();
             cur = lo;
+            te_valid = false;
         }
         const uint64_t ku = u - P.unit_first[lo];
+        bool preloaded = false;
+        if (S.list) {  // one tile per unit: entries [toff[ku], toff[ku + 1])
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = lane + 32 * h;
+                if (j < N) {
+                    if (te_valid) {
+                        S.carry[j] = S.tend[j];
+                        S.tend[j] = te[h];
+                    } else {
+                        S.carry[j] = ldg_u32(S.rec[j].toff + ku);
+                        S.tend[j] = ldg_u32(S.rec[j].toff + ku + 1);
+                    }
+                }
+            }
+            te_valid = u + 1 < u1 && u + 1 < P.unit_first[lo + 1];
+            if (te_valid) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int j = lane + 32 * h;
+                    if (j < N) te[h] = ldg_u32(S.rec[j].toff + ku + 2);
+                }
+            }
+            preloaded = true;
+        }
         if (P.desc[lo].w == 4)
-            fold_dense_unit<4>(P, lo, ku, S, lane, phase, bad);
+            fold_dense_unit<4>(P, lo, ku, S, lane, phase, preloaded, bad);
         else
-            fold_dense_unit<2>(P, lo, ku, S, lane, phase, bad);
+            fold_dense_unit<2>(P, lo, ku, S, lane, phase, preloaded, bad);
         if (__any_sync(0xffffffffu, bad)) {
             if (lane == 0) tc_set_err(P.err, TC_ERR_CORRUPT);
             break;
