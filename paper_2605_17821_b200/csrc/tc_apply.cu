@@ -140,9 +140,11 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
             tc_set_err(P.err, s_code);
             P.info[0] = 0;
             P.info[1] = 0;
+            P.info[2] = 0;
+            P.info[3] = 0;
         } else {
             const unsigned R = s_nrec[0];
-            uint64_t u = 0;
+            uint64_t u = 0, ndense = 0;
             for (unsigned r = 0; r < R; ++r) {
                 P.unit_first[r] = u;
                 FoldRec& a = P.desc[r];
@@ -153,10 +155,13 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
                 uint64_t sum = 0;
                 for (int k = 0; k < P.nrec; ++k) sum += P.desc[static_cast<size_t>(k) * P.cap + r].count;
                 a.dense = sum * 1000ull > static_cast<uint64_t>(a.m) * P.dense_permille ? 1u : 0u;
+                ndense += a.dense;
             }
             P.unit_first[R] = u;
             P.info[0] = R;
             P.info[1] = u;
+            P.info[2] = ndense;      // chunks for fold_dense_kernel
+            P.info[3] = R - ndense;  // chunks for fold_kernel
         }
     }
 }
@@ -367,6 +372,7 @@ __global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const __grid_cons
     __shared__ uint32_t s_imask[kFoldWarps][kSubGroups * 32];  // index-mode records: built mask words
     if (*reinterpret_cast<volatile unsigned*>(P.err) != 0) return;  // sticky error pending
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (P.info[3] == 0) return;  // every chunk is folded by fold_dense_kernel
     const uint64_t R = P.info[0];
     const uint64_t total = P.info[1];
     const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * kFoldWarps;
@@ -886,6 +892,7 @@ __global__ void __launch_bounds__(kDenseThreads, kDenseBlocksPerSM) fold_dense_k
     if (*reinterpret_cast<volatile unsigned*>(P.err) != 0) return;  // sticky error pending
     const int lane = threadIdx.x & 31;
     const int N = P.nrec;
+    if (P.info[2] == 0) return;  // no dense chunk
     const uint64_t R = P.info[0];
     const uint64_t total = P.info[1];
     if (blockIdx.x * kDenseRun >= total) return;

@@ -121,7 +121,7 @@ struct FoldParams {
     uint32_t dense_permille;  // chunk r is dense when sum_j count_j * 1000 > m * dense_permille
     FoldRec* desc;          // [nrec][cap]
     uint64_t* unit_first;   // [cap + 1]
-    unsigned long long* info;  // [0] = records per diff, [1] = total units
+    unsigned long long* info;  // [0] records per diff, [1] total units, [2] dense chunks, [3] scattered chunks
     unsigned int* err;
 };
 

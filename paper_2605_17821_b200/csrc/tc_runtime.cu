@@ -22,7 +22,7 @@ struct tc_ctx {
     // index-mode mask staging: kMaskStageWords per scan block
     void* mstage = nullptr;
     size_t mstage_bytes = 0;
-    // fold scratch: desc [nrec*cap] | unit_first [cap+1] | info [2]
+    // fold scratch: desc [nrec*cap] | unit_first [cap+1] | info [4]
     void* fold = nullptr;
     size_t fold_bytes = 0;
     unsigned int* err = nullptr;  // sticky device error word
@@ -418,7 +418,7 @@ tc_status tc_diff_apply(tc_ctx* ctx, void* const* state, const uint64_t* n_words
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaSetDevice(ctx->device);
     const size_t desc_bytes = sizeof(FoldRec) * cap * n_records;
-    const size_t need = desc_bytes + 8 * (cap + 1) + 16;
+    const size_t need = desc_bytes + 8 * (cap + 1) + 32;
     tc_status st = ensure(&ctx->fold, &ctx->fold_bytes, need, s);
     if (st != TC_OK) return st;
     uint8_t* base = static_cast<uint8_t*>(ctx->fold);
