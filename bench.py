@@ -35,6 +35,21 @@ sys.path.insert(0, ROOT)
 # independent hardware work queues for the compute / copy / comm streams (the default of 8
 # connections can alias two streams onto one queue and serialize them)
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# stdout carries only the JSON line: anything a library writes to fd 1 (NCCL's version banner)
+# goes to stderr, and the JSON is written through a private duplicate of the original stdout
+_JSON_OUT = sys.stdout
+
+
+def _private_stdout():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
+def emit(res):
+    _JSON_OUT.write(json.dumps(res) + "\n")
+    _JSON_OUT.flush()
 
 import numpy as np  # noqa: E402
 
@@ -218,9 +233,11 @@ def run_ours(args):
     free = torch.cuda.mem_get_info(dev)[0]
     est = int(min(cap, (args.f * 1.1 + 0.05) * W + (64 << 20)))
     spill_need = (sum(sizes) // 4096 + 1) * (8192 + 1024)  # encode scratch (index mode: 8 KB spill + mask stage)
-    rec_cap = cap if 2 * cap + spill_need + (8 << 30) < free else est
+    rec_cap = cap if 2 * cap + est + spill_need + (8 << 30) < free else est
     recs = [torch.empty(rec_cap, dtype=torch.uint8, device=dev) for _ in range(2)]
-    recv = torch.empty(rec_cap, dtype=torch.uint8, device=dev) if comm else None
+    # the Tier-2 receive buffer: the neighbour's record (its capacity is exchanged by
+    # tc_replicate_peer, so it need not be the worst-case bound)
+    recv = torch.empty(est, dtype=torch.uint8, device=dev) if comm else None
     # the encode kernel writes each record's length straight into mapped pinned memory, so the
     # host learns it without a copy-engine round trip
     ob_host = tc.HostBuffer(64)
@@ -388,7 +405,9 @@ def run_ours(args):
     restore = None
     if args.restore_chain > 0:
         restore = restore_bench(tc, ctx, X, Y, A, R, recs[0], sizes, wb, seed, p53, T, C, s_comp,
-                                args.restore_chain, args.structure, peak, dev, state["index"])
+                                args.restore_chain, args.structure, peak, dev, state["index"], comm=comm,
+                                spare=recs[1] if len(recs) > 1 else None,
+                                recovery=args.recovery if args.recovery is not None else workload == "cfg4")
         # put the step buffers back to the X / Y pair (X intact; Y, A, R were reused)
         with torch.cuda.stream(s_comp):
             for i in range(len(sizes)):
@@ -481,7 +500,7 @@ def run_ours(args):
         }
         if args.cpu_baseline and world == 1:
             res["cpu_baseline"] = cpu_baseline(workload, args)
-        print(json.dumps(res), flush=True)
+        emit(res)
     if comm is not None:
         comm.close()
     if world > 1:
@@ -646,7 +665,7 @@ def run_streaming(args, rank, world, local, dev):
             "e2e": None, "e2e_note": "not measured for cfg5: a per-step H2D of the 70.9 GB state would only "
                                      "measure PCIe (see the cfg2 line for the e2e contract)",
         }
-        print(json.dumps(res), flush=True)
+        emit(res)
     if comm is not None:
         comm.close()
     if world > 1:
@@ -654,8 +673,115 @@ def run_streaming(args, rank, world, local, dev):
         dist.destroy_process_group()
 
 
+def recovery_bench(tc, ctx, comm, X, Z, R, recs, lens, hosts, spare, s, dev):
+    """Config 4's "chained restore from base + differentials after a simulated GPU failure"
+    (BASELINE.json configs[3]; the paper's T_rollback + T_rerun).  The rank's state R
+    is overwritten (its HBM contents are lost), then rebuilt and checked against the chain head Z:
+    Tier-1: H2D of the base shard and the records from pinned host memory + one fold;
+    Tier-2 (N > 1): every rank pulls its base and records back from the ring neighbour that holds
+    them (tc_replicate_peer TO_PREV over NVLink) + one fold.  CUDA events, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    world = dist.get_world_size() if dist.is_initialized() else 1
+
+    def mx(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    out = {"records": len(recs), "base_bytes": sum(x.numel() * x.element_size() for x in X),
+           "record_bytes_total": sum(lens)}
+    # Tier-1 copy of the base (the last base checkpoint, staged once)
+    hb = [tc.HostBuffer(x.numel() * x.element_size()) for x in X]
+    for h, x in zip(hb, X):
+        tc.stage_host(h, x, x.numel() * x.element_size(), tc.D2H, stream=s)
+    s.synchronize()
+
+    def fail():
+        with torch.cuda.stream(s):
+            for r_ in R:
+                r_.fill_(0x5A)  # the failed GPU's state is gone
+        s.synchronize()
+
+    fail()
+    staged = [torch.empty(max(n, 16), dtype=torch.uint8, device=dev) for n in lens]
+    e = [ev() for _ in range(4)]
+    e[0].record(s)
+    for r_, h in zip(R, hb):
+        tc.stage_host(r_, h, r_.numel() * r_.element_size(), tc.H2D, stream=s)
+    e[1].record(s)
+    for d, h, n in zip(staged, hosts, lens):
+        tc.stage_host(d, h, n, tc.H2D, stream=s)
+    e[2].record(s)
+    tc.diff_apply(ctx, R, 0, staged, lens, stream=s)
+    e[3].record(s)
+    s.synchronize()
+    ctx.check(s)
+    ok1 = all(torch.equal(r_, z) for r_, z in zip(R, Z))
+    out["tier1"] = {"base_h2d_ms": round(mx(e[0].elapsed_time(e[1])), 3),
+                    "records_h2d_ms": round(mx(e[1].elapsed_time(e[2])), 3),
+                    "fold_ms": round(mx(e[2].elapsed_time(e[3])), 3),
+                    "total_ms": round(mx(e[0].elapsed_time(e[3])), 3),
+                    "restored_equals_head": bool(ok1)}
+    for h in hb:
+        h.free()
+    if comm is not None:
+        # save side (untimed): base segments and records -> the next rank's holding buffer, laid
+        # out by the previous rank's sizes (shards and records differ in size between ranks)
+        mine = [x.numel() * x.element_size() for x in X] + list(lens)
+        every = [None] * world
+        dist.all_gather_object(every, mine)
+        prev_sizes = every[(dist.get_rank() - 1) % world]
+        offs, o = [], 0
+        for n in prev_sizes:
+            offs.append(o)
+            o += (n + 15) // 16 * 16
+        holder = spare if spare is not None and spare.numel() >= o else None
+        if holder is None:
+            free = torch.cuda.mem_get_info(dev)[0]
+            if free > o + (4 << 30):
+                holder = torch.empty(o, dtype=torch.uint8, device=dev)
+        if holder is None:
+            out["tier2"] = {"skipped": "no room for the neighbour's base + records on this GPU"}
+            return out
+        srcs = [x.view(torch.uint8) for x in X] + [r[:n] for r, n in zip(recs, lens)]
+        for src, off, pn in zip(srcs, offs, prev_sizes):
+            nb = torch.tensor([src.numel()], dtype=torch.int64, device=dev)
+            comm.replicate_peer(src, nb, holder[off: off + pn], tc.TO_NEXT, stream=s)
+        s.synchronize()
+        fail()
+        dist.barrier()
+        dsts = [r_.view(torch.uint8) for r_ in R] + [d[:n] for d, n in zip(staged, lens)]
+        nbs = [torch.tensor([pn], dtype=torch.int64, device=dev) for pn in prev_sizes]
+        e = [ev() for _ in range(4)]
+        e[0].record(s)
+        for i, (d, off, nb, pn) in enumerate(zip(dsts, offs, nbs, prev_sizes)):
+            if i == len(X):
+                e[1].record(s)
+            comm.replicate_peer(holder[off: off + pn], nb, d, tc.TO_PREV, stream=s)
+        e[2].record(s)
+        tc.diff_apply(ctx, R, 0, staged, lens, stream=s)
+        e[3].record(s)
+        s.synchronize()
+        ctx.check(s)
+        ok2 = all(torch.equal(r_, z) for r_, z in zip(R, Z))
+        out["tier2"] = {"base_pull_ms": round(mx(e[0].elapsed_time(e[1])), 3),
+                        "records_pull_ms": round(mx(e[1].elapsed_time(e[2])), 3),
+                        "fold_ms": round(mx(e[2].elapsed_time(e[3])), 3),
+                        "total_ms": round(mx(e[0].elapsed_time(e[3])), 3),
+                        "base_pull_gbs": round(out["base_bytes"] / mx(e[0].elapsed_time(e[1])) / 1e6, 1),
+                        "restored_equals_head": bool(ok2)}
+        del holder
+    del staged
+    return out
+
+
 def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nrec, structure, peak, dev,
-                  index_mode=False):
+                  index_mode=False, comm=None, spare=None, recovery=False):
     """a7 at N = nrec (SURVEY §8(a), config 4's "chained restore of 8 differentials"): build a real
     chain of `nrec` incremental records (versions 1..nrec, each a fresh f-change set), then
     (1) fold all of them onto a base copy in one tc_diff_apply call (records resident in HBM), and
@@ -724,6 +850,7 @@ def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nre
         del staged
     ctx.check(s)
     ok = all(torch.equal(r_, z) for r_, z in zip(R, Z))
+    rec_out = recovery_bench(tc, ctx, comm, X, Z, R, recs, lens, hosts, spare, s, dev) if recovery else None
     # algorithmic bytes of the fold: every record's mask + tile_off + header, the winning values
     # read and the state words written (word-granular), SURVEY §8(d)
     meta = 0
@@ -750,7 +877,8 @@ def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nre
             "stream_bytes": stream_b, "hbm_gbs_stream": round(stream_b / fm / 1e6, 1),
             "frac_hbm_stream": round(stream_b / fm / 1e6 / peak, 4),
             "tier1_restore_ms": round(statistics.median(t1_ms), 3),
-            "restored_equals_head": bool(ok)}
+            "restored_equals_head": bool(ok),
+            "failure_recovery": rec_out}
 
 
 def replicate_probe(tc, comm, rec, obytes, recv, rec_bytes, dev, s_comm):
@@ -943,10 +1071,11 @@ def run_reference(args):
                          "host": host_desc()},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(res), flush=True)
+    emit(res)
 
 
 def main():
+    _private_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -964,6 +1093,8 @@ def main():
                     help="record format: mask, index (u16 positions), or adaptive per step from density")
     ap.add_argument("--restore-chain", type=int, default=8, help="records in the chained-restore probe (0: off)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--recovery", type=int, default=None,
+                    help="simulated-failure recovery probe (Tier-1 and, N > 1, Tier-2); default: on for cfg4")
     ap.add_argument("--fold-dense-permille", type=int, default=None,
                     help="restore strategy threshold (tc_ctx_set_fold_dense_permille); default: libtc's")
     ap.add_argument("--cpu-baseline", type=int, default=1)

@@ -18,6 +18,32 @@ import torch
 
 
 # --------------------------------------------------------------------- ring + consensus ----
+def bind_local_numa(device: int) -> str:
+    """Bind this process to the CPUs of GPU `device`'s NUMA node, so the pinned Tier-1 staging
+    buffers allocated afterwards (first touch) live in host memory local to the GPU's PCIe root
+    ("local volatile memory", §1).  Reads the PCI bus id from torch and the node's
+    CPU list from sysfs; a no-op (with the reason returned) where either is unavailable."""
+    import os
+
+    try:
+        p = torch.cuda.get_device_properties(device)
+        bus = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        base = f"/sys/bus/pci/devices/{bus}"
+        node = int(open(f"{base}/numa_node").read().strip())
+        cpus_txt = open(f"{base}/local_cpulist").read().strip()
+    except (OSError, ValueError, AttributeError, RuntimeError) as e:
+        return f"no binding ({type(e).__name__})"
+    cpus = set()
+    for part in cpus_txt.split(","):
+        a, _, b = part.partition("-")
+        cpus.update(range(int(a), int(b or a) + 1))
+    cpus &= os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else cpus
+    if not cpus:
+        return f"no binding (GPU {bus} on node {node}: no allowed CPU in {cpus_txt})"
+    os.sched_setaffinity(0, cpus)
+    return f"GPU {bus} NUMA node {node}: bound to CPUs {cpus_txt}"
+
+
 def ring_peers(rank: int, world: int) -> tuple[int, int]:
     """(next, prev): rank r replicates to (r+1) mod P and holds the replica of (r-1) mod P."""
     if world < 1 or not 0 <= rank < world:
