@@ -197,6 +197,45 @@ tc_status tc_replicate_peer(tc_comm* comm, const void* send, const uint64_t* sen
                             void* recv, uint64_t recv_cap, uint64_t* recv_bytes, int direction,
                             tc_stream comm_stream);
 
+/* Tier-2 without NCCL: device-initiated push over NVLink peer memory (SURVEY.md §8(f) NEXT row
+ * 1, "the ring peer's registered window ... Tier-2 via NVLink stores"; §3.1 ring
+ * mapping, §3.2 size exchange — here the size travels with the payload).
+ * The RECEIVER owns a slot (the neighbour's record lands there) and a 16-byte mailbox
+ * {u64 bytes, u64 version}, both allocated with tc_ipc_alloc in its own GPU memory; it passes
+ * their handles to its ring neighbour (the caller's transport, e.g. torch.distributed), which
+ * maps them with tc_ipc_open.  One process per GPU; peers on one NVLink/NVSwitch domain. */
+#define TC_IPC_HANDLE_BYTES 64
+/* cudaMalloc `bytes` on the current device, zero-filled, and its IPC handle.  Errors:
+ * TC_ERR_NOMEM, TC_ERR_CUDA. */
+tc_status tc_ipc_alloc(uint64_t bytes, void** dev_ptr, uint8_t handle[TC_IPC_HANDLE_BYTES]);
+tc_status tc_ipc_free(void* dev_ptr);
+/* Map a peer process's tc_ipc_alloc allocation into this process (peer access enabled lazily);
+ * *dev_ptr is valid on the current device until tc_ipc_close. */
+tc_status tc_ipc_open(const uint8_t handle[TC_IPC_HANDLE_BYTES], void** dev_ptr);
+tc_status tc_ipc_close(void* dev_ptr);
+/* Copy the record at `src` (its length: the u64 at `src_bytes`, device or mapped pinned
+ * memory, as written by tc_diff_encode — read on the device, no host round trip) into the
+ * peer slot `peer_dst` (capacity peer_cap) with NVLink stores from every SM, then publish
+ * {bytes, version} to `peer_mailbox` with a system-scope release.  A record larger than
+ * peer_cap is not copied; the mailbox then carries bytes = UINT64_MAX (the receiver's
+ * tc_peer_wait reports TC_ERR_CAPACITY).  version >= 1.  Stream-ordered on `stream`; the
+ * caller orders reuse of a slot (e.g. one slot per in-flight version). */
+tc_status tc_push_peer(tc_ctx* ctx, const void* src, const uint64_t* src_bytes, void* peer_dst,
+                       uint64_t peer_cap, void* peer_mailbox, uint64_t version, tc_stream stream);
+/* Encode (as tc_diff_encode) and push the record to the peer slot in one stream-ordered call:
+ * the Tier-2 copy leaves as soon as the record is complete, with no host synchronization and
+ * no NCCL. */
+tc_status tc_diff_encode_push(tc_ctx* ctx, const tc_segment* segs, int nseg, const tc_encode_opts* opts,
+                              uint64_t version, uint64_t ref_version, void* out, uint64_t out_cap,
+                              uint64_t* out_bytes, void* peer_dst, uint64_t peer_cap,
+                              void* peer_mailbox, tc_stream stream);
+/* Receiver: stream-ordered wait until this GPU's mailbox holds `version` (device spin with a
+ * watchdog, system-scope acquire); then *bytes_out (device or mapped pinned memory, may be
+ * NULL) = the received length.  Sticky errors: TC_ERR_CAPACITY (the record did not fit the
+ * slot), TC_ERR_INTERNAL (nothing arrived within the watchdog, ~10 s). */
+tc_status tc_peer_wait(tc_ctx* ctx, const void* mailbox, uint64_t version, uint64_t* bytes_out,
+                       tc_stream stream);
+
 /* ------------------------------------------------------------------- RETRIEVE ---- */
 /* Restore (§3.3 fused multi-step replay: "reads ...
  * exactly once, applies ... in temporal order ... and writes the final results back").

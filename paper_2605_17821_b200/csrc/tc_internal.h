@@ -132,6 +132,12 @@ cudaError_t launch_fold(const FoldParams& p, cudaStream_t s, int num_sms, uint64
 // thread-local detail string
 void set_error(const std::string& msg);
 
+// tc_ctx accessors for the other translation units (the struct is private to tc_runtime.cu)
+unsigned int* ctx_err(tc_ctx* c);
+int ctx_device(tc_ctx* c);
+int ctx_num_sms(tc_ctx* c);
+void ctx_add_launches(tc_ctx* c, uint64_t n);
+
 }  // namespace tc
 
 // device-side sticky error: first error wins

@@ -25,7 +25,7 @@ struct tc_ctx {
     // fold scratch: desc [nrec*cap] | unit_first [cap+1] | info [4]
     void* fold = nullptr;
     size_t fold_bytes = 0;
-    unsigned int* err = nullptr;  // sticky device error word
+    unsigned int* err = nullptr;  // [0] sticky device error word, [1] tc_push_peer block counter
     uint64_t launches = 0;
     uint32_t fold_dense_permille = 30;  // tc_ctx_set_fold_dense_permille
 };
@@ -467,3 +467,10 @@ tc_status tc_host_free(void* p) {
 }
 
 }  // extern "C"
+
+namespace tc {
+unsigned int* ctx_err(tc_ctx* c) { return c->err; }
+int ctx_device(tc_ctx* c) { return c->device; }
+int ctx_num_sms(tc_ctx* c) { return c->num_sms; }
+void ctx_add_launches(tc_ctx* c, uint64_t n) { c->launches += n; }
+}  // namespace tc

@@ -78,6 +78,17 @@ def _load():
                                 ctypes.POINTER(vp), ctypes.POINTER(u64), cint, vp]
     L.tc_synth_base.argtypes = [vp, u64, u32, u64, u32, u64, vp]
     L.tc_synth_step.argtypes = [vp, u64, u32, u64, u32, u64, u64, cint, u64, vp]
+    L.tc_ipc_alloc.argtypes = [u64, ctypes.POINTER(vp), ctypes.c_char_p]
+    L.tc_ipc_free.argtypes = [vp]
+    L.tc_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
+    L.tc_ipc_close.argtypes = [vp]
+    L.tc_push_peer.argtypes = [vp, vp, vp, vp, u64, vp, u64, vp]
+    L.tc_diff_encode_push.argtypes = [vp, ctypes.POINTER(Segment), cint, ctypes.POINTER(EncodeOpts), u64, u64,
+                                      vp, u64, vp, vp, u64, vp, vp]
+    L.tc_peer_wait.argtypes = [vp, vp, u64, vp, vp]
+    for name in ("tc_ipc_alloc", "tc_ipc_free", "tc_ipc_open", "tc_ipc_close", "tc_push_peer",
+                 "tc_diff_encode_push", "tc_peer_wait"):
+        getattr(L, name).restype = cint
     for name in ("tc_ctx_create", "tc_ctx_destroy", "tc_ctx_check", "tc_diff_bound", "tc_diff_encode",
                  "tc_stage_host", "tc_diff_bound_range", "tc_diff_encode_range", "tc_host_alloc", "tc_host_free", "tc_comm_get_unique_id", "tc_comm_init", "tc_comm_destroy",
                  "tc_replicate_peer", "tc_diff_apply", "tc_synth_base", "tc_synth_step"):
@@ -198,6 +209,80 @@ def diff_encode(ctx: Ctx, ref, cur, out: torch.Tensor, out_bytes: torch.Tensor, 
     _check(LIB.tc_diff_encode(ctx.h, segs, len(ref), ctypes.byref(o), version, ref_version, out.data_ptr(),
                               out.numel() * out.element_size(), out_bytes.data_ptr(), _stream(stream)),
            "tc_diff_encode")
+
+
+IPC_HANDLE_BYTES = 64
+
+
+class IpcBuffer:
+    """Receiver side of the NVLink push (tc_ipc_alloc): device memory in this GPU whose IPC
+    handle (``.handle``, 64 bytes) the ring neighbour maps.  ``.tensor`` is a zero-copy uint8
+    CUDA view (``__cuda_array_interface__``)."""
+
+    def __init__(self, nbytes: int):
+        p = vp()
+        h = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+        _check(LIB.tc_ipc_alloc(int(nbytes), ctypes.byref(p), h), "tc_ipc_alloc")
+        self.ptr, self.nbytes, self.handle = p.value, int(nbytes), h.raw
+        self.__cuda_array_interface__ = {"shape": (self.nbytes,), "typestr": "|u1", "data": (self.ptr, False),
+                                         "version": 2, "strides": None}
+        self.tensor = torch.as_tensor(self, device="cuda")
+
+    def data_ptr(self):
+        return self.ptr
+
+    def numel(self):
+        return self.nbytes
+
+    def element_size(self):
+        return 1
+
+    def free(self):
+        if self.ptr:
+            self.tensor = None
+            LIB.tc_ipc_free(self.ptr)
+            self.ptr = None
+
+
+class PeerMapping:
+    """Sender side: a neighbour's IpcBuffer mapped into this process (tc_ipc_open)."""
+
+    def __init__(self, handle: bytes, nbytes: int):
+        p = vp()
+        _check(LIB.tc_ipc_open(handle, ctypes.byref(p)), "tc_ipc_open")
+        self.ptr, self.nbytes = p.value, int(nbytes)
+
+    def data_ptr(self):
+        return self.ptr
+
+    def close(self):
+        if self.ptr:
+            LIB.tc_ipc_close(self.ptr)
+            self.ptr = None
+
+
+def push_peer(ctx: Ctx, src: torch.Tensor, src_bytes, peer_dst, peer_cap: int, peer_mailbox, version: int,
+              stream=None):
+    """Enqueue tc_push_peer: the record at ``src`` (length: the u64 at ``src_bytes``) -> the peer slot."""
+    _check(LIB.tc_push_peer(ctx.h, src.data_ptr(), src_bytes.data_ptr(), peer_dst.data_ptr(), int(peer_cap),
+                            peer_mailbox.data_ptr(), version, _stream(stream)), "tc_push_peer")
+
+
+def diff_encode_push(ctx: Ctx, ref, cur, out: torch.Tensor, out_bytes, version: int, ref_version: int, peer_dst,
+                     peer_cap: int, peer_mailbox, tile_words=4096, chunk_words=1 << 28, advance_ref=True,
+                     stream=None, index_mode=False):
+    """Enqueue tc_diff_encode_push: encode, then push the record into the ring neighbour's slot."""
+    segs = segments(ref, cur)
+    o = _opts(tile_words, chunk_words, advance_ref, index_mode)
+    _check(LIB.tc_diff_encode_push(ctx.h, segs, len(ref), ctypes.byref(o), version, ref_version, out.data_ptr(),
+                                   out.numel() * out.element_size(), out_bytes.data_ptr(), peer_dst.data_ptr(),
+                                   int(peer_cap), peer_mailbox.data_ptr(), _stream(stream)), "tc_diff_encode_push")
+
+
+def peer_wait(ctx: Ctx, mailbox, version: int, bytes_out=None, stream=None):
+    """Enqueue tc_peer_wait on this GPU's mailbox (IpcBuffer) for ``version``."""
+    _check(LIB.tc_peer_wait(ctx.h, mailbox.data_ptr(), version, None if bytes_out is None else bytes_out.data_ptr(),
+                            _stream(stream)), "tc_peer_wait")
 
 
 def diff_bound_range(n_words: int, word_bytes: int, first_chunk: int, n_chunks: int, tile_words=4096,
