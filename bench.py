@@ -238,6 +238,21 @@ def run_ours(args):
     # the Tier-2 receive buffer: the neighbour's record (its capacity is exchanged by
     # tc_replicate_peer, so it need not be the worst-case bound)
     recv = torch.empty(est, dtype=torch.uint8, device=dev) if comm else None
+    # NCCL-free Tier-2 (--tier2 push): two IPC slots + mailboxes on this GPU receive the previous
+    # rank's records; the next rank's are mapped here and written with NVLink stores
+    push = None
+    if comm is not None and args.tier2 == "push":
+        import torch.distributed as dist
+
+        mine = {"slots": [tc.IpcBuffer(est) for _ in range(2)], "mail": [tc.IpcBuffer(16) for _ in range(2)]}
+        hs = [None] * world
+        dist.all_gather_object(hs, [b.handle for b in mine["slots"]] + [m.handle for m in mine["mail"]])
+        nxt_h = hs[(rank + 1) % world]
+        pctx = tc.Ctx(local)
+        pctx.set_push_ctas(args.push_ctas)
+        push = {"mine": mine, "cap": est, "ctx": pctx, "ctas": args.push_ctas,
+                "peer_slots": [tc.PeerMapping(h, est) for h in nxt_h[:2]],
+                "peer_mail": [tc.PeerMapping(h, 16) for h in nxt_h[2:]]}
     # the encode kernel writes each record's length straight into mapped pinned memory, so the
     # host learns it without a copy-engine round trip
     ob_host = tc.HostBuffer(64)
@@ -304,7 +319,7 @@ def run_ours(args):
         # Tier-2: ring-neighbour replication, issued from a background thread (the size exchange
         # blocks its caller until both neighbours are ready; the training-side thread must not)
         fut = None
-        if comm is not None:
+        if comm is not None and push is None:
             def _replicate(slot=slot, e1=e1, nb=nbytes):
                 s_comm.wait_event(e1)
                 r0, r1 = ev(), ev()
@@ -320,6 +335,17 @@ def run_ours(args):
         tc.diff_apply(ctx, R, state["rest_version"], [recs[slot]], [nbytes], stream=s_comp)
         f1.record(s_comp)
         host_t["fold"].append(time.perf_counter() - th0)
+        if push is not None:
+            # Tier-2 push: kernels only (no host synchronization, no helper thread), started after
+            # the fold so its NVLink stores overlap the next encode rather than the latency-bound fold
+            s_comm.wait_event(f1)
+            r0, r1 = ev(), ev()
+            r0.record(s_comm)
+            tc.push_peer(push["ctx"], recs[slot], obytes[slot], push["peer_slots"][slot], push["cap"],
+                         push["peer_mail"][slot], v, stream=s_comm)
+            tc.peer_wait(push["ctx"], push["mine"]["mail"][slot], v, None, stream=s_comm)
+            r1.record(s_comm)
+            fut = _Done((r0, r1, nbytes))
         state["rest_version"] = v
         state["ref_version"] = v
         state["content"] = "Y" if state["content"] == "X" else "X"
@@ -353,7 +379,7 @@ def run_ours(args):
     clocks = Clocks(local)
     clocks.start()
     time.sleep(0.3)
-    launches0 = ctx.launches
+    launches0 = ctx.launches + (push["ctx"].launches if push else 0)
     t_start, t_end = ev(), ev()
     t_start.record(s_comp)
     sizes_seen = []
@@ -367,11 +393,13 @@ def run_ours(args):
     t_end.record(s_comp)
     sync_all()
     torch.cuda.synchronize()
-    launches = ctx.launches - launches0
+    launches = ctx.launches + (push["ctx"].launches if push else 0) - launches0
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
     ctx.check(s_comp)
+    if push:
+        push["ctx"].check(s_comm)
     ms = t_start.elapsed_time(t_end)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -419,7 +447,7 @@ def run_ours(args):
         state["content"] = "X"
     rep_probe = None
     if comm is not None:
-        rep_probe = replicate_probe(tc, comm, recs[0], obytes, recv, rec_bytes, dev, s_comm)
+        rep_probe = replicate_probe(tc, comm, recs[0], obytes, recv, rec_bytes, dev, s_comm, push)
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, tc, ctx, dev, sizes, wb, X, Y, A, R, recs, obytes, host_ring, rec_cap, T, C,
@@ -454,8 +482,9 @@ def run_ours(args):
                 "record_format": args.format,
                 "record_modes_timed": sorted(set(state["modes"])),
                 "l2": f"no flush: every step streams {W / 1e9:.1f} GB of state per rank (> 126 MB L2)",
-                "step": "encode(advance_ref) + D2H stage + " + ("NCCL ring replicate + " if world > 1 else "")
-                        + "fold onto restore replica",
+                "step": "encode(advance_ref) + D2H stage + " + (
+                    ("NVLink push to the ring neighbour's IPC slot + " if push else "NCCL ring replicate + ")
+                    if world > 1 else "") + "fold onto restore replica",
                 "parallelism": f"dp{world} (independent ZeRO shards; Tier-2 ring r->r+1)" if world > 1 else "1 GPU",
             },
             "roofline": {
@@ -673,6 +702,16 @@ def run_streaming(args, rank, world, local, dev):
         dist.destroy_process_group()
 
 
+class _Done:
+    """An already-completed future (the push path enqueues kernels and returns at once)."""
+
+    def __init__(self, value):
+        self.value = value
+
+    def result(self):
+        return self.value
+
+
 def recovery_bench(tc, ctx, comm, X, Z, R, recs, lens, hosts, spare, s, dev):
     """Config 4's "chained restore from base + differentials after a simulated GPU failure"
     (BASELINE.json configs[3]; the paper's T_rollback + T_rerun).  The rank's state R
@@ -881,45 +920,83 @@ def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nre
             "failure_recovery": rec_out}
 
 
-def replicate_probe(tc, comm, rec, obytes, recv, rec_bytes, dev, s_comm):
-    """Tier-2 in isolation: ring shifts of this step's record (size exchange + payload through
-    tc_replicate_peer) and of a fixed 1 GiB payload, CUDA events on the comm stream, max over
-    ranks."""
+def replicate_probe(tc, comm, rec, obytes, recv, rec_bytes, dev, s_comm, push=None):
+    """Tier-2 in isolation: ring shifts of this step's record and of a fixed 1 GiB payload through
+    tc_replicate_peer (NCCL: size exchange + send/recv) and, with --tier2 push, through
+    tc_push_peer + tc_peer_wait (NVLink stores into the neighbour's IPC slot).  CUDA events on
+    the comm stream, max over ranks."""
     import torch
     import torch.distributed as dist
 
-    def timed(send, nb, rcv, reps=5):
-        for _ in range(2):
-            comm.replicate_peer(send, nb, rcv, tc.TO_NEXT, stream=s_comm)
+    def timed(fn, reps=5):
+        for i in range(2):
+            fn(i)
         s_comm.synchronize()
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s_comm)
-        for _ in range(reps):
-            comm.replicate_peer(send, nb, rcv, tc.TO_NEXT, stream=s_comm)
+        for i in range(reps):
+            fn(2 + i)
         e1.record(s_comm)
         s_comm.synchronize()
         t = torch.tensor([e0.elapsed_time(e1) / reps], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    nb_dev = torch.tensor([rec_bytes], dtype=torch.int64, device=dev)
-    ms_rec = timed(rec, nb_dev, recv)
+    def frac(g):
+        return {"gbs_per_direction": round(g, 1), "frac_nvlink_nominal": round(g / NVLINK_GBS, 4),
+                "frac_nvlink_measured": round(g / NVLINK_MEASURED_GBS, 4)}
+
     G = 1 << 30
+    nb_dev = torch.tensor([rec_bytes], dtype=torch.int64, device=dev)
     big = torch.empty(G, dtype=torch.uint8, device=dev)
     big_r = torch.empty(G, dtype=torch.uint8, device=dev)
-    ms_1g = timed(big, torch.tensor([G], dtype=torch.int64, device=dev), big_r)
-    del big, big_r
-    g_rec = rec_bytes / ms_rec / 1e6
-    g_1g = G / ms_1g / 1e6
-    return {"record_bytes": rec_bytes, "ms": round(ms_rec, 4), "gbs_per_direction": round(g_rec, 1),
-            "frac_nvlink_nominal": round(g_rec / NVLINK_GBS, 4),
-            "frac_nvlink_measured": round(g_rec / NVLINK_MEASURED_GBS, 4),
-            "ring_shift_1GiB": {"ms": round(ms_1g, 4), "gbs_per_direction": round(g_1g, 1),
-                                "frac_nvlink_nominal": round(g_1g / NVLINK_GBS, 4),
-                                "frac_nvlink_measured": round(g_1g / NVLINK_MEASURED_GBS, 4)},
-            "note": "isolated tc_replicate_peer ring shift (size exchange + NCCL send/recv), max over ranks; "
-                    "nominal 900 GB/s, measured peer copy 770 GB/s (B200_PROFILING.md)"}
+    gb_dev = torch.tensor([G], dtype=torch.int64, device=dev)
+    ms_rec = timed(lambda i: comm.replicate_peer(rec, nb_dev, recv, tc.TO_NEXT, stream=s_comm))
+    ms_1g = timed(lambda i: comm.replicate_peer(big, gb_dev, big_r, tc.TO_NEXT, stream=s_comm))
+    del big_r
+    out = {"record_bytes": rec_bytes, "ms": round(ms_rec, 4), **frac(rec_bytes / ms_rec / 1e6),
+           "ring_shift_1GiB": {"ms": round(ms_1g, 4), **frac(G / ms_1g / 1e6)},
+           "note": "isolated tc_replicate_peer ring shift (size exchange + NCCL send/recv), max over ranks; "
+                   "nominal 900 GB/s, measured peer copy 770 GB/s (B200_PROFILING.md)"}
+    if push is not None:
+        pc = push["ctx"]
+        base = 1 << 40  # mailbox versions of the probe, above any step's version
+
+        def push_rec(i):
+            tc.push_peer(pc, rec, nb_dev, push["peer_slots"][0], push["cap"], push["peer_mail"][0], base + i,
+                         stream=s_comm)
+            tc.peer_wait(pc, push["mine"]["mail"][0], base + i, None, stream=s_comm)
+
+        ms_prec = timed(push_rec)
+        land, lmail = tc.IpcBuffer(G), tc.IpcBuffer(16)
+        hs = [None] * dist.get_world_size()
+        dist.all_gather_object(hs, [land.handle, lmail.handle])
+        nx = hs[(dist.get_rank() + 1) % len(hs)]
+        pl, pm = tc.PeerMapping(nx[0], G), tc.PeerMapping(nx[1], 16)
+
+        def push_1g(i):
+            tc.push_peer(pc, big, gb_dev, pl, G, pm, base + i, stream=s_comm)
+            tc.peer_wait(pc, lmail, base + i, None, stream=s_comm)
+
+        ms_p1g = timed(push_1g)
+        pc.set_push_ctas(2 * torch.cuda.get_device_properties(dev).multi_processor_count)
+        ms_p1g_max = timed(push_1g)
+        pc.set_push_ctas(push["ctas"])
+        pc.check(s_comm)
+        dist.barrier()
+        pl.close()
+        pm.close()
+        land.free()
+        lmail.free()
+        out["push"] = {"ms": round(ms_prec, 4), **frac(rec_bytes / ms_prec / 1e6),
+                       "ctas": push["ctas"],
+                       "ring_shift_1GiB": {"ms": round(ms_p1g, 4), **frac(G / ms_p1g / 1e6)},
+                       "ring_shift_1GiB_all_sms": {"ms": round(ms_p1g_max, 4), **frac(G / ms_p1g_max / 1e6)},
+                       "note": "tc_push_peer (NVLink stores from every SM into the neighbour's IPC-mapped slot, "
+                               "mailbox publish) + tc_peer_wait on the receiver; no NCCL, no host sync"}
+    del big
+    return out
 
 
 def run_e2e(args, tc, ctx, dev, sizes, wb, X, Y, A, R, recs, obytes, host_ring, rec_cap, T, C, state, world,
@@ -1093,6 +1170,10 @@ def main():
                     help="record format: mask, index (u16 positions), or adaptive per step from density")
     ap.add_argument("--restore-chain", type=int, default=8, help="records in the chained-restore probe (0: off)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--push-ctas", type=int, default=16,
+                    help="CTAs of the Tier-2 NVLink push inside the step (fewer = less interference)")
+    ap.add_argument("--tier2", default="push", choices=["push", "nccl"],
+                    help="Tier-2 replication: NVLink stores into the neighbour's IPC slot, or NCCL send/recv")
     ap.add_argument("--recovery", type=int, default=None,
                     help="simulated-failure recovery probe (Tier-1 and, N > 1, Tier-2); default: on for cfg4")
     ap.add_argument("--fold-dense-permille", type=int, default=None,

@@ -129,6 +129,10 @@ uint64_t tc_ctx_launches(const tc_ctx* ctx);
  * identical state.  Default 30 (3 %); 0 = always stream; UINT32_MAX = always scatter.
  * Takes effect for later tc_diff_apply calls.  Errors: TC_ERR_INVALID (NULL ctx). */
 tc_status tc_ctx_set_fold_dense_permille(tc_ctx* ctx, uint32_t permille);
+/* CTAs of tc_push_peer's NVLink copy on this ctx (0 = default 32).  More CTAs = more stores in
+ * flight (a 1 GiB push: ~530 GB/s at 16, ~600 at 32, ~700 at 296 per direction) but more
+ * interference with kernels running beside it.  Errors: TC_ERR_INVALID. */
+tc_status tc_ctx_set_push_ctas(tc_ctx* ctx, uint32_t ctas);
 
 /* ----------------------------------------------------------------------- SAVE ---- */
 /* Worst-case diff bytes for this shard layout (every word changed); host only.

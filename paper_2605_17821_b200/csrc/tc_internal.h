@@ -137,6 +137,7 @@ unsigned int* ctx_err(tc_ctx* c);
 int ctx_device(tc_ctx* c);
 int ctx_num_sms(tc_ctx* c);
 void ctx_add_launches(tc_ctx* c, uint64_t n);
+uint32_t ctx_push_ctas(tc_ctx* c);
 
 }  // namespace tc
 

@@ -16,7 +16,9 @@
 namespace {
 
 constexpr uint32_t kPushThreads = 512;
-constexpr uint32_t kWaitSpinLimit = 1u << 25;  // x ~300 ns sleep: ~10 s watchdog
+constexpr int kPushDepth = 8;
+constexpr int kPushCtas = 32;        // enough stores in flight for NVLink; leaves the SMs to the encode / fold        // 16-byte loads in flight per thread before their remote stores
+constexpr uint32_t kWaitSpinLimit = 1u << 22;  // x ~2 us sleep: ~10 s watchdog
 
 tc_status fail(tc_status s, const std::string& msg) {
     tc::set_error(msg);
@@ -45,7 +47,7 @@ __device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long
     return v;
 }
 
-// Grid-stride copy of the record, 4 independent 16-byte loads in flight per thread before their
+// Grid-stride copy of the record, kPushDepth independent 16-byte loads in flight per thread before their
 // (remote) stores; every block fences at system scope and counts itself out, the last one
 // publishes {bytes, version} with a release store into the peer's mailbox.
 __global__ void __launch_bounds__(kPushThreads) push_kernel(const uint4* __restrict__ src, const uint64_t* src_bytes,
@@ -57,13 +59,12 @@ __global__ void __launch_bounds__(kPushThreads) push_kernel(const uint4* __restr
         const uint64_t n = nb / 16;
         const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
         uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-        for (; i + 3 * stride < n; i += 4 * stride) {
-            const uint4 a = __ldg(src + i), b = __ldg(src + i + stride), c = __ldg(src + i + 2 * stride),
-                        d = __ldg(src + i + 3 * stride);
-            dst[i] = a;
-            dst[i + stride] = b;
-            dst[i + 2 * stride] = c;
-            dst[i + 3 * stride] = d;
+        for (; i + (kPushDepth - 1) * stride < n; i += kPushDepth * stride) {
+            uint4 v[kPushDepth];
+#pragma unroll
+            for (int q = 0; q < kPushDepth; ++q) v[q] = __ldg(src + i + q * stride);
+#pragma unroll
+            for (int q = 0; q < kPushDepth; ++q) dst[i + q * stride] = v[q];
         }
         for (; i < n; i += stride) dst[i] = __ldg(src + i);
     }
@@ -88,7 +89,7 @@ __global__ void peer_wait_kernel(const unsigned long long* mail, uint64_t versio
             tc_set_err(err, TC_ERR_INTERNAL);
             return;
         }
-        __nanosleep(256);
+        __nanosleep(2000);
     }
     unsigned long long b = ld_relaxed_sys(mail);
     if (b == ~0ull) {
@@ -152,7 +153,8 @@ tc_status tc_push_peer(tc_ctx* ctx, const void* src, const uint64_t* src_bytes, 
         return fail(TC_ERR_INVALID, "src_bytes / peer_mailbox missing or misaligned");
     if (version == 0) return fail(TC_ERR_INVALID, "version must be >= 1");
     cudaSetDevice(tc::ctx_device(ctx));
-    push_kernel<<<tc::ctx_num_sms(ctx), kPushThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+    const int ctas = tc::ctx_push_ctas(ctx) ? static_cast<int>(tc::ctx_push_ctas(ctx)) : kPushCtas;
+    push_kernel<<<ctas, kPushThreads, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const uint4*>(src), src_bytes, static_cast<uint4*>(peer_dst), peer_cap,
         static_cast<unsigned long long*>(peer_mailbox), version, tc::ctx_err(ctx) + 1);
     cudaError_t e = cudaGetLastError();

@@ -28,6 +28,7 @@ struct tc_ctx {
     unsigned int* err = nullptr;  // [0] sticky device error word, [1] tc_push_peer block counter
     uint64_t launches = 0;
     uint32_t fold_dense_permille = 30;  // tc_ctx_set_fold_dense_permille
+    uint32_t push_ctas = 0;              // tc_ctx_set_push_ctas (0: default)
 };
 
 namespace tc {
@@ -150,6 +151,13 @@ tc_status tc_ctx_create(int device, tc_ctx** out) {
         return cuda_fail(e, "cudaMalloc(err)");
     }
     *out = c;
+    return TC_OK;
+}
+
+tc_status tc_ctx_set_push_ctas(tc_ctx* c, uint32_t ctas) {
+    if (!c) return fail(TC_ERR_INVALID, "ctx is NULL");
+    if (ctas > 65535) return fail(TC_ERR_INVALID, "ctas must be <= 65535");
+    c->push_ctas = ctas;
     return TC_OK;
 }
 
@@ -473,4 +481,5 @@ unsigned int* ctx_err(tc_ctx* c) { return c->err; }
 int ctx_device(tc_ctx* c) { return c->device; }
 int ctx_num_sms(tc_ctx* c) { return c->num_sms; }
 void ctx_add_launches(tc_ctx* c, uint64_t n) { c->launches += n; }
+uint32_t ctx_push_ctas(tc_ctx* c) { return c->push_ctas; }
 }  // namespace tc
