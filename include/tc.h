@@ -146,8 +146,13 @@ tc_status tc_diff_bound(const tc_segment* segs, int nseg, const tc_encode_opts* 
  *   segs/nseg      the shard (device pointers), 1 <= nseg <= TC_MAX_SEGMENTS
  *   opts           NULL = defaults {4096, 1, 2^28}
  *   version        the iteration index of `cur`; ref_version that of `ref` (the chain link)
- *   out/out_cap    device buffer for the concatenated records; out_cap must be >=
- *                  tc_diff_bound(...) (else TC_ERR_CAPACITY, synchronously)
+ *   out/out_cap    device buffer for the concatenated records.  out_cap >= tc_diff_bound(...)
+ *                  always suffices; a smaller buffer (sized for the expected change fraction)
+ *                  is allowed: a record that does not fit is not written (nothing is written at
+ *                  or past out + out_cap), the device reports TC_ERR_CAPACITY (sticky, at
+ *                  tc_ctx_check) and *out_bytes still receives the length the diff needs.  With
+ *                  advance_ref the reference has then still advanced, so this version's diff is
+ *                  lost: the caller takes a base checkpoint (§3.1 base stream)
  *   out_bytes      device (or mapped pinned host) u64 the kernel sets to the diff's length
  *   stream         the encode is enqueued here; it reads ref/cur and (advance_ref) writes ref
  * Output bytes are identical to the oracle's for the same (inputs, T, C) (bit-exact). */
@@ -160,7 +165,8 @@ tc_status tc_diff_encode(tc_ctx* ctx, const tc_segment* segs, int nseg,
  * full tc_diff_encode output (same header segment_id / chunk_word_offset), so concatenating the
  * ranges of every segment in order reproduces the full diff.  Used when the full bound does not
  * fit in HBM next to the state (40B-shaped shards: SURVEY.md §7 build plan step 9).  `seg`
- * describes the WHOLE segment; out_cap >= tc_diff_bound_range(...) (else TC_ERR_CAPACITY);
+ * describes the WHOLE segment; out_cap as for tc_diff_encode (tc_diff_bound_range(...) always
+ * suffices; a smaller buffer gets the same device-side TC_ERR_CAPACITY behaviour);
  * *out_bytes (device or mapped pinned) receives the range's length. */
 tc_status tc_diff_bound_range(const tc_segment* seg, const tc_encode_opts* opts, uint64_t first_chunk,
                               uint64_t n_chunks, uint64_t* max_bytes);

@@ -142,9 +142,10 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
             P.info[1] = 0;
             P.info[2] = 0;
             P.info[3] = 0;
+            P.info[4] = 0;
         } else {
             const unsigned R = s_nrec[0];
-            uint64_t u = 0, ndense = 0;
+            uint64_t u = 0, ndense = 0, nlist = 0;
             for (unsigned r = 0; r < R; ++r) {
                 P.unit_first[r] = u;
                 FoldRec& a = P.desc[r];
@@ -155,13 +156,20 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
                 uint64_t sum = 0;
                 for (int k = 0; k < P.nrec; ++k) sum += P.desc[static_cast<size_t>(k) * P.cap + r].count;
                 a.dense = sum * 1000ull > static_cast<uint64_t>(a.m) * P.dense_permille ? 1u : 0u;
-                ndense += a.dense;
+                if (a.dense && a.T == kListT) {  // all index mode at T = 4096: the list kernel
+                    bool all_idx = true;
+                    for (int k = 0; k < P.nrec; ++k) all_idx = all_idx && P.desc[static_cast<size_t>(k) * P.cap + r].idx;
+                    if (all_idx) a.dense = 2u;
+                }
+                ndense += a.dense == 1u;
+                nlist += a.dense == 2u;
             }
             P.unit_first[R] = u;
             P.info[0] = R;
             P.info[1] = u;
-            P.info[2] = ndense;      // chunks for fold_dense_kernel
-            P.info[3] = R - ndense;  // chunks for fold_kernel
+            P.info[2] = ndense;              // chunks for fold_dense_kernel
+            P.info[3] = R - ndense - nlist;  // chunks for fold_kernel
+            P.info[4] = nlist;               // chunks for fold_list_kernel
         }
     }
 }
@@ -443,7 +451,6 @@ struct DenseSmem {
     uint32_t want[TC_MAX_FOLD];           // tile_off entry at the unit end
     uint32_t imask[kDSub / 32];           // index-mode positions -> mask words / touched lines
     uint64_t bar;                         // tile load barrier
-    uint32_t list;                        // every record is index mode with T == kDSub
 };
 
 __device__ __forceinline__ uint32_t ldg_u16(const uint8_t* base, uint32_t k) {
@@ -573,108 +580,6 @@ __device__ __forceinline__ void expand_run(word_t* tw, const word_t* sv, const u
     }
 }
 
-// "List" sub-unit: every record is an index-mode record whose tile is exactly this sub-unit
-// (T == kDSub), so record j's entries for it are [carry_j, tend_j): positions and values are
-// contiguous runs, staged with coalesced 16-byte copies and scattered into the tile oldest
-// record first, with no mask arithmetic.  Rounds fill the stage with whole records; a record
-// larger than the stage goes through it in pieces.
-template <int W>
-__device__ __forceinline__ uint32_t list_run_bytes(uint32_t a, uint32_t b, uint32_t& pb) {
-    if (b <= a) {
-        pb = 0;
-        return 0u;
-    }
-    pb = ((2u * b + 15u) & ~15u) - ((2u * a) & ~15u);
-    return pb + static_cast<uint32_t>(((static_cast<uint64_t>(b) * W + 15) & ~uint64_t(15)) -
-                                      (static_cast<uint64_t>(a) * W & ~uint64_t(15)));
-}
-
-template <int W>
-__device__ __forceinline__ void dense_list_sub(int N, uint32_t nw, DenseSmem& S, uint32_t& phase, int lane, bool& bad) {
-    using word_t = typename Word<W>::T;
-    constexpr uint32_t kStage = kDBatch * kWin;
-    constexpr uint32_t kPiece = ((kStage - 64) / (2 + W)) & ~7u;  // entries of a piece
-    word_t* tw = reinterpret_cast<word_t*>(S.tile);
-    uint8_t* sb = reinterpret_cast<uint8_t*>(S.stage);
-    uint32_t* touched = S.imask;  // per 32-word line: written
-#pragma unroll
-    for (uint32_t q = 0; q < kMW; ++q) touched[32 * q + lane] = 0u;
-    bool tile_ready = false;
-    int r = 0;
-    uint32_t a = S.carry[0], lastx = 0;
-    while (r < N) {
-        // the round's items, walked twice with the same logic: copies, then scatter
-        int r_end = r;
-        uint32_t a_end = a;
-        for (int pass = 0; pass < 2; ++pass) {
-            int rr = r;
-            uint32_t aa = a, used = 0, pb;
-            while (rr < N) {
-                const uint32_t k1 = S.tend[rr];
-                uint32_t bb = k1;
-                uint32_t sz = list_run_bytes<W>(aa, bb, pb);
-                if (used + sz > kStage) {
-                    if (used) break;
-                    bb = aa + kPiece;  // a piece of a record larger than the stage
-                    sz = list_run_bytes<W>(aa, bb, pb);
-                }
-                const DenseRec& D = S.rec[rr];
-                if (pass == 0) {
-                    if (sz) {
-                        const uint8_t* ps = D.body + ((2u * aa) & ~15u);
-                        const uint8_t* vs = D.values + (static_cast<uint64_t>(aa) * W & ~uint64_t(15));
-                        for (uint32_t o = 16 * lane; o < pb; o += 512) cp_async16(sb + used + o, ps + o);
-                        for (uint32_t o = 16 * lane; o < sz - pb; o += 512) cp_async16(sb + used + pb + o, vs + o);
-                    }
-                } else {
-                    const uint16_t* px = reinterpret_cast<const uint16_t*>(sb + used + ((2u * aa) & 15u));
-                    const word_t* pv = reinterpret_cast<const word_t*>(sb + used + pb + ((aa * W) & 15u));
-                    const uint32_t k0 = S.carry[rr];  // the record's first entry of this tile
-                    for (uint32_t k = lane; k < bb - aa; k += 32) {
-                        const uint32_t x = px[k];
-                        const bool has_prev = aa + k > k0;
-                        const uint32_t prev = k > 0 ? px[k - 1] : lastx;
-                        if (x >= nw || (has_prev && prev >= x)) {
-                            bad = true;
-                            continue;
-                        }
-                        tw[x] = pv[k];
-                        touched[x >> 5] = 1u;
-                    }
-                    if (bb > aa) lastx = px[bb - aa - 1];
-                    __syncwarp();
-                }
-                used += sz;
-                if (bb < k1) {  // piece: the round ends inside record rr
-                    aa = bb;
-                    break;
-                }
-                ++rr;
-                if (rr < N) aa = S.carry[rr];
-            }
-            if (pass == 0) {
-                r_end = rr;
-                a_end = aa;
-                cp_async_wait_all();
-                if (!tile_ready) {
-                    mbar_wait_parity(&S.bar, phase);
-                    phase ^= 1u;
-                    tile_ready = true;
-                }
-                __syncwarp();
-            }
-        }
-        if (r_end == r && a_end == a) break;  // no progress: cannot happen (a piece always fits)
-        r = r_end;
-        a = a_end;
-    }
-    if (!tile_ready) {
-        mbar_wait_parity(&S.bar, phase);
-        phase ^= 1u;
-    }
-    __syncwarp();
-}
-
 template <int W>
 __device__ void fold_dense_unit(const FoldParams& P, uint64_t r, uint64_t ku, DenseSmem& S, int lane,
                                 uint32_t& phase, bool preloaded, bool& bad) {
@@ -717,23 +622,7 @@ __device__ void fold_dense_unit(const FoldParams& P, uint64_t r, uint64_t ku, De
         const uint32_t p0 = sub + 32 * kMW * lane;  // first word of this lane's mask words
         bool tile_ready = false;
 
-        if (S.list) {
-            __syncwarp();  // carry / tend of this unit are written
-            for (int j = lane; j < N; j += 32) {
-                const uint32_t k0 = S.carry[j], k1 = S.tend[j];
-                if (k1 < k0 || k1 > S.rec[j].count || (ku == 0 && k0 != 0) || (uend == m && k1 != S.rec[j].count))
-                    bad = true;
-            }
-            if (__any_sync(0xffffffffu, bad)) {  // drain the tile load, write nothing
-                mbar_wait_parity(&S.bar, phase);
-                phase ^= 1u;
-                return;
-            }
-            dense_list_sub<W>(N, nw, S, phase, lane, bad);
-#pragma unroll
-            for (uint32_t q = 0; q < kMW; ++q) uni[q] = S.imask[kMW * lane + q];
-        }
-        for (int j0 = 0; j0 < (S.list ? 0 : N); j0 += kDBatch) {
+        for (int j0 = 0; j0 < N; j0 += kDBatch) {
             const int nb = N - j0 < kDBatch ? N - j0 : kDBatch;
             uint32_t mk[kDBatch][kMW], pre[kDBatch], tot[kDBatch], rb[kDBatch], xa[kDBatch], xb[kDBatch];
             __syncwarp();  // carry / tend / want of this unit are written
@@ -885,8 +774,7 @@ __device__ void fold_dense_unit(const FoldParams& P, uint64_t r, uint64_t ku, De
 }
 
 // Persistent: each CTA (= one warp) folds runs of kDenseRun consecutive units, the runs grid-
-// strided over the CTAs.  In list chunks the running counts carry from unit to unit and the next
-// unit's tile end is loaded while the current unit is folded.
+// strided over the CTAs.
 __global__ void __launch_bounds__(kDenseThreads, kDenseBlocksPerSM) fold_dense_kernel(const __grid_constant__ FoldParams P) {
     __shared__ DenseSmem S;
     if (*reinterpret_cast<volatile unsigned*>(P.err) != 0) return;  // sticky error pending
@@ -901,7 +789,267 @@ __global__ void __launch_bounds__(kDenseThreads, kDenseBlocksPerSM) fold_dense_k
     bool bad = false;
     uint32_t phase = 0;
     uint64_t cur = ~uint64_t(0);  // chunk whose record table is in S.rec
-    uint32_t te[2] = {0u, 0u};     // list chunks: tile end entries of unit u (lane j: records j, j + 32)
+    uint64_t lo = 0, u1 = 0;
+    for (uint64_t u = 0;; ++u) {
+        if (u >= u1) {  // the next run of consecutive units
+            const uint64_t run = u1 == 0 ? blockIdx.x : u1 / kDenseRun + gridDim.x - 1;
+            if (run * kDenseRun >= total) break;
+            u = run * kDenseRun;
+            u1 = u + kDenseRun < total ? u + kDenseRun : total;
+            uint64_t hi = R;
+            lo = 0;
+            while (hi - lo > 1) {
+                const uint64_t mid = (lo + hi) >> 1;
+                if (P.unit_first[mid] <= u) lo = mid; else hi = mid;
+            }
+        }
+        while (u >= P.unit_first[lo + 1]) ++lo;
+        if (P.desc[lo].dense != 1u) {  // folded by fold_kernel / fold_list_kernel: skip the chunk
+            u = (P.unit_first[lo + 1] < u1 ? P.unit_first[lo + 1] : u1) - 1;
+            continue;
+        }
+        if (lo != cur) {
+            __syncwarp();
+            for (int j = lane; j < N; j += 32) {
+                const FoldRec& F = P.desc[static_cast<size_t>(j) * P.cap + lo];
+                DenseRec D;
+                D.body = F.idx ? F.idx : F.mask;
+                D.values = F.values;
+                D.toff = reinterpret_cast<const uint32_t*>(F.toff);
+                D.count = static_cast<uint32_t>(F.count);
+                D.is_idx = F.idx != nullptr;
+                S.rec[j] = D;
+            }
+            __syncwarp();
+            cur = lo;
+        }
+        const uint64_t ku = u - P.unit_first[lo];
+        const bool preloaded = false;
+        if (P.desc[lo].w == 4)
+            fold_dense_unit<4>(P, lo, ku, S, lane, phase, preloaded, bad);
+        else
+            fold_dense_unit<2>(P, lo, ku, S, lane, phase, preloaded, bad);
+        if (__any_sync(0xffffffffu, bad)) {
+            if (lane == 0) tc_set_err(P.err, TC_ERR_CORRUPT);
+            break;
+        }
+    }
+    bulk_wait_all();  // the bulk stores are done before the CTA's shared memory goes away
+}
+
+// ---------------------------------------------------------------- list fold ----------
+// Dense chains whose records are all index mode at T = kListT (the adaptive step's format): one
+// unit = one tile, and record j's entries for tile t are [tile_off_j[t], tile_off_j[t+1]) — its
+// positions and values are two contiguous runs.  A CTA of 4 warps per unit: one TMA bulk copy
+// brings the tile's state into shared memory; the runs are staged with 16-byte cp.async copies
+// (rounds that fill the stage with whole records; a record larger than the stage goes through
+// in pieces) and scattered into the tile by position, oldest record first (a barrier between
+// records: newest wins); touched 32-word lines go back with 16-byte stores (whole lines, no
+// partial-sector writes).  Running counts carry from unit to unit within a run of consecutive
+// units, and the next tile's end entries are loaded one unit ahead.
+constexpr uint32_t kListThreads = 128;
+constexpr uint32_t kListBlocksPerSM = 5;
+constexpr uint32_t kListStage = 8192;
+
+struct ListSmem {
+    uint4 tile[2][kListT * 4 / 16];  // the unit's state (16 KB for fp32), double-buffered
+    uint4 stage[kListStage / 16];    // position / value runs of a round
+    const uint8_t* pos[TC_MAX_FOLD];
+    const uint8_t* val[TC_MAX_FOLD];
+    const uint32_t* toff[TC_MAX_FOLD];
+    uint32_t count[TC_MAX_FOLD];
+    uint32_t carry[TC_MAX_FOLD];     // first entry of the tile, per record
+    uint32_t tend[TC_MAX_FOLD];      // end entry of the tile, per record
+    uint32_t touched[kListT / 32];   // per 32-word line: written
+    uint32_t pb[TC_MAX_FOLD];        // per record: position-run bytes, total run bytes, stage offset
+    uint32_t sz[TC_MAX_FOLD];
+    uint32_t soff[TC_MAX_FOLD];
+    uint32_t fits;                   // every record's runs fit the stage at once
+    uint64_t bar[2];
+};
+
+// bytes of the 16-byte-aligned covers of the position run and the value run of entries [a, b)
+template <int W>
+__device__ __forceinline__ uint32_t list_run_bytes(uint32_t a, uint32_t b, uint32_t& pb) {
+    if (b <= a) {
+        pb = 0;
+        return 0u;
+    }
+    pb = ((2u * b + 15u) & ~15u) - ((2u * a) & ~15u);
+    return pb + static_cast<uint32_t>(((static_cast<uint64_t>(b) * W + 15) & ~uint64_t(15)) -
+                                      (static_cast<uint64_t>(a) * W & ~uint64_t(15)));
+}
+
+template <int W>
+__device__ __forceinline__ void list_unit(ListSmem& S, uint4* tile, uint64_t* bar, int N, uint32_t nw, uint8_t* st,
+                                          uint32_t& phase, int tid,
+                                          bool& bad) {
+    using word_t = typename Word<W>::T;
+    constexpr uint32_t kPiece = ((kListStage - 64) / (2 + W)) & ~7u;  // entries of a piece
+    constexpr uint32_t kVec = 16 / W;
+    word_t* tw = reinterpret_cast<word_t*>(tile);
+    word_t* state = reinterpret_cast<word_t*>(st);
+    uint8_t* sb = reinterpret_cast<uint8_t*>(S.stage);
+    bool tile_ready = false;
+    // the stage layout: each record's runs once (thread r), offsets by thread 0
+    if (tid < N) {
+        uint32_t pb;
+        S.sz[tid] = list_run_bytes<W>(S.carry[tid], S.tend[tid], pb);
+        S.pb[tid] = pb;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t o = 0;
+        for (int r = 0; r < N; ++r) {
+            S.soff[r] = o;
+            o += S.sz[r];
+        }
+        S.fits = o <= kListStage;
+    }
+    __syncthreads();
+    if (S.fits) {  // the common case: every run staged at once, then scattered record by record
+        for (int r = 0; r < N; ++r) {
+            const uint32_t sz = S.sz[r], pb = S.pb[r], off = S.soff[r], k0 = S.carry[r];
+            const uint8_t* ps = S.pos[r] + ((2u * k0) & ~15u);
+            const uint8_t* vs = S.val[r] + (static_cast<uint64_t>(k0) * W & ~uint64_t(15));
+            for (uint32_t o = 16 * tid; o < sz; o += 16 * kListThreads)
+                cp_async16(sb + off + o, o < pb ? ps + o : vs + (o - pb));
+        }
+        cp_async_wait_all();
+        mbar_wait_parity(bar, phase);
+        phase ^= 1u;
+        __syncthreads();
+        for (int r = 0; r < N; ++r) {
+            const uint32_t k0 = S.carry[r], n = S.tend[r] - k0;
+            if (n == 0) continue;  // CTA-uniform
+            const uint16_t* px = reinterpret_cast<const uint16_t*>(sb + S.soff[r] + ((2u * k0) & 15u));
+            const word_t* pv = reinterpret_cast<const word_t*>(sb + S.soff[r] + S.pb[r] + ((k0 * W) & 15u));
+            for (uint32_t k = tid; k < n; k += kListThreads) {
+                const uint32_t x = px[k];
+                if (x >= nw || (k > 0 && px[k - 1] >= x)) {  // inside the tile, strictly increasing
+                    bad = true;
+                    continue;
+                }
+                tw[x] = pv[k];
+                S.touched[x >> 5] = 1u;
+            }
+            __syncthreads();  // this record's writes before the next (newer) record's
+        }
+        tile_ready = true;
+    }
+    int r = S.fits ? N : 0;
+    uint32_t a = S.carry[0], lastx = 0;
+    while (r < N) {  // runs larger than the stage: rounds, a record split into pieces if needed
+        // one round, walked twice with the same (CTA-uniform) logic: copies, then scatter
+        int r_end = r;
+        uint32_t a_end = a;
+        for (int pass = 0; pass < 2; ++pass) {
+            int rr = r;
+            uint32_t aa = a, used = 0, pb;
+            while (rr < N) {
+                const uint32_t k1 = S.tend[rr];
+                uint32_t bb = k1;
+                uint32_t sz = list_run_bytes<W>(aa, bb, pb);
+                if (used + sz > kListStage) {
+                    if (used) break;
+                    bb = aa + kPiece;  // a piece of a record larger than the stage
+                    sz = list_run_bytes<W>(aa, bb, pb);
+                }
+                if (pass == 0) {
+                    const uint8_t* ps = S.pos[rr] + ((2u * aa) & ~15u);
+                    const uint8_t* vs = S.val[rr] + (static_cast<uint64_t>(aa) * W & ~uint64_t(15));
+                    for (uint32_t o = 16 * tid; o < pb; o += 16 * kListThreads) cp_async16(sb + used + o, ps + o);
+                    for (uint32_t o = 16 * tid; o < sz - pb; o += 16 * kListThreads)
+                        cp_async16(sb + used + pb + o, vs + o);
+                } else {
+                    const uint16_t* px = reinterpret_cast<const uint16_t*>(sb + used + ((2u * aa) & 15u));
+                    const word_t* pv = reinterpret_cast<const word_t*>(sb + used + pb + ((aa * W) & 15u));
+                    const uint32_t k0 = S.carry[rr];
+                    for (uint32_t k = tid; k < bb - aa; k += kListThreads) {
+                        const uint32_t x = px[k];
+                        const uint32_t prev = k > 0 ? px[k - 1] : lastx;
+                        if (x >= nw || (aa + k > k0 && prev >= x)) {  // inside the tile, strictly increasing
+                            bad = true;
+                            continue;
+                        }
+                        tw[x] = pv[k];
+                        S.touched[x >> 5] = 1u;
+                    }
+                    if (bb > aa) lastx = px[bb - aa - 1];
+                    __syncthreads();  // this record's writes before the next (newer) record's
+                }
+                used += sz;
+                if (bb < k1) {  // a piece: the round ends inside record rr
+                    aa = bb;
+                    break;
+                }
+                ++rr;
+                if (rr < N) aa = S.carry[rr];
+            }
+            if (pass == 0) {
+                r_end = rr;
+                a_end = aa;
+                cp_async_wait_all();
+                if (!tile_ready) {
+                    mbar_wait_parity(bar, phase);
+                    phase ^= 1u;
+                    tile_ready = true;
+                }
+                __syncthreads();
+            }
+        }
+        __syncthreads();  // the stage is read before the next round's copies
+        r = r_end;
+        a = a_end;
+    }
+    if (!tile_ready) {
+        mbar_wait_parity(bar, phase);
+        phase ^= 1u;
+        __syncthreads();
+    }
+    // touched lines back, 16 bytes per thread
+    const uint32_t npieces = (nw + kVec - 1) / kVec;
+    for (uint32_t q = tid; q < npieces; q += kListThreads) {
+        const uint32_t wi = q * kVec;
+        if (S.touched[wi >> 5]) {
+            if (wi + kVec <= nw)
+                *reinterpret_cast<uint4*>(state + wi) = tile[q];
+            else
+                for (uint32_t i = wi; i < nw; ++i) state[i] = tw[i];
+        }
+    }
+    fence_proxy_async_smem();  // these tile reads precede the next bulk load into the tile
+}
+
+__global__ void __launch_bounds__(kListThreads, kListBlocksPerSM) fold_list_kernel(const __grid_constant__ FoldParams P) {
+    __shared__ ListSmem S;
+    if (*reinterpret_cast<volatile unsigned*>(P.err) != 0) return;  // sticky error pending
+    if (P.info[4] == 0) return;                                       // no list chunk
+    const int tid = threadIdx.x;
+    const int N = P.nrec;
+    const uint64_t R = P.info[0];
+    const uint64_t total = P.info[1];
+    if (blockIdx.x * kDenseRun >= total) return;
+    if (tid == 0) {
+        mbar_init(&S.bar[0], 1);
+        mbar_init(&S.bar[1], 1);
+    }
+    __syncthreads();
+    bool bad = false;
+    uint32_t phase[2] = {0u, 0u};
+    bool issued[2] = {false, false};  // CTA-uniform: buffer holds / is loading the next unit's tile
+    int b = 0;
+    auto issue = [&](int buf, const uint8_t* src, uint32_t bytes) {
+        if (tid == 0) {
+            const uint32_t bulk = bytes & ~15u;
+            mbar_arrive_expect_tx(&S.bar[buf], bulk);
+            if (bulk) bulk_g2s(S.tile[buf], src, bulk, &S.bar[buf]);
+            for (uint32_t i = bulk; i < bytes; ++i) reinterpret_cast<uint8_t*>(S.tile[buf])[i] = src[i];
+        }
+        issued[buf] = true;
+    };
+    uint64_t cur = ~uint64_t(0);
+    uint32_t te = 0;  // thread j < N: record j's end entry of the next tile (prefetched)
     bool te_valid = false;
     uint64_t lo = 0, u1 = 0;
     for (uint64_t u = 0;; ++u) {
@@ -919,68 +1067,69 @@ __global__ void __launch_bounds__(kDenseThreads, kDenseBlocksPerSM) fold_dense_k
             te_valid = false;
         }
         while (u >= P.unit_first[lo + 1]) ++lo;
-        if (!P.desc[lo].dense) {  // folded by fold_kernel: skip the chunk
+        const FoldRec& L = P.desc[lo];
+        if (L.dense != 2u) {  // folded by another kernel: skip the chunk
             u = (P.unit_first[lo + 1] < u1 ? P.unit_first[lo + 1] : u1) - 1;
             te_valid = false;
             continue;
         }
         if (lo != cur) {
-            __syncwarp();
-            for (int j = lane; j < N; j += 32) {
-                const FoldRec& F = P.desc[static_cast<size_t>(j) * P.cap + lo];
-                DenseRec D;
-                D.body = F.idx ? F.idx : F.mask;
-                D.values = F.values;
-                D.toff = reinterpret_cast<const uint32_t*>(F.toff);
-                D.count = static_cast<uint32_t>(F.count);
-                D.is_idx = F.idx != nullptr;
-                S.rec[j] = D;
+            if (tid < N) {
+                const FoldRec& F = P.desc[static_cast<size_t>(tid) * P.cap + lo];
+                S.pos[tid] = F.idx;
+                S.val[tid] = F.values;
+                S.toff[tid] = reinterpret_cast<const uint32_t*>(F.toff);
+                S.count[tid] = static_cast<uint32_t>(F.count);
             }
-            bool list = P.desc[lo].T == kDSub;
-            for (int j = lane; j < N; j += 32) list = list && P.desc[static_cast<size_t>(j) * P.cap + lo].idx != nullptr;
-            list = __all_sync(0xffffffffu, list);
-            if (lane == 0) S.list = list;
-            __syncwarp();
             cur = lo;
             te_valid = false;
         }
-        const uint64_t ku = u - P.unit_first[lo];
-        bool preloaded = false;
-        if (S.list) {  // one tile per unit: entries [toff[ku], toff[ku + 1])
-            __syncwarp();
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int j = lane + 32 * h;
-                if (j < N) {
-                    if (te_valid) {
-                        S.carry[j] = S.tend[j];
-                        S.tend[j] = te[h];
-                    } else {
-                        S.carry[j] = ldg_u32(S.rec[j].toff + ku);
-                        S.tend[j] = ldg_u32(S.rec[j].toff + ku + 1);
-                    }
-                }
-            }
-            te_valid = u + 1 < u1 && u + 1 < P.unit_first[lo + 1];
-            if (te_valid) {
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int j = lane + 32 * h;
-                    if (j < N) te[h] = ldg_u32(S.rec[j].toff + ku + 2);
-                }
-            }
-            preloaded = true;
+        const uint32_t ku = static_cast<uint32_t>(u - P.unit_first[lo]);
+        const uint32_t m = L.m, w = L.w;
+        const uint32_t nw = m - ku * kListT < kListT ? m - ku * kListT : kListT;
+        uint8_t* st = P.state[L.seg] + (L.chunk_off + static_cast<uint64_t>(ku) * kListT) * w;
+        // this unit's tile (unless prefetched) and the next unit's into the other buffer (both
+        // buffers' previous contents were read by every thread before the last barrier)
+        if (!issued[b]) issue(b, st, nw * w);
+        const bool next = u + 1 < u1 && u + 1 < P.unit_first[lo + 1];
+        if (next) {
+            const uint32_t nw1 = m - (ku + 1) * kListT < kListT ? m - (ku + 1) * kListT : kListT;
+            issue(b ^ 1, st + static_cast<uint64_t>(kListT) * w, nw1 * w);
         }
-        if (P.desc[lo].w == 4)
-            fold_dense_unit<4>(P, lo, ku, S, lane, phase, preloaded, bad);
+        if (tid < kListT / 32) S.touched[tid] = 0u;
+        __syncthreads();  // the record table is in place
+        if (tid < N) {  // this tile's entry range per record; the next tile's end, one unit ahead
+            if (te_valid) {
+                S.carry[tid] = S.tend[tid];
+                S.tend[tid] = te;
+            } else {
+                S.carry[tid] = ldg_u32(S.toff[tid] + ku);
+                S.tend[tid] = ldg_u32(S.toff[tid] + ku + 1);
+            }
+            const uint32_t k0 = S.carry[tid], k1 = S.tend[tid];
+            if (k1 < k0 || k1 > S.count[tid] || (ku == 0 && k0 != 0) || ((ku + 1) * kListT >= m && k1 != S.count[tid]))
+                bad = true;
+        }
+        if (next && tid < N) te = ldg_u32(S.toff[tid] + ku + 2);
+        te_valid = next;
+        if (__syncthreads_or(bad)) {  // a corrupt tile_off: write nothing
+            bad = true;
+            break;
+        }
+        if (w == 4)
+            list_unit<4>(S, S.tile[b], &S.bar[b], N, nw, st, phase[b], tid, bad);
         else
-            fold_dense_unit<2>(P, lo, ku, S, lane, phase, preloaded, bad);
-        if (__any_sync(0xffffffffu, bad)) {
-            if (lane == 0) tc_set_err(P.err, TC_ERR_CORRUPT);
+            list_unit<2>(S, S.tile[b], &S.bar[b], N, nw, st, phase[b], tid, bad);
+        issued[b] = false;
+        b ^= 1;
+        if (__syncthreads_or(bad)) {  // also: every thread is done with the tile
+            bad = true;
             break;
         }
     }
-    bulk_wait_all();  // the bulk stores are done before the CTA's shared memory goes away
+    for (int q = 0; q < 2; ++q)  // a tile load that was never consumed
+        if (issued[q]) mbar_wait_parity(&S.bar[q], phase[q]);
+    if (bad && tid == 0) tc_set_err(P.err, TC_ERR_CORRUPT);
 }
 
 }  // namespace
@@ -1004,7 +1153,16 @@ cudaError_t launch_fold(const FoldParams& p, cudaStream_t s, int num_sms, uint64
             occ_d = 1;
     }
     fold_dense_kernel<<<num_sms * occ_d, kDenseThreads, 0, s>>>(p);
-    *launches += 3;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    static int occ_l = 0;
+    if (!occ_l) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_l, fold_list_kernel, kListThreads, 0) != cudaSuccess ||
+            occ_l < 1)
+            occ_l = 1;
+    }
+    fold_list_kernel<<<num_sms * occ_l, kListThreads, 0, s>>>(p);
+    *launches += 4;
     return cudaGetLastError();
 }
 

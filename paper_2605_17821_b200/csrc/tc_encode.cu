@@ -255,8 +255,12 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
     }
     rs &= ~1ull;
 
-    // ---- mask words (mask mode) and block-relative tile_off entries, in their final place ----
-    {
+    // ---- mask words (mask mode) and block-relative tile_off entries, in their final place
+    //      (only where the record's fixed sections fit the output buffer) ----
+    const uint64_t fixed = imode ? index_idx_off(I.m, P.T) : record_fixed_bytes(I.m, P.T);
+    if (rs + fixed > P.out_cap) {
+        if (tid == 0) tc_set_err(P.err, TC_ERR_CAPACITY);
+    } else {
         uint8_t* rec = P.out + rs;
         const uint64_t n_mask = cdiv(I.m, 32);
         uint32_t* gmask = reinterpret_cast<uint32_t*>(rec + kHdrBytes);
@@ -281,6 +285,9 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
             const uint64_t n_mask = cdiv(I.m, 32);
             const uint64_t n_tiles = cdiv(I.m, P.T);
             const uint64_t rec_total = imode ? record_bytes_index(I.m, P.T, W, count) : record_bytes(I.m, P.T, W, count);
+            const unsigned long long next = rs + rec_total;
+            if (next > P.out_cap) tc_set_err(P.err, TC_ERR_CAPACITY);  // this record is not written
+            else {
             uint8_t* rec = P.out + rs;
             uint64_t* h = reinterpret_cast<uint64_t*>(rec);
             h[0] = 0x31444354ull /* "TCD1" */ | (1ull << 32) | (static_cast<uint64_t>(W) << 48) |
@@ -308,7 +315,7 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
             gtoff[n_tiles] = static_cast<uint32_t>(count);
             for (uint64_t x = n_tiles + 1; x < pad16(4 * (n_tiles + 1)) / 4; ++x) gtoff[x] = 0;
             for (uint64_t x = W * count; x < pad16(W * count); ++x) gval[x] = 0;
-            const unsigned long long next = rs + rec_total;
+            }
             st_relaxed(&P.rstart[I.chunk + 1], next | 1ull);
             if (I.chunk + 1 == P.total_chunks) *P.out_bytes = next;
         }
@@ -483,18 +490,21 @@ __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __gri
     uint8_t* idst = nullptr;
     const uint8_t* src = nullptr;
     uint32_t w = 4;
-    bool dense = false;
+    bool dense = false, fits = true;
     if (valid) {
         const BlockInfo I = decode_block(P, b);
         w = I.w;
         const unsigned long long prefix = P.gpre[g] + wp + inc - c - P.cbase[I.chunk];
         const unsigned long long rs = ld_relaxed(&P.rstart[I.chunk]) & ~1ull;
+        const uint64_t ccount = P.chunk_acc[I.chunk] & kAccCountMask;
+        fits = rs + (imode ? record_bytes_index(I.m, P.T, I.w, ccount) : record_bytes(I.m, P.T, I.w, ccount)) <=
+               P.out_cap;  // else kernel A flagged TC_ERR_CAPACITY: nothing of this record is written
         uint8_t* rec = P.out + rs;
         const uint64_t n_mask = cdiv(I.m, 32);
         uint32_t* gtoff = reinterpret_cast<uint32_t*>(rec + (imode ? index_toff_off() : kHdrBytes + pad16(4 * n_mask)));
         const uint32_t pr = static_cast<uint32_t>(prefix);
         const uint32_t B = I.w == 4 ? kEncBlockWords4 : kEncBlockWords2;
-        if (I.nb) {  // kernel A wrote the tile_off entries of the block block-relative
+        if (I.nb && fits) {  // kernel A wrote the tile_off entries of the block block-relative
             if (P.T >= B) {
                 if ((I.p0 & (P.T - 1)) == 0) gtoff[I.p0 / P.T] += pr;
             } else {
@@ -503,7 +513,6 @@ __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __gri
             }
         }
         if (imode) {
-            const uint64_t ccount = P.chunk_acc[I.chunk] & kAccCountMask;
             dst = rec + index_val_off(I.m, P.T, ccount) + prefix * I.w;
             idst = rec + index_idx_off(I.m, P.T) + prefix * 2;
             src = P.spill + b * (2 * kSpillBytes);
@@ -511,11 +520,11 @@ __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __gri
             dst = rec + record_fixed_bytes(I.m, P.T) + prefix * I.w;
             src = P.spill + b * kSpillBytes;
         }
-        dense = (info & kDenseFlag) != 0 && c != 0;
+        dense = (info & kDenseFlag) != 0 && c != 0 && fits;
     }
 
     // ---- sparse blocks of this warp: packed words spill slot -> record, 4 blocks per batch ----
-    uint32_t todo = __ballot_sync(0xffffffffu, valid && !dense && c != 0);
+    uint32_t todo = __ballot_sync(0xffffffffu, valid && fits && !dense && c != 0);
     while (todo) {
         int bl[4];
         uint32_t cn[4], wq[4];

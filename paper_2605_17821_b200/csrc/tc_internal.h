@@ -21,6 +21,7 @@ constexpr uint32_t kEncBlockWords2 = 8192;  // 2-byte words
 // Fold: one warp per unit of max(T, kFoldWords) words.
 constexpr uint32_t kFoldThreads = 256;
 constexpr uint32_t kFoldWords = 4096;  // minimum fold unit (one warp: 128 mask words)
+constexpr uint32_t kListT = 4096;      // tile size of the chains fold_list_kernel takes (one tile = one unit)
 
 __host__ __device__ inline uint64_t pad16(uint64_t x) { return (x + 15) & ~uint64_t(15); }
 __host__ __device__ inline uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
@@ -67,6 +68,7 @@ struct EncParams {
     uint64_t n_groups;           // ceil(total_blocks / kEmitGroup)
     uint64_t version, ref_version;
     uint8_t* out;
+    uint64_t out_cap;            // records are written only where they fit (else TC_ERR_CAPACITY)
     uint64_t* out_bytes;
     // scratch (tc_ctx), zeroed per call: ticket | chunk_acc | rstart | group_sum
     unsigned long long* ticket;
@@ -104,7 +106,7 @@ struct FoldRec {           // one record of one diff, as located by the walker
     uint32_t T;
     uint32_t seg;
     uint32_t w;
-    uint32_t dense;        // desc[r] of diff 0 only: chunk r is folded by the dense kernel
+    uint32_t dense;        // desc[r] of diff 0 only: 0 fold_kernel, 1 fold_dense_kernel, 2 fold_list_kernel
     uint32_t pad_;
 };
 
@@ -121,7 +123,7 @@ struct FoldParams {
     uint32_t dense_permille;  // chunk r is dense when sum_j count_j * 1000 > m * dense_permille
     FoldRec* desc;          // [nrec][cap]
     uint64_t* unit_first;   // [cap + 1]
-    unsigned long long* info;  // [0] records per diff, [1] total units, [2] dense chunks, [3] scattered chunks
+    unsigned long long* info;  // [0] records per diff, [1] total units, chunks for [2] fold_dense, [3] fold, [4] fold_list
     unsigned int* err;
 };
 

@@ -22,7 +22,7 @@ struct tc_ctx {
     // index-mode mask staging: kMaskStageWords per scan block
     void* mstage = nullptr;
     size_t mstage_bytes = 0;
-    // fold scratch: desc [nrec*cap] | unit_first [cap+1] | info [4]
+    // fold scratch: desc [nrec*cap] | unit_first [cap+1] | info [5]
     void* fold = nullptr;
     size_t fold_bytes = 0;
     unsigned int* err = nullptr;  // [0] sticky device error word, [1] tc_push_peer block counter
@@ -233,8 +233,8 @@ struct SegSpec {
 }  // namespace
 
 static tc_status encode_impl(tc_ctx* ctx, const SegSpec* specs, int nseg, const tc_encode_opts& o,
-                             uint64_t version, uint64_t ref_version, void* out, uint64_t* out_bytes,
-                             cudaStream_t s) {
+                             uint64_t version, uint64_t ref_version, void* out, uint64_t out_cap,
+                             uint64_t* out_bytes, cudaStream_t s) {
     cudaSetDevice(ctx->device);
     tc_status st = TC_OK;
     EncParams P;
@@ -268,6 +268,7 @@ static tc_status encode_impl(tc_ctx* ctx, const SegSpec* specs, int nseg, const 
     P.version = version;
     P.ref_version = ref_version;
     P.out = static_cast<uint8_t*>(out);
+    P.out_cap = out_cap;
     P.out_bytes = out_bytes;
     P.advance_ref = o.advance_ref ? 1 : 0;
     P.index_mode = o.index_mode ? 1 : 0;
@@ -334,15 +335,12 @@ extern "C" tc_status tc_diff_encode(tc_ctx* ctx, const tc_segment* segs, int nse
     if (st != TC_OK) return st;
     if (!out || !aligned16(out)) return fail(TC_ERR_INVALID, "out must be a 16-byte aligned device pointer");
     if (!out_bytes) return fail(TC_ERR_INVALID, "out_bytes is NULL");
-    uint64_t bound = 0;
-    st = tc_diff_bound(segs, nseg, &o, &bound);
-    if (st != TC_OK) return st;
-    if (out_cap < bound) return fail(TC_ERR_CAPACITY, "out_cap < tc_diff_bound()");
     SegSpec sp[TC_MAX_SEGMENTS];
     for (int i = 0; i < nseg; ++i)
         sp[i] = {static_cast<uint8_t*>(segs[i].ref), static_cast<const uint8_t*>(segs[i].cur), segs[i].n_words,
                  segs[i].word_bytes, static_cast<uint32_t>(i), 0};
-    return encode_impl(ctx, sp, nseg, o, version, ref_version, out, out_bytes, static_cast<cudaStream_t>(stream));
+    return encode_impl(ctx, sp, nseg, o, version, ref_version, out, out_cap, out_bytes,
+                       static_cast<cudaStream_t>(stream));
 }
 
 extern "C" tc_status tc_diff_bound_range(const tc_segment* seg, const tc_encode_opts* opts, uint64_t first_chunk,
@@ -374,10 +372,9 @@ extern "C" tc_status tc_diff_encode_range(tc_ctx* ctx, const tc_segment* seg, ui
     if (st != TC_OK) return st;
     if (!out || !aligned16(out)) return fail(TC_ERR_INVALID, "out must be a 16-byte aligned device pointer");
     if (!out_bytes) return fail(TC_ERR_INVALID, "out_bytes is NULL");
-    uint64_t bound = 0;
+    uint64_t bound = 0;  // validates the range; out_cap may be smaller (checked on the device)
     st = tc_diff_bound_range(seg, &o, first_chunk, n_chunks, &bound);
     if (st != TC_OK) return st;
-    if (out_cap < bound) return fail(TC_ERR_CAPACITY, "out_cap < tc_diff_bound_range()");
     const uint64_t off = first_chunk * o.chunk_words;
     const uint64_t n = seg->n_words > off ? seg->n_words - off : 0;
     const uint64_t len = n < n_chunks * o.chunk_words ? n : n_chunks * o.chunk_words;
@@ -385,7 +382,8 @@ extern "C" tc_status tc_diff_encode_range(tc_ctx* ctx, const tc_segment* seg, ui
     SegSpec sp = {seg->n_words ? static_cast<uint8_t*>(seg->ref) + off * w : nullptr,
                   seg->n_words ? static_cast<const uint8_t*>(seg->cur) + off * w : nullptr, len,
                   seg->word_bytes, segment_id, off};
-    return encode_impl(ctx, &sp, 1, o, version, ref_version, out, out_bytes, static_cast<cudaStream_t>(stream));
+    return encode_impl(ctx, &sp, 1, o, version, ref_version, out, out_cap, out_bytes,
+                       static_cast<cudaStream_t>(stream));
 }
 
 tc_status tc_diff_apply(tc_ctx* ctx, void* const* state, const uint64_t* n_words, const uint32_t* word_bytes,
@@ -426,7 +424,7 @@ tc_status tc_diff_apply(tc_ctx* ctx, void* const* state, const uint64_t* n_words
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaSetDevice(ctx->device);
     const size_t desc_bytes = sizeof(FoldRec) * cap * n_records;
-    const size_t need = desc_bytes + 8 * (cap + 1) + 32;
+    const size_t need = desc_bytes + 8 * (cap + 1) + 48;
     tc_status st = ensure(&ctx->fold, &ctx->fold_bytes, need, s);
     if (st != TC_OK) return st;
     uint8_t* base = static_cast<uint8_t*>(ctx->fold);

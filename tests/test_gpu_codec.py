@@ -108,13 +108,53 @@ def test_encode_is_deterministic(ctx):
     assert np.array_equal(a, b)
 
 
-def test_encode_capacity_error(ctx):
-    ref = torch.zeros(1000, dtype=torch.int32, device="cuda")
-    out = torch.zeros(100, dtype=torch.uint8, device="cuda")
+@pytest.mark.parametrize("index_mode", [False, True])
+@pytest.mark.parametrize("sizes,wb,f,T,C", [
+    ([30000, 20001], [4, 2], 0.05, 4096, 1 << 28),
+    ([70001], [4], 0.3, 256, 8192),   # several chunks: the overflow lands in a later record
+])
+def test_encode_capacity_checked_on_device(ctx, tco, sizes, wb, f, T, C, index_mode):
+    """out_cap below the worst-case bound: a diff that fits is byte-exact; one that does not is
+    refused on the device (sticky CAPACITY), writes nothing at or past out_cap, and reports the
+    length it needs (include/tc.h tc_diff_encode)."""
+    ref_np = [synth.base(n, w, 3, i) for i, (n, w) in enumerate(zip(sizes, wb))]
+    cur_np = synth.state(sizes, wb, 3, 1, f)
+    rc, exp = tco.encode([a.copy() for a in ref_np], cur_np, tile_words=T, chunk_words=C, advance_ref=False,
+                         version=1, ref_version=0, index_mode=index_mode)
+    assert rc == 0
+    n = exp.size
+    ref = [to_dev(a) for a in ref_np]
+    cur = [to_dev(a) for a in cur_np]
+    for cap in (n, n - 16, n // 2, 100):
+        buf = torch.full((n + 4096,), 0xAB, dtype=torch.uint8, device="cuda")
+        ob = torch.zeros(1, dtype=torch.int64, device="cuda")
+        tc.diff_encode(ctx, ref, cur, buf[:cap], ob, 1, 0, T, C, advance_ref=False, index_mode=index_mode)
+        rc = ctx.check_status()
+        got = buf.cpu().numpy()
+        assert int(ob.item()) == n
+        if cap == n:
+            assert rc == tc.OK and np.array_equal(got[:n], exp)
+        else:
+            assert rc == tc.ERR_CAPACITY
+            assert (got[cap:] == 0xAB).all(), "bytes written past out_cap"
+
+
+def test_range_encode_capacity_checked_on_device(ctx, tco):
+    n_words, T, C = 50000, 1024, 8192
+    ref_np = synth.base(n_words, 4, 9, 0)
+    cur_np = synth.state([n_words], [4], 9, 1, 0.2)[0]
+    ref, cur = to_dev(ref_np), to_dev(cur_np)
+    cap_full = tc.diff_bound_range(n_words, 4, 1, 3, T, C)
+    buf = torch.full((cap_full,), 0xAB, dtype=torch.uint8, device="cuda")
     ob = torch.zeros(1, dtype=torch.int64, device="cuda")
-    with pytest.raises(tc.TcError) as e:
-        tc.diff_encode(ctx, [ref], [ref.clone()], out, ob, 1, 0)
-    assert e.value.status == tc.ERR_CAPACITY
+    tc.diff_encode_range(ctx, ref, cur, 0, 1, 3, buf, ob, 1, 0, T, C, advance_ref=False)
+    ctx.check()
+    need = int(ob.item())
+    small = need - 32
+    buf.fill_(0xAB)
+    tc.diff_encode_range(ctx, ref, cur, 0, 1, 3, buf[:small], ob, 1, 0, T, C, advance_ref=False)
+    assert ctx.check_status() == tc.ERR_CAPACITY and int(ob.item()) == need
+    assert (buf[small:].cpu().numpy() == 0xAB).all()
 
 
 # ------------------------------------------------------------------ fold -------------
@@ -281,7 +321,7 @@ def test_launch_counter(ctx):
     tc.diff_encode(ctx, [ref], [ref.clone()], out, ob, 1, 0)
     tc.diff_apply(ctx, [ref], 0, [out], [int(ob.item())])
     ctx.check()
-    assert ctx.launches == before + 6  # encode (mask, prefix, emit) + fold (walker, scatter, stream)
+    assert ctx.launches == before + 7  # encode (mask, prefix, emit) + fold (walker, scatter, stream, list)
 
 
 @pytest.mark.parametrize("advance", [True, False])
