@@ -848,11 +848,11 @@ __global__ void __launch_bounds__(kDenseThreads, kDenseBlocksPerSM) fold_dense_k
 // partial-sector writes).  Running counts carry from unit to unit within a run of consecutive
 // units, and the next tile's end entries are loaded one unit ahead.
 constexpr uint32_t kListThreads = 128;
-constexpr uint32_t kListBlocksPerSM = 5;
+constexpr uint32_t kListBlocksPerSM = 8;
 constexpr uint32_t kListStage = 8192;
 
 struct ListSmem {
-    uint4 tile[2][kListT * 4 / 16];  // the unit's state (16 KB for fp32), double-buffered
+    uint4 tile[kListT * 4 / 16];     // the unit's state (16 KB for fp32)
     uint4 stage[kListStage / 16];    // position / value runs of a round
     const uint8_t* pos[TC_MAX_FOLD];
     const uint8_t* val[TC_MAX_FOLD];
@@ -865,7 +865,7 @@ struct ListSmem {
     uint32_t sz[TC_MAX_FOLD];
     uint32_t soff[TC_MAX_FOLD];
     uint32_t fits;                   // every record's runs fit the stage at once
-    uint64_t bar[2];
+    uint64_t bar;
 };
 
 // bytes of the 16-byte-aligned covers of the position run and the value run of entries [a, b)
@@ -1030,24 +1030,10 @@ __global__ void __launch_bounds__(kListThreads, kListBlocksPerSM) fold_list_kern
     const uint64_t R = P.info[0];
     const uint64_t total = P.info[1];
     if (blockIdx.x * kDenseRun >= total) return;
-    if (tid == 0) {
-        mbar_init(&S.bar[0], 1);
-        mbar_init(&S.bar[1], 1);
-    }
+    if (tid == 0) mbar_init(&S.bar, 1);
     __syncthreads();
     bool bad = false;
-    uint32_t phase[2] = {0u, 0u};
-    bool issued[2] = {false, false};  // CTA-uniform: buffer holds / is loading the next unit's tile
-    int b = 0;
-    auto issue = [&](int buf, const uint8_t* src, uint32_t bytes) {
-        if (tid == 0) {
-            const uint32_t bulk = bytes & ~15u;
-            mbar_arrive_expect_tx(&S.bar[buf], bulk);
-            if (bulk) bulk_g2s(S.tile[buf], src, bulk, &S.bar[buf]);
-            for (uint32_t i = bulk; i < bytes; ++i) reinterpret_cast<uint8_t*>(S.tile[buf])[i] = src[i];
-        }
-        issued[buf] = true;
-    };
+    uint32_t phase = 0;
     uint64_t cur = ~uint64_t(0);
     uint32_t te = 0;  // thread j < N: record j's end entry of the next tile (prefetched)
     bool te_valid = false;
@@ -1088,14 +1074,14 @@ __global__ void __launch_bounds__(kListThreads, kListBlocksPerSM) fold_list_kern
         const uint32_t m = L.m, w = L.w;
         const uint32_t nw = m - ku * kListT < kListT ? m - ku * kListT : kListT;
         uint8_t* st = P.state[L.seg] + (L.chunk_off + static_cast<uint64_t>(ku) * kListT) * w;
-        // this unit's tile (unless prefetched) and the next unit's into the other buffer (both
-        // buffers' previous contents were read by every thread before the last barrier)
-        if (!issued[b]) issue(b, st, nw * w);
-        const bool next = u + 1 < u1 && u + 1 < P.unit_first[lo + 1];
-        if (next) {
-            const uint32_t nw1 = m - (ku + 1) * kListT < kListT ? m - (ku + 1) * kListT : kListT;
-            issue(b ^ 1, st + static_cast<uint64_t>(kListT) * w, nw1 * w);
+        // the tile (its previous contents were read by every thread before the last barrier)
+        if (tid == 0) {
+            const uint32_t bytes = nw * w, bulk = bytes & ~15u;
+            mbar_arrive_expect_tx(&S.bar, bulk);
+            if (bulk) bulk_g2s(S.tile, st, bulk, &S.bar);
+            for (uint32_t i = bulk; i < bytes; ++i) reinterpret_cast<uint8_t*>(S.tile)[i] = st[i];
         }
+        const bool next = u + 1 < u1 && u + 1 < P.unit_first[lo + 1];
         if (tid < kListT / 32) S.touched[tid] = 0u;
         __syncthreads();  // the record table is in place
         if (tid < N) {  // this tile's entry range per record; the next tile's end, one unit ahead
@@ -1112,23 +1098,21 @@ __global__ void __launch_bounds__(kListThreads, kListBlocksPerSM) fold_list_kern
         }
         if (next && tid < N) te = ldg_u32(S.toff[tid] + ku + 2);
         te_valid = next;
-        if (__syncthreads_or(bad)) {  // a corrupt tile_off: write nothing
+        if (__syncthreads_or(bad)) {  // a corrupt tile_off: drain the tile load, write nothing
+            mbar_wait_parity(&S.bar, phase);
+            phase ^= 1u;
             bad = true;
             break;
         }
         if (w == 4)
-            list_unit<4>(S, S.tile[b], &S.bar[b], N, nw, st, phase[b], tid, bad);
+            list_unit<4>(S, S.tile, &S.bar, N, nw, st, phase, tid, bad);
         else
-            list_unit<2>(S, S.tile[b], &S.bar[b], N, nw, st, phase[b], tid, bad);
-        issued[b] = false;
-        b ^= 1;
+            list_unit<2>(S, S.tile, &S.bar, N, nw, st, phase, tid, bad);
         if (__syncthreads_or(bad)) {  // also: every thread is done with the tile
             bad = true;
             break;
         }
     }
-    for (int q = 0; q < 2; ++q)  // a tile load that was never consumed
-        if (issued[q]) mbar_wait_parity(&S.bar[q], phase[q]);
     if (bad && tid == 0) tc_set_err(P.err, TC_ERR_CORRUPT);
 }
 
