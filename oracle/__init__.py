@@ -16,6 +16,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "tco.c")
+SRC_GRAD = os.path.join(HERE, "tco_grad.c")
 LIB = os.path.join(HERE, "libtco.so")
 
 OK, ERR_INVALID, ERR_CORRUPT, ERR_PROTOCOL, ERR_CAPACITY = 0, 1, 5, 6, 8
@@ -25,11 +26,12 @@ _lib = None
 
 def build(force: bool = False) -> str:
     """Compile tco.c into oracle/libtco.so (plain -O2, no vector intrinsics)."""
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(
-        os.path.getmtime(SRC), os.path.getmtime(os.path.join(HERE, "tco.h"))
-    ):
+    deps = [SRC, SRC_GRAD, os.path.join(HERE, "tco.h"), os.path.join(HERE, "tco_grad.h")]
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(d) for d in deps):
+        # -ffp-contract=off: every fp32 product and sum rounded as written (tco_grad.h)
         subprocess.check_call(
-            ["gcc", "-O2", "-std=c11", "-Wall", "-Wextra", "-shared", "-fPIC", "-o", LIB, SRC]
+            ["gcc", "-O2", "-std=c11", "-Wall", "-Wextra", "-ffp-contract=off", "-shared", "-fPIC", "-o", LIB,
+             SRC, SRC_GRAD, "-lm"]
         )
     return LIB
 
@@ -53,6 +55,23 @@ def lib():
         L.tco_apply.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.POINTER(u64), vp, u64]
         L.tco_fold.restype = ctypes.c_int
         L.tco_fold.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.POINTER(u64), vp, vp, ctypes.c_int]
+        f32 = ctypes.c_float
+        L.tco_grad_bound.restype = u64
+        L.tco_grad_bound.argtypes = [u64, u64, u64]
+        L.tco_grad_compress.restype = ctypes.c_int
+        L.tco_grad_compress.argtypes = [vp, u64, u64, u32, u32, u64, u64, vp, u64, ctypes.POINTER(u64)]
+        L.tco_grad_decompress.restype = ctypes.c_int
+        L.tco_grad_decompress.argtypes = [vp, u64, vp, u64]
+        L.tco_f32_to_f16.restype = ctypes.c_uint16
+        L.tco_f32_to_f16.argtypes = [f32]
+        L.tco_f16_to_f32.restype = f32
+        L.tco_f16_to_f32.argtypes = [ctypes.c_uint16]
+        L.tco_f32_to_bf16.restype = ctypes.c_uint16
+        L.tco_f32_to_bf16.argtypes = [f32]
+        L.tco_adam_step.restype = None
+        L.tco_adam_step.argtypes = [vp, vp, vp, vp, u64, vp, f32, f32, f32, f32, f32, f32]
+        L.tco_adam_replay.restype = ctypes.c_int
+        L.tco_adam_replay.argtypes = [vp, vp, vp, vp, u64, vp, vp, ctypes.c_int, f32, f32, f32, f32, vp, vp, vp]
         _lib = L
     return _lib
 
@@ -128,3 +147,80 @@ def fold(state, state_version: int, diffs):
     sv = ctypes.c_uint64(state_version)
     rc = lib().tco_fold(sp, _ptr(n), _ptr(w), len(state), ctypes.byref(sv), dp, _ptr(db), len(ds))
     return rc, sv.value
+
+
+# ---------------------------------------------------------------------------------------------
+# The paper's own (lossy) differential: adaptive gradient codec + Adam replay (oracle/tco_grad.h)
+SMALL_THRESHOLD = 100_000   # P:395 "100K-element INT8 threshold"
+K_DEFAULT = 0.01            # P:395 "k = 0.01"
+SAMPLE_SIZE = 4096          # SPEC.md:146 sample of 4096 entries
+CHUNK_LIMIT = (1 << 31) - 4096  # the largest multiple of 4096 below 2^31 (INT32 local indices)
+
+
+def sample_rank(k: float, sample_size: int) -> int:
+    """ceil((1-k) * S), clamped to [1, S]: the 1-based rank of the threshold in the sorted sample."""
+    import math
+
+    return max(1, min(sample_size, math.ceil((1.0 - k) * sample_size)))
+
+
+def grad_bound(n: int, small_threshold: int = SMALL_THRESHOLD, chunk_elems: int = CHUNK_LIMIT) -> int:
+    return int(lib().tco_grad_bound(n, small_threshold, chunk_elems))
+
+
+def grad_compress(x: np.ndarray, seed: int, k: float = K_DEFAULT, small_threshold: int = SMALL_THRESHOLD,
+                  sample_size: int = SAMPLE_SIZE, chunk_elems: int = CHUNK_LIMIT):
+    """Compress an fp32 gradient shard.  Returns (rc, payload bytes)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    cap = grad_bound(x.size, small_threshold, chunk_elems)
+    out = np.zeros(cap, dtype=np.uint8)
+    ob = ctypes.c_uint64(0)
+    rc = lib().tco_grad_compress(_ptr(x) if x.size else None, x.size, small_threshold, sample_size,
+                                 sample_rank(k, sample_size), chunk_elems, seed, _ptr(out), cap, ctypes.byref(ob))
+    return rc, out[: ob.value].copy()
+
+
+def grad_decompress(payload: np.ndarray, n: int):
+    """Returns (rc, fp32 array of n)."""
+    p = np.ascontiguousarray(payload, dtype=np.uint8)
+    out = np.zeros(max(n, 1), dtype=np.float32)
+    rc = lib().tco_grad_decompress(_ptr(p), p.size, _ptr(out), n)
+    return rc, out[:n]
+
+
+def f32_to_f16_bits(f: float) -> int:
+    return int(lib().tco_f32_to_f16(float(f)))
+
+
+def f16_bits_to_f32(h: int) -> float:
+    return float(lib().tco_f16_to_f32(int(h)))
+
+
+def f32_to_bf16_bits(f: float) -> int:
+    return int(lib().tco_f32_to_bf16(float(f)))
+
+
+def adam_consts(step: int, b1: float, b2: float):
+    """c1 = 1 - b1^t, c2 = 1 - b2^t for 1-based step t, in double, rounded to fp32."""
+    return np.float32(1.0 - b1 ** step), np.float32(1.0 - b2 ** step)
+
+
+def adam_step(master, m, v, w16, g, step: int, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8):
+    """In place on float32 master/m/v and uint16 (bf16 bits) w16; ``step`` 1-based."""
+    c1, c2 = adam_consts(step, b1, b2)
+    g = np.ascontiguousarray(g, dtype=np.float32)
+    lib().tco_adam_step(_ptr(master), _ptr(m), _ptr(v), _ptr(w16), master.size, _ptr(g), lr, b1, b2, eps,
+                        float(c1), float(c2))
+
+
+def adam_replay(master, m, v, w16, payloads, first_step: int, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8) -> int:
+    """Sequential replay: payload j is the gradient of step first_step + j.  In place; returns rc."""
+    ps = [np.ascontiguousarray(p, dtype=np.uint8) for p in payloads]
+    pp = (ctypes.c_void_p * len(ps))(*[_ptr(p) for p in ps])
+    pb = np.array([p.size for p in ps], dtype=np.uint64)
+    cs = [adam_consts(first_step + j, b1, b2) for j in range(len(ps))]
+    c1 = np.array([c[0] for c in cs], dtype=np.float32)
+    c2 = np.array([c[1] for c in cs], dtype=np.float32)
+    scratch = np.zeros(max(master.size, 1), dtype=np.float32)
+    return int(lib().tco_adam_replay(_ptr(master), _ptr(m), _ptr(v), _ptr(w16), master.size, pp, _ptr(pb), len(ps),
+                                     lr, b1, b2, eps, _ptr(c1), _ptr(c2), _ptr(scratch)))
