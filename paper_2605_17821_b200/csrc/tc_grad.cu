@@ -1,0 +1,777 @@
+// tc_grad.cu — the paper's own differential on sm_100a: adaptive gradient compression (INT8
+// dense below the small-tensor threshold; sampled magnitude threshold + one keeping pass into
+// FP16 values / INT32 chunk-local indices above it), decompression, the native Adam step, and
+// the fused multi-step Adam replay (include/tc_grad.h).
+//
+// PAPER.md:203 §3.2 (codec), §3.3 + P:322 §4 (fused replay)
+// (Adam), SPEC.md:99-157 (codec interface), SPEC.md:343-354 (fused == sequential).  Every fp32
+// operation of the Adam update is an explicit round-to-nearest intrinsic, in the order the oracle
+// (oracle/tco_grad.c, built with -ffp-contract=off) writes it, so the two agree bit for bit.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <string>
+
+#include "../../include/tc_grad.h"
+#include "tc_internal.h"
+
+namespace {
+
+constexpr uint32_t kGB = 4096;         // elements per compaction block / replay tile
+constexpr uint32_t kGThreads = 256;    // 16 elements per thread
+constexpr uint32_t kGPer = kGB / kGThreads;
+constexpr uint32_t kGSpill = 256;      // entries a block keeps in its spill slot (6 bytes each)
+constexpr uint32_t kSampleMax = 8192;  // largest supported sample (sorted in shared memory)
+constexpr uint64_t kDefaultChunk = (1ull << 31) - 4096;
+constexpr uint64_t kHdr = 64;
+
+tc_status fail(tc_status s, const std::string& msg) {
+    tc::set_error(msg);
+    return s;
+}
+tc_status cuda_fail(cudaError_t e, const char* what) {
+    tc::set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? TC_ERR_NOMEM : TC_ERR_CUDA;
+}
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+__host__ __device__ inline uint64_t pad16u(uint64_t x) { return (x + 15) & ~uint64_t(15); }
+
+struct Opts {
+    uint64_t small, chunk;
+    uint32_t sample, rank;
+};
+
+tc_status resolve(const tc_grad_opts* o, Opts* r) {
+    const uint64_t small = o && o->small_threshold ? o->small_threshold : 100000;
+    const double k = o && o->k > 0 ? o->k : 0.01;
+    const uint32_t sample = o && o->sample_size ? o->sample_size : 4096;
+    const uint64_t chunk = o && o->chunk_elems ? o->chunk_elems : kDefaultChunk;
+    if (!(k > 0.0 && k <= 1.0)) return fail(TC_ERR_INVALID, "k must be in (0, 1]");
+    if (sample > kSampleMax) return fail(TC_ERR_INVALID, "sample_size must be <= 8192");
+    if (chunk % kGB != 0 || chunk > 2147483647ull) return fail(TC_ERR_INVALID, "chunk_elems: a multiple of 4096, < 2^31");
+    double t = std::ceil((1.0 - k) * static_cast<double>(sample));
+    uint32_t rank = t < 1.0 ? 1u : (t > sample ? sample : static_cast<uint32_t>(t));
+    *r = {small, chunk, sample, rank};
+    return TC_OK;
+}
+
+uint64_t bound_of(uint64_t n, const Opts& o) {
+    if (n < o.small) return kHdr + pad16u(n);
+    const uint64_t chunks = n ? (n + o.chunk - 1) / o.chunk : 1;
+    return kHdr + 16 * chunks + pad16u(2 * n) + pad16u(4 * n);
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ void put_header(uint8_t* out, uint32_t variant, uint32_t chunks, float s, uint64_t n,
+                                           uint64_t kept, uint64_t chunk, uint64_t seed, uint64_t total) {
+    uint64_t* h = reinterpret_cast<uint64_t*>(out);
+    h[0] = 0x31474354ull /* "TCG1" */ | (static_cast<uint64_t>(variant) << 32);
+    h[1] = static_cast<uint64_t>(chunks) | (static_cast<uint64_t>(__float_as_uint(s)) << 32);
+    h[2] = n;
+    h[3] = kept;
+    h[4] = chunk;
+    h[5] = seed;
+    h[6] = total;
+    h[7] = 0;
+}
+
+// ------------------------------------------------------------------ INT8 dense ----------
+__global__ void __launch_bounds__(1024) grad_int8_kernel(const float* __restrict__ x, uint64_t n, uint64_t chunk,
+                                                         uint64_t seed, uint8_t* out, uint64_t cap,
+                                                         uint64_t* out_bytes, unsigned* err) {
+    __shared__ float s_max[32];
+    const int tid = threadIdx.x;
+    float mx = 0.0f;
+    for (uint64_t i = tid; i < n; i += 1024) mx = fmaxf(mx, fabsf(x[i]));
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+    if ((tid & 31) == 0) s_max[tid >> 5] = mx;
+    __syncthreads();
+    mx = 0.0f;
+    for (int k = 0; k < 32; ++k) mx = fmaxf(mx, s_max[k]);
+    const float scale = mx > 0.0f ? __fdiv_rn(mx, 127.0f) : 1.0f;
+    const uint64_t total = kHdr + pad16u(n);
+    if (tid == 0) *reinterpret_cast<volatile uint64_t*>(out_bytes) = total;
+    if (total > cap) {
+        if (tid == 0) tc_set_err(err, TC_ERR_CAPACITY);
+        return;
+    }
+    if (tid == 0) put_header(out, 1, 0, scale, n, n, chunk, seed, total);
+    int8_t* q = reinterpret_cast<int8_t*>(out + kHdr);
+    for (uint64_t i = tid; i < pad16u(n); i += 1024) {
+        float r = 0.0f;
+        if (i < n) r = fminf(fmaxf(rintf(__fdiv_rn(x[i], scale)), -127.0f), 127.0f);
+        q[i] = static_cast<int8_t>(r);
+    }
+}
+
+// ----------------------------------------------------------------- sparse form ----------
+struct SparseParams {
+    const float* x;
+    uint64_t n, chunk, nblocks, nchunks, seed, cap;
+    uint32_t sample, rank;
+    uint8_t* out;
+    uint64_t* out_bytes;
+    float* thr;                  // [1]
+    uint32_t* bcount;            // [nblocks] kept | dense flag
+    unsigned long long* boff;    // [nblocks + 1] exclusive prefix; [nblocks] = kept
+    uint8_t* spill;              // [nblocks][kGSpill * 6]: f16 values | i32 local indices
+    unsigned* err;
+};
+constexpr uint32_t kDenseBit = 0x80000000u;
+
+// the threshold: rank-th smallest magnitude of `sample` seeded draws (bitonic sort in smem)
+__global__ void __launch_bounds__(1024) grad_sample_kernel(const __grid_constant__ SparseParams P) {
+    __shared__ float s[kSampleMax];
+    const int tid = threadIdx.x;
+    uint32_t S2 = 1;
+    while (S2 < P.sample) S2 <<= 1;
+    for (uint32_t j = tid; j < S2; j += 1024)
+        s[j] = j < P.sample ? fabsf(P.x[splitmix64(P.seed + j) % P.n]) : __int_as_float(0x7f800000);
+    __syncthreads();
+    for (uint32_t k = 2; k <= S2; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = tid; i < S2; i += 1024) {
+                const uint32_t l = i ^ j;
+                if (l > i) {
+                    const float a = s[i], b = s[l];
+                    const bool up = (i & k) == 0;
+                    if ((a > b) == up) {
+                        s[i] = b;
+                        s[l] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    if (tid == 0) *P.thr = s[P.rank - 1];
+}
+
+// the keeping predicate: |x| >= threshold, zeros never kept
+__device__ __forceinline__ bool keep(float v, float thr) { return v != 0.0f && fabsf(v) >= thr; }
+
+// pass 1: per block counts; sparse blocks pack their entries (index order) into the spill slot
+__global__ void __launch_bounds__(kGThreads) grad_count_kernel(const __grid_constant__ SparseParams P) {
+    __shared__ uint32_t s_cnt[kGPer * (kGThreads / 32)];
+    __shared__ uint32_t s_total;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint64_t b = blockIdx.x;
+    const uint64_t base = b * kGB;
+    const float thr = *P.thr;
+    float v[kGPer];
+    uint32_t bal[kGPer];
+#pragma unroll
+    for (uint32_t j = 0; j < kGPer; ++j) {
+        const uint64_t i = base + j * kGThreads + tid;
+        v[j] = i < P.n ? P.x[i] : 0.0f;
+    }
+#pragma unroll
+    for (uint32_t j = 0; j < kGPer; ++j) {
+        bal[j] = __ballot_sync(0xffffffffu, keep(v[j], thr));
+        if (lane == 0) s_cnt[j * (kGThreads / 32) + wid] = __popc(bal[j]);
+    }
+    __syncthreads();
+    if (tid < 32) {  // exclusive scan of the 128 (j, warp) counts, in index order
+        uint32_t c[4], t = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            c[q] = s_cnt[tid * 4 + q];
+            t += c[q];
+        }
+        uint32_t inc = t;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += y;
+        }
+        uint32_t run = inc - t;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            s_cnt[tid * 4 + q] = run;
+            run += c[q];
+        }
+        if (tid == 31) s_total = inc;
+    }
+    __syncthreads();
+    const uint32_t total = s_total;
+    if (tid == 0) P.bcount[b] = total | (total > kGSpill ? kDenseBit : 0u);
+    if (total == 0 || total > kGSpill) return;
+    uint16_t* sv = reinterpret_cast<uint16_t*>(P.spill + b * (kGSpill * 6));
+    int32_t* si = reinterpret_cast<int32_t*>(P.spill + b * (kGSpill * 6) + kGSpill * 2);
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (uint32_t j = 0; j < kGPer; ++j) {
+        if ((bal[j] >> lane) & 1u) {
+            const uint32_t k = s_cnt[j * (kGThreads / 32) + wid] + __popc(bal[j] & lt);
+            const uint64_t i = base + j * kGThreads + tid;
+            sv[k] = __half_as_ushort(__float2half_rn(v[j]));
+            si[k] = static_cast<int32_t>(i - i / P.chunk * P.chunk);
+        }
+    }
+}
+
+// block offsets, the payload length, and the capacity check
+__global__ void __launch_bounds__(1024) grad_prefix_kernel(const __grid_constant__ SparseParams P) {
+    __shared__ unsigned long long s_carry;
+    __shared__ unsigned long long s_warp[32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (uint64_t base = 0; base < P.nblocks; base += 1024) {
+        const uint64_t i = base + tid;
+        const unsigned long long c = i < P.nblocks ? (P.bcount[i] & ~kDenseBit) : 0ull;
+        unsigned long long x = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+        }
+        if (lane == 31) s_warp[wid] = x;
+        __syncthreads();
+        unsigned long long wp = 0, tot = 0;
+        for (int k = 0; k < 32; ++k) {
+            wp += k < wid ? s_warp[k] : 0ull;
+            tot += s_warp[k];
+        }
+        const unsigned long long carry = s_carry;
+        if (i < P.nblocks) P.boff[i] = carry + wp + x - c;
+        __syncthreads();
+        if (tid == 0) s_carry = carry + tot;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        const uint64_t kept = s_carry;
+        P.boff[P.nblocks] = kept;
+        const uint64_t total = kHdr + 16 * P.nchunks + pad16u(2 * kept) + pad16u(4 * kept);
+        *reinterpret_cast<volatile uint64_t*>(P.out_bytes) = total;
+        if (total > P.cap) tc_set_err(P.err, TC_ERR_CAPACITY);
+    }
+}
+
+// pass 2: entries to their final place (dense blocks re-read their gradient); block 0 writes the
+// header, the chunk table and the pads
+__global__ void __launch_bounds__(kGThreads) grad_emit_kernel(const __grid_constant__ SparseParams P) {
+    __shared__ uint32_t s_cnt[kGPer * (kGThreads / 32)];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint64_t b = blockIdx.x;
+    const uint64_t kept = P.boff[P.nblocks];
+    const uint64_t voff = kHdr + 16 * P.nchunks, ioff = voff + pad16u(2 * kept);
+    const uint64_t total = ioff + pad16u(4 * kept);
+    if (total > P.cap) return;  // CAPACITY was reported by the prefix kernel
+    uint16_t* gv = reinterpret_cast<uint16_t*>(P.out + voff);
+    int32_t* gi = reinterpret_cast<int32_t*>(P.out + ioff);
+    if (b == 0) {
+        if (tid == 0) put_header(P.out, 2, static_cast<uint32_t>(P.nchunks), *P.thr, P.n, kept, P.chunk, P.seed, total);
+        for (uint64_t c = tid; c < P.nchunks; c += kGThreads) {
+            const uint64_t b0 = c * (P.chunk / kGB), b1 = (c + 1) * (P.chunk / kGB);
+            const uint64_t cnt = P.boff[b1 < P.nblocks ? b1 : P.nblocks] - P.boff[b0];
+            uint64_t* t = reinterpret_cast<uint64_t*>(P.out + kHdr + 16 * c);
+            t[0] = c * P.chunk;
+            t[1] = cnt;
+        }
+        for (uint64_t x = 2 * kept + tid; x < pad16u(2 * kept); x += kGThreads) P.out[voff + x] = 0;
+        for (uint64_t x = 4 * kept + tid; x < pad16u(4 * kept); x += kGThreads) P.out[ioff + x] = 0;
+    }
+    const uint32_t info = P.bcount[b];
+    const uint32_t cnt = info & ~kDenseBit;
+    if (cnt == 0) return;
+    const uint64_t off = P.boff[b];
+    if (!(info & kDenseBit)) {
+        const uint16_t* sv = reinterpret_cast<const uint16_t*>(P.spill + b * (kGSpill * 6));
+        const int32_t* si = reinterpret_cast<const int32_t*>(P.spill + b * (kGSpill * 6) + kGSpill * 2);
+        for (uint32_t k = tid; k < cnt; k += kGThreads) {
+            gv[off + k] = sv[k];
+            gi[off + k] = si[k];
+        }
+        return;
+    }
+    // dense block: the same ballot order as pass 1, straight into the payload
+    const uint64_t base = b * kGB;
+    const float thr = *P.thr;
+    float v[kGPer];
+    uint32_t bal[kGPer];
+#pragma unroll
+    for (uint32_t j = 0; j < kGPer; ++j) {
+        const uint64_t i = base + j * kGThreads + tid;
+        v[j] = i < P.n ? P.x[i] : 0.0f;
+        bal[j] = __ballot_sync(0xffffffffu, keep(v[j], thr));
+        if (lane == 0) s_cnt[j * (kGThreads / 32) + wid] = __popc(bal[j]);
+    }
+    __syncthreads();
+    if (tid < 32) {
+        uint32_t c[4], t = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            c[q] = s_cnt[tid * 4 + q];
+            t += c[q];
+        }
+        uint32_t inc = t;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += y;
+        }
+        uint32_t run = inc - t;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            s_cnt[tid * 4 + q] = run;
+            run += c[q];
+        }
+    }
+    __syncthreads();
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (uint32_t j = 0; j < kGPer; ++j) {
+        if ((bal[j] >> lane) & 1u) {
+            const uint64_t k = off + s_cnt[j * (kGThreads / 32) + wid] + __popc(bal[j] & lt);
+            const uint64_t i = base + j * kGThreads + tid;
+            gv[k] = __half_as_ushort(__float2half_rn(v[j]));
+            gi[k] = static_cast<int32_t>(i - i / P.chunk * P.chunk);
+        }
+    }
+}
+
+// ------------------------------------------------------------- decompression ----------
+struct Payload {           // as located and validated by the walker
+    const int8_t* q;       // dense codes (variant 1)
+    const uint16_t* val;   // sparse FP16 values
+    const int32_t* idx;    // sparse local indices
+    const uint64_t* table; // sparse chunk table {base, count}
+    unsigned long long* cpre;  // [chunks + 1] entry prefix (walker output)
+    unsigned long long* tstart;  // [tiles + 1] first entry of each kGB tile (replay only)
+    float scale;
+    uint32_t variant;
+    uint64_t chunks, chunk, kept;
+};
+
+__global__ void grad_walk_kernel(const uint8_t* p, uint64_t bytes, uint64_t n, Payload* out, unsigned* err) {
+    if (threadIdx.x != 0) return;
+    const uint64_t* h = reinterpret_cast<const uint64_t*>(p);
+    Payload R = {};
+    bool bad = bytes < kHdr || static_cast<uint32_t>(h[0]) != 0x31474354u;
+    if (!bad) {
+        R.variant = static_cast<uint32_t>(h[0] >> 32);
+        R.chunks = static_cast<uint32_t>(h[1]);
+        R.scale = __uint_as_float(static_cast<uint32_t>(h[1] >> 32));
+        R.kept = h[3];
+        R.chunk = h[4];
+        const uint64_t total = h[6];
+        bad = h[2] != n || total != bytes || (R.variant & ~0xffu) != 0;
+        if (!bad && (R.variant & 0xffu) == 1) {
+            R.variant = 1;
+            bad = R.kept != n || total != kHdr + pad16u(n);
+            R.q = reinterpret_cast<const int8_t*>(p + kHdr);
+        } else if (!bad && (R.variant & 0xffu) == 2) {
+            R.variant = 2;
+            const uint64_t want = n ? (n + R.chunk - 1) / (R.chunk ? R.chunk : 1) : 1;
+            bad = R.chunk == 0 || R.chunk > 2147483647ull || R.kept > n || R.chunks != want ||
+                  total != kHdr + 16 * R.chunks + pad16u(2 * R.kept) + pad16u(4 * R.kept);
+            if (!bad) {
+                R.table = reinterpret_cast<const uint64_t*>(p + kHdr);
+                R.val = reinterpret_cast<const uint16_t*>(p + kHdr + 16 * R.chunks);
+                R.idx = reinterpret_cast<const int32_t*>(p + kHdr + 16 * R.chunks + pad16u(2 * R.kept));
+                unsigned long long k = 0;
+                for (uint64_t c = 0; c < R.chunks && !bad; ++c) {
+                    const uint64_t base = R.table[2 * c], cnt = R.table[2 * c + 1];
+                    const uint64_t len = base + R.chunk < n ? R.chunk : n - base;
+                    if (base != c * R.chunk || cnt > len || k + cnt > R.kept) bad = true;
+                    out->cpre[c] = k;
+                    k += cnt;
+                }
+                if (!bad && k != R.kept) bad = true;
+                out->cpre[R.chunks] = k;
+            }
+        } else {
+            bad = true;
+        }
+    }
+    if (bad) {
+        tc_set_err(err, TC_ERR_CORRUPT);
+        R.variant = 0;
+    }
+    R.cpre = out->cpre;
+    R.tstart = out->tstart;
+    *out = R;
+}
+
+__device__ __forceinline__ uint64_t chunk_of(const Payload& R, uint64_t k) {
+    uint64_t lo = 0, hi = R.chunks;  // cpre[lo] <= k < cpre[lo + 1]
+    while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (R.cpre[mid] <= k) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// entry k -> (global position, value); checks the index against its chunk and its predecessor
+__device__ __forceinline__ bool entry(const Payload& R, uint64_t n, uint64_t k, uint64_t* pos, float* val) {
+    const uint64_t c = chunk_of(R, k);
+    const uint64_t base = c * R.chunk;
+    const uint64_t len = base + R.chunk < n ? R.chunk : n - base;
+    const int32_t i = R.idx[k];
+    if (i < 0 || static_cast<uint64_t>(i) >= len || (k > R.cpre[c] && R.idx[k - 1] >= i)) return false;
+    *pos = base + static_cast<uint64_t>(i);
+    *val = __half2float(__ushort_as_half(R.val[k]));
+    return true;
+}
+
+__global__ void grad_decompress_kernel(const Payload* RP, uint64_t n, float* out, unsigned* err) {
+    if (*reinterpret_cast<volatile unsigned*>(err) != 0) return;
+    const Payload R = *RP;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (R.variant == 1) {
+        for (uint64_t i = t; i < n; i += stride) out[i] = __fmul_rn(R.scale, static_cast<float>(R.q[i]));
+    } else if (R.variant == 2) {
+        for (uint64_t i = t; i < n; i += stride) out[i] = 0.0f;
+    }
+}
+
+__global__ void grad_scatter_kernel(const Payload* RP, uint64_t n, float* out, unsigned* err) {
+    if (*reinterpret_cast<volatile unsigned*>(err) != 0) return;
+    const Payload R = *RP;
+    if (R.variant != 2) return;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < R.kept; k += stride) {
+        uint64_t pos;
+        float v;
+        if (!entry(R, n, k, &pos, &v)) {
+            tc_set_err(err, TC_ERR_CORRUPT);
+            return;
+        }
+        out[pos] = v;
+    }
+}
+
+// first entry of every kGB tile (replay): lower bound of the tile start among the sorted positions
+__global__ void grad_tile_start_kernel(const Payload* RP, uint64_t n, uint64_t tiles, unsigned* err) {
+    if (*reinterpret_cast<volatile unsigned*>(err) != 0) return;
+    const Payload R = *RP;
+    if (R.variant != 2) return;
+    for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t <= tiles;
+         t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t want = t * kGB;
+        uint64_t lo = 0, hi = R.kept;  // first k with position(k) >= want
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            const uint64_t c = chunk_of(R, mid);
+            const uint64_t pos = c * R.chunk + static_cast<uint64_t>(static_cast<uint32_t>(R.idx[mid]));
+            if (pos < want) lo = mid + 1; else hi = mid;
+        }
+        R.tstart[t] = lo;
+    }
+}
+
+// ------------------------------------------------------------------- Adam ----------
+struct AdamC {
+    float lr, b1, b2, eps;
+};
+
+__device__ __forceinline__ void adam_update(float& master, float& m, float& v, float g, const AdamC& a, float c1,
+                                            float c2) {
+    const float omb1 = __fsub_rn(1.0f, a.b1), omb2 = __fsub_rn(1.0f, a.b2);
+    m = __fadd_rn(__fmul_rn(a.b1, m), __fmul_rn(omb1, g));
+    v = __fadd_rn(__fmul_rn(a.b2, v), __fmul_rn(omb2, __fmul_rn(g, g)));
+    const float mhat = __fdiv_rn(m, c1);
+    const float vhat = __fdiv_rn(v, c2);
+    const float upd = __fdiv_rn(__fmul_rn(a.lr, mhat), __fadd_rn(__fsqrt_rn(vhat), a.eps));
+    master = __fsub_rn(master, upd);
+}
+
+__global__ void adam_step_kernel(float* __restrict__ master, float* __restrict__ m, float* __restrict__ v,
+                                 uint16_t* __restrict__ w16, uint64_t n, const float* __restrict__ g, AdamC a,
+                                 float c1, float c2) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        float w = master[i], mi = m[i], vi = v[i];
+        adam_update(w, mi, vi, g[i], a, c1, c2);
+        master[i] = w;
+        m[i] = mi;
+        v[i] = vi;
+        w16[i] = __bfloat16_as_ushort(__float2bfloat16_rn(w));
+    }
+}
+
+struct ReplayParams {
+    float* master;
+    float* m;
+    float* v;
+    uint64_t n, tiles;
+    int nsteps;              // fused steps (payloads 0 .. nsteps-1)
+    AdamC a;
+    float c1[TC_MAX_FOLD], c2[TC_MAX_FOLD];
+    const Payload* pay;      // [nsteps], walker output
+    unsigned* err;
+};
+
+// one CTA per tile of kGB elements: (master, m, v) in registers for all fused steps
+__global__ void __launch_bounds__(kGThreads) adam_replay_kernel(const __grid_constant__ ReplayParams P) {
+    __shared__ float s_g[kGB];
+    if (*reinterpret_cast<volatile unsigned*>(P.err) != 0) return;
+    const int tid = threadIdx.x;
+    bool bad = false;
+    for (uint64_t t = blockIdx.x; t < P.tiles; t += gridDim.x) {
+        const uint64_t base = t * kGB;
+        float w[kGPer], mm[kGPer], vv[kGPer];
+#pragma unroll
+        for (uint32_t j = 0; j < kGPer; ++j) {
+            const uint64_t i = base + j * kGThreads + tid;
+            w[j] = i < P.n ? P.master[i] : 0.0f;
+            mm[j] = i < P.n ? P.m[i] : 0.0f;
+            vv[j] = i < P.n ? P.v[i] : 0.0f;
+        }
+        for (int s = 0; s < P.nsteps; ++s) {
+            const Payload& R = P.pay[s];
+            if (R.variant == 1) {
+#pragma unroll
+                for (uint32_t j = 0; j < kGPer; ++j) {
+                    const uint64_t i = base + j * kGThreads + tid;
+                    const float g = i < P.n ? __fmul_rn(R.scale, static_cast<float>(R.q[i])) : 0.0f;
+                    adam_update(w[j], mm[j], vv[j], g, P.a, P.c1[s], P.c2[s]);
+                }
+            } else {
+#pragma unroll
+                for (uint32_t j = 0; j < kGPer; ++j) s_g[j * kGThreads + tid] = 0.0f;
+                __syncthreads();
+                const uint64_t k0 = R.tstart[t], k1 = R.tstart[t + 1];
+                for (uint64_t k = k0 + tid; k < k1; k += kGThreads) {
+                    uint64_t pos;
+                    float val;
+                    if (!entry(R, P.n, k, &pos, &val) || pos < base || pos >= base + kGB) {
+                        bad = true;
+                        continue;
+                    }
+                    s_g[pos - base] = val;
+                }
+                __syncthreads();
+#pragma unroll
+                for (uint32_t j = 0; j < kGPer; ++j) adam_update(w[j], mm[j], vv[j], s_g[j * kGThreads + tid], P.a, P.c1[s], P.c2[s]);
+                __syncthreads();
+            }
+        }
+#pragma unroll
+        for (uint32_t j = 0; j < kGPer; ++j) {
+            const uint64_t i = base + j * kGThreads + tid;
+            if (i < P.n) {
+                P.master[i] = w[j];
+                P.m[i] = mm[j];
+                P.v[i] = vv[j];
+            }
+        }
+    }
+    if (bad) tc_set_err(P.err, TC_ERR_CORRUPT);
+}
+
+AdamC adam_consts(const tc_adam_hp* hp) {
+    AdamC a;
+    a.lr = static_cast<float>(hp ? hp->lr : 1e-3);
+    a.b1 = static_cast<float>(hp ? hp->beta1 : 0.9);
+    a.b2 = static_cast<float>(hp ? hp->beta2 : 0.999);
+    a.eps = static_cast<float>(hp ? hp->eps : 1e-8);
+    return a;
+}
+void bias(const tc_adam_hp* hp, uint64_t step, float* c1, float* c2) {
+    const double b1 = hp ? hp->beta1 : 0.9, b2 = hp ? hp->beta2 : 0.999;
+    *c1 = static_cast<float>(1.0 - std::pow(b1, static_cast<double>(step)));
+    *c2 = static_cast<float>(1.0 - std::pow(b2, static_cast<double>(step)));
+}
+
+tc_status check_state(const tc_adam_state* st) {
+    if (!st || !st->n) return st ? TC_OK : fail(TC_ERR_INVALID, "state is NULL");
+    if (!st->master || !st->m || !st->v || !st->w16 || !aligned16(st->master) || !aligned16(st->m) ||
+        !aligned16(st->v) || !aligned16(st->w16))
+        return fail(TC_ERR_INVALID, "state pointers must be 16-byte aligned device pointers");
+    return TC_OK;
+}
+
+int grid_for(tc_ctx* ctx, uint64_t work, int threads) {
+    const uint64_t want = (work + threads - 1) / threads;
+    const uint64_t cap = static_cast<uint64_t>(tc::ctx_num_sms(ctx)) * 8;
+    return static_cast<int>(want < cap ? (want ? want : 1) : cap);
+}
+
+}  // namespace
+
+extern "C" {
+
+tc_status tc_grad_bound(uint64_t n, const tc_grad_opts* opts, uint64_t* max_bytes) {
+    if (!max_bytes) return fail(TC_ERR_INVALID, "max_bytes is NULL");
+    Opts o;
+    tc_status st = resolve(opts, &o);
+    if (st != TC_OK) return st;
+    *max_bytes = bound_of(n, o);
+    return TC_OK;
+}
+
+tc_status tc_grad_compress(tc_ctx* ctx, const float* grad, uint64_t n, const tc_grad_opts* opts, uint64_t seed,
+                           void* out, uint64_t out_cap, uint64_t* out_bytes, tc_stream stream) {
+    if (!ctx || !out || !aligned16(out) || !out_bytes || (n && !grad))
+        return fail(TC_ERR_INVALID, "bad arguments (ctx, 16-byte aligned out, out_bytes, grad)");
+    Opts o;
+    tc_status st = resolve(opts, &o);
+    if (st != TC_OK) return st;
+    cudaSetDevice(tc::ctx_device(ctx));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    unsigned* err = tc::ctx_err(ctx);
+    if (n < o.small) {
+        grad_int8_kernel<<<1, 1024, 0, s>>>(grad, n, o.chunk, seed, static_cast<uint8_t*>(out), out_cap, out_bytes, err);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "grad_int8 launch");
+        tc::ctx_add_launches(ctx, 1);
+        return TC_OK;
+    }
+    SparseParams P = {};
+    P.x = grad;
+    P.n = n;
+    P.chunk = o.chunk;
+    P.nblocks = (n + kGB - 1) / kGB;
+    P.nchunks = (n + o.chunk - 1) / o.chunk;
+    P.seed = seed;
+    P.cap = out_cap;
+    P.sample = o.sample;
+    P.rank = o.rank;
+    P.out = static_cast<uint8_t*>(out);
+    P.out_bytes = out_bytes;
+    P.err = err;
+    const size_t b_cnt = 16, b_bc = b_cnt + pad16u(4 * P.nblocks), b_off = b_bc + pad16u(8 * (P.nblocks + 1));
+    const size_t need = b_off + P.nblocks * (kGSpill * 6);
+    void* scratch = nullptr;
+    st = tc::ctx_grad_scratch(ctx, need, s, &scratch);
+    if (st != TC_OK) return st;
+    uint8_t* sb = static_cast<uint8_t*>(scratch);
+    P.thr = reinterpret_cast<float*>(sb);
+    P.bcount = reinterpret_cast<uint32_t*>(sb + b_cnt);
+    P.boff = reinterpret_cast<unsigned long long*>(sb + b_bc);
+    P.spill = sb + b_off;
+    grad_sample_kernel<<<1, 1024, 0, s>>>(P);
+    grad_count_kernel<<<static_cast<unsigned>(P.nblocks), kGThreads, 0, s>>>(P);
+    grad_prefix_kernel<<<1, 1024, 0, s>>>(P);
+    grad_emit_kernel<<<static_cast<unsigned>(P.nblocks), kGThreads, 0, s>>>(P);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "grad compress launch");
+    tc::ctx_add_launches(ctx, 4);
+    return TC_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// walker outputs for `count` payloads of n elements: [count] Payload | per payload cpre and tstart
+tc_status walk_payloads(tc_ctx* ctx, const void* const* payloads, const uint64_t* bytes, int count, uint64_t n,
+                        bool tiles, cudaStream_t s, Payload** dev) {
+    uint64_t per = 0;
+    // worst case chunk count per payload: the smallest legal chunk (4096)
+    const uint64_t max_chunks = n / kGB + 2;
+    const uint64_t ntiles = (n + kGB - 1) / kGB;
+    per = pad16u(8 * (max_chunks + 1)) + (tiles ? pad16u(8 * (ntiles + 1)) : 0);
+    const size_t need = pad16u(sizeof(Payload) * count) + per * count;
+    void* scratch = nullptr;
+    tc_status st = tc::ctx_grad_scratch(ctx, need, s, &scratch);
+    if (st != TC_OK) return st;
+    Payload* P = static_cast<Payload*>(scratch);
+    uint8_t* area = static_cast<uint8_t*>(scratch) + pad16u(sizeof(Payload) * count);
+    for (int j = 0; j < count; ++j) {
+        Payload init = {};
+        init.cpre = reinterpret_cast<unsigned long long*>(area + per * j);
+        init.tstart = tiles ? reinterpret_cast<unsigned long long*>(area + per * j + pad16u(8 * (max_chunks + 1)))
+                            : nullptr;
+        cudaError_t e = cudaMemcpyAsync(P + j, &init, sizeof(Payload), cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return cuda_fail(e, "payload descriptor");
+        grad_walk_kernel<<<1, 32, 0, s>>>(static_cast<const uint8_t*>(payloads[j]), bytes[j], n, P + j,
+                                           tc::ctx_err(ctx));
+        if (tiles) grad_tile_start_kernel<<<grid_for(ctx, ntiles + 1, 256), 256, 0, s>>>(P + j, n, ntiles, tc::ctx_err(ctx));
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "payload walk launch");
+    tc::ctx_add_launches(ctx, static_cast<uint64_t>(count) * (tiles ? 2 : 1));
+    *dev = P;
+    return TC_OK;
+}
+}  // namespace
+
+extern "C" {
+
+tc_status tc_grad_decompress(tc_ctx* ctx, const void* payload, uint64_t bytes, float* out, uint64_t n,
+                             tc_stream stream) {
+    if (!ctx || !payload || !aligned16(payload) || (n && (!out || !aligned16(out))))
+        return fail(TC_ERR_INVALID, "bad arguments (ctx, 16-byte aligned payload / out)");
+    cudaSetDevice(tc::ctx_device(ctx));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Payload* P = nullptr;
+    tc_status st = walk_payloads(ctx, &payload, &bytes, 1, n, false, s, &P);
+    if (st != TC_OK) return st;
+    grad_decompress_kernel<<<grid_for(ctx, n, 256), 256, 0, s>>>(P, n, out, tc::ctx_err(ctx));
+    grad_scatter_kernel<<<grid_for(ctx, n / 64 + 1, 256), 256, 0, s>>>(P, n, out, tc::ctx_err(ctx));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "grad decompress launch");
+    tc::ctx_add_launches(ctx, 2);
+    return TC_OK;
+}
+
+tc_status tc_adam_step(tc_ctx* ctx, const tc_adam_state* stt, const float* grad, const tc_adam_hp* hp, uint64_t step,
+                       tc_stream stream) {
+    if (!ctx || step == 0) return fail(TC_ERR_INVALID, "ctx is NULL or step == 0 (steps are 1-based)");
+    tc_status st = check_state(stt);
+    if (st != TC_OK) return st;
+    if (!stt->n) return TC_OK;
+    if (!grad) return fail(TC_ERR_INVALID, "grad is NULL");
+    cudaSetDevice(tc::ctx_device(ctx));
+    float c1, c2;
+    bias(hp, step, &c1, &c2);
+    adam_step_kernel<<<grid_for(ctx, stt->n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        stt->master, stt->m, stt->v, stt->w16, stt->n, grad, adam_consts(hp), c1, c2);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "adam step launch");
+    tc::ctx_add_launches(ctx, 1);
+    return TC_OK;
+}
+
+tc_status tc_adam_replay(tc_ctx* ctx, const tc_adam_state* stt, const void* const* payloads,
+                         const uint64_t* payload_bytes, int n_payloads, const tc_adam_hp* hp, uint64_t first_step,
+                         float* scratch, tc_stream stream) {
+    if (!ctx || first_step == 0) return fail(TC_ERR_INVALID, "ctx is NULL or first_step == 0");
+    if (!payloads || !payload_bytes || n_payloads < 1 || n_payloads > TC_MAX_FOLD)
+        return fail(TC_ERR_INVALID, "n_payloads must be in [1, TC_MAX_FOLD]");
+    tc_status st = check_state(stt);
+    if (st != TC_OK) return st;
+    if (stt->n && (!scratch || !aligned16(scratch))) return fail(TC_ERR_INVALID, "scratch must be a 16-byte aligned device buffer");
+    for (int j = 0; j < n_payloads; ++j)
+        if (!payloads[j] || !aligned16(payloads[j])) return fail(TC_ERR_INVALID, "payload pointers must be 16-byte aligned");
+    cudaSetDevice(tc::ctx_device(ctx));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int nf = n_payloads - 1;
+    if (nf > 0 && stt->n) {
+        Payload* P = nullptr;
+        st = walk_payloads(ctx, payloads, payload_bytes, nf, stt->n, true, s, &P);
+        if (st != TC_OK) return st;
+        ReplayParams R = {};
+        R.master = stt->master;
+        R.m = stt->m;
+        R.v = stt->v;
+        R.n = stt->n;
+        R.tiles = (stt->n + kGB - 1) / kGB;
+        R.nsteps = nf;
+        R.a = adam_consts(hp);
+        for (int j = 0; j < nf; ++j) bias(hp, first_step + j, &R.c1[j], &R.c2[j]);
+        R.pay = P;
+        R.err = tc::ctx_err(ctx);
+        adam_replay_kernel<<<grid_for(ctx, R.tiles * kGThreads, kGThreads), kGThreads, 0, s>>>(R);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "adam replay launch");
+        tc::ctx_add_launches(ctx, 1);
+    }
+    // the last step through the native path
+    st = tc_grad_decompress(ctx, payloads[nf], payload_bytes[nf], scratch, stt->n, stream);
+    if (st != TC_OK) return st;
+    return tc_adam_step(ctx, stt, scratch, hp, first_step + nf, stream);
+}
+
+}  // extern "C"

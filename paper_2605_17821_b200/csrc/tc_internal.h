@@ -140,6 +140,7 @@ int ctx_device(tc_ctx* c);
 int ctx_num_sms(tc_ctx* c);
 void ctx_add_launches(tc_ctx* c, uint64_t n);
 uint32_t ctx_push_ctas(tc_ctx* c);
+tc_status ctx_grad_scratch(tc_ctx* c, size_t bytes, cudaStream_t s, void** out);
 
 }  // namespace tc
 

@@ -29,6 +29,8 @@ struct tc_ctx {
     uint64_t launches = 0;
     uint32_t fold_dense_permille = 30;  // tc_ctx_set_fold_dense_permille
     uint32_t push_ctas = 0;              // tc_ctx_set_push_ctas (0: default)
+    void* grad = nullptr;                // gradient codec / replay scratch (tc_grad.cu)
+    size_t grad_bytes = 0;
 };
 
 namespace tc {
@@ -175,6 +177,7 @@ tc_status tc_ctx_destroy(tc_ctx* c) {
     if (c->fold) cudaFree(c->fold);
     if (c->spill) cudaFree(c->spill);
     if (c->mstage) cudaFree(c->mstage);
+    if (c->grad) cudaFree(c->grad);
     if (c->err) cudaFree(c->err);
     delete c;
     return TC_OK;
@@ -480,4 +483,9 @@ int ctx_device(tc_ctx* c) { return c->device; }
 int ctx_num_sms(tc_ctx* c) { return c->num_sms; }
 void ctx_add_launches(tc_ctx* c, uint64_t n) { c->launches += n; }
 uint32_t ctx_push_ctas(tc_ctx* c) { return c->push_ctas; }
+tc_status ctx_grad_scratch(tc_ctx* c, size_t bytes, cudaStream_t s, void** out) {
+    tc_status st = ensure(&c->grad, &c->grad_bytes, bytes, s);
+    *out = c->grad;
+    return st;
+}
 }  // namespace tc

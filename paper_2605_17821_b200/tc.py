@@ -35,6 +35,21 @@ class EncodeOpts(ctypes.Structure):
                 ("reserved", u32)]
 
 
+class GradOpts(ctypes.Structure):
+    """tc_grad_opts (include/tc_grad.h)."""
+    _fields_ = [("small_threshold", u64), ("k", ctypes.c_double), ("sample_size", u32), ("reserved", u32),
+                ("chunk_elems", u64)]
+
+
+class AdamHP(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_double), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double),
+                ("eps", ctypes.c_double)]
+
+
+class AdamState(ctypes.Structure):
+    _fields_ = [("master", vp), ("m", vp), ("v", vp), ("w16", vp), ("n", u64)]
+
+
 class TcError(RuntimeError):
     def __init__(self, status: int, where: str, detail: str = ""):
         self.status = status
@@ -87,6 +102,14 @@ def _load():
     L.tc_diff_encode_push.argtypes = [vp, ctypes.POINTER(Segment), cint, ctypes.POINTER(EncodeOpts), u64, u64,
                                       vp, u64, vp, vp, u64, vp, vp]
     L.tc_peer_wait.argtypes = [vp, vp, u64, vp, vp]
+    L.tc_grad_bound.argtypes = [u64, ctypes.POINTER(GradOpts), ctypes.POINTER(u64)]
+    L.tc_grad_compress.argtypes = [vp, vp, u64, ctypes.POINTER(GradOpts), u64, vp, u64, vp, vp]
+    L.tc_grad_decompress.argtypes = [vp, vp, u64, vp, u64, vp]
+    L.tc_adam_step.argtypes = [vp, ctypes.POINTER(AdamState), vp, ctypes.POINTER(AdamHP), u64, vp]
+    L.tc_adam_replay.argtypes = [vp, ctypes.POINTER(AdamState), ctypes.POINTER(vp), ctypes.POINTER(u64), cint,
+                                 ctypes.POINTER(AdamHP), u64, vp, vp]
+    for name in ("tc_grad_bound", "tc_grad_compress", "tc_grad_decompress", "tc_adam_step", "tc_adam_replay"):
+        getattr(L, name).restype = cint
     for name in ("tc_ipc_alloc", "tc_ipc_free", "tc_ipc_open", "tc_ipc_close", "tc_push_peer",
                  "tc_diff_encode_push", "tc_peer_wait"):
         getattr(L, name).restype = cint
@@ -112,7 +135,7 @@ def _check(rc: int, where: str):
 def header_symbols():
     """Every function the public headers declare (for the ABI export test)."""
     names = []
-    for h in ("tc.h", "tc_synth.h"):
+    for h in ("tc.h", "tc_synth.h", "tc_grad.h"):
         with open(os.path.join(INCLUDE, h)) as fh:
             txt = fh.read()
         names += re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(tc_\w+)\s*\(", txt, re.M)
@@ -417,3 +440,54 @@ def synth_step(words: torch.Tensor, seed: int, seg: int, t: int, p53: int, struc
                stream=None):
     _check(LIB.tc_synth_step(words.data_ptr(), words.numel(), _wb(words), seed, seg, t, p53, structure, start,
                              _stream(stream)), "tc_synth_step")
+
+
+# ------------------------------------------------ the paper's lossy differential (tc_grad.h)
+def _gopts(k=0.01, small_threshold=100_000, sample_size=4096, chunk_elems=(1 << 31) - 4096):
+    return GradOpts(int(small_threshold), float(k), int(sample_size), 0, int(chunk_elems))
+
+
+def grad_bound(n: int, **opts) -> int:
+    out = u64(0)
+    o = _gopts(**opts)
+    _check(LIB.tc_grad_bound(int(n), ctypes.byref(o), ctypes.byref(out)), "tc_grad_bound")
+    return out.value
+
+
+def grad_compress(ctx: Ctx, grad: torch.Tensor, seed: int, out: torch.Tensor, out_bytes: torch.Tensor,
+                  stream=None, **opts):
+    """Enqueue tc_grad_compress of the fp32 CUDA tensor ``grad`` into ``out`` (uint8)."""
+    o = _gopts(**opts)
+    _check(LIB.tc_grad_compress(ctx.h, grad.data_ptr(), grad.numel(), ctypes.byref(o), int(seed), out.data_ptr(),
+                                out.numel() * out.element_size(), out_bytes.data_ptr(), _stream(stream)),
+           "tc_grad_compress")
+
+
+def grad_decompress(ctx: Ctx, payload: torch.Tensor, nbytes: int, out: torch.Tensor, stream=None):
+    _check(LIB.tc_grad_decompress(ctx.h, payload.data_ptr(), int(nbytes), out.data_ptr(), out.numel(),
+                                  _stream(stream)), "tc_grad_decompress")
+
+
+def _adam(master, m, v, w16):
+    return AdamState(master.data_ptr(), m.data_ptr(), v.data_ptr(), w16.data_ptr(), master.numel())
+
+
+def _hp(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8):
+    return AdamHP(lr, beta1, beta2, eps)
+
+
+def adam_step(ctx: Ctx, master, m, v, w16, grad, step: int, stream=None, **hp):
+    """Enqueue tc_adam_step (fp32 master/m/v, int16 tensor of bf16 bits w16, fp32 grad; 1-based step)."""
+    st, h = _adam(master, m, v, w16), _hp(**hp)
+    _check(LIB.tc_adam_step(ctx.h, ctypes.byref(st), grad.data_ptr(), ctypes.byref(h), int(step), _stream(stream)),
+           "tc_adam_step")
+
+
+def adam_replay(ctx: Ctx, master, m, v, w16, payloads, payload_bytes, first_step: int, scratch, stream=None, **hp):
+    """Enqueue tc_adam_replay: payloads[:-1] fused, the last through the native step."""
+    st, h = _adam(master, m, v, w16), _hp(**hp)
+    k = len(payloads)
+    pp = (vp * k)(*[p.data_ptr() for p in payloads])
+    pb = (u64 * k)(*[int(b) for b in payload_bytes])
+    _check(LIB.tc_adam_replay(ctx.h, ctypes.byref(st), pp, pb, k, ctypes.byref(h), int(first_step),
+                              scratch.data_ptr(), _stream(stream)), "tc_adam_replay")

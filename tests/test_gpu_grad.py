@@ -1,0 +1,166 @@
+"""GPU parity of the paper's lossy differential (NEXT row 3, include/tc_grad.h) against the
+oracle (oracle/tco_grad.c): compressed payload bytes, decompressed values, the Adam step and the
+fused multi-step replay — all bit-exact — plus the capacity and corruption paths."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import oracle  # noqa: E402
+from paper_2605_17821_b200 import tc  # noqa: E402
+
+RNG = np.random.default_rng(23)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = tc.Ctx(0)
+    yield c
+    c.close()
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def gpu_compress(ctx, x, seed, **opts):
+    cap = tc.grad_bound(x.size, **opts)
+    out = torch.full((cap + 64,), 0xAB, dtype=torch.uint8, device="cuda")
+    ob = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tc.grad_compress(ctx, dev(x), seed, out[:cap], ob, **opts)
+    ctx.check()
+    n = int(ob.item())
+    return out[:n].cpu().numpy(), out
+
+
+def grad_of(kind, n):
+    if kind == "normal":
+        return (RNG.standard_normal(n) * 1e-2).astype(np.float32)
+    if kind == "zeros_mixed":
+        x = RNG.standard_normal(n).astype(np.float32)
+        x[RNG.random(n) < 0.5] = 0.0
+        return x
+    if kind == "ties":
+        return RNG.integers(-3, 4, n).astype(np.float32)
+    if kind == "zero":
+        return np.zeros(n, np.float32)
+    if kind == "wide":
+        return (RNG.standard_normal(n) * 10.0 ** RNG.integers(-20, 20, n)).astype(np.float32)
+    raise ValueError(kind)
+
+
+CASES = [
+    (10, "normal", {}), (4097, "wide", {}), (99_999, "normal", {}),        # INT8 dense
+    (100_000, "normal", {}), (100_001, "ties", {}), (1_000_003, "normal", {}),
+    (300_000, "zeros_mixed", {"k": 0.1}), (250_000, "zero", {}), (200_000, "wide", {"k": 0.3}),
+    (123_457, "normal", {"chunk_elems": 4096 * 3}),                       # chunk rebasing
+    (70_000, "normal", {"small_threshold": 1000, "k": 0.6}),              # dense blocks (spill overflow)
+]
+
+
+@pytest.mark.parametrize("n,kind,opts", CASES)
+def test_compress_decompress_match_oracle(ctx, n, kind, opts):
+    x = grad_of(kind, n)
+    rc, exp = oracle.grad_compress(x, seed=n, **opts)
+    assert rc == 0
+    got, full = gpu_compress(ctx, x, n, **opts)
+    assert got.size == exp.size and np.array_equal(got, exp), "payload bytes differ from the oracle"
+    rc, y = oracle.grad_decompress(exp, n)
+    out = torch.full((n,), float("nan"), dtype=torch.float32, device="cuda")
+    tc.grad_decompress(ctx, full, got.size, out)
+    ctx.check()
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), y.view(np.uint32))
+
+
+def test_compress_capacity_on_device(ctx):
+    x = grad_of("normal", 400_000)
+    rc, exp = oracle.grad_compress(x, seed=1)
+    out = torch.full((exp.size,), 0xAB, dtype=torch.uint8, device="cuda")
+    ob = torch.zeros(1, dtype=torch.int64, device="cuda")
+    small = exp.size - 32
+    tc.grad_compress(ctx, dev(x), 1, out[:small], ob)
+    assert ctx.check_status() == tc.ERR_CAPACITY and int(ob.item()) == exp.size
+    assert (out[small:].cpu().numpy() == 0xAB).all()
+
+
+def test_decompress_tamper_corrupt(ctx):
+    x = grad_of("normal", 150_000)
+    rc, p = oracle.grad_compress(x, seed=4)
+    kept = int(np.frombuffer(p[24:32].tobytes(), np.uint64)[0])
+    ioff = 64 + 16 + (2 * kept + 15) // 16 * 16
+    out = torch.zeros(150_000, dtype=torch.float32, device="cuda")
+    for how in ("range", "order", "truncate", "magic"):
+        bad = p.copy()
+        if how == "range":
+            bad[ioff: ioff + 4] = np.frombuffer(np.int32(150_000).tobytes(), np.uint8)
+        elif how == "order":
+            bad[ioff: ioff + 8] = bad[[ioff + 4, ioff + 5, ioff + 6, ioff + 7, ioff, ioff + 1, ioff + 2, ioff + 3]]
+        elif how == "truncate":
+            bad = bad[:-16]
+        else:
+            bad[0] = ord("X")
+        assert oracle.grad_decompress(bad, 150_000)[0] == oracle.ERR_CORRUPT
+        tc.grad_decompress(ctx, dev(np.concatenate([bad, np.zeros(16, np.uint8)])), bad.size, out)
+        assert ctx.check_status() == tc.ERR_CORRUPT, how
+
+
+def state(n, seed):
+    r = np.random.default_rng(seed)
+    return [r.standard_normal(n).astype(np.float32), (r.standard_normal(n) * 1e-3).astype(np.float32),
+            (np.abs(r.standard_normal(n)) * 1e-6).astype(np.float32), np.zeros(n, np.uint16)]
+
+
+def to_gpu_state(st):
+    return [dev(st[0]), dev(st[1]), dev(st[2]), dev(st[3].view(np.int16))]
+
+
+def same_state(g, o):
+    return all(np.array_equal(a.cpu().numpy().view(np.uint32 if a.dtype == torch.float32 else np.uint16),
+                              b.view(np.uint32 if b.dtype == np.float32 else np.uint16)) for a, b in zip(g, o))
+
+
+@pytest.mark.parametrize("hp", [{}, {"lr": 0.1}, {"lr": 3e-4, "beta1": 0.8, "beta2": 0.99, "eps": 1e-6}])
+def test_adam_step_matches_oracle(ctx, hp):
+    n = 70_001
+    st = state(n, 5)
+    g = grad_of("wide", n)
+    g[:100] = 0.0
+    gs = to_gpu_state(st)
+    for t in (1, 2, 1000):
+        tc.adam_step(ctx, *gs, dev(g), t, **hp)
+        oracle.adam_step(st[0], st[1], st[2], st[3], g, t, **{"lr": 1e-3, "b1": 0.9, "b2": 0.999, "eps": 1e-8,
+                                                               **{{"beta1": "b1", "beta2": "b2"}.get(k, k): v
+                                                                  for k, v in hp.items()}})
+    ctx.check()
+    assert same_state(gs, st)
+
+
+@pytest.mark.parametrize("N", [1, 2, 5, 10])
+@pytest.mark.parametrize("n,kind,opts", [(50_000, "normal", {}), (300_001, "normal", {}),
+                                          (200_000, "zeros_mixed", {"k": 0.05, "chunk_elems": 4096 * 7})])
+def test_fused_replay_matches_sequential_oracle(ctx, N, n, kind, opts):
+    """fused replay of N payloads == sequential decompress + adam_step, bit-exact."""
+    st = state(n, N)
+    pays = [oracle.grad_compress(grad_of(kind, n), seed=100 + j, **opts)[1] for j in range(N)]
+    gs = to_gpu_state(st)
+    assert oracle.adam_replay(st[0], st[1], st[2], st[3], pays, first_step=7) == 0
+    dp = [dev(np.concatenate([p, np.zeros(16, np.uint8)])) for p in pays]
+    scratch = torch.empty(n, dtype=torch.float32, device="cuda")
+    tc.adam_replay(ctx, *gs, dp, [p.size for p in pays], 7, scratch)
+    ctx.check()
+    assert same_state(gs, st)
+
+
+def test_replay_corrupt_payload(ctx):
+    n = 120_000
+    st = state(n, 1)
+    pays = [oracle.grad_compress(grad_of("normal", n), seed=j)[1] for j in range(3)]
+    bad = pays[1].copy()
+    bad[0] = ord("X")
+    gs = to_gpu_state(st)
+    dp = [dev(np.concatenate([p, np.zeros(16, np.uint8)])) for p in (pays[0], bad, pays[2])]
+    tc.adam_replay(ctx, *gs, dp, [pays[0].size, bad.size, pays[2].size], 1, torch.empty(n, device="cuda"))
+    assert ctx.check_status() == tc.ERR_CORRUPT
