@@ -467,6 +467,7 @@ __global__ void grad_tile_start_kernel(const Payload* RP, uint64_t n, uint64_t t
             if (pos < want) lo = mid + 1; else hi = mid;
         }
         R.tstart[t] = lo;
+        if (t == tiles && lo != R.kept) tc_set_err(err, TC_ERR_CORRUPT);  // entries past the last tile
     }
 }
 
@@ -480,9 +481,14 @@ __device__ __forceinline__ void adam_update(float& master, float& m, float& v, f
     const float omb1 = __fsub_rn(1.0f, a.b1), omb2 = __fsub_rn(1.0f, a.b2);
     m = __fadd_rn(__fmul_rn(a.b1, m), __fmul_rn(omb1, g));
     v = __fadd_rn(__fmul_rn(a.b2, v), __fmul_rn(omb2, __fmul_rn(g, g)));
-    const float mhat = __fdiv_rn(m, c1);
-    const float vhat = __fdiv_rn(v, c2);
-    const float upd = __fdiv_rn(__fmul_rn(a.lr, mhat), __fadd_rn(__fsqrt_rn(vhat), a.eps));
+    // zero operands take the IEEE result directly (0 / c = 0 with 0's sign for c > 0, sqrt(+0) = +0):
+    // the same values as the divisions, without their slow path — which zero dividends trigger,
+    // and most entries of a sparse gradient stream are zero
+    const float mhat = m != 0.0f ? __fdiv_rn(m, c1) : m;
+    const float vhat = v != 0.0f ? __fdiv_rn(v, c2) : v;
+    const float num = __fmul_rn(a.lr, mhat);
+    const float den = __fadd_rn(vhat != 0.0f ? __fsqrt_rn(vhat) : vhat, a.eps);
+    const float upd = num != 0.0f ? __fdiv_rn(num, den) : num;
     master = __fsub_rn(master, upd);
 }
 
@@ -512,60 +518,138 @@ struct ReplayParams {
     unsigned* err;
 };
 
-// one CTA per tile of kGB elements: (master, m, v) in registers for all fused steps
-__global__ void __launch_bounds__(kGThreads) adam_replay_kernel(const __grid_constant__ ReplayParams P) {
+// one CTA of 1024 threads per tile of kGB elements, 4 per thread: (master, m, v) stay in
+// registers for all fused steps (full occupancy; the IEEE-rounded divisions and square root of
+// every step make this kernel issue-bound, so latency hiding matters more than per-thread work)
+constexpr uint32_t kRThreads = 1024;
+constexpr uint32_t kRPer = kGB / kRThreads;
+constexpr uint32_t kRStage = 2048;  // staged sparse entries of one tile (all fused steps)
+
+struct ReplayStep {                 // per fused step, in shared memory
+    const int8_t* q;
+    const uint16_t* val;
+    const int32_t* idx;
+    const unsigned long long* tstart;
+    uint64_t chunk;
+    float scale;
+    uint32_t variant;
+};
+
+__global__ void __launch_bounds__(kRThreads) adam_replay_kernel(const __grid_constant__ ReplayParams P) {
     __shared__ float s_g[kGB];
+    __shared__ uint16_t s_pos[kRStage];
+    __shared__ float s_val[kRStage];
+    __shared__ ReplayStep s_step[TC_MAX_FOLD];
+    __shared__ uint32_t s_run[TC_MAX_FOLD + 1];   // staged entries before step s
+    __shared__ unsigned long long s_k0[TC_MAX_FOLD];
+    __shared__ uint32_t s_fits;
     if (*reinterpret_cast<volatile unsigned*>(P.err) != 0) return;
     const int tid = threadIdx.x;
+    if (tid < P.nsteps) {
+        const Payload& R = P.pay[tid];
+        s_step[tid] = {R.q, R.val, R.idx, R.tstart, R.chunk, R.scale, R.variant};
+    }
+    __syncthreads();
     bool bad = false;
     for (uint64_t t = blockIdx.x; t < P.tiles; t += gridDim.x) {
         const uint64_t base = t * kGB;
-        float w[kGPer], mm[kGPer], vv[kGPer];
+        float w[kRPer], mm[kRPer], vv[kRPer];
 #pragma unroll
-        for (uint32_t j = 0; j < kGPer; ++j) {
-            const uint64_t i = base + j * kGThreads + tid;
+        for (uint32_t j = 0; j < kRPer; ++j) {
+            const uint64_t i = base + j * kRThreads + tid;
             w[j] = i < P.n ? P.master[i] : 0.0f;
             mm[j] = i < P.n ? P.m[i] : 0.0f;
             vv[j] = i < P.n ? P.v[i] : 0.0f;
         }
+        // every sparse step's entries of this tile, staged at once: one round trip per tile
+        if (tid < P.nsteps) {
+            const ReplayStep& R = s_step[tid];
+            unsigned long long k0 = 0, k1 = 0;
+            if (R.variant == 2) {
+                k0 = R.tstart[t];
+                k1 = R.tstart[t + 1];
+                if (k1 < k0) k1 = k0;
+            }
+            s_k0[tid] = k0;
+            s_run[tid + 1] = static_cast<uint32_t>(k1 - k0 < kRStage ? k1 - k0 : kRStage + 1);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t o = 0;
+            s_run[0] = 0;
+            for (int s = 0; s < P.nsteps; ++s) {
+                o += s_run[s + 1];
+                s_run[s + 1] = o;
+            }
+            s_fits = o <= kRStage;
+        }
+        __syncthreads();
+        const bool fits = s_fits != 0;
+        if (fits) {
+            const uint32_t total = s_run[P.nsteps];
+            for (uint32_t e = tid; e < total; e += kRThreads) {
+                int s = 0;
+                while (s_run[s + 1] <= e) ++s;
+                const ReplayStep& R = s_step[s];
+                const uint64_t k = s_k0[s] + (e - s_run[s]);
+                // the tile lies in one chunk (chunk lengths are multiples of kGB)
+                const uint64_t pos = base / R.chunk * R.chunk + static_cast<uint64_t>(static_cast<uint32_t>(R.idx[k]));
+                if (R.idx[k] < 0 || pos < base || pos >= base + kGB || pos >= P.n) bad = true;
+                s_pos[e] = static_cast<uint16_t>((pos - base) & (kGB - 1));
+                s_val[e] = __half2float(__ushort_as_half(R.val[k]));
+            }
+            __syncthreads();
+            for (uint32_t e = tid; e < total; e += kRThreads) {  // increasing within each run
+                int s = 0;
+                while (s_run[s + 1] <= e) ++s;
+                if (e > s_run[s] && s_pos[e - 1] >= s_pos[e]) bad = true;
+            }
+        }
         for (int s = 0; s < P.nsteps; ++s) {
-            const Payload& R = P.pay[s];
+            const ReplayStep& R = s_step[s];
             if (R.variant == 1) {
 #pragma unroll
-                for (uint32_t j = 0; j < kGPer; ++j) {
-                    const uint64_t i = base + j * kGThreads + tid;
+                for (uint32_t j = 0; j < kRPer; ++j) {
+                    const uint64_t i = base + j * kRThreads + tid;
                     const float g = i < P.n ? __fmul_rn(R.scale, static_cast<float>(R.q[i])) : 0.0f;
                     adam_update(w[j], mm[j], vv[j], g, P.a, P.c1[s], P.c2[s]);
                 }
-            } else {
+                continue;
+            }
 #pragma unroll
-                for (uint32_t j = 0; j < kGPer; ++j) s_g[j * kGThreads + tid] = 0.0f;
-                __syncthreads();
-                const uint64_t k0 = R.tstart[t], k1 = R.tstart[t + 1];
-                for (uint64_t k = k0 + tid; k < k1; k += kGThreads) {
+            for (uint32_t j = 0; j < kRPer; ++j) s_g[j * kRThreads + tid] = 0.0f;
+            __syncthreads();
+            if (fits) {
+                for (uint32_t e = s_run[s] + tid; e < s_run[s + 1]; e += kRThreads) s_g[s_pos[e]] = s_val[e];
+            } else {  // more entries than the stage: straight from the payload
+                const Payload& RP = P.pay[s];
+                const uint64_t k0 = RP.tstart[t], k1 = RP.tstart[t + 1];
+                for (uint64_t k = k0 + tid; k < k1; k += kRThreads) {
                     uint64_t pos;
                     float val;
-                    if (!entry(R, P.n, k, &pos, &val) || pos < base || pos >= base + kGB) {
+                    if (!entry(RP, P.n, k, &pos, &val) || pos < base || pos >= base + kGB) {
                         bad = true;
                         continue;
                     }
                     s_g[pos - base] = val;
                 }
-                __syncthreads();
-#pragma unroll
-                for (uint32_t j = 0; j < kGPer; ++j) adam_update(w[j], mm[j], vv[j], s_g[j * kGThreads + tid], P.a, P.c1[s], P.c2[s]);
-                __syncthreads();
             }
+            __syncthreads();
+#pragma unroll
+            for (uint32_t j = 0; j < kRPer; ++j)
+                adam_update(w[j], mm[j], vv[j], s_g[j * kRThreads + tid], P.a, P.c1[s], P.c2[s]);
+            __syncthreads();
         }
 #pragma unroll
-        for (uint32_t j = 0; j < kGPer; ++j) {
-            const uint64_t i = base + j * kGThreads + tid;
+        for (uint32_t j = 0; j < kRPer; ++j) {
+            const uint64_t i = base + j * kRThreads + tid;
             if (i < P.n) {
                 P.master[i] = w[j];
                 P.m[i] = mm[j];
                 P.v[i] = vv[j];
             }
         }
+        __syncthreads();  // the stage and the run table are reused by the next tile
     }
     if (bad) tc_set_err(P.err, TC_ERR_CORRUPT);
 }
@@ -763,7 +847,7 @@ tc_status tc_adam_replay(tc_ctx* ctx, const tc_adam_state* stt, const void* cons
         for (int j = 0; j < nf; ++j) bias(hp, first_step + j, &R.c1[j], &R.c2[j]);
         R.pay = P;
         R.err = tc::ctx_err(ctx);
-        adam_replay_kernel<<<grid_for(ctx, R.tiles * kGThreads, kGThreads), kGThreads, 0, s>>>(R);
+        adam_replay_kernel<<<grid_for(ctx, R.tiles * kRThreads, kRThreads), kRThreads, 0, s>>>(R);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "adam replay launch");
         tc::ctx_add_launches(ctx, 1);
