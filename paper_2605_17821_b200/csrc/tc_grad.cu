@@ -21,7 +21,6 @@ namespace {
 
 constexpr uint32_t kGB = 4096;         // elements per compaction block / replay tile
 constexpr uint32_t kGThreads = 256;    // 16 elements per thread
-constexpr uint32_t kGPer = kGB / kGThreads;
 constexpr uint32_t kGSpill = 256;      // entries a block keeps in its spill slot (6 bytes each)
 constexpr uint32_t kSampleMax = 8192;  // largest supported sample (sorted in shared memory)
 constexpr uint64_t kDefaultChunk = (1ull << 31) - 4096;
@@ -122,10 +121,14 @@ struct SparseParams {
     uint64_t* out_bytes;
     float* thr;                  // [1]
     uint32_t* bcount;            // [nblocks] kept | dense flag
-    unsigned long long* boff;    // [nblocks + 1] exclusive prefix; [nblocks] = kept
+    unsigned long long* gsum;    // [ngroups] kept per group of kGGroup blocks (zeroed per call)
+    unsigned long long* gpre;    // [ngroups + 1] exclusive prefix of gsum; [ngroups] = kept
+    unsigned long long* cstart;  // [nchunks + 1] first entry of each chunk
     uint8_t* spill;              // [nblocks][kGSpill * 6]: f16 values | i32 local indices
+    uint64_t ngroups;
     unsigned* err;
 };
+constexpr uint32_t kGGroup = 256;  // blocks per emit CTA (a thread per block)
 constexpr uint32_t kDenseBit = 0x80000000u;
 
 // the threshold: rank-th smallest magnitude of `sample` seeded draws (bitonic sort in smem)
@@ -158,76 +161,81 @@ __global__ void __launch_bounds__(1024) grad_sample_kernel(const __grid_constant
 // the keeping predicate: |x| >= threshold, zeros never kept
 __device__ __forceinline__ bool keep(float v, float thr) { return v != 0.0f && fabsf(v) >= thr; }
 
-// pass 1: per block counts; sparse blocks pack their entries (index order) into the spill slot
-__global__ void __launch_bounds__(kGThreads) grad_count_kernel(const __grid_constant__ SparseParams P) {
-    __shared__ uint32_t s_cnt[kGPer * (kGThreads / 32)];
-    __shared__ uint32_t s_total;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint64_t b = blockIdx.x;
-    const uint64_t base = b * kGB;
-    const float thr = *P.thr;
-    float v[kGPer];
-    uint32_t bal[kGPer];
-#pragma unroll
-    for (uint32_t j = 0; j < kGPer; ++j) {
-        const uint64_t i = base + j * kGThreads + tid;
-        v[j] = i < P.n ? P.x[i] : 0.0f;
-    }
-#pragma unroll
-    for (uint32_t j = 0; j < kGPer; ++j) {
-        bal[j] = __ballot_sync(0xffffffffu, keep(v[j], thr));
-        if (lane == 0) s_cnt[j * (kGThreads / 32) + wid] = __popc(bal[j]);
-    }
-    __syncthreads();
-    if (tid < 32) {  // exclusive scan of the 128 (j, warp) counts, in index order
-        uint32_t c[4], t = 0;
+// the 16 flags of one thread's elements [i0, i0 + 16) (4 x 16-byte loads; elements past n are 0)
+__device__ __forceinline__ uint32_t flags16(const float* x, uint64_t n, uint64_t i0, float thr, float (&v)[16]) {
+    if (i0 + 16 <= n) {
+        const float4* p = reinterpret_cast<const float4*>(x + i0);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            c[q] = s_cnt[tid * 4 + q];
-            t += c[q];
+            const float4 f = __ldg(p + q);
+            v[4 * q] = f.x;
+            v[4 * q + 1] = f.y;
+            v[4 * q + 2] = f.z;
+            v[4 * q + 3] = f.w;
         }
-        uint32_t inc = t;
+    } else {
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
-            if (lane >= d) inc += y;
-        }
-        uint32_t run = inc - t;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            s_cnt[tid * 4 + q] = run;
-            run += c[q];
-        }
-        if (tid == 31) s_total = inc;
+        for (int e = 0; e < 16; ++e) v[e] = i0 + e < n ? x[i0 + e] : 0.0f;
     }
-    __syncthreads();
-    const uint32_t total = s_total;
-    if (tid == 0) P.bcount[b] = total | (total > kGSpill ? kDenseBit : 0u);
-    if (total == 0 || total > kGSpill) return;
-    uint16_t* sv = reinterpret_cast<uint16_t*>(P.spill + b * (kGSpill * 6));
-    int32_t* si = reinterpret_cast<int32_t*>(P.spill + b * (kGSpill * 6) + kGSpill * 2);
-    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t f = 0;
 #pragma unroll
-    for (uint32_t j = 0; j < kGPer; ++j) {
-        if ((bal[j] >> lane) & 1u) {
-            const uint32_t k = s_cnt[j * (kGThreads / 32) + wid] + __popc(bal[j] & lt);
-            const uint64_t i = base + j * kGThreads + tid;
-            sv[k] = __half_as_ushort(__float2half_rn(v[j]));
-            si[k] = static_cast<int32_t>(i - i / P.chunk * P.chunk);
-        }
-    }
+    for (int e = 0; e < 16; ++e) f |= keep(v[e], thr) ? (1u << e) : 0u;
+    return f;
 }
 
-// block offsets, the payload length, and the capacity check
+// pass 1: thread t of block b takes elements [b*kGB + 16t, +16): per-thread counts, a block scan
+// in index order, the group sums; sparse blocks pack their entries into the spill slot
+__global__ void __launch_bounds__(kGThreads) grad_count_kernel(const __grid_constant__ SparseParams P) {
+    __shared__ uint32_t s_warp[kGThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint64_t b = blockIdx.x;
+    const uint64_t i0 = b * kGB + 16ull * tid;
+    const float thr = *P.thr;
+    float v[16];
+    const uint32_t f = flags16(P.x, P.n, i0, thr, v);
+    const uint32_t c = __popc(f);
+    uint32_t inc = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += y;
+    }
+    if (lane == 31) s_warp[wid] = inc;
+    __syncthreads();
+    uint32_t wp = 0, total = 0;
+#pragma unroll
+    for (int k = 0; k < static_cast<int>(kGThreads / 32); ++k) {
+        wp += k < wid ? s_warp[k] : 0u;
+        total += s_warp[k];
+    }
+    if (tid == 0) {
+        P.bcount[b] = total | (total > kGSpill ? kDenseBit : 0u);
+        if (total) atomicAdd(&P.gsum[b / kGGroup], static_cast<unsigned long long>(total));
+    }
+    if (total == 0 || total > kGSpill || f == 0) return;
+    uint16_t* sv = reinterpret_cast<uint16_t*>(P.spill + b * (kGSpill * 6));
+    int32_t* si = reinterpret_cast<int32_t*>(P.spill + b * (kGSpill * 6) + kGSpill * 2);
+    uint32_t k = wp + inc - c;
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+        if ((f >> e) & 1u) {
+            const uint64_t i = i0 + e;
+            sv[k] = __half_as_ushort(__float2half_rn(v[e]));
+            si[k] = static_cast<int32_t>(i - i / P.chunk * P.chunk);
+            ++k;
+        }
+}
+
+// group prefix, chunk starts, payload length + capacity, header, chunk table and pads (1 CTA)
 __global__ void __launch_bounds__(1024) grad_prefix_kernel(const __grid_constant__ SparseParams P) {
     __shared__ unsigned long long s_carry;
     __shared__ unsigned long long s_warp[32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (tid == 0) s_carry = 0;
     __syncthreads();
-    for (uint64_t base = 0; base < P.nblocks; base += 1024) {
+    for (uint64_t base = 0; base < P.ngroups; base += 1024) {
         const uint64_t i = base + tid;
-        const unsigned long long c = i < P.nblocks ? (P.bcount[i] & ~kDenseBit) : 0ull;
+        const unsigned long long c = i < P.ngroups ? P.gsum[i] : 0ull;
         unsigned long long x = c;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -242,99 +250,106 @@ __global__ void __launch_bounds__(1024) grad_prefix_kernel(const __grid_constant
             tot += s_warp[k];
         }
         const unsigned long long carry = s_carry;
-        if (i < P.nblocks) P.boff[i] = carry + wp + x - c;
+        if (i < P.ngroups) P.gpre[i] = carry + wp + x - c;
         __syncthreads();
         if (tid == 0) s_carry = carry + tot;
         __syncthreads();
     }
-    if (tid == 0) {
-        const uint64_t kept = s_carry;
-        P.boff[P.nblocks] = kept;
-        const uint64_t total = kHdr + 16 * P.nchunks + pad16u(2 * kept) + pad16u(4 * kept);
-        *reinterpret_cast<volatile uint64_t*>(P.out_bytes) = total;
-        if (total > P.cap) tc_set_err(P.err, TC_ERR_CAPACITY);
+    const uint64_t kept = s_carry;
+    const uint64_t bpc = P.chunk / kGB;  // blocks per chunk
+    for (uint64_t c = tid; c <= P.nchunks; c += 1024) {
+        unsigned long long st = kept;
+        if (c < P.nchunks) {
+            const uint64_t fb = c * bpc, g = fb / kGGroup;
+            st = P.gpre[g];
+            for (uint64_t bb = g * kGGroup; bb < fb; ++bb) st += P.bcount[bb] & ~kDenseBit;
+        }
+        P.cstart[c] = st;
     }
-}
-
-// pass 2: entries to their final place (dense blocks re-read their gradient); block 0 writes the
-// header, the chunk table and the pads
-__global__ void __launch_bounds__(kGThreads) grad_emit_kernel(const __grid_constant__ SparseParams P) {
-    __shared__ uint32_t s_cnt[kGPer * (kGThreads / 32)];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint64_t b = blockIdx.x;
-    const uint64_t kept = P.boff[P.nblocks];
     const uint64_t voff = kHdr + 16 * P.nchunks, ioff = voff + pad16u(2 * kept);
     const uint64_t total = ioff + pad16u(4 * kept);
-    if (total > P.cap) return;  // CAPACITY was reported by the prefix kernel
+    if (tid == 0) {
+        P.gpre[P.ngroups] = kept;
+        *reinterpret_cast<volatile uint64_t*>(P.out_bytes) = total;
+        if (total > P.cap) tc_set_err(P.err, TC_ERR_CAPACITY);
+        else put_header(P.out, 2, static_cast<uint32_t>(P.nchunks), *P.thr, P.n, kept, P.chunk, P.seed, total);
+    }
+    if (total > P.cap) return;
+    __syncthreads();  // cstart complete
+    for (uint64_t c = tid; c < P.nchunks; c += 1024) {
+        uint64_t* t = reinterpret_cast<uint64_t*>(P.out + kHdr + 16 * c);
+        t[0] = c * P.chunk;
+        t[1] = P.cstart[c + 1] - P.cstart[c];
+    }
+    for (uint64_t x = 2 * kept + tid; x < pad16u(2 * kept); x += 1024) P.out[voff + x] = 0;
+    for (uint64_t x = 4 * kept + tid; x < pad16u(4 * kept); x += 1024) P.out[ioff + x] = 0;
+}
+
+// pass 2: a CTA per group of kGGroup blocks; a thread per block finds its offset, then each warp
+// copies its 32 blocks' spilled entries (dense blocks: re-read and packed by the warp)
+__global__ void __launch_bounds__(kGThreads) grad_emit_kernel(const __grid_constant__ SparseParams P) {
+    __shared__ uint32_t s_warp[kGThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const uint64_t g = blockIdx.x;
+    const uint64_t kept = P.gpre[P.ngroups];
+    const uint64_t voff = kHdr + 16 * P.nchunks, ioff = voff + pad16u(2 * kept);
+    if (ioff + pad16u(4 * kept) > P.cap) return;  // CAPACITY was reported by the prefix kernel
     uint16_t* gv = reinterpret_cast<uint16_t*>(P.out + voff);
     int32_t* gi = reinterpret_cast<int32_t*>(P.out + ioff);
-    if (b == 0) {
-        if (tid == 0) put_header(P.out, 2, static_cast<uint32_t>(P.nchunks), *P.thr, P.n, kept, P.chunk, P.seed, total);
-        for (uint64_t c = tid; c < P.nchunks; c += kGThreads) {
-            const uint64_t b0 = c * (P.chunk / kGB), b1 = (c + 1) * (P.chunk / kGB);
-            const uint64_t cnt = P.boff[b1 < P.nblocks ? b1 : P.nblocks] - P.boff[b0];
-            uint64_t* t = reinterpret_cast<uint64_t*>(P.out + kHdr + 16 * c);
-            t[0] = c * P.chunk;
-            t[1] = cnt;
-        }
-        for (uint64_t x = 2 * kept + tid; x < pad16u(2 * kept); x += kGThreads) P.out[voff + x] = 0;
-        for (uint64_t x = 4 * kept + tid; x < pad16u(4 * kept); x += kGThreads) P.out[ioff + x] = 0;
+    const uint64_t b = g * kGGroup + tid;
+    const uint32_t info = b < P.nblocks ? P.bcount[b] : 0u;
+    const uint32_t c = info & ~kDenseBit;
+    uint32_t inc = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += y;
     }
-    const uint32_t info = P.bcount[b];
-    const uint32_t cnt = info & ~kDenseBit;
-    if (cnt == 0) return;
-    const uint64_t off = P.boff[b];
-    if (!(info & kDenseBit)) {
-        const uint16_t* sv = reinterpret_cast<const uint16_t*>(P.spill + b * (kGSpill * 6));
-        const int32_t* si = reinterpret_cast<const int32_t*>(P.spill + b * (kGSpill * 6) + kGSpill * 2);
-        for (uint32_t k = tid; k < cnt; k += kGThreads) {
-            gv[off + k] = sv[k];
-            gi[off + k] = si[k];
-        }
-        return;
-    }
-    // dense block: the same ballot order as pass 1, straight into the payload
-    const uint64_t base = b * kGB;
+    if (lane == 31) s_warp[wid] = inc;
+    __syncthreads();
+    uint32_t wp = 0;
+#pragma unroll
+    for (int k = 0; k < static_cast<int>(kGThreads / 32); ++k) wp += k < wid ? s_warp[k] : 0u;
+    const unsigned long long off = P.gpre[g] + wp + inc - c;
     const float thr = *P.thr;
-    float v[kGPer];
-    uint32_t bal[kGPer];
-#pragma unroll
-    for (uint32_t j = 0; j < kGPer; ++j) {
-        const uint64_t i = base + j * kGThreads + tid;
-        v[j] = i < P.n ? P.x[i] : 0.0f;
-        bal[j] = __ballot_sync(0xffffffffu, keep(v[j], thr));
-        if (lane == 0) s_cnt[j * (kGThreads / 32) + wid] = __popc(bal[j]);
-    }
-    __syncthreads();
-    if (tid < 32) {
-        uint32_t c[4], t = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            c[q] = s_cnt[tid * 4 + q];
-            t += c[q];
+    for (int i = 0; i < 32; ++i) {  // the warp's blocks, one at a time
+        const uint32_t ci = __shfl_sync(0xffffffffu, info, i);
+        const uint32_t cnt = ci & ~kDenseBit;
+        if (cnt == 0) continue;
+        const unsigned long long o = __shfl_sync(0xffffffffu, off, i);
+        const uint64_t bb = g * kGGroup + wid * 32 + i;
+        if (!(ci & kDenseBit)) {
+            const uint16_t* sv = reinterpret_cast<const uint16_t*>(P.spill + bb * (kGSpill * 6));
+            const int32_t* si = reinterpret_cast<const int32_t*>(P.spill + bb * (kGSpill * 6) + kGSpill * 2);
+            for (uint32_t k = lane; k < cnt; k += 32) {
+                gv[o + k] = sv[k];
+                gi[o + k] = si[k];
+            }
+            continue;
         }
-        uint32_t inc = t;
+        // dense block: the count kernel's order (16-element runs of threads 0..255), 32 runs a pass
+        unsigned long long run = o;
+        for (uint32_t t0 = 0; t0 < kGThreads; t0 += 32) {
+            const uint64_t i0 = bb * kGB + 16ull * (t0 + lane);
+            float v[16];
+            const uint32_t f = flags16(P.x, P.n, i0, thr, v);
+            const uint32_t cf = __popc(f);
+            uint32_t x = cf;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
-            if (lane >= d) inc += y;
-        }
-        uint32_t run = inc - t;
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+                if (lane >= d) x += y;
+            }
+            unsigned long long k = run + x - cf;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            s_cnt[tid * 4 + q] = run;
-            run += c[q];
-        }
-    }
-    __syncthreads();
-    const uint32_t lt = (1u << lane) - 1u;
-#pragma unroll
-    for (uint32_t j = 0; j < kGPer; ++j) {
-        if ((bal[j] >> lane) & 1u) {
-            const uint64_t k = off + s_cnt[j * (kGThreads / 32) + wid] + __popc(bal[j] & lt);
-            const uint64_t i = base + j * kGThreads + tid;
-            gv[k] = __half_as_ushort(__float2half_rn(v[j]));
-            gi[k] = static_cast<int32_t>(i - i / P.chunk * P.chunk);
+            for (int e = 0; e < 16; ++e)
+                if ((f >> e) & 1u) {
+                    const uint64_t ii = i0 + e;
+                    gv[k] = __half_as_ushort(__float2half_rn(v[e]));
+                    gi[k] = static_cast<int32_t>(ii - ii / P.chunk * P.chunk);
+                    ++k;
+                }
+            run += __shfl_sync(0xffffffffu, x, 31);
         }
     }
 }
@@ -697,8 +712,8 @@ tc_status tc_grad_bound(uint64_t n, const tc_grad_opts* opts, uint64_t* max_byte
 
 tc_status tc_grad_compress(tc_ctx* ctx, const float* grad, uint64_t n, const tc_grad_opts* opts, uint64_t seed,
                            void* out, uint64_t out_cap, uint64_t* out_bytes, tc_stream stream) {
-    if (!ctx || !out || !aligned16(out) || !out_bytes || (n && !grad))
-        return fail(TC_ERR_INVALID, "bad arguments (ctx, 16-byte aligned out, out_bytes, grad)");
+    if (!ctx || !out || !aligned16(out) || !out_bytes || (n && (!grad || !aligned16(grad))))
+        return fail(TC_ERR_INVALID, "bad arguments (ctx, 16-byte aligned out / grad, out_bytes)");
     Opts o;
     tc_status st = resolve(opts, &o);
     if (st != TC_OK) return st;
@@ -725,20 +740,26 @@ tc_status tc_grad_compress(tc_ctx* ctx, const float* grad, uint64_t n, const tc_
     P.out = static_cast<uint8_t*>(out);
     P.out_bytes = out_bytes;
     P.err = err;
-    const size_t b_cnt = 16, b_bc = b_cnt + pad16u(4 * P.nblocks), b_off = b_bc + pad16u(8 * (P.nblocks + 1));
-    const size_t need = b_off + P.nblocks * (kGSpill * 6);
+    P.ngroups = (P.nblocks + kGGroup - 1) / kGGroup;
+    const size_t o_bc = 16, o_gs = o_bc + pad16u(4 * P.nblocks), o_gp = o_gs + pad16u(8 * P.ngroups);
+    const size_t o_cs = o_gp + pad16u(8 * (P.ngroups + 1)), o_sp = o_cs + pad16u(8 * (P.nchunks + 1));
+    const size_t need = o_sp + P.nblocks * (kGSpill * 6);
     void* scratch = nullptr;
     st = tc::ctx_grad_scratch(ctx, need, s, &scratch);
     if (st != TC_OK) return st;
     uint8_t* sb = static_cast<uint8_t*>(scratch);
     P.thr = reinterpret_cast<float*>(sb);
-    P.bcount = reinterpret_cast<uint32_t*>(sb + b_cnt);
-    P.boff = reinterpret_cast<unsigned long long*>(sb + b_bc);
-    P.spill = sb + b_off;
+    P.bcount = reinterpret_cast<uint32_t*>(sb + o_bc);
+    P.gsum = reinterpret_cast<unsigned long long*>(sb + o_gs);
+    P.gpre = reinterpret_cast<unsigned long long*>(sb + o_gp);
+    P.cstart = reinterpret_cast<unsigned long long*>(sb + o_cs);
+    P.spill = sb + o_sp;
+    cudaError_t e0 = cudaMemsetAsync(P.gsum, 0, 8 * P.ngroups, s);
+    if (e0 != cudaSuccess) return cuda_fail(e0, "cudaMemsetAsync(group sums)");
     grad_sample_kernel<<<1, 1024, 0, s>>>(P);
     grad_count_kernel<<<static_cast<unsigned>(P.nblocks), kGThreads, 0, s>>>(P);
     grad_prefix_kernel<<<1, 1024, 0, s>>>(P);
-    grad_emit_kernel<<<static_cast<unsigned>(P.nblocks), kGThreads, 0, s>>>(P);
+    grad_emit_kernel<<<static_cast<unsigned>(P.ngroups), kGThreads, 0, s>>>(P);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "grad compress launch");
     tc::ctx_add_launches(ctx, 4);
