@@ -16,6 +16,12 @@
 
 #include "../../include/tc_grad.h"
 #include "tc_internal.h"
+#include "tc_ptx.cuh"
+
+using tc::bulk_g2s;
+using tc::mbar_arrive_expect_tx;
+using tc::mbar_init;
+using tc::mbar_wait_parity;
 
 namespace {
 
@@ -539,6 +545,8 @@ struct ReplayParams {
 constexpr uint32_t kRThreads = 1024;
 constexpr uint32_t kRPer = kGB / kRThreads;
 constexpr uint32_t kRStage = 2048;  // staged sparse entries of one tile (all fused steps)
+constexpr uint32_t kRGroup = 8;     // fused steps whose dense gradient tiles share two barriers
+constexpr size_t kRDynSmem = sizeof(float) * (kRGroup + 3) * kGB;
 
 struct ReplayStep {                 // per fused step, in shared memory
     const int8_t* q;
@@ -551,7 +559,9 @@ struct ReplayStep {                 // per fused step, in shared memory
 };
 
 __global__ void __launch_bounds__(kRThreads) adam_replay_kernel(const __grid_constant__ ReplayParams P) {
-    __shared__ float s_g[kGB];
+    extern __shared__ float s_gd[];  // [kRGroup][kGB] dense gradient tiles | [3][kGB] next tile's state
+    float* s_next = s_gd + kRGroup * kGB;
+    __shared__ uint64_t s_bar;
     __shared__ uint16_t s_pos[kRStage];
     __shared__ float s_val[kRStage];
     __shared__ ReplayStep s_step[TC_MAX_FOLD];
@@ -564,17 +574,46 @@ __global__ void __launch_bounds__(kRThreads) adam_replay_kernel(const __grid_con
         const Payload& R = P.pay[tid];
         s_step[tid] = {R.q, R.val, R.idx, R.tstart, R.chunk, R.scale, R.variant};
     }
+    if (tid == 0) mbar_init(&s_bar, 1);
     __syncthreads();
     bool bad = false;
+    uint32_t phase = 0;
+    // a full tile's (master, m, v) comes in by TMA while the previous tile is folded (one CTA
+    // per SM: without this the SM would alternate between loading and computing)
+    auto prefetch = [&](uint64_t tt) {
+        if (tid == 0) {
+            mbar_arrive_expect_tx(&s_bar, 3 * kGB * 4);
+            bulk_g2s(s_next, P.master + tt * kGB, kGB * 4, &s_bar);
+            bulk_g2s(s_next + kGB, P.m + tt * kGB, kGB * 4, &s_bar);
+            bulk_g2s(s_next + 2 * kGB, P.v + tt * kGB, kGB * 4, &s_bar);
+        }
+    };
+    const uint64_t full_tiles = P.n / kGB;
+    bool pending = blockIdx.x < full_tiles;
+    if (pending) prefetch(blockIdx.x);
     for (uint64_t t = blockIdx.x; t < P.tiles; t += gridDim.x) {
         const uint64_t base = t * kGB;
         float w[kRPer], mm[kRPer], vv[kRPer];
+        if (t < full_tiles) {
+            mbar_wait_parity(&s_bar, phase);
+            phase ^= 1u;
 #pragma unroll
-        for (uint32_t j = 0; j < kRPer; ++j) {
-            const uint64_t i = base + j * kRThreads + tid;
-            w[j] = i < P.n ? P.master[i] : 0.0f;
-            mm[j] = i < P.n ? P.m[i] : 0.0f;
-            vv[j] = i < P.n ? P.v[i] : 0.0f;
+            for (uint32_t j = 0; j < kRPer; ++j) {
+                w[j] = s_next[j * kRThreads + tid];
+                mm[j] = s_next[kGB + j * kRThreads + tid];
+                vv[j] = s_next[2 * kGB + j * kRThreads + tid];
+            }
+            __syncthreads();  // every thread has its state: the buffer is free
+            pending = t + gridDim.x < full_tiles;
+            if (pending) prefetch(t + gridDim.x);
+        } else {
+#pragma unroll
+            for (uint32_t j = 0; j < kRPer; ++j) {
+                const uint64_t i = base + j * kRThreads + tid;
+                w[j] = i < P.n ? P.master[i] : 0.0f;
+                mm[j] = i < P.n ? P.m[i] : 0.0f;
+                vv[j] = i < P.n ? P.v[i] : 0.0f;
+            }
         }
         // every sparse step's entries of this tile, staged at once: one round trip per tile
         if (tid < P.nsteps) {
@@ -620,23 +659,47 @@ __global__ void __launch_bounds__(kRThreads) adam_replay_kernel(const __grid_con
                 if (e > s_run[s] && s_pos[e - 1] >= s_pos[e]) bad = true;
             }
         }
-        for (int s = 0; s < P.nsteps; ++s) {
-            const ReplayStep& R = s_step[s];
-            if (R.variant == 1) {
+        for (int g0 = 0; g0 < P.nsteps; g0 += static_cast<int>(kRGroup)) {
+            const int g1 = g0 + static_cast<int>(kRGroup) < P.nsteps ? g0 + static_cast<int>(kRGroup) : P.nsteps;
+            if (fits) {
+                // the group's sparse gradients as dense tiles: two barriers for up to kRGroup steps
+                for (int s = g0; s < g1; ++s)
+                    if (s_step[s].variant == 2) {
 #pragma unroll
-                for (uint32_t j = 0; j < kRPer; ++j) {
-                    const uint64_t i = base + j * kRThreads + tid;
-                    const float g = i < P.n ? __fmul_rn(R.scale, static_cast<float>(R.q[i])) : 0.0f;
-                    adam_update(w[j], mm[j], vv[j], g, P.a, P.c1[s], P.c2[s]);
+                        for (uint32_t j = 0; j < kRPer; ++j) s_gd[(s - g0) * kGB + j * kRThreads + tid] = 0.0f;
+                    }
+                __syncthreads();
+                for (int s = g0; s < g1; ++s)
+                    for (uint32_t e = s_run[s] + tid; e < s_run[s + 1]; e += kRThreads)
+                        s_gd[(s - g0) * kGB + s_pos[e]] = s_val[e];
+                __syncthreads();
+                for (int s = g0; s < g1; ++s) {
+                    const ReplayStep& R = s_step[s];
+#pragma unroll
+                    for (uint32_t j = 0; j < kRPer; ++j) {
+                        const uint64_t i = base + j * kRThreads + tid;
+                        const float g = R.variant == 1 ? (i < P.n ? __fmul_rn(R.scale, static_cast<float>(R.q[i])) : 0.0f)
+                                                       : s_gd[(s - g0) * kGB + j * kRThreads + tid];
+                        adam_update(w[j], mm[j], vv[j], g, P.a, P.c1[s], P.c2[s]);
+                    }
                 }
+                __syncthreads();  // before the next group's tiles
                 continue;
             }
+            for (int s = g0; s < g1; ++s) {  // more entries than the stage: a step at a time
+                const ReplayStep& R = s_step[s];
+                if (R.variant == 1) {
 #pragma unroll
-            for (uint32_t j = 0; j < kRPer; ++j) s_g[j * kRThreads + tid] = 0.0f;
-            __syncthreads();
-            if (fits) {
-                for (uint32_t e = s_run[s] + tid; e < s_run[s + 1]; e += kRThreads) s_g[s_pos[e]] = s_val[e];
-            } else {  // more entries than the stage: straight from the payload
+                    for (uint32_t j = 0; j < kRPer; ++j) {
+                        const uint64_t i = base + j * kRThreads + tid;
+                        const float g = i < P.n ? __fmul_rn(R.scale, static_cast<float>(R.q[i])) : 0.0f;
+                        adam_update(w[j], mm[j], vv[j], g, P.a, P.c1[s], P.c2[s]);
+                    }
+                    continue;
+                }
+#pragma unroll
+                for (uint32_t j = 0; j < kRPer; ++j) s_gd[j * kRThreads + tid] = 0.0f;
+                __syncthreads();
                 const Payload& RP = P.pay[s];
                 const uint64_t k0 = RP.tstart[t], k1 = RP.tstart[t + 1];
                 for (uint64_t k = k0 + tid; k < k1; k += kRThreads) {
@@ -646,14 +709,14 @@ __global__ void __launch_bounds__(kRThreads) adam_replay_kernel(const __grid_con
                         bad = true;
                         continue;
                     }
-                    s_g[pos - base] = val;
+                    s_gd[pos - base] = val;
                 }
-            }
-            __syncthreads();
+                __syncthreads();
 #pragma unroll
-            for (uint32_t j = 0; j < kRPer; ++j)
-                adam_update(w[j], mm[j], vv[j], s_g[j * kRThreads + tid], P.a, P.c1[s], P.c2[s]);
-            __syncthreads();
+                for (uint32_t j = 0; j < kRPer; ++j)
+                    adam_update(w[j], mm[j], vv[j], s_gd[j * kRThreads + tid], P.a, P.c1[s], P.c2[s]);
+                __syncthreads();
+            }
         }
 #pragma unroll
         for (uint32_t j = 0; j < kRPer; ++j) {
@@ -666,6 +729,7 @@ __global__ void __launch_bounds__(kRThreads) adam_replay_kernel(const __grid_con
         }
         __syncthreads();  // the stage and the run table are reused by the next tile
     }
+    if (pending) mbar_wait_parity(&s_bar, phase);  // (not reached: the loop consumes every prefetch)
     if (bad) tc_set_err(P.err, TC_ERR_CORRUPT);
 }
 
@@ -868,7 +932,13 @@ tc_status tc_adam_replay(tc_ctx* ctx, const tc_adam_state* stt, const void* cons
         for (int j = 0; j < nf; ++j) bias(hp, first_step + j, &R.c1[j], &R.c2[j]);
         R.pay = P;
         R.err = tc::ctx_err(ctx);
-        adam_replay_kernel<<<grid_for(ctx, R.tiles * kRThreads, kRThreads), kRThreads, 0, s>>>(R);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(adam_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kRDynSmem));
+            attr = true;
+        }
+        adam_replay_kernel<<<grid_for(ctx, R.tiles * kRThreads, kRThreads), kRThreads, kRDynSmem, s>>>(R);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "adam replay launch");
         tc::ctx_add_launches(ctx, 1);
