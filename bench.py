@@ -452,6 +452,9 @@ def run_ours(args):
     if not args.no_e2e:
         e2e = run_e2e(args, tc, ctx, dev, sizes, wb, X, Y, A, R, recs, obytes, host_ring, rec_cap, T, C,
                       state, world, s_comp, s_copy)
+    lossy = None
+    if args.lossy and world == 1:
+        lossy = lossy_probe(tc, ctx, X, Y, A, R, recs[0], s_comp, dev, peak)
     traffic = load_traffic(workload, args.f)
 
     if rank == 0:
@@ -518,6 +521,7 @@ def run_ours(args):
                     "note": "inside the pipelined step: shares HBM with encode/fold, PCIe with the "
                             "Tier-1 D2H, and waits for the slower neighbour's encode"},
                 "replicate": rep_probe,
+                "lossy_differential": lossy,
                 "restore_chain": restore,
                 "record_bytes": rec_bytes,
                 "changed_words": changed,
@@ -999,6 +1003,107 @@ def replicate_probe(tc, comm, rec, obytes, recv, rec_bytes, dev, s_comm, push=No
     return out
 
 
+def lossy_probe(tc, ctx, X, Y, A, R, rec, s, dev, peak, N=5, k=0.01, reps=3):
+    """NEXT row 3: the paper's lossy differential on this rank's shard size — compress
+    one fp32 gradient of the shard (sparse form), decompress it, and replay N payloads through Adam
+    fused vs sequentially.  Runs after the step measurements in the step's own buffers (viewed as
+    fp32 gradient / master / m / v / scratch; the bf16 weight segment as the 16-bit copy)."""
+    import torch
+
+    n = X[1].numel()
+    g = Y[1].view(torch.float32)
+    master, m, v, w16 = X[1].view(torch.float32), X[2].view(torch.float32), X[3].view(torch.float32), X[0]
+    if w16.numel() != n or any(t.numel() != n for t in (Y[1], X[2], X[3], A[0], A[1], A[2], A[3], R[1])):
+        return {"skipped": "needs four equal-length segments"}
+    dense = R[1].view(torch.float32)
+    slot = (rec.numel() // N) & ~15
+    cap = tc.grad_bound(n, k=k)
+    if slot < min(cap, int(6.5 * k * 3 * n)):
+        return {"skipped": "record buffer too small for the payloads"}
+    pays = [rec[j * slot:(j + 1) * slot] for j in range(N)]
+    ob = torch.zeros(N, dtype=torch.int64, device=dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def timed(fn):
+        out = []
+        for _ in range(reps):
+            a, b = ev(), ev()
+            a.record(s)
+            fn()
+            b.record(s)
+            s.synchronize()
+            out.append(a.elapsed_time(b))
+        return statistics.median(out)
+
+    with torch.cuda.stream(s):
+        for j in range(N):
+            torch.randn(n, out=g, generator=torch.Generator(device=dev).manual_seed(j))
+            g.mul_(1e-2)
+            tc.grad_compress(ctx, g, j, pays[j], ob[j:j + 1], stream=s, k=k)
+        torch.randn(n, out=master, generator=torch.Generator(device=dev).manual_seed(99))
+        m.zero_()
+        v.zero_()
+        w16.zero_()
+        snap = [A[1].view(torch.float32), A[2].view(torch.float32), A[3].view(torch.float32), A[0]]
+        for dst, src in zip(snap, (master, m, v, w16)):
+            dst.copy_(src)
+    s.synchronize()
+    ctx.check(s)
+    nb = [int(x) for x in ob.tolist()]
+    tmp_ob = torch.zeros(1, dtype=torch.int64, device=dev)
+    ms_c = timed(lambda: tc.grad_compress(ctx, g, N - 1, pays[N - 1], tmp_ob, stream=s, k=k))
+    ms_d = timed(lambda: tc.grad_decompress(ctx, pays[0], nb[0], dense, stream=s))
+
+    def reset():
+        with torch.cuda.stream(s):
+            for dst, src in zip((master, m, v, w16), snap):
+                dst.copy_(src)
+
+    f_ms, s_ms = [], []
+    same = True
+    for _ in range(reps):
+        reset()
+        a, b = ev(), ev()
+        a.record(s)
+        tc.adam_replay(ctx, master, m, v, w16, pays, nb, 1, dense, stream=s)
+        b.record(s)
+        s.synchronize()
+        f_ms.append(a.elapsed_time(b))
+        fused = [Y[1].view(torch.float32), Y[2].view(torch.float32), Y[3].view(torch.float32)]
+        with torch.cuda.stream(s):  # the gradient buffer is free by now: keep the fused result there
+            for dst, src in zip(fused, (master, m, v)):
+                dst.copy_(src)
+        reset()
+        a, b = ev(), ev()
+        a.record(s)
+        for j in range(N):
+            tc.grad_decompress(ctx, pays[j], nb[j], dense, stream=s)
+            tc.adam_step(ctx, master, m, v, w16, dense, 1 + j, stream=s)
+        b.record(s)
+        s.synchronize()
+        s_ms.append(a.elapsed_time(b))
+        with torch.cuda.stream(s):
+            for x, y in zip((master, m, v), fused):
+                for o in range(0, n, 1 << 27):  # slices: no full-size temporaries
+                    same = same and torch.equal(x[o:o + (1 << 27)], y[o:o + (1 << 27)])
+    ctx.check(s)
+    kept = (nb[-1] - 80) // 6
+    c_b, d_b = 4 * n + nb[-1] + 6 * kept, 4 * n + nb[0]
+    fm, sm = statistics.median(f_ms), statistics.median(s_ms)
+    f_b = 24 * n + sum(nb[:-1]) + (4 * n + nb[-1]) + (4 * n + 24 * n + 2 * n)
+    return {"n": n, "N": N, "k": k, "payload_bytes": nb[0], "kept": kept,
+            "compress": {"ms": round(ms_c, 3), "gbs": round(c_b / ms_c / 1e6, 1),
+                         "frac_hbm": round(c_b / ms_c / 1e6 / peak, 4)},
+            "decompress": {"ms": round(ms_d, 3), "gbs": round(d_b / ms_d / 1e6, 1),
+                           "frac_hbm": round(d_b / ms_d / 1e6 / peak, 4)},
+            "replay_fused_ms": round(fm, 3), "replay_fused_gbs": round(f_b / fm / 1e6, 1),
+            "replay_sequential_ms": round(sm, 3), "speedup_fused_vs_sequential": round(sm / fm, 3),
+            "fused_equals_sequential": bool(same),
+            "note": "NEXT row 3 (DESIGN.md §12): sampled-threshold top-k (k = 0.01) FP16+INT32 payloads of an fp32 "
+                    "gradient the size of one shard segment; fused = N-1 Adam steps in one pass + the native step; "
+                    "paper context: 16.6 s fused vs 26.0 s sequential (A800, 20B, 100 steps, P:586)"}
+
+
 def run_e2e(args, tc, ctx, dev, sizes, wb, X, Y, A, R, recs, obytes, host_ring, rec_cap, T, C, state, world,
             s_comp, s_copy):
     """e2e through the C ABI with host buffers: per step H2D of the new state version from pinned
@@ -1170,6 +1275,8 @@ def main():
                     help="record format: mask, index (u16 positions), or adaptive per step from density")
     ap.add_argument("--restore-chain", type=int, default=8, help="records in the chained-restore probe (0: off)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--lossy", type=int, default=1,
+                    help="N=1: also measure the paper's lossy differential (NEXT row 3) in the step's buffers")
     ap.add_argument("--push-ctas", type=int, default=16,
                     help="CTAs of the Tier-2 NVLink push inside the step (fewer = less interference)")
     ap.add_argument("--tier2", default="push", choices=["push", "nccl"],
