@@ -449,27 +449,46 @@ __global__ void grad_decompress_kernel(const Payload* RP, uint64_t n, float* out
     const Payload R = *RP;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     const uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (R.variant == 1) {
+    if (R.variant == 1)
         for (uint64_t i = t; i < n; i += stride) out[i] = __fmul_rn(R.scale, static_cast<float>(R.q[i]));
-    } else if (R.variant == 2) {
-        for (uint64_t i = t; i < n; i += stride) out[i] = 0.0f;
-    }
 }
 
-__global__ void grad_scatter_kernel(const Payload* RP, uint64_t n, float* out, unsigned* err) {
+// sparse payload -> dense, one pass: a CTA per kGB tile expands the tile's entries (from the
+// tile-start table) in shared memory and writes the whole tile with 16-byte stores
+__global__ void __launch_bounds__(kGThreads) grad_expand_kernel(const Payload* RP, uint64_t n, uint64_t tiles,
+                                                                float* out, unsigned* err) {
+    __shared__ __align__(16) float s_t[kGB];
     if (*reinterpret_cast<volatile unsigned*>(err) != 0) return;
     const Payload R = *RP;
     if (R.variant != 2) return;
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < R.kept; k += stride) {
-        uint64_t pos;
-        float v;
-        if (!entry(R, n, k, &pos, &v)) {
-            tc_set_err(err, TC_ERR_CORRUPT);
-            return;
+    const int tid = threadIdx.x;
+    bool bad = false;
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const uint64_t base = t * kGB;
+        for (uint32_t i = tid; i < kGB; i += kGThreads) s_t[i] = 0.0f;
+        __syncthreads();
+        const uint64_t k0 = R.tstart[t], k1 = R.tstart[t + 1];
+        const uint64_t cbase = base / R.chunk * R.chunk;  // the tile lies in one chunk
+        for (uint64_t k = k0 + tid; k < k1; k += kGThreads) {
+            const int32_t i = R.idx[k];
+            const uint64_t pos = cbase + static_cast<uint64_t>(static_cast<uint32_t>(i));
+            if (i < 0 || pos < base || pos >= base + kGB || pos >= n || (k > k0 && R.idx[k - 1] >= i)) {
+                bad = true;
+                continue;
+            }
+            s_t[pos - base] = __half2float(__ushort_as_half(R.val[k]));
         }
-        out[pos] = v;
+        __syncthreads();
+        const uint32_t nw = n - base < kGB ? static_cast<uint32_t>(n - base) : kGB;
+        for (uint32_t q = tid; q * 4 < nw; q += kGThreads) {
+            if (q * 4 + 4 <= nw && (reinterpret_cast<uintptr_t>(out + base) & 15u) == 0)
+                *reinterpret_cast<float4*>(out + base + q * 4) = reinterpret_cast<const float4*>(s_t)[q];
+            else
+                for (uint32_t i = q * 4; i < nw && i < q * 4 + 4; ++i) out[base + i] = s_t[i];
+        }
+        __syncthreads();
     }
+    if (bad) tc_set_err(err, TC_ERR_CORRUPT);
 }
 
 // first entry of every kGB tile (replay): lower bound of the tile start among the sorted positions
@@ -874,11 +893,15 @@ tc_status tc_grad_decompress(tc_ctx* ctx, const void* payload, uint64_t bytes, f
         return fail(TC_ERR_INVALID, "bad arguments (ctx, 16-byte aligned payload / out)");
     cudaSetDevice(tc::ctx_device(ctx));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // the variant is only known on the device: both the dequantize pass (INT8) and the tile
+    // expansion (sparse) are launched; each returns at once for the other variant
     Payload* P = nullptr;
-    tc_status st = walk_payloads(ctx, &payload, &bytes, 1, n, false, s, &P);
+    tc_status st = walk_payloads(ctx, &payload, &bytes, 1, n, n >= 1, s, &P);
     if (st != TC_OK) return st;
+    const uint64_t tiles = (n + kGB - 1) / kGB;
     grad_decompress_kernel<<<grid_for(ctx, n, 256), 256, 0, s>>>(P, n, out, tc::ctx_err(ctx));
-    grad_scatter_kernel<<<grid_for(ctx, n / 64 + 1, 256), 256, 0, s>>>(P, n, out, tc::ctx_err(ctx));
+    grad_expand_kernel<<<grid_for(ctx, tiles * kGThreads, kGThreads), kGThreads, 0, s>>>(P, n, tiles, out,
+                                                                                        tc::ctx_err(ctx));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "grad decompress launch");
     tc::ctx_add_launches(ctx, 2);
