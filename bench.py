@@ -910,7 +910,10 @@ def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nre
     W = sum(n_ * w_ for n_, w_ in zip(sizes, wb))
     # the streaming fold (chunks whose records change > 3 % of the words) reads the
     # whole state and the records and writes back every touched 32-word line
-    dense = sum(counts) * 1000 > sum(sizes) * 30
+    # the default strategy of tc_diff_apply (include/tc.h): index-mode chains at T = 4096 stream
+    # when long (N >= 4, >= 0.5 % in total) or dense (> 6 %)
+    tot, words = sum(counts), sum(sizes)
+    dense = index_mode and T == 4096 and ((nrec >= 4 and tot * 1000 >= words * 5) or tot * 1000 > words * 60)
     stream_b = W + line_bytes + sum(lens)
     return {"records": nrec, "record_format": "index" if index_mode else "mask",
             "strategy": "stream" if dense else "scatter",

@@ -123,10 +123,12 @@ tc_status tc_ctx_destroy(tc_ctx* ctx);
 tc_status tc_ctx_check(tc_ctx* ctx, tc_stream stream);
 /* Number of kernel launches libtc has enqueued through this ctx since creation. */
 uint64_t tc_ctx_launches(const tc_ctx* ctx);
-/* Restore strategy threshold: tc_diff_apply folds a chunk by streaming it
- * through shared memory (full-line writes) when the N records together change more than
- * permille/1000 of its words, and by scattering the winning words otherwise.  Both produce
- * identical state.  Default 30 (3 %); 0 = always stream; UINT32_MAX = always scatter.
+/* Restore strategy.  tc_diff_apply folds a chunk either by scattering the
+ * winning words in place or by streaming the chunk's tiles through shared memory (whole-line
+ * writes).  Chains of index-mode records at T = 4096 are streamed when they are long (>= 4
+ * records changing >= 0.5 % of the words in total) or dense (> permille/1000 of the words in
+ * total); all other chunks are scattered.  Default 60 (6 %).  0 = stream every chunk (mask-mode
+ * chunks too); UINT32_MAX = scatter every chunk.  Every strategy produces the same state.
  * Takes effect for later tc_diff_apply calls.  Errors: TC_ERR_INVALID (NULL ctx). */
 tc_status tc_ctx_set_fold_dense_permille(tc_ctx* ctx, uint32_t permille);
 /* CTAs of tc_push_peer's NVLink copy on this ctx (0 = default 32).  More CTAs = more stores in

@@ -155,11 +155,20 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
                 // streaming the whole chunk through shared memory beats scattered writes
                 uint64_t sum = 0;
                 for (int k = 0; k < P.nrec; ++k) sum += P.desc[static_cast<size_t>(k) * P.cap + r].count;
-                a.dense = sum * 1000ull > static_cast<uint64_t>(a.m) * P.dense_permille ? 1u : 0u;
-                if (a.dense && a.T == kListT) {  // all index mode at T = 4096: the list kernel
-                    bool all_idx = true;
-                    for (int k = 0; k < P.nrec; ++k) all_idx = all_idx && P.desc[static_cast<size_t>(k) * P.cap + r].idx;
-                    if (all_idx) a.dense = 2u;
+                // strategy (measured): chains of index-mode records at T = 4096 are
+                // streamed by the list kernel when they are long (N >= 4, >= 0.5 % of the words in
+                // total) or dense (> dense_permille); everything else is scattered.  0 = stream
+                // every chunk (mask-mode chunks through fold_dense_kernel), UINT32_MAX = scatter all.
+                bool all_idx = a.T == kListT;
+                for (int k = 0; k < P.nrec && all_idx; ++k) all_idx = P.desc[static_cast<size_t>(k) * P.cap + r].idx != nullptr;
+                const uint64_t mm = a.m;
+                if (P.dense_permille == 0u) {
+                    a.dense = all_idx ? 2u : 1u;
+                } else if (P.dense_permille == 0xffffffffu || !all_idx) {
+                    a.dense = 0u;
+                } else {
+                    const bool stream = (P.nrec >= 4 && sum * 1000ull >= mm * 5ull) || sum * 1000ull > mm * P.dense_permille;
+                    a.dense = stream ? 2u : 0u;
                 }
                 ndense += a.dense == 1u;
                 nlist += a.dense == 2u;

@@ -27,7 +27,7 @@ struct tc_ctx {
     size_t fold_bytes = 0;
     unsigned int* err = nullptr;  // [0] sticky device error word, [1] tc_push_peer block counter
     uint64_t launches = 0;
-    uint32_t fold_dense_permille = 30;  // tc_ctx_set_fold_dense_permille
+    uint32_t fold_dense_permille = 60;  // tc_ctx_set_fold_dense_permille
     uint32_t push_ctas = 0;              // tc_ctx_set_push_ctas (0: default)
     void* grad = nullptr;                // gradient codec / replay scratch (tc_grad.cu)
     size_t grad_bytes = 0;
