@@ -69,6 +69,19 @@ tc_status tc_adam_replay(tc_ctx* ctx, const tc_adam_state* st, const void* const
                          const uint64_t* payload_bytes, int n_payloads, const tc_adam_hp* hp,
                          uint64_t first_step, float* scratch, tc_stream stream);
 
+/* The native Adam step fused with the lossless differential of its own update (SURVEY.md §8(f)
+ * NEXT row 2: "Adam already holds the old w/m/v and the new values in registers").  One pass
+ * reads grad and the state, writes the updated state (only the words that changed) and one
+ * change mask per state segment; the records are then built from those masks and the new state
+ * (no reference copy, no re-read of ref and cur).  The diff has four segments, in this order:
+ * 0 = w16 (2-byte words), 1 = master, 2 = m, 3 = v (4-byte words); version = step, ref_version
+ * = step - 1; opts as for tc_diff_encode (advance_ref is ignored: the state itself advances).
+ * Bytes equal tc_diff_encode(ref = state before, cur = state after).  out_cap as for
+ * tc_diff_encode (device-checked, sticky TC_ERR_CAPACITY). */
+tc_status tc_adam_step_encode(tc_ctx* ctx, const tc_adam_state* st, const float* grad, const tc_adam_hp* hp,
+                              uint64_t step, const tc_encode_opts* opts, void* out, uint64_t out_cap,
+                              uint64_t* out_bytes, tc_stream stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -119,7 +119,15 @@ struct SmemA {
 };
 
 // ------------------------------------------------------------------ kernel A ------------
-template <int W>
+__device__ __forceinline__ uint32_t ldg_cur(const uint32_t* p) { return __ldg(p); }
+__device__ __forceinline__ uint16_t ldg_cur(const uint16_t* p) {
+    return static_cast<uint16_t>(__ldg(reinterpret_cast<const unsigned short*>(p)));
+}
+
+// MASK_IN: the change mask comes precomputed (EncSeg::mask_in, e.g. from the fused Adam step,
+// tc_adam_step_encode) and `cur` is the only state: no ref, no compare, no ref advance; changed
+// words are gathered from global cur.  Everything from the counts on is the same code.
+template <int W, bool MASK_IN>
 __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_t* tile, int tid) {
     using word_t = typename Word<W>::T;
     constexpr uint32_t B = Word<W>::kBlock;
@@ -132,6 +140,14 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
     word_t* gref = reinterpret_cast<word_t*>(S.ref) + I.chunk_off + I.p0;
     const word_t* gcur = reinterpret_cast<const word_t*>(S.cur) + I.chunk_off + I.p0;
 
+    const bool adv = P.advance_ref != 0;
+    const uint32_t mw0 = wid * MPW;
+    uint32_t mine = 0;  // lane q keeps mask word mw0 + q
+    if constexpr (MASK_IN) {
+        const uint32_t q = mw0 + lane;
+        if (lane < static_cast<int>(MPW) && q * 32 < I.nb)
+            mine = __ldg(S.mask_in + ((I.chunk_off + I.p0) >> 5) + q);
+    } else {
     // words past the bulk copy: the < 16-byte tail, and equal padding up to B so that pass 1
     // needs no bounds test
     if (I.nb < B) {
@@ -148,8 +164,6 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
     // ---- pass 1: 128-bit shared loads, per-lane change bits -> mask words; fused ref advance.
     //      Lane l of iteration q compares words [VW*(32q'+l), +VW) (VW = 16 / W): its VW change
     //      bits are OR-shuffled across the VW/... lanes of one 32-word mask word (LSB-first). ----
-    const bool adv = P.advance_ref != 0;
-    const uint32_t mw0 = wid * MPW;
     {
         constexpr uint32_t VW = 16 / W;          // words per 128-bit vector (4 | 8)
         constexpr uint32_t LPM = 32 / VW;        // lanes per mask word (8 | 4)
@@ -180,9 +194,9 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
         }
         __syncwarp();
     }
-    uint32_t mine = 0;  // lane q keeps mask word mw0 + q
     if (lane < static_cast<int>(MPW))
         mine = reinterpret_cast<const uint32_t*>(tile)[(2 * B * W) / 4 + mw0 + lane];
+    }
     // ---- counts: lane-per-mask-word popcount scan over the warp's range (the barrier below
     //      also publishes thread 0's prefetched record start) ----
     const uint32_t c = __popc(mine);
@@ -220,7 +234,7 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
             while (wv) {
                 const uint32_t b = __ffs(wv) - 1;
                 wv &= wv - 1;
-                slot[k] = scur[q0 + b];
+                slot[k] = MASK_IN ? ldg_cur(gcur + q0 + b) : scur[q0 + b];
                 if (imode) islot[k] = static_cast<uint16_t>((I.p0 + q0 + b) & tmask);
                 ++k;
             }
@@ -234,7 +248,7 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
                 const uint32_t o = __shfl_sync(0xffffffffu, pre, src);
                 if ((bb >> lane) & 1u) {
                     const uint32_t q = (mw0 + src) * 32 + lane;
-                    slot[o + __popc(bb & lt)] = scur[q];
+                    slot[o + __popc(bb & lt)] = MASK_IN ? ldg_cur(gcur + q) : scur[q];
                     if (imode) islot[o + __popc(bb & lt)] = static_cast<uint16_t>((I.p0 + q) & tmask);
                 }
             }
@@ -322,6 +336,7 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
     }
 }
 
+template <bool MASK_IN>
 __global__ void __launch_bounds__(kEncThreads, 6) encode_mask_kernel(const __grid_constant__ EncParams P) {
     extern __shared__ __align__(128) uint8_t tile[];
     __shared__ SmemA sm;
@@ -332,7 +347,7 @@ __global__ void __launch_bounds__(kEncThreads, 6) encode_mask_kernel(const __gri
         sm.I = I;
         mbar_init(&sm.bar, 1);
         sm.rs = I.chunk == 0 ? 1ull : 0ull;  // chunk 0 starts at 0; others: prefetched below
-        const uint32_t bulk = (I.nb * I.w) & ~15u;
+        const uint32_t bulk = MASK_IN ? 0u : (I.nb * I.w) & ~15u;
         if (bulk) {
             const EncSeg& S = P.seg[I.seg];
             const uint8_t* gref = S.ref + (I.chunk_off + I.p0) * I.w;
@@ -347,9 +362,9 @@ __global__ void __launch_bounds__(kEncThreads, 6) encode_mask_kernel(const __gri
     __syncthreads();
     if (tid == 0 && sm.I.chunk != 0) sm.rs = ld_relaxed(&P.rstart[sm.I.chunk]);  // value | 1 once published
     if (sm.I.w == 4)
-        mask_block<4>(P, sm, tile, tid);
+        mask_block<4, MASK_IN>(P, sm, tile, tid);
     else
-        mask_block<2>(P, sm, tile, tid);
+        mask_block<2, MASK_IN>(P, sm, tile, tid);
 }
 
 // ------------------------------------------------------------------ kernel P ------------
@@ -616,11 +631,15 @@ constexpr size_t kEncDynSmem = 2 * 16384 + 1024;  // ref | cur | mask words
 cudaError_t launch_encode(const EncParams& p, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(encode_mask_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(encode_mask_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(encode_mask_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr_set = true;
     }
     if (p.total_blocks == 0) return cudaSuccess;
-    encode_mask_kernel<<<static_cast<unsigned>(p.total_blocks), kEncThreads, kEncDynSmem, s>>>(p);
+    if (p.seg[0].mask_in)
+        encode_mask_kernel<true><<<static_cast<unsigned>(p.total_blocks), kEncThreads, kEncDynSmem, s>>>(p);
+    else
+        encode_mask_kernel<false><<<static_cast<unsigned>(p.total_blocks), kEncThreads, kEncDynSmem, s>>>(p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     encode_prefix_kernel<<<1, 1024, 0, s>>>(p);

@@ -546,6 +546,46 @@ __global__ void adam_step_kernel(float* __restrict__ master, float* __restrict__
     }
 }
 
+// NEXT row 2: the Adam step and the change masks of the lossless diff of its own update.  A warp
+// takes 32 consecutive elements per iteration; the four segments' change bits are ballots (one
+// mask word each); a word is stored only where it changed.
+__global__ void adam_mask_kernel(float* __restrict__ master, float* __restrict__ m, float* __restrict__ v,
+                                 uint16_t* __restrict__ w16, uint64_t n, const float* __restrict__ g, AdamC a,
+                                 float c1, float c2, uint32_t* __restrict__ mk_w, uint32_t* __restrict__ mk_master,
+                                 uint32_t* __restrict__ mk_m, uint32_t* __restrict__ mk_v) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t words = (n + 31) / 32;
+    const uint64_t wstride = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
+    for (uint64_t wd = static_cast<uint64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5); wd < words;
+         wd += wstride) {
+        const uint64_t i = wd * 32 + lane;
+        bool cw = false, cmaster = false, cm = false, cv = false;
+        if (i < n) {
+            const float w0 = master[i], m0 = m[i], v0 = v[i];
+            const uint16_t h0 = w16[i];
+            float w = w0, mm = m0, vv = v0;
+            adam_update(w, mm, vv, g[i], a, c1, c2);
+            const uint16_t h = __bfloat16_as_ushort(__float2bfloat16_rn(w));
+            cmaster = __float_as_uint(w) != __float_as_uint(w0);
+            cm = __float_as_uint(mm) != __float_as_uint(m0);
+            cv = __float_as_uint(vv) != __float_as_uint(v0);
+            cw = h != h0;
+            if (cmaster) master[i] = w;
+            if (cm) m[i] = mm;
+            if (cv) v[i] = vv;
+            if (cw) w16[i] = h;
+        }
+        const uint32_t bw = __ballot_sync(0xffffffffu, cw), bmaster = __ballot_sync(0xffffffffu, cmaster);
+        const uint32_t bm = __ballot_sync(0xffffffffu, cm), bv = __ballot_sync(0xffffffffu, cv);
+        if (lane == 0) {
+            mk_w[wd] = bw;
+            mk_master[wd] = bmaster;
+            mk_m[wd] = bm;
+            mk_v[wd] = bv;
+        }
+    }
+}
+
 struct ReplayParams {
     float* master;
     float* m;
@@ -970,6 +1010,39 @@ tc_status tc_adam_replay(tc_ctx* ctx, const tc_adam_state* stt, const void* cons
     st = tc_grad_decompress(ctx, payloads[nf], payload_bytes[nf], scratch, stt->n, stream);
     if (st != TC_OK) return st;
     return tc_adam_step(ctx, stt, scratch, hp, first_step + nf, stream);
+}
+
+tc_status tc_adam_step_encode(tc_ctx* ctx, const tc_adam_state* stt, const float* grad, const tc_adam_hp* hp,
+                              uint64_t step, const tc_encode_opts* opts, void* out, uint64_t out_cap,
+                              uint64_t* out_bytes, tc_stream stream) {
+    if (!ctx || step == 0) return fail(TC_ERR_INVALID, "ctx is NULL or step == 0 (steps are 1-based)");
+    tc_status st = check_state(stt);
+    if (st != TC_OK) return st;
+    if (!out || !aligned16(out) || !out_bytes) return fail(TC_ERR_INVALID, "out must be 16-byte aligned; out_bytes set");
+    if (stt->n && !grad) return fail(TC_ERR_INVALID, "grad is NULL");
+    cudaSetDevice(tc::ctx_device(ctx));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint64_t n = stt->n, words = (n + 31) / 32;
+    const size_t per = pad16u(4 * (words ? words : 1));
+    void* scratch = nullptr;
+    st = tc::ctx_grad_scratch(ctx, 4 * per, s, &scratch);
+    if (st != TC_OK) return st;
+    uint32_t* mk[4];
+    for (int k = 0; k < 4; ++k) mk[k] = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + k * per);
+    if (n) {
+        float c1, c2;
+        bias(hp, step, &c1, &c2);
+        adam_mask_kernel<<<grid_for(ctx, words * 32, 256), 256, 0, s>>>(stt->master, stt->m, stt->v, stt->w16, n, grad,
+                                                                         adam_consts(hp), c1, c2, mk[0], mk[1], mk[2],
+                                                                         mk[3]);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "adam mask launch");
+        tc::ctx_add_launches(ctx, 1);
+    }
+    tc_segment segs[4] = {{nullptr, stt->w16, n, 2, 0}, {nullptr, stt->master, n, 4, 0},
+                          {nullptr, stt->m, n, 4, 0}, {nullptr, stt->v, n, 4, 0}};
+    const uint32_t* const masks[4] = {mk[0], mk[1], mk[2], mk[3]};
+    return tc::encode_from_masks(ctx, segs, masks, 4, opts, step, step - 1, out, out_cap, out_bytes, s);
 }
 
 }  // extern "C"

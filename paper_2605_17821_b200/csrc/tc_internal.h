@@ -56,6 +56,7 @@ struct EncSeg {
     uint32_t seg_id;        // segment_id written in the headers
     uint32_t pad_;
     uint64_t word_base;     // added to chunk offsets in the headers (range encodes)
+    const uint32_t* mask_in;  // precomputed change mask of the segment (MASK_IN encode), else nullptr
 };
 
 struct EncParams {
@@ -141,6 +142,9 @@ int ctx_num_sms(tc_ctx* c);
 void ctx_add_launches(tc_ctx* c, uint64_t n);
 uint32_t ctx_push_ctas(tc_ctx* c);
 tc_status ctx_grad_scratch(tc_ctx* c, size_t bytes, cudaStream_t s, void** out);
+tc_status encode_from_masks(tc_ctx* ctx, const tc_segment* segs, const uint32_t* const* masks, int nseg,
+                            const tc_encode_opts* opts, uint64_t version, uint64_t ref_version, void* out,
+                            uint64_t out_cap, uint64_t* out_bytes, cudaStream_t s);
 
 }  // namespace tc
 

@@ -232,6 +232,7 @@ struct SegSpec {
     uint32_t w;
     uint32_t seg_id;
     uint64_t word_base;
+    const uint32_t* mask_in = nullptr;  // precomputed change mask (tc::encode_from_masks)
 };
 }  // namespace
 
@@ -252,6 +253,7 @@ static tc_status encode_impl(tc_ctx* ctx, const SegSpec* specs, int nseg, const 
         E.w = g.w;
         E.seg_id = g.seg_id;
         E.word_base = g.word_base;
+        E.mask_in = g.mask_in;
         E.block_words = g.w == 4 ? kEncBlockWords4 : kEncBlockWords2;
         E.first_block = blocks;
         E.first_chunk = chunks;
@@ -487,5 +489,29 @@ tc_status ctx_grad_scratch(tc_ctx* c, size_t bytes, cudaStream_t s, void** out) 
     tc_status st = ensure(&c->grad, &c->grad_bytes, bytes, s);
     *out = c->grad;
     return st;
+}
+}  // namespace tc
+
+namespace tc {
+// Encode `cur` against the change masks `masks[s]` (bit i of u32 word i/32 = word i of segment s
+// changed) instead of a reference: the records tc_diff_encode(ref, cur) would produce for any ref
+// with those differences (tc_adam_step_encode).  No reference is read or advanced.
+tc_status encode_from_masks(tc_ctx* ctx, const tc_segment* segs, const uint32_t* const* masks, int nseg,
+                            const tc_encode_opts* opts, uint64_t version, uint64_t ref_version, void* out,
+                            uint64_t out_cap, uint64_t* out_bytes, cudaStream_t s) {
+    tc_encode_opts o;
+    default_opts(opts, &o);
+    o.advance_ref = 0;
+    tc_status st = check_opts(o);
+    if (st != TC_OK) return st;
+    if (nseg < 1 || nseg > TC_MAX_SEGMENTS) return fail(TC_ERR_INVALID, "1 <= nseg <= TC_MAX_SEGMENTS");
+    SegSpec sp[TC_MAX_SEGMENTS];
+    for (int i = 0; i < nseg; ++i) {
+        if ((segs[i].n_words && (!segs[i].cur || !masks[i])) || (segs[i].word_bytes != 2 && segs[i].word_bytes != 4))
+            return fail(TC_ERR_INVALID, "bad segment / mask");
+        sp[i] = {nullptr, static_cast<const uint8_t*>(segs[i].cur), segs[i].n_words, segs[i].word_bytes,
+                 static_cast<uint32_t>(i), 0, masks[i]};
+    }
+    return encode_impl(ctx, sp, nseg, o, version, ref_version, out, out_cap, out_bytes, s);
 }
 }  // namespace tc

@@ -108,7 +108,10 @@ def _load():
     L.tc_adam_step.argtypes = [vp, ctypes.POINTER(AdamState), vp, ctypes.POINTER(AdamHP), u64, vp]
     L.tc_adam_replay.argtypes = [vp, ctypes.POINTER(AdamState), ctypes.POINTER(vp), ctypes.POINTER(u64), cint,
                                  ctypes.POINTER(AdamHP), u64, vp, vp]
-    for name in ("tc_grad_bound", "tc_grad_compress", "tc_grad_decompress", "tc_adam_step", "tc_adam_replay"):
+    L.tc_adam_step_encode.argtypes = [vp, ctypes.POINTER(AdamState), vp, ctypes.POINTER(AdamHP), u64,
+                                      ctypes.POINTER(EncodeOpts), vp, u64, vp, vp]
+    for name in ("tc_grad_bound", "tc_grad_compress", "tc_grad_decompress", "tc_adam_step", "tc_adam_replay",
+                 "tc_adam_step_encode"):
         getattr(L, name).restype = cint
     for name in ("tc_ipc_alloc", "tc_ipc_free", "tc_ipc_open", "tc_ipc_close", "tc_push_peer",
                  "tc_diff_encode_push", "tc_peer_wait"):
@@ -491,3 +494,14 @@ def adam_replay(ctx: Ctx, master, m, v, w16, payloads, payload_bytes, first_step
     pb = (u64 * k)(*[int(b) for b in payload_bytes])
     _check(LIB.tc_adam_replay(ctx.h, ctypes.byref(st), pp, pb, k, ctypes.byref(h), int(first_step),
                               scratch.data_ptr(), _stream(stream)), "tc_adam_replay")
+
+
+def adam_step_encode(ctx: Ctx, master, m, v, w16, grad, step: int, out: torch.Tensor, out_bytes, tile_words=4096,
+                     chunk_words=1 << 28, index_mode=False, stream=None, **hp):
+    """Enqueue tc_adam_step_encode: the Adam step + the lossless diff of its update (segments w16,
+    master, m, v) into ``out``."""
+    st, h = _adam(master, m, v, w16), _hp(**hp)
+    o = _opts(tile_words, chunk_words, False, index_mode)
+    _check(LIB.tc_adam_step_encode(ctx.h, ctypes.byref(st), grad.data_ptr(), ctypes.byref(h), int(step), ctypes.byref(o),
+                                   out.data_ptr(), out.numel() * out.element_size(), out_bytes.data_ptr(),
+                                   _stream(stream)), "tc_adam_step_encode")

@@ -16,6 +16,11 @@ RNG = np.random.default_rng(23)
 
 
 @pytest.fixture(scope="module")
+def tco_lossless():
+    return oracle
+
+
+@pytest.fixture(scope="module")
 def ctx():
     c = tc.Ctx(0)
     yield c
@@ -164,3 +169,34 @@ def test_replay_corrupt_payload(ctx):
     dp = [dev(np.concatenate([p, np.zeros(16, np.uint8)])) for p in (pays[0], bad, pays[2])]
     tc.adam_replay(ctx, *gs, dp, [pays[0].size, bad.size, pays[2].size], 1, torch.empty(n, device="cuda"))
     assert ctx.check_status() == tc.ERR_CORRUPT
+
+
+@pytest.mark.parametrize("index_mode", [False, True])
+@pytest.mark.parametrize("n,T,C,zero_frac", [(1, 4096, 1 << 28, 0.0), (1000, 4096, 1 << 28, 0.5),
+                                             (70_001, 256, 8192, 0.9), (300_000, 4096, 1 << 28, 0.99)])
+def test_adam_step_encode_matches_oracle(ctx, tco_lossless, n, T, C, zero_frac, index_mode):
+    """NEXT row 2: the fused Adam step + lossless diff == oracle adam_step, then oracle encode of
+    (state before -> state after), byte for byte; the state equals the oracle's."""
+    r = np.random.default_rng(n)
+    st = [r.standard_normal(n).astype(np.float32), np.zeros(n, np.float32), np.zeros(n, np.float32),
+          np.zeros(n, np.uint16)]
+    st[1][: n // 2] = (r.standard_normal(n // 2) * 1e-3).astype(np.float32)
+    st[2][: n // 2] = (np.abs(r.standard_normal(n // 2)) * 1e-6).astype(np.float32)
+    g = (r.standard_normal(n) * 1e-2).astype(np.float32)
+    g[r.random(n) < zero_frac] = 0.0
+    before = [a.copy() for a in st]
+    oracle.adam_step(st[0], st[1], st[2], st[3], g, 5)
+    ref = [before[3], before[0].view(np.uint32), before[1].view(np.uint32), before[2].view(np.uint32)]
+    cur = [st[3], st[0].view(np.uint32), st[1].view(np.uint32), st[2].view(np.uint32)]
+    rc, exp = tco_lossless.encode([a.copy() for a in ref], cur, tile_words=T, chunk_words=C, advance_ref=False,
+                                  version=5, ref_version=4, index_mode=index_mode)
+    assert rc == 0
+    gs = to_gpu_state(before)
+    cap = tc.diff_bound([n] * 4, [2, 4, 4, 4], T, C, index_mode)
+    out = torch.full((cap,), 0xAB, dtype=torch.uint8, device="cuda")
+    ob = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tc.adam_step_encode(ctx, *gs, dev(g), 5, out, ob, T, C, index_mode)
+    ctx.check()
+    nb = int(ob.item())
+    assert nb == exp.size and np.array_equal(out[:nb].cpu().numpy(), exp)
+    assert same_state(gs, st)
