@@ -22,7 +22,7 @@ PROF = os.path.join(ROOT, "profiles")
 
 def short(name):
     for k in ("encode_mask_kernel", "encode_prefix_kernel", "encode_emit_kernel", "fold_walk_kernel",
-              "fold_dense_kernel", "fold_kernel", "synth_base_kernel", "synth_step_kernel", "stage_sizes_kernel"):
+              "fold_dense_kernel", "fold_list_kernel", "fold_kernel", "synth_base_kernel", "synth_step_kernel", "stage_sizes_kernel"):
         if k in name:
             return k
     return name.split("(")[0][-60:]
@@ -63,7 +63,8 @@ def main():
         per = launches(a.launches)
         ours = {i: d for i, d in per.items() if d["name"].startswith(("encode", "fold"))}
         # a step whose chunks all go one way launches the other fold kernel to exit at once
-        ours = {i: d for i, d in ours.items() if d.get("ns", 0) > 20e3 or not d["name"].startswith("fold_dense")}
+        ours = {i: d for i, d in ours.items()
+                if d.get("ns", 0) > 20e3 or not d["name"].startswith(("fold_dense", "fold_list"))}
         agg = defaultdict(lambda: [0, 0.0, 0.0])
         for d in ours.values():
             g = agg[d["name"]]
@@ -82,7 +83,7 @@ def main():
         open(os.path.join(PROF, f"{a.tag}_launch_summary.md"), "w").write("\n".join(out) + "\n")
         enc = sum(agg[k][2] / max(1, agg[k][0]) for k in ("encode_mask_kernel", "encode_prefix_kernel",
                                                            "encode_emit_kernel") if k in agg)
-        fold = sum(agg[k][2] / max(1, agg[k][0]) for k in ("fold_walk_kernel", "fold_kernel", "fold_dense_kernel") if k in agg)
+        fold = sum(agg[k][2] / max(1, agg[k][0]) for k in ("fold_walk_kernel", "fold_kernel", "fold_dense_kernel", "fold_list_kernel") if k in agg)
         traffic[key] = {"encode": int(enc), "fold": int(fold), "source": f"profiles/{a.tag}_launches.csv"}
         json.dump(traffic, open(traffic_path, "w"), indent=1)
         print("\n".join(out))
