@@ -1118,8 +1118,22 @@ def run_e2e(args, tc, ctx, dev, sizes, wb, X, Y, A, R, recs, obytes, host_ring, 
     import torch.distributed as dist
 
     steps = min(args.steps, args.e2e_steps)
-    bX = [tc.HostBuffer(x.numel() * x.element_size()) for x in X]
-    bY = [tc.HostBuffer(y.numel() * y.element_size()) for y in Y]
+    # pinned host copies of both state versions; every rank must get them before any collective
+    try:
+        bX = [tc.HostBuffer(x.numel() * x.element_size()) for x in X]
+        bY = [tc.HostBuffer(y.numel() * y.element_size()) for y in Y]
+        got = 1
+    except tc.TcError:
+        bX = bY = []
+        got = 0
+    if world > 1:
+        t = torch.tensor([got], dtype=torch.int32, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        got = int(t.item())
+    if not got:
+        for b in bX + bY:
+            b.free()
+        raise RuntimeError("pinned host memory for two state versions per rank is not available")
     hX = [b.view(x.dtype) for b, x in zip(bX, X)]
     hY = [b.view(y.dtype) for b, y in zip(bY, Y)]
     for h, d in zip(hX + hY, X + Y):
