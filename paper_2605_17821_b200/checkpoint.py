@@ -9,6 +9,11 @@ libtc (tc.py); nothing here computes on the data.
                       (PAPER.md:226 version = iteration; P:207 batching N; P:306-310 watermark)
     Checkpointer      per-rank save_step (encode -> Tier-1 D2H -> Tier-2 ring) and restore
                       (fetch from Tier-1 / Tier-2, then one fold of the chain) on libtc
+    plan_chunks       paced base replication plan (§3.2)
+    BaseReplicator    a base checkpoint intercepted once in memory, staged to Tier-1, replicated
+                      to the ring neighbour in paced chunks over NVLink stores, committed
+                      all-or-nothing; sync flush on spillover
+    plan_loading      the retrieval cascade Tier-1 -> Tier-2 peer (§3.3)
 """
 from __future__ import annotations
 
@@ -206,3 +211,168 @@ class Checkpointer:
             self.t1.pop(e.version, None)
             self.t2.pop(e.version, None)
             self.dev_rec.pop(e.version, None)
+
+
+# ------------------------------------------------------- NEXT row 4: paced base replication ----
+MiB = 1 << 20
+
+
+@dataclass
+class ChunkPlan:
+    """Paced replication of one base checkpoint (SPEC.md:233 ChunkPlan; §3.2 "evenly
+    divides this volume across the available training iterations ... reserving a brief safety
+    margin ... caps the maximum chunk size")."""
+    total_bytes: int
+    interval: int        # I: iterations between bases
+    margin: int          # s: safety margin (iterations)
+    cap: int             # C: chunk cap (bytes)
+    chunk_bytes: int
+    iters: int           # iterations the transfer is scheduled over
+    spillover: bool      # more iterations than I - s: the rest is flushed synchronously
+
+
+def plan_chunks(total_bytes: int, interval: int, margin: int | None = None, cap: int = 256 * MiB) -> ChunkPlan:
+    """chunk = min(C, ceil(total / max(1, I - s))); iterations = ceil(total / chunk); spillover iff
+    iterations > I - s.  s defaults to ceil(0.1 I)."""
+    if interval < 1 or cap < 1 or total_bytes < 0:
+        raise ValueError("interval >= 1, cap >= 1, total >= 0")
+    if margin is None:
+        margin = -(-interval // 10)
+    avail = max(1, interval - margin)
+    if total_bytes == 0:
+        return ChunkPlan(0, interval, margin, cap, 0, 0, False)
+    chunk = min(cap, -(-total_bytes // avail))
+    iters = -(-total_bytes // chunk)
+    return ChunkPlan(total_bytes, interval, margin, cap, chunk, iters, iters > avail)
+
+
+class BaseReplicator:
+    """One rank's base stream.  `intercept` serializes the shard once
+    into a flat device payload (§3.2 "in-memory byte payloads", no write-then-read)
+    and stages it to Tier-1 (pinned host); `pump` (once per training iteration) pushes the next
+    paced chunk into the ring neighbour's staging buffer with NVLink stores (tc_push_peer); the
+    replica becomes visible (its commit mailbox carries the version) only when every byte has
+    arrived — all-or-nothing; `flush` sends the remainder at once (the sync flush on
+    spillover).  Collective at construction (IPC handle exchange); one per rank."""
+
+    def __init__(self, shard_bytes: int, rank: int, world: int, device: int, stream=None):
+        import torch.distributed as dist
+
+        from . import tc
+
+        self.tc = tc
+        self.n = int(shard_bytes)
+        self.rank, self.world = rank, world
+        self.dev = torch.device("cuda", device)
+        self.s = stream or torch.cuda.Stream(self.dev)
+        self.ctx = tc.Ctx(device)
+        self.ctx.set_push_ctas(16)
+        self.payload = torch.empty(max(16, (self.n + 15) // 16 * 16), dtype=torch.uint8, device=self.dev)
+        self.host = tc.HostBuffer(max(1, self.n))
+        # this GPU receives the previous rank's base here; progress mailbox per chunk, commit mailbox
+        self.stage = tc.IpcBuffer(max(16, (self.n + 15) // 16 * 16))
+        self.progress = tc.IpcBuffer(16)
+        self.commit = tc.IpcBuffer(16)
+        hs = [None] * world
+        dist.all_gather_object(hs, [self.stage.handle, self.progress.handle, self.commit.handle, self.n])
+        nx = hs[(rank + 1) % world]
+        self.peer_n = int(nx[3])
+        self.peer_stage = tc.PeerMapping(nx[0], self.peer_n)
+        self.peer_progress = tc.PeerMapping(nx[1], 16)
+        self.peer_commit = tc.PeerMapping(nx[2], 16)
+        self.len_dev = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.zero_dev = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.plan = None
+        self.sent = 0
+        self.version = 0
+        self.seq = 0
+        self.log = []   # (iteration, kind, bytes): chunk | sync_flush | commit
+
+    def intercept(self, segments, version: int, interval: int, margin: int | None = None, cap: int = 256 * MiB):
+        """Serialize the shard (device segments, in order) once, stage it to Tier-1, plan the pacing."""
+        if self.plan is not None and self.sent < self.plan.total_bytes:
+            self.flush(version)  # the previous base must be complete before it is overwritten
+        with torch.cuda.stream(self.s):
+            o = 0
+            for t in segments:
+                b = t.contiguous().view(torch.uint8).reshape(-1)
+                self.payload[o:o + b.numel()].copy_(b)
+                o += b.numel()
+        if o != self.n:
+            raise ValueError(f"shard is {o} bytes, replicator built for {self.n}")
+        self.tc.stage_host(self.host, self.payload, self.n, self.tc.D2H, stream=self.s)
+        self.plan = plan_chunks(self.n, interval, margin, cap)
+        self.sent, self.version = 0, int(version)
+        return self.plan
+
+    def _push(self, nbytes: int):
+        # 16-byte aligned cover of [sent, sent + nbytes) (payload and stage are padded to 16 bytes;
+        # an overlap re-sends bytes the peer already holds, with the same values)
+        a0 = self.sent & ~15
+        end = min((self.n + 15) // 16 * 16, (self.sent + nbytes + 15) // 16 * 16)
+        self.len_dev.fill_(end - a0)
+        self.seq += 1
+        self.tc.push_peer(self.ctx, self.payload[a0:], self.len_dev, _Offset(self.peer_stage, a0),
+                          (self.peer_n + 15) // 16 * 16 - a0, self.peer_progress, self.seq, stream=self.s)
+        self.sent += nbytes
+
+    def _commit(self, it: int):
+        self.seq += 1
+        self.tc.push_peer(self.ctx, self.payload, self.zero_dev, self.peer_stage, 0, self.peer_commit, self.version,
+                          stream=self.s)
+        self.log.append((it, "commit", 0))
+
+    def pump(self, it: int):
+        """This iteration's paced chunk (no-op once the base is out)."""
+        if self.plan is None or self.sent >= self.plan.total_bytes:
+            return
+        with torch.cuda.stream(self.s):
+            nb = min(self.plan.chunk_bytes, self.plan.total_bytes - self.sent)
+            self._push(nb)
+            self.log.append((it, "chunk", nb))
+            if self.sent >= self.plan.total_bytes:
+                self._commit(it)
+
+    def flush(self, it: int):
+        """Synchronous flush of the remaining bytes (spillover at the next base boundary)."""
+        if self.plan is None or self.sent >= self.plan.total_bytes:
+            return
+        with torch.cuda.stream(self.s):
+            rest = self.plan.total_bytes - self.sent
+            self._push(rest)
+            self.log.append((it, "sync_flush", rest))
+            self._commit(it)
+        self.s.synchronize()
+
+    def committed_version(self) -> int:
+        """Version of the previous rank's base held complete in this GPU's staging buffer (0: none)."""
+        return int(self.commit.tensor[8:16].view(torch.int64).item())
+
+    def received(self) -> torch.Tensor:
+        return self.stage.tensor[: self.peer_n]
+
+    def close(self):
+        for p_ in (self.peer_stage, self.peer_progress, self.peer_commit):
+            p_.close()
+        torch.cuda.synchronize(self.dev)
+
+
+class _Offset:
+    """A PeerMapping shifted by a byte offset (tc_push_peer writes at data_ptr())."""
+
+    def __init__(self, mapping, off: int):
+        self.p = mapping.data_ptr() + off
+
+    def data_ptr(self):
+        return self.p
+
+
+def plan_loading(have_t1: bool, have_t2: bool) -> str:
+    """The retrieval cascade ordered by cost (§3.3): Tier-1 (local
+    host) if the rank's copy survived, else the ring peer's Tier-2 replica, else Tier-3 (out of
+    scope here: reported as unavailable)."""
+    if have_t1:
+        return "t1"
+    if have_t2:
+        return "t2"
+    return "t3"

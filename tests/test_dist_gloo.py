@@ -85,3 +85,46 @@ def test_diff_chain_links_batches_reclaim():
     assert c.base_version == 55 and c.entries[0].version == 56
     with pytest.raises(ValueError):
         c.reclaim(40)
+
+
+# ------------------------------------------------------ NEXT row 4: paced base replication ----
+def test_plan_chunks_spec_examples():
+    """1 GiB, I = 50, s = 5, C = 256 MiB -> ceil(1 GiB / 45) per iteration over 45
+    iterations, no spillover; 0 bytes -> no chunks; 20 GiB, I = 10, s = 2 -> capped at 256 MiB,
+    80 iterations, spillover."""
+    from paper_2605_17821_b200.checkpoint import MiB, plan_chunks
+
+    p = plan_chunks(1 << 30, 50, 5, 256 * MiB)
+    assert p.chunk_bytes == -(-(1 << 30) // 45) and p.iters == 45 and not p.spillover
+    assert round(p.chunk_bytes / MiB) == 23
+    p = plan_chunks(0, 50, 5)
+    assert p.chunk_bytes == 0 and p.iters == 0 and not p.spillover
+    p = plan_chunks(20 << 30, 10, 2, 256 * MiB)
+    assert p.chunk_bytes == 256 * MiB and p.iters == 80 and p.spillover
+    assert plan_chunks(1 << 20, 50).margin == 5  # default s = ceil(0.1 I)
+
+
+def test_plan_chunks_invariants():
+    import random
+
+    from paper_2605_17821_b200.checkpoint import plan_chunks
+
+    rng = random.Random(3)
+    for _ in range(2000):
+        total, interval = rng.randrange(0, 1 << 40), rng.randrange(1, 500)
+        margin, cap = rng.randrange(0, interval + 3), rng.randrange(1, 1 << 30)
+        p = plan_chunks(total, interval, margin, cap)
+        if total == 0:
+            assert p.iters == 0
+            continue
+        avail = max(1, interval - margin)
+        assert p.chunk_bytes == min(cap, -(-total // avail))
+        assert p.iters == -(-total // p.chunk_bytes) and p.chunk_bytes * p.iters >= total
+        assert p.spillover == (p.iters > avail)
+
+
+def test_plan_loading_cascade():
+    from paper_2605_17821_b200.checkpoint import plan_loading
+
+    assert plan_loading(True, True) == "t1" and plan_loading(True, False) == "t1"
+    assert plan_loading(False, True) == "t2" and plan_loading(False, False) == "t3"
