@@ -8,15 +8,18 @@
 // the corresponding N-1 incremental gradients in temporal order ... and writes the final
 // results back" (§3.3).
 //
-// Kernels:
+// Kernels (every fold launches all four; each returns at once when no chunk is its kind):
 //   fold_walk_kernel  (1 CTA)  walks every record header of every diff, validates structure
 //                              (-> CORRUPT), the version chain (-> PROTOCOL) and
 //                              the common chunk layout (-> INVALID); builds the descriptor
-//                              table and the per-record unit prefix.
-//   fold_kernel       (persistent, one warp per unit of max(T, 1024) words; see the fold
-//                              section) newest-first winner masks, popcount warp scans for
-//                              the value offsets, warp-broadcast scatter of the winning
-//                              words; tile_off consistency checked on the way (-> CORRUPT).
+//                              table and the per-record unit prefix; picks each chunk's strategy.
+//   fold_kernel       (persistent, one warp per unit of max(T, 4096) words) scatter: newest-
+//                              first winner masks, popcount warp scans for the value offsets,
+//                              scatter of the winning words (a sparse single index record
+//                              straight from its entry ranges); tile_off checked on the way.
+//   fold_list_kernel  (a CTA per 4096-word tile) streaming fold of all-index T = 4096 chains:
+//                              tile in shared memory, records' runs staged, oldest -> newest.
+//   fold_dense_kernel (one warp per CTA) streaming fold of any other chain (opt-in).
 #include <cuda_runtime.h>
 
 #include "tc_internal.h"
@@ -470,10 +473,10 @@ __global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const __grid_cons
 }
 
 // ------------------------------------------------------------- dense fold ----------
-// Chunks whose N records together change more than dense_permille of the words (the walker's
-// `dense` flag) are folded by streaming: at union densities of a few percent most 32-byte
-// sectors hold a changed word, and scattered partial-sector writes cost a DRAM read-modify-
-// write each (the scatter fold of the cfg2 N = 8 chain: 16-17 ms).
+// The streaming fold's general path (walker kind 1: chunks that are not an all-index T = 4096
+// chain; selected by the dense_permille = 0 setting — by default such chunks are scattered, which
+// measured faster).  Streaming pays off when most 32-byte sectors hold a changed
+// word, where scattered partial-sector writes cost a DRAM read-modify-write each.
 // One warp per CTA; per sub-unit of kDSub words (lane l owns mask words kMW*l .. kMW*l+kMW-1):
 //   1. one TMA bulk copy brings the sub-unit's state into a shared tile (mbarrier);
 //   2. for a batch of up to kDBatch records, all in flight together: the mask words (index
@@ -642,7 +645,7 @@ __device__ __forceinline__ void expand_run(word_t* tw, const word_t* sv, const u
 
 template <int W>
 __device__ void fold_dense_unit(const FoldParams& P, uint64_t r, uint64_t ku, DenseSmem& S, int lane,
-                                uint32_t& phase, bool preloaded, bool& bad) {
+                                uint32_t& phase, bool& bad) {
     using word_t = typename Word<W>::T;
     const int N = P.nrec;
     const FoldRec& L = P.desc[r];
@@ -655,13 +658,11 @@ __device__ void fold_dense_unit(const FoldParams& P, uint64_t r, uint64_t ku, De
     uint8_t* sb = reinterpret_cast<uint8_t*>(S.stage);
     const uint32_t lt = (1u << lane) - 1u;
 
-    if (!preloaded) {
-        for (int j = lane; j < N; j += 32) {  // running counts at the unit start, tile end, unit end
-            const uint32_t* toff = S.rec[j].toff;
-            S.carry[j] = ldg_u32(toff + ustart / T);
-            S.tend[j] = ldg_u32(toff + ustart / T + 1);
-            S.want[j] = uend < m ? ldg_u32(toff + uend / T) : ldg_u32(toff + (m + T - 1) / T);
-        }
+    for (int j = lane; j < N; j += 32) {  // running counts at the unit start, tile end, unit end
+        const uint32_t* toff = S.rec[j].toff;
+        S.carry[j] = ldg_u32(toff + ustart / T);
+        S.tend[j] = ldg_u32(toff + ustart / T + 1);
+        S.want[j] = uend < m ? ldg_u32(toff + uend / T) : ldg_u32(toff + (m + T - 1) / T);
     }
 
     for (uint32_t sub = ustart; sub < uend; sub += kDSub) {
@@ -884,11 +885,10 @@ __global__ void __launch_bounds__(kDenseThreads, kDenseBlocksPerSM) fold_dense_k
             cur = lo;
         }
         const uint64_t ku = u - P.unit_first[lo];
-        const bool preloaded = false;
         if (P.desc[lo].w == 4)
-            fold_dense_unit<4>(P, lo, ku, S, lane, phase, preloaded, bad);
+            fold_dense_unit<4>(P, lo, ku, S, lane, phase, bad);
         else
-            fold_dense_unit<2>(P, lo, ku, S, lane, phase, preloaded, bad);
+            fold_dense_unit<2>(P, lo, ku, S, lane, phase, bad);
         if (__any_sync(0xffffffffu, bad)) {
             if (lane == 0) tc_set_err(P.err, TC_ERR_CORRUPT);
             break;
