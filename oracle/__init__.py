@@ -69,9 +69,9 @@ def lib():
         L.tco_f32_to_bf16.restype = ctypes.c_uint16
         L.tco_f32_to_bf16.argtypes = [f32]
         L.tco_adam_step.restype = None
-        L.tco_adam_step.argtypes = [vp, vp, vp, vp, u64, vp, f32, f32, f32, f32, f32, f32]
+        L.tco_adam_step.argtypes = [vp, vp, vp, vp, u64, vp, f32, f32, f32, f32, f32]
         L.tco_adam_replay.restype = ctypes.c_int
-        L.tco_adam_replay.argtypes = [vp, vp, vp, vp, u64, vp, vp, ctypes.c_int, f32, f32, f32, f32, vp, vp, vp]
+        L.tco_adam_replay.argtypes = [vp, vp, vp, vp, u64, vp, vp, ctypes.c_int, f32, f32, f32, vp, vp, vp]
         _lib = L
     return _lib
 
@@ -200,17 +200,20 @@ def f32_to_bf16_bits(f: float) -> int:
     return int(lib().tco_f32_to_bf16(float(f)))
 
 
-def adam_consts(step: int, b1: float, b2: float):
-    """c1 = 1 - b1^t, c2 = 1 - b2^t for 1-based step t, in double, rounded to fp32."""
-    return np.float32(1.0 - b1 ** step), np.float32(1.0 - b2 ** step)
+def adam_consts(step: int, lr: float, b1: float, b2: float):
+    """step_size = lr / (1 - b1^t), inv_c2s = 1 / sqrt(1 - b2^t) for 1-based step t, in double,
+    rounded to fp32 (tco_grad.h)."""
+    import math
+
+    return np.float32(lr / (1.0 - b1 ** step)), np.float32(1.0 / math.sqrt(1.0 - b2 ** step))
 
 
 def adam_step(master, m, v, w16, g, step: int, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8):
     """In place on float32 master/m/v and uint16 (bf16 bits) w16; ``step`` 1-based."""
-    c1, c2 = adam_consts(step, b1, b2)
+    ss, ic = adam_consts(step, lr, b1, b2)
     g = np.ascontiguousarray(g, dtype=np.float32)
-    lib().tco_adam_step(_ptr(master), _ptr(m), _ptr(v), _ptr(w16), master.size, _ptr(g), lr, b1, b2, eps,
-                        float(c1), float(c2))
+    lib().tco_adam_step(_ptr(master), _ptr(m), _ptr(v), _ptr(w16), master.size, _ptr(g), b1, b2, eps,
+                        float(ss), float(ic))
 
 
 def adam_replay(master, m, v, w16, payloads, first_step: int, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8) -> int:
@@ -218,9 +221,9 @@ def adam_replay(master, m, v, w16, payloads, first_step: int, lr=1e-3, b1=0.9, b
     ps = [np.ascontiguousarray(p, dtype=np.uint8) for p in payloads]
     pp = (ctypes.c_void_p * len(ps))(*[_ptr(p) for p in ps])
     pb = np.array([p.size for p in ps], dtype=np.uint64)
-    cs = [adam_consts(first_step + j, b1, b2) for j in range(len(ps))]
-    c1 = np.array([c[0] for c in cs], dtype=np.float32)
-    c2 = np.array([c[1] for c in cs], dtype=np.float32)
+    cs = [adam_consts(first_step + j, lr, b1, b2) for j in range(len(ps))]
+    ss = np.array([c[0] for c in cs], dtype=np.float32)
+    ic = np.array([c[1] for c in cs], dtype=np.float32)
     scratch = np.zeros(max(master.size, 1), dtype=np.float32)
     return int(lib().tco_adam_replay(_ptr(master), _ptr(m), _ptr(v), _ptr(w16), master.size, pp, _ptr(pb), len(ps),
-                                     lr, b1, b2, eps, _ptr(c1), _ptr(c2), _ptr(scratch)))
+                                     b1, b2, eps, _ptr(ss), _ptr(ic), _ptr(scratch)))

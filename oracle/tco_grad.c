@@ -213,16 +213,15 @@ int tco_grad_decompress(const uint8_t* p, uint64_t bytes, float* out, uint64_t n
     return OK;
 }
 
-void tco_adam_step(float* master, float* m, float* v, uint16_t* w16, uint64_t n, const float* g, float lr,
-                   float b1, float b2, float eps, float c1, float c2) {
+void tco_adam_step(float* master, float* m, float* v, uint16_t* w16, uint64_t n, const float* g, float b1, float b2,
+                   float eps, float step_size, float inv_c2s) {
     const float omb1 = 1.0f - b1, omb2 = 1.0f - b2;
     for (uint64_t i = 0; i < n; ++i) {
         const float gi = g[i];
         const float mi = b1 * m[i] + omb1 * gi;
         const float vi = b2 * v[i] + omb2 * (gi * gi);
-        const float mhat = mi / c1;
-        const float vhat = vi / c2;
-        const float upd = (lr * mhat) / (sqrtf(vhat) + eps);
+        const float denom = sqrtf(vi) * inv_c2s + eps;
+        const float upd = step_size * (mi / denom);
         m[i] = mi;
         v[i] = vi;
         master[i] = master[i] - upd;
@@ -231,12 +230,12 @@ void tco_adam_step(float* master, float* m, float* v, uint16_t* w16, uint64_t n,
 }
 
 int tco_adam_replay(float* master, float* m, float* v, uint16_t* w16, uint64_t n, const uint8_t* const* payloads,
-                    const uint64_t* bytes, int n_payloads, float lr, float b1, float b2, float eps,
-                    const float* c1, const float* c2, float* scratch) {
+                    const uint64_t* bytes, int n_payloads, float b1, float b2, float eps, const float* step_size,
+                    const float* inv_c2s, float* scratch) {
     for (int j = 0; j < n_payloads; ++j) {
         const int rc = tco_grad_decompress(payloads[j], bytes[j], scratch, n);
         if (rc != OK) return rc;
-        tco_adam_step(master, m, v, w16, n, scratch, lr, b1, b2, eps, c1[j], c2[j]);
+        tco_adam_step(master, m, v, w16, n, scratch, b1, b2, eps, step_size[j], inv_c2s[j]);
     }
     return OK;
 }

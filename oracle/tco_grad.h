@@ -18,10 +18,12 @@
  *   - decompress: INT8 -> scale * q; sparse -> zeros with the FP16 values widened at
  *     base_offset + index (§4 "sparse payloads are fused into dense tensors and INT8
  *     payloads are dequantized from their stored scales").
- *   - adam_step: m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2; master -= lr (m/c1) / (sqrt(v/c2) + eps)
- *     with c1 = 1 - b1^t, c2 = 1 - b2^t (given, the caller computes them in double); weights =
- *     bf16 round-to-nearest-even of master.  Operation order is fixed as
- *     written (every product and sum rounded to fp32; build with -ffp-contract=off).
+ *   - adam_step (standard bias-corrected Adam, in the efficient ordering of the
+ *     Adam paper's Algorithm 1 note / PyTorch's implementation): m = b1 m + (1-b1) g;
+ *     v = b2 v + (1-b2) g^2; denom = sqrt(v) * inv_c2s + eps; master -= step_size * (m / denom),
+ *     with step_size = lr / (1 - b1^t) and inv_c2s = 1 / sqrt(1 - b2^t) evaluated by the caller in
+ *     double and rounded to fp32; weights = bf16 round-to-nearest-even of master.  Operation order
+ *     is fixed as written (every product, sum and quotient rounded to fp32; -ffp-contract=off).
  *   - replay: payloads applied in temporal order, one adam_step each (the sequential definition
  *     the fused replay must reproduce bit-exactly).
  * Readings: DESIGN.md §12.
@@ -60,12 +62,12 @@ int tco_grad_decompress(const uint8_t* p, uint64_t bytes, float* out, uint64_t n
 uint16_t tco_f32_to_f16(float f);
 float tco_f16_to_f32(uint16_t h);
 uint16_t tco_f32_to_bf16(float f);
-void tco_adam_step(float* master, float* m, float* v, uint16_t* w16, uint64_t n, const float* g, float lr,
-                   float b1, float b2, float eps, float c1, float c2);
-/* payloads[j] at step first_step + j uses c1[j], c2[j]; scratch: n floats */
+void tco_adam_step(float* master, float* m, float* v, uint16_t* w16, uint64_t n, const float* g, float b1, float b2,
+                   float eps, float step_size, float inv_c2s);
+/* payloads[j] at step first_step + j uses step_size[j], inv_c2s[j]; scratch: n floats */
 int tco_adam_replay(float* master, float* m, float* v, uint16_t* w16, uint64_t n, const uint8_t* const* payloads,
-                    const uint64_t* bytes, int n_payloads, float lr, float b1, float b2, float eps,
-                    const float* c1, const float* c2, float* scratch);
+                    const uint64_t* bytes, int n_payloads, float b1, float b2, float eps, const float* step_size,
+                    const float* inv_c2s, float* scratch);
 
 #ifdef __cplusplus
 }
