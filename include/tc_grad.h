@@ -31,8 +31,10 @@ typedef struct tc_grad_opts {
 } tc_grad_opts;
 
 typedef struct tc_adam_hp {
-    /* defaults 1e-3, 0.9, 0.999, 1e-8.  The update uses their fp32 roundings; the bias
-     * corrections c1 = 1 - beta1^t, c2 = 1 - beta2^t are evaluated in double, then rounded */
+    /* defaults 1e-3, 0.9, 0.999, 1e-8.  Per element: m = b1 m + (1-b1) g;
+     * v = b2 v + (1-b2) g^2; master -= step_size * (m / (sqrt(v) * inv_c2s + eps)), with
+     * step_size = lr / (1 - beta1^t) and inv_c2s = 1 / sqrt(1 - beta2^t) evaluated in double and
+     * rounded to fp32; beta1, beta2, eps used as their fp32 roundings (oracle/tco_grad.h) */
     double lr, beta1, beta2, eps;
 } tc_adam_hp;
 

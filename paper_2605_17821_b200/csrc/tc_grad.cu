@@ -513,32 +513,29 @@ __global__ void grad_tile_start_kernel(const Payload* RP, uint64_t n, uint64_t t
 
 // ------------------------------------------------------------------- Adam ----------
 struct AdamC {
-    float lr, b1, b2, eps;
+    float b1, b2, eps;
 };
 
-__device__ __forceinline__ void adam_update(float& master, float& m, float& v, float g, const AdamC& a, float c1,
-                                            float c2) {
+__device__ __forceinline__ void adam_update(float& master, float& m, float& v, float g, const AdamC& a, float ss,
+                                            float ic) {
+    // oracle/tco_grad.c order: m, v; denom = sqrt(v) * inv_c2s + eps; master -= step_size * (m / denom).
+    // Zero operands take the IEEE result directly (sqrt(+0) = +0, 0 / d = 0 with 0's sign for d > 0):
+    // the same values without the slow paths that zeros trigger (most of a sparse gradient is zero)
     const float omb1 = __fsub_rn(1.0f, a.b1), omb2 = __fsub_rn(1.0f, a.b2);
     m = __fadd_rn(__fmul_rn(a.b1, m), __fmul_rn(omb1, g));
     v = __fadd_rn(__fmul_rn(a.b2, v), __fmul_rn(omb2, __fmul_rn(g, g)));
-    // zero operands take the IEEE result directly (0 / c = 0 with 0's sign for c > 0, sqrt(+0) = +0):
-    // the same values as the divisions, without their slow path — which zero dividends trigger,
-    // and most entries of a sparse gradient stream are zero
-    const float mhat = m != 0.0f ? __fdiv_rn(m, c1) : m;
-    const float vhat = v != 0.0f ? __fdiv_rn(v, c2) : v;
-    const float num = __fmul_rn(a.lr, mhat);
-    const float den = __fadd_rn(vhat != 0.0f ? __fsqrt_rn(vhat) : vhat, a.eps);
-    const float upd = num != 0.0f ? __fdiv_rn(num, den) : num;
-    master = __fsub_rn(master, upd);
+    const float den = __fadd_rn(__fmul_rn(v != 0.0f ? __fsqrt_rn(v) : v, ic), a.eps);
+    const float q = m != 0.0f ? __fdiv_rn(m, den) : m;
+    master = __fsub_rn(master, __fmul_rn(ss, q));
 }
 
 __global__ void adam_step_kernel(float* __restrict__ master, float* __restrict__ m, float* __restrict__ v,
                                  uint16_t* __restrict__ w16, uint64_t n, const float* __restrict__ g, AdamC a,
-                                 float c1, float c2) {
+                                 float ss, float ic) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
         float w = master[i], mi = m[i], vi = v[i];
-        adam_update(w, mi, vi, g[i], a, c1, c2);
+        adam_update(w, mi, vi, g[i], a, ss, ic);
         master[i] = w;
         m[i] = mi;
         v[i] = vi;
@@ -551,7 +548,7 @@ __global__ void adam_step_kernel(float* __restrict__ master, float* __restrict__
 // mask word each); a word is stored only where it changed.
 __global__ void adam_mask_kernel(float* __restrict__ master, float* __restrict__ m, float* __restrict__ v,
                                  uint16_t* __restrict__ w16, uint64_t n, const float* __restrict__ g, AdamC a,
-                                 float c1, float c2, uint32_t* __restrict__ mk_w, uint32_t* __restrict__ mk_master,
+                                 float ss, float ic, uint32_t* __restrict__ mk_w, uint32_t* __restrict__ mk_master,
                                  uint32_t* __restrict__ mk_m, uint32_t* __restrict__ mk_v) {
     const int lane = threadIdx.x & 31;
     const uint64_t words = (n + 31) / 32;
@@ -564,7 +561,7 @@ __global__ void adam_mask_kernel(float* __restrict__ master, float* __restrict__
             const float w0 = master[i], m0 = m[i], v0 = v[i];
             const uint16_t h0 = w16[i];
             float w = w0, mm = m0, vv = v0;
-            adam_update(w, mm, vv, g[i], a, c1, c2);
+            adam_update(w, mm, vv, g[i], a, ss, ic);
             const uint16_t h = __bfloat16_as_ushort(__float2bfloat16_rn(w));
             cmaster = __float_as_uint(w) != __float_as_uint(w0);
             cm = __float_as_uint(mm) != __float_as_uint(m0);
@@ -593,7 +590,7 @@ struct ReplayParams {
     uint64_t n, tiles;
     int nsteps;              // fused steps (payloads 0 .. nsteps-1)
     AdamC a;
-    float c1[TC_MAX_FOLD], c2[TC_MAX_FOLD];
+    float ss[TC_MAX_FOLD], ic[TC_MAX_FOLD];  // per fused step: lr / (1 - b1^t), 1 / sqrt(1 - b2^t)
     const Payload* pay;      // [nsteps], walker output
     unsigned* err;
 };
@@ -739,7 +736,7 @@ __global__ void __launch_bounds__(kRThreads) adam_replay_kernel(const __grid_con
                         const uint64_t i = base + j * kRThreads + tid;
                         const float g = R.variant == 1 ? (i < P.n ? __fmul_rn(R.scale, static_cast<float>(R.q[i])) : 0.0f)
                                                        : s_gd[(s - g0) * kGB + j * kRThreads + tid];
-                        adam_update(w[j], mm[j], vv[j], g, P.a, P.c1[s], P.c2[s]);
+                        adam_update(w[j], mm[j], vv[j], g, P.a, P.ss[s], P.ic[s]);
                     }
                 }
                 __syncthreads();  // before the next group's tiles
@@ -752,7 +749,7 @@ __global__ void __launch_bounds__(kRThreads) adam_replay_kernel(const __grid_con
                     for (uint32_t j = 0; j < kRPer; ++j) {
                         const uint64_t i = base + j * kRThreads + tid;
                         const float g = i < P.n ? __fmul_rn(R.scale, static_cast<float>(R.q[i])) : 0.0f;
-                        adam_update(w[j], mm[j], vv[j], g, P.a, P.c1[s], P.c2[s]);
+                        adam_update(w[j], mm[j], vv[j], g, P.a, P.ss[s], P.ic[s]);
                     }
                     continue;
                 }
@@ -773,7 +770,7 @@ __global__ void __launch_bounds__(kRThreads) adam_replay_kernel(const __grid_con
                 __syncthreads();
 #pragma unroll
                 for (uint32_t j = 0; j < kRPer; ++j)
-                    adam_update(w[j], mm[j], vv[j], s_gd[j * kRThreads + tid], P.a, P.c1[s], P.c2[s]);
+                    adam_update(w[j], mm[j], vv[j], s_gd[j * kRThreads + tid], P.a, P.ss[s], P.ic[s]);
                 __syncthreads();
             }
         }
@@ -794,16 +791,16 @@ __global__ void __launch_bounds__(kRThreads) adam_replay_kernel(const __grid_con
 
 AdamC adam_consts(const tc_adam_hp* hp) {
     AdamC a;
-    a.lr = static_cast<float>(hp ? hp->lr : 1e-3);
     a.b1 = static_cast<float>(hp ? hp->beta1 : 0.9);
     a.b2 = static_cast<float>(hp ? hp->beta2 : 0.999);
     a.eps = static_cast<float>(hp ? hp->eps : 1e-8);
     return a;
 }
-void bias(const tc_adam_hp* hp, uint64_t step, float* c1, float* c2) {
-    const double b1 = hp ? hp->beta1 : 0.9, b2 = hp ? hp->beta2 : 0.999;
-    *c1 = static_cast<float>(1.0 - std::pow(b1, static_cast<double>(step)));
-    *c2 = static_cast<float>(1.0 - std::pow(b2, static_cast<double>(step)));
+// step_size = lr / (1 - beta1^t), inv_c2s = 1 / sqrt(1 - beta2^t): in double, rounded to fp32
+void bias(const tc_adam_hp* hp, uint64_t step, float* ss, float* ic) {
+    const double lr = hp ? hp->lr : 1e-3, b1 = hp ? hp->beta1 : 0.9, b2 = hp ? hp->beta2 : 0.999;
+    *ss = static_cast<float>(lr / (1.0 - std::pow(b1, static_cast<double>(step))));
+    *ic = static_cast<float>(1.0 / std::sqrt(1.0 - std::pow(b2, static_cast<double>(step))));
 }
 
 tc_status check_state(const tc_adam_state* st) {
@@ -956,10 +953,10 @@ tc_status tc_adam_step(tc_ctx* ctx, const tc_adam_state* stt, const float* grad,
     if (!stt->n) return TC_OK;
     if (!grad) return fail(TC_ERR_INVALID, "grad is NULL");
     cudaSetDevice(tc::ctx_device(ctx));
-    float c1, c2;
-    bias(hp, step, &c1, &c2);
+    float ss, ic;
+    bias(hp, step, &ss, &ic);
     adam_step_kernel<<<grid_for(ctx, stt->n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        stt->master, stt->m, stt->v, stt->w16, stt->n, grad, adam_consts(hp), c1, c2);
+        stt->master, stt->m, stt->v, stt->w16, stt->n, grad, adam_consts(hp), ss, ic);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "adam step launch");
     tc::ctx_add_launches(ctx, 1);
@@ -992,7 +989,7 @@ tc_status tc_adam_replay(tc_ctx* ctx, const tc_adam_state* stt, const void* cons
         R.tiles = (stt->n + kGB - 1) / kGB;
         R.nsteps = nf;
         R.a = adam_consts(hp);
-        for (int j = 0; j < nf; ++j) bias(hp, first_step + j, &R.c1[j], &R.c2[j]);
+        for (int j = 0; j < nf; ++j) bias(hp, first_step + j, &R.ss[j], &R.ic[j]);
         R.pay = P;
         R.err = tc::ctx_err(ctx);
         static bool attr = false;
@@ -1030,10 +1027,10 @@ tc_status tc_adam_step_encode(tc_ctx* ctx, const tc_adam_state* stt, const float
     uint32_t* mk[4];
     for (int k = 0; k < 4; ++k) mk[k] = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(scratch) + k * per);
     if (n) {
-        float c1, c2;
-        bias(hp, step, &c1, &c2);
+        float ss, ic;
+        bias(hp, step, &ss, &ic);
         adam_mask_kernel<<<grid_for(ctx, words * 32, 256), 256, 0, s>>>(stt->master, stt->m, stt->v, stt->w16, n, grad,
-                                                                         adam_consts(hp), c1, c2, mk[0], mk[1], mk[2],
+                                                                         adam_consts(hp), ss, ic, mk[0], mk[1], mk[2],
                                                                          mk[3]);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "adam mask launch");
