@@ -532,8 +532,29 @@ __device__ __forceinline__ void adam_update(float& master, float& m, float& v, f
 __global__ void adam_step_kernel(float* __restrict__ master, float* __restrict__ m, float* __restrict__ v,
                                  uint16_t* __restrict__ w16, uint64_t n, const float* __restrict__ g, AdamC a,
                                  float ss, float ic) {
+    // 4 elements per thread with 16-byte loads / stores (8-byte for the bf16 weights)
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t nv = n / 4;
+    for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < nv; q += stride) {
+        float4 w = reinterpret_cast<const float4*>(master)[q];
+        float4 mm = reinterpret_cast<const float4*>(m)[q];
+        float4 vv = reinterpret_cast<const float4*>(v)[q];
+        const float4 gg = __ldg(reinterpret_cast<const float4*>(g) + q);
+        adam_update(w.x, mm.x, vv.x, gg.x, a, ss, ic);
+        adam_update(w.y, mm.y, vv.y, gg.y, a, ss, ic);
+        adam_update(w.z, mm.z, vv.z, gg.z, a, ss, ic);
+        adam_update(w.w, mm.w, vv.w, gg.w, a, ss, ic);
+        reinterpret_cast<float4*>(master)[q] = w;
+        reinterpret_cast<float4*>(m)[q] = mm;
+        reinterpret_cast<float4*>(v)[q] = vv;
+        ushort4 h;
+        h.x = __bfloat16_as_ushort(__float2bfloat16_rn(w.x));
+        h.y = __bfloat16_as_ushort(__float2bfloat16_rn(w.y));
+        h.z = __bfloat16_as_ushort(__float2bfloat16_rn(w.z));
+        h.w = __bfloat16_as_ushort(__float2bfloat16_rn(w.w));
+        reinterpret_cast<ushort4*>(w16)[q] = h;
+    }
+    for (uint64_t i = nv * 4 + static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
         float w = master[i], mi = m[i], vi = v[i];
         adam_update(w, mi, vi, g[i], a, ss, ic);
         master[i] = w;
@@ -955,7 +976,8 @@ tc_status tc_adam_step(tc_ctx* ctx, const tc_adam_state* stt, const float* grad,
     cudaSetDevice(tc::ctx_device(ctx));
     float ss, ic;
     bias(hp, step, &ss, &ic);
-    adam_step_kernel<<<grid_for(ctx, stt->n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+    if (!aligned16(grad)) return fail(TC_ERR_INVALID, "grad must be 16-byte aligned");
+    adam_step_kernel<<<grid_for(ctx, stt->n / 4 + 1, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
         stt->master, stt->m, stt->v, stt->w16, stt->n, grad, adam_consts(hp), ss, ic);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "adam step launch");
