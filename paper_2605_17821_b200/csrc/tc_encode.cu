@@ -637,7 +637,7 @@ cudaError_t launch_encode(const EncParams& p, cudaStream_t s) {
     }
     if (p.total_blocks == 0) return cudaSuccess;
     if (p.seg[0].mask_in)
-        encode_mask_kernel<true><<<static_cast<unsigned>(p.total_blocks), kEncThreads, kEncDynSmem, s>>>(p);
+        encode_mask_kernel<true><<<static_cast<unsigned>(p.total_blocks), kEncThreads, 0, s>>>(p);  // no tile to stage
     else
         encode_mask_kernel<false><<<static_cast<unsigned>(p.total_blocks), kEncThreads, kEncDynSmem, s>>>(p);
     cudaError_t e = cudaGetLastError();

@@ -564,42 +564,80 @@ __global__ void adam_step_kernel(float* __restrict__ master, float* __restrict__
     }
 }
 
-// NEXT row 2: the Adam step and the change masks of the lossless diff of its own update.  A warp
-// takes 32 consecutive elements per iteration; the four segments' change bits are ballots (one
-// mask word each); a word is stored only where it changed.
-__global__ void adam_mask_kernel(float* __restrict__ master, float* __restrict__ m, float* __restrict__ v,
-                                 uint16_t* __restrict__ w16, uint64_t n, const float* __restrict__ g, AdamC a,
-                                 float ss, float ic, uint32_t* __restrict__ mk_w, uint32_t* __restrict__ mk_master,
-                                 uint32_t* __restrict__ mk_m, uint32_t* __restrict__ mk_v) {
+// NEXT row 2: the Adam step and the change masks of the lossless diff of its own update.  A
+// thread takes 4 consecutive elements (16-byte loads of master / m / v / grad, 8-byte of the
+// bf16 weights), so a warp covers 128 elements = 4 mask words per segment: each lane's 4 change
+// bits are OR-shuffled across the 8 lanes of one 32-element mask word (LSB-first, reading R6).
+// A vector is stored only where one of its words changed (the others are rewritten equal).
+__device__ __forceinline__ uint32_t or8(uint32_t bits, int lane) {
+    uint32_t x = bits << (4 * (lane & 7));
+    x |= __shfl_xor_sync(0xffffffffu, x, 1);
+    x |= __shfl_xor_sync(0xffffffffu, x, 2);
+    x |= __shfl_xor_sync(0xffffffffu, x, 4);
+    return x;
+}
+
+__global__ void __launch_bounds__(256) adam_mask_kernel(float* __restrict__ master, float* __restrict__ m,
+                                                        float* __restrict__ v, uint16_t* __restrict__ w16, uint64_t n,
+                                                        const float* __restrict__ g, AdamC a, float ss, float ic,
+                                                        uint32_t* __restrict__ mk_w, uint32_t* __restrict__ mk_master,
+                                                        uint32_t* __restrict__ mk_m, uint32_t* __restrict__ mk_v) {
     const int lane = threadIdx.x & 31;
-    const uint64_t words = (n + 31) / 32;
-    const uint64_t wstride = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
-    for (uint64_t wd = static_cast<uint64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5); wd < words;
-         wd += wstride) {
-        const uint64_t i = wd * 32 + lane;
-        bool cw = false, cmaster = false, cm = false, cv = false;
-        if (i < n) {
-            const float w0 = master[i], m0 = m[i], v0 = v[i];
-            const uint16_t h0 = w16[i];
-            float w = w0, mm = m0, vv = v0;
-            adam_update(w, mm, vv, g[i], a, ss, ic);
-            const uint16_t h = __bfloat16_as_ushort(__float2bfloat16_rn(w));
-            cmaster = __float_as_uint(w) != __float_as_uint(w0);
-            cm = __float_as_uint(mm) != __float_as_uint(m0);
-            cv = __float_as_uint(vv) != __float_as_uint(v0);
-            cw = h != h0;
-            if (cmaster) master[i] = w;
-            if (cm) m[i] = mm;
-            if (cv) v[i] = vv;
-            if (cw) w16[i] = h;
+    const uint64_t nq = (n + 3) / 4, groups = (nq + 31) / 32, words = (n + 31) / 32;
+    const uint64_t gstride = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
+    for (uint64_t gq = static_cast<uint64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5); gq < groups;
+         gq += gstride) {
+        const uint64_t q = gq * 32 + lane;
+        uint32_t cw = 0, cmaster = 0, cm = 0, cv = 0;
+        if (q * 4 + 4 <= n) {
+            const float4 w0 = reinterpret_cast<const float4*>(master)[q];
+            const float4 m0 = reinterpret_cast<const float4*>(m)[q];
+            const float4 v0 = reinterpret_cast<const float4*>(v)[q];
+            const float4 gg = __ldg(reinterpret_cast<const float4*>(g) + q);
+            const ushort4 h0 = reinterpret_cast<const ushort4*>(w16)[q];
+            float4 w = w0, mm = m0, vv = v0;
+            adam_update(w.x, mm.x, vv.x, gg.x, a, ss, ic);
+            adam_update(w.y, mm.y, vv.y, gg.y, a, ss, ic);
+            adam_update(w.z, mm.z, vv.z, gg.z, a, ss, ic);
+            adam_update(w.w, mm.w, vv.w, gg.w, a, ss, ic);
+            ushort4 h;
+            h.x = __bfloat16_as_ushort(__float2bfloat16_rn(w.x));
+            h.y = __bfloat16_as_ushort(__float2bfloat16_rn(w.y));
+            h.z = __bfloat16_as_ushort(__float2bfloat16_rn(w.z));
+            h.w = __bfloat16_as_ushort(__float2bfloat16_rn(w.w));
+            auto ne = [](float x, float y) { return __float_as_uint(x) != __float_as_uint(y); };
+            cmaster = ne(w.x, w0.x) | ne(w.y, w0.y) << 1 | ne(w.z, w0.z) << 2 | ne(w.w, w0.w) << 3;
+            cm = ne(mm.x, m0.x) | ne(mm.y, m0.y) << 1 | ne(mm.z, m0.z) << 2 | ne(mm.w, m0.w) << 3;
+            cv = ne(vv.x, v0.x) | ne(vv.y, v0.y) << 1 | ne(vv.z, v0.z) << 2 | ne(vv.w, v0.w) << 3;
+            cw = (h.x != h0.x) | (h.y != h0.y) << 1 | (h.z != h0.z) << 2 | (h.w != h0.w) << 3;
+            if (cmaster) reinterpret_cast<float4*>(master)[q] = w;
+            if (cm) reinterpret_cast<float4*>(m)[q] = mm;
+            if (cv) reinterpret_cast<float4*>(v)[q] = vv;
+            if (cw) reinterpret_cast<ushort4*>(w16)[q] = h;
+        } else {
+            for (uint64_t i = q * 4; i < n; ++i) {  // the last, partial quad
+                const uint32_t bit = 1u << (i - q * 4);
+                const float w0 = master[i], m0 = m[i], v0 = v[i];
+                const uint16_t h0 = w16[i];
+                float w = w0, mm = m0, vv = v0;
+                adam_update(w, mm, vv, g[i], a, ss, ic);
+                const uint16_t h = __bfloat16_as_ushort(__float2bfloat16_rn(w));
+                if (__float_as_uint(w) != __float_as_uint(w0)) { master[i] = w; cmaster |= bit; }
+                if (__float_as_uint(mm) != __float_as_uint(m0)) { m[i] = mm; cm |= bit; }
+                if (__float_as_uint(vv) != __float_as_uint(v0)) { v[i] = vv; cv |= bit; }
+                if (h != h0) { w16[i] = h; cw |= bit; }
+            }
         }
-        const uint32_t bw = __ballot_sync(0xffffffffu, cw), bmaster = __ballot_sync(0xffffffffu, cmaster);
-        const uint32_t bm = __ballot_sync(0xffffffffu, cm), bv = __ballot_sync(0xffffffffu, cv);
-        if (lane == 0) {
-            mk_w[wd] = bw;
-            mk_master[wd] = bmaster;
-            mk_m[wd] = bm;
-            mk_v[wd] = bv;
+        cw = or8(cw, lane);
+        cmaster = or8(cmaster, lane);
+        cm = or8(cm, lane);
+        cv = or8(cv, lane);
+        const uint64_t wd = gq * 4 + (lane >> 3);
+        if ((lane & 7) == 0 && wd < words) {
+            mk_w[wd] = cw;
+            mk_master[wd] = cmaster;
+            mk_m[wd] = cm;
+            mk_v[wd] = cv;
         }
     }
 }
@@ -1038,7 +1076,7 @@ tc_status tc_adam_step_encode(tc_ctx* ctx, const tc_adam_state* stt, const float
     tc_status st = check_state(stt);
     if (st != TC_OK) return st;
     if (!out || !aligned16(out) || !out_bytes) return fail(TC_ERR_INVALID, "out must be 16-byte aligned; out_bytes set");
-    if (stt->n && !grad) return fail(TC_ERR_INVALID, "grad is NULL");
+    if (stt->n && (!grad || !aligned16(grad))) return fail(TC_ERR_INVALID, "grad is NULL or not 16-byte aligned");
     cudaSetDevice(tc::ctx_device(ctx));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const uint64_t n = stt->n, words = (n + 31) / 32;
@@ -1051,7 +1089,7 @@ tc_status tc_adam_step_encode(tc_ctx* ctx, const tc_adam_state* stt, const float
     if (n) {
         float ss, ic;
         bias(hp, step, &ss, &ic);
-        adam_mask_kernel<<<grid_for(ctx, words * 32, 256), 256, 0, s>>>(stt->master, stt->m, stt->v, stt->w16, n, grad,
+        adam_mask_kernel<<<grid_for(ctx, (n + 3) / 4, 256), 256, 0, s>>>(stt->master, stt->m, stt->v, stt->w16, n, grad,
                                                                          adam_consts(hp), ss, ic, mk[0], mk[1], mk[2],
                                                                          mk[3]);
         cudaError_t e = cudaGetLastError();

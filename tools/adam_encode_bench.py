@@ -2,7 +2,8 @@
 (tc_adam_step_encode) against the unfused path (tc_adam_step, then tc_diff_encode of the state
 against the advancing reference copy), on a cfg2-sized shard (1.56 G parameters: bf16 weights +
 fp32 master / m / v).  Two gradient regimes: dense (every moment changes: the record is ~ the
-state) and sparse (1 % nonzero, fresh moments: the record is ~2 % of the state).  CUDA events,
+state) and sparse (1 % nonzero, fresh moments: ~1 % of the words change), the sparse one in both
+record modes (mask, index).  CUDA events,
 inputs resident; prints one JSON line.
 
     python tools/adam_encode_bench.py [--n 1557611200] [--reps 3]
@@ -36,18 +37,18 @@ def main():
     w16 = torch.empty(n, dtype=torch.int16, device=dev)
     g = torch.empty_like(master)
     refs = [torch.empty_like(w16), torch.empty_like(master), torch.empty_like(master), torch.empty_like(master)]
-    cap = tc.diff_bound([n] * 4, [2, 4, 4, 4], 4096, 1 << 28)
+    cap = max(tc.diff_bound([n] * 4, [2, 4, 4, 4], 4096, 1 << 28, index_mode=im) for im in (False, True))
     out = torch.empty(cap, dtype=torch.uint8, device=dev)
     ob = torch.zeros(1, dtype=torch.int64, device=dev)
     W = 14 * n
     res = {"n": n, "state_bytes": W}
-    for regime in ("sparse", "dense"):
+    for regime, imode in (("sparse", False), ("sparse_index", True), ("dense", False)):
         gen = torch.Generator(device=dev).manual_seed(1)
         with torch.cuda.stream(s):
             torch.randn(n, out=master, generator=gen)
             torch.randn(n, out=g, generator=gen)
             g.mul_(1e-2)
-            if regime == "sparse":
+            if regime.startswith("sparse"):
                 g.mul_((torch.rand(n, device=dev, generator=gen) < 0.01).float())
                 m.zero_()
                 v.zero_()
@@ -57,7 +58,8 @@ def main():
                 torch.randn(n, out=v, generator=gen)
                 v.abs_().mul_(1e-6)
             w16.copy_(master.to(torch.bfloat16).view(torch.int16))
-        snap = [t.clone() for t in (master, m, v, w16)]
+            snap = [t.clone() for t in (master, m, v, w16)]  # on s: after the initialisation above
+        s.synchronize()
 
         def reset():
             with torch.cuda.stream(s):
@@ -75,37 +77,42 @@ def main():
             reset()
             e0, e1 = ev(), ev()
             e0.record(s)
-            tc.adam_step_encode(ctx, master, m, v, w16, g, 7, out, ob, stream=s)
+            tc.adam_step_encode(ctx, master, m, v, w16, g, 7, out, ob, stream=s, index_mode=imode)
             e1.record(s)
             s.synchronize()
             fused.append(e0.elapsed_time(e1))
             nb_f = int(ob.item())
-            f_rec = out[:nb_f].clone() if nb_f < (2 << 30) else None
+            f_rec = out[:nb_f].clone()  # the fused record, compared with the unfused one below
             reset()
             e0, e1, e2 = ev(), ev(), ev()
             e0.record(s)
             tc.adam_step(ctx, master, m, v, w16, g, 7, stream=s)
             e1.record(s)
             tc.diff_encode(ctx, refs, [w16, master.view(torch.int32), m.view(torch.int32), v.view(torch.int32)],
-                           out, ob, 7, 6, stream=s)
+                           out, ob, 7, 6, stream=s, index_mode=imode)
             e2.record(s)
             s.synchronize()
             unfused.append((e0.elapsed_time(e1), e1.elapsed_time(e2)))
-            same = f_rec is None or torch.equal(out[:nb_f], f_rec)
+            same = int(ob.item()) == nb_f and torch.equal(out[:nb_f], f_rec)
             del f_rec
         ctx.check(s)
         fm = statistics.median(fused)
         am = statistics.median(x[0] for x in unfused)
         em = statistics.median(x[1] for x in unfused)
         nb = int(ob.item())
-        # bytes: fused = grad + state read, changed words written, masks written + read, record
+        changed_bytes, off = 0, 0  # the words the step rewrote: Σ count·w over the record headers
+        while off < nb:
+            h = out[off:off + 64].cpu().numpy().view("<u8")
+            changed_bytes += int(h[4]) * ((int(h[0]) >> 48) & 0xFF)
+            off += int(h[7])
         res[regime] = {"record_bytes": nb, "record_equal": bool(same),
                        "fused_ms": round(fm, 3), "fused_state_gbs": round(W / fm / 1e6, 1),
                        "unfused_adam_ms": round(am, 3), "unfused_encode_ms": round(em, 3),
                        "unfused_ms": round(am + em, 3), "speedup": round((am + em) / fm, 3),
-                       "fused_frac_hbm_min_bytes": round((4 * n + W + W + nb) / fm / 1e6 / peak, 4)}
+                       "changed_bytes": changed_bytes,
+                       "fused_frac_hbm_min_bytes": round((4 * n + W + changed_bytes + nb) / fm / 1e6 / peak, 4)}
     res["note"] = ("NEXT row 2 (DESIGN.md §13): tc_adam_step_encode vs tc_adam_step + tc_diff_encode(ref copy); "
-                   "fused_frac_hbm_min_bytes counts grad + state read + state written + record")
+                   "fused_frac_hbm_min_bytes counts grad + state read + changed words written + record")
     print(json.dumps(res))
 
 
