@@ -21,6 +21,9 @@
 //                           the chunk's record start is known (chunk c waits only for chunk c-1's
 //                           counts, i.e. only at chunk boundaries); the block completing a chunk
 //                           writes its header and publishes the next record start.
+//   A' encode_maskin_kernel the mask-input variant (tc_adam_step_encode: the mask comes from the
+//                           Adam pass, no ref): persistent warps, a warp per block, 4 blocks per
+//                           ticket; same outputs as A.
 //   P  encode_prefix_kernel (1 CTA) exclusive scans of the per-group and per-chunk counts.
 //   B  encode_emit_kernel   one CTA per 256 blocks: block-wide scan of the block counts -> each
 //                           block's in-chunk prefix (a thread per block, which also adds it to
@@ -124,10 +127,63 @@ __device__ __forceinline__ uint16_t ldg_cur(const uint16_t* p) {
     return static_cast<uint16_t>(__ldg(reinterpret_cast<const unsigned short*>(p)));
 }
 
-// MASK_IN: the change mask comes precomputed (EncSeg::mask_in, e.g. from the fused Adam step,
-// tc_adam_step_encode) and `cur` is the only state: no ref, no compare, no ref advance; changed
-// words are gathered from global cur.  Everything from the counts on is the same code.
-template <int W, bool MASK_IN>
+// Block / chunk bookkeeping (one thread, after its own stores; nobody waits for it): one packed
+// atomic {done blocks : 24 | changed words : 40} per chunk tells the block that completes the
+// chunk, which writes the header and publishes the next record start.  `nblocks` blocks of chunk
+// I.chunk with `total` changed words between them are counted at once (kernel A: one block).
+__device__ __forceinline__ void note_block(const EncParams& P, unsigned long long b, uint32_t total, bool sparse) {
+    P.info[b] = total | (sparse ? 0u : kDenseFlag);
+    atomicAdd(&P.group_sum[b / kEmitGroup], static_cast<unsigned long long>(total));
+}
+
+template <int W>
+__device__ __forceinline__ void count_blocks(const EncParams& P, const BlockInfo& I, uint32_t nblocks,
+                                             unsigned long long total, unsigned long long rs) {
+    const bool imode = P.index_mode != 0;
+    const unsigned long long old =
+        atomicAdd(&P.chunk_acc[I.chunk], (static_cast<unsigned long long>(nblocks) << kAccDoneShift) | total);
+    if ((old >> kAccDoneShift) + nblocks == I.nblk) {
+        const uint64_t count = (old & kAccCountMask) + total;
+        const uint64_t n_mask = cdiv(I.m, 32);
+        const uint64_t n_tiles = cdiv(I.m, P.T);
+        const uint64_t rec_total = imode ? record_bytes_index(I.m, P.T, W, count) : record_bytes(I.m, P.T, W, count);
+        const unsigned long long next = rs + rec_total;
+        if (next > P.out_cap) tc_set_err(P.err, TC_ERR_CAPACITY);  // this record is not written
+        else {
+        uint8_t* rec = P.out + rs;
+        uint64_t* h = reinterpret_cast<uint64_t*>(rec);
+        h[0] = 0x31444354ull /* "TCD1" */ | (1ull << 32) | (static_cast<uint64_t>(W) << 48) |
+               ((imode ? 3ull : 1ull) << 56);
+        h[1] = static_cast<uint64_t>(P.T) | (static_cast<uint64_t>(P.seg[I.seg].seg_id) << 32);
+        h[2] = P.seg[I.seg].word_base + I.chunk_off;
+        h[3] = I.m;
+        h[4] = count;
+        h[5] = P.version;
+        h[6] = P.ref_version;
+        h[7] = rec_total;
+        uint32_t* gtoff;
+        uint8_t* gval;
+        if (imode) {
+            gtoff = reinterpret_cast<uint32_t*>(rec + index_toff_off());
+            uint8_t* gidx = rec + index_idx_off(I.m, P.T);
+            for (uint64_t x = 2 * count; x < pad16(2 * count); ++x) gidx[x] = 0;
+            gval = rec + index_val_off(I.m, P.T, count);
+        } else {
+            uint32_t* gmask = reinterpret_cast<uint32_t*>(rec + kHdrBytes);
+            for (uint64_t x = n_mask; x < pad16(4 * n_mask) / 4; ++x) gmask[x] = 0;
+            gtoff = reinterpret_cast<uint32_t*>(rec + kHdrBytes + pad16(4 * n_mask));
+            gval = rec + record_fixed_bytes(I.m, P.T);
+        }
+        gtoff[n_tiles] = static_cast<uint32_t>(count);
+        for (uint64_t x = n_tiles + 1; x < pad16(4 * (n_tiles + 1)) / 4; ++x) gtoff[x] = 0;
+        for (uint64_t x = W * count; x < pad16(W * count); ++x) gval[x] = 0;
+        }
+        st_relaxed(&P.rstart[I.chunk + 1], next | 1ull);
+        if (I.chunk + 1 == P.total_chunks) *P.out_bytes = next;
+    }
+}
+
+template <int W>
 __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_t* tile, int tid) {
     using word_t = typename Word<W>::T;
     constexpr uint32_t B = Word<W>::kBlock;
@@ -143,11 +199,6 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
     const bool adv = P.advance_ref != 0;
     const uint32_t mw0 = wid * MPW;
     uint32_t mine = 0;  // lane q keeps mask word mw0 + q
-    if constexpr (MASK_IN) {
-        const uint32_t q = mw0 + lane;
-        if (lane < static_cast<int>(MPW) && q * 32 < I.nb)
-            mine = __ldg(S.mask_in + ((I.chunk_off + I.p0) >> 5) + q);
-    } else {
     // words past the bulk copy: the < 16-byte tail, and equal padding up to B so that pass 1
     // needs no bounds test
     if (I.nb < B) {
@@ -196,7 +247,6 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
     }
     if (lane < static_cast<int>(MPW))
         mine = reinterpret_cast<const uint32_t*>(tile)[(2 * B * W) / 4 + mw0 + lane];
-    }
     // ---- counts: lane-per-mask-word popcount scan over the warp's range (the barrier below
     //      also publishes thread 0's prefetched record start) ----
     const uint32_t c = __popc(mine);
@@ -234,7 +284,7 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
             while (wv) {
                 const uint32_t b = __ffs(wv) - 1;
                 wv &= wv - 1;
-                slot[k] = MASK_IN ? ldg_cur(gcur + q0 + b) : scur[q0 + b];
+                slot[k] = scur[q0 + b];
                 if (imode) islot[k] = static_cast<uint16_t>((I.p0 + q0 + b) & tmask);
                 ++k;
             }
@@ -248,7 +298,7 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
                 const uint32_t o = __shfl_sync(0xffffffffu, pre, src);
                 if ((bb >> lane) & 1u) {
                     const uint32_t q = (mw0 + src) * 32 + lane;
-                    slot[o + __popc(bb & lt)] = MASK_IN ? ldg_cur(gcur + q) : scur[q];
+                    slot[o + __popc(bb & lt)] = scur[q];
                     if (imode) islot[o + __popc(bb & lt)] = static_cast<uint16_t>((I.p0 + q) & tmask);
                 }
             }
@@ -286,57 +336,12 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
         }
     }
 
-    // ---- block / chunk bookkeeping (thread 0, after its own stores; nobody waits for it):
-    //      one packed atomic {done blocks : 24 | changed words : 40} per chunk tells the block
-    //      that completes the chunk, which writes the header and publishes the next record start ----
     if (tid == 0) {
-        P.info[I.b] = total | (sparse ? 0u : kDenseFlag);
-        atomicAdd(&P.group_sum[I.b / kEmitGroup], static_cast<unsigned long long>(total));
-        const unsigned long long old =
-            atomicAdd(&P.chunk_acc[I.chunk], (1ull << kAccDoneShift) | static_cast<unsigned long long>(total));
-        if ((old >> kAccDoneShift) + 1 == I.nblk) {
-            const uint64_t count = (old & kAccCountMask) + total;
-            const uint64_t n_mask = cdiv(I.m, 32);
-            const uint64_t n_tiles = cdiv(I.m, P.T);
-            const uint64_t rec_total = imode ? record_bytes_index(I.m, P.T, W, count) : record_bytes(I.m, P.T, W, count);
-            const unsigned long long next = rs + rec_total;
-            if (next > P.out_cap) tc_set_err(P.err, TC_ERR_CAPACITY);  // this record is not written
-            else {
-            uint8_t* rec = P.out + rs;
-            uint64_t* h = reinterpret_cast<uint64_t*>(rec);
-            h[0] = 0x31444354ull /* "TCD1" */ | (1ull << 32) | (static_cast<uint64_t>(W) << 48) |
-                   ((imode ? 3ull : 1ull) << 56);
-            h[1] = static_cast<uint64_t>(P.T) | (static_cast<uint64_t>(P.seg[I.seg].seg_id) << 32);
-            h[2] = P.seg[I.seg].word_base + I.chunk_off;
-            h[3] = I.m;
-            h[4] = count;
-            h[5] = P.version;
-            h[6] = P.ref_version;
-            h[7] = rec_total;
-            uint32_t* gtoff;
-            uint8_t* gval;
-            if (imode) {
-                gtoff = reinterpret_cast<uint32_t*>(rec + index_toff_off());
-                uint8_t* gidx = rec + index_idx_off(I.m, P.T);
-                for (uint64_t x = 2 * count; x < pad16(2 * count); ++x) gidx[x] = 0;
-                gval = rec + index_val_off(I.m, P.T, count);
-            } else {
-                uint32_t* gmask = reinterpret_cast<uint32_t*>(rec + kHdrBytes);
-                for (uint64_t x = n_mask; x < pad16(4 * n_mask) / 4; ++x) gmask[x] = 0;
-                gtoff = reinterpret_cast<uint32_t*>(rec + kHdrBytes + pad16(4 * n_mask));
-                gval = rec + record_fixed_bytes(I.m, P.T);
-            }
-            gtoff[n_tiles] = static_cast<uint32_t>(count);
-            for (uint64_t x = n_tiles + 1; x < pad16(4 * (n_tiles + 1)) / 4; ++x) gtoff[x] = 0;
-            for (uint64_t x = W * count; x < pad16(W * count); ++x) gval[x] = 0;
-            }
-            st_relaxed(&P.rstart[I.chunk + 1], next | 1ull);
-            if (I.chunk + 1 == P.total_chunks) *P.out_bytes = next;
-        }
+        note_block(P, I.b, total, sparse);
+        count_blocks<W>(P, I, 1, total, rs);
     }
 }
 
-template <bool MASK_IN>
 __global__ void __launch_bounds__(kEncThreads, 6) encode_mask_kernel(const __grid_constant__ EncParams P) {
     extern __shared__ __align__(128) uint8_t tile[];
     __shared__ SmemA sm;
@@ -347,7 +352,7 @@ __global__ void __launch_bounds__(kEncThreads, 6) encode_mask_kernel(const __gri
         sm.I = I;
         mbar_init(&sm.bar, 1);
         sm.rs = I.chunk == 0 ? 1ull : 0ull;  // chunk 0 starts at 0; others: prefetched below
-        const uint32_t bulk = MASK_IN ? 0u : (I.nb * I.w) & ~15u;
+        const uint32_t bulk = (I.nb * I.w) & ~15u;
         if (bulk) {
             const EncSeg& S = P.seg[I.seg];
             const uint8_t* gref = S.ref + (I.chunk_off + I.p0) * I.w;
@@ -362,9 +367,205 @@ __global__ void __launch_bounds__(kEncThreads, 6) encode_mask_kernel(const __gri
     __syncthreads();
     if (tid == 0 && sm.I.chunk != 0) sm.rs = ld_relaxed(&P.rstart[sm.I.chunk]);  // value | 1 once published
     if (sm.I.w == 4)
-        mask_block<4, MASK_IN>(P, sm, tile, tid);
+        mask_block<4>(P, sm, tile, tid);
     else
-        mask_block<2, MASK_IN>(P, sm, tile, tid);
+        mask_block<2>(P, sm, tile, tid);
+}
+
+// ------------------------------------------------------------------ kernel A' -----------
+// Mask-input variant of kernel A (EncSeg::mask_in: the change mask comes precomputed, e.g. from
+// the fused Adam step, tc_adam_step_encode; `cur` is the only state: no ref, no compare, no ref
+// advance).  Without a tile to stage a block is a few hundred bytes of mask words, so one WARP
+// takes a block (persistent warps, each claiming tickets in order): lane l holds mask words
+// [l·K, l·K+K) of the block (K = 4 | 8, 16-byte loads), popcounts + one warp scan give the
+// offsets, a sparse block gathers its changed words from global cur into its spill slot (lane-
+// serial, or mask word by mask word when a lane holds many), and the rest — mask / tile_off
+// stores, index-mode staging, bookkeeping — is kernel A's, so kernels P and B are unchanged.
+// Returns the block's changed words; *rs_out = the chunk's record start.
+template <int W>
+__device__ __forceinline__ uint32_t maskin_block(const EncParams& P, const BlockInfo& I, unsigned long long rs,
+                                                 int lane, unsigned long long* rs_out) {
+    using word_t = typename Word<W>::T;
+    constexpr uint32_t B = Word<W>::kBlock;
+    constexpr uint32_t K = B / 32 / 32;  // mask words per lane (4 | 8)
+    const EncSeg& S = P.seg[I.seg];
+    const word_t* gcur = reinterpret_cast<const word_t*>(S.cur) + I.chunk_off + I.p0;
+    const uint32_t* gm = S.mask_in + ((I.chunk_off + I.p0) >> 5) + lane * K;
+    const uint32_t nmw = (I.nb + 31) / 32;
+    uint32_t mw[K];
+    // 16-byte loads where the chunk start keeps them aligned (chunk_words need only be a
+    // multiple of T >= 32, so a chunk's first mask word can sit at any 4-byte offset)
+    if ((lane + 1) * K <= nmw && ((I.chunk_off >> 5) & 3) == 0) {
+#pragma unroll
+        for (uint32_t v = 0; v < K / 4; ++v) {
+            const uint4 x = __ldg(reinterpret_cast<const uint4*>(gm) + v);
+            mw[4 * v] = x.x, mw[4 * v + 1] = x.y, mw[4 * v + 2] = x.z, mw[4 * v + 3] = x.w;
+        }
+    } else {
+#pragma unroll
+        for (uint32_t j = 0; j < K; ++j) mw[j] = lane * K + j < nmw ? __ldg(gm + j) : 0u;
+    }
+    uint32_t c = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < K; ++j) c += __popc(mw[j]);
+    uint32_t inc = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += t;
+    }
+    const uint32_t lpre = inc - c;  // changed words of the block before this lane's mask words
+    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+    const bool sparse = total * W <= kSpillBytes;
+    const bool imode = P.index_mode != 0;
+    const uint32_t tmask = P.T - 1;
+
+    if (sparse && total) {
+        const size_t slot_bytes = imode ? 2 * kSpillBytes : kSpillBytes;
+        word_t* slot = reinterpret_cast<word_t*>(P.spill + I.b * slot_bytes);
+        uint16_t* islot = reinterpret_cast<uint16_t*>(P.spill + I.b * slot_bytes + kSpillBytes);
+        const uint32_t maxc = __reduce_max_sync(0xffffffffu, c);
+        if (maxc <= 16u) {
+            // few per lane: each lane packs its own words, 4 gathers in flight before the stores
+            uint32_t rem[K];
+#pragma unroll
+            for (uint32_t j = 0; j < K; ++j) rem[j] = mw[j];
+            uint32_t k = lpre;
+            for (uint32_t r = 0; r < maxc; r += 4) {
+                word_t v[4];
+                uint32_t q[4];
+#pragma unroll
+                for (uint32_t u = 0; u < 4; ++u) {
+                    q[u] = 0xffffffffu;
+#pragma unroll
+                    for (uint32_t j = 0; j < K; ++j)
+                        if (q[u] == 0xffffffffu && rem[j]) {
+                            q[u] = (lane * K + j) * 32 + __ffs(rem[j]) - 1;
+                            rem[j] &= rem[j] - 1;
+                        }
+                    if (q[u] != 0xffffffffu) v[u] = ldg_cur(gcur + q[u]);
+                }
+#pragma unroll
+                for (uint32_t u = 0; u < 4; ++u)
+                    if (q[u] != 0xffffffffu) {
+                        slot[k] = v[u];
+                        if (imode) islot[k] = static_cast<uint16_t>((I.p0 + q[u]) & tmask);
+                        ++k;
+                    }
+            }
+        } else {
+            // mask word by mask word: lane l takes word l of it (coalesced gathers); the K mask
+            // words of a source lane are gathered with every load in flight before the stores
+            const uint32_t lt = (1u << lane) - 1u;
+            constexpr uint32_t kSrc = 1;  // source lanes per batch
+            for (uint32_t src = 0; src < 32; src += kSrc) {
+                word_t v[kSrc * K];
+                uint32_t d[kSrc * K];
+#pragma unroll
+                for (uint32_t h = 0; h < kSrc; ++h) {
+                    uint32_t o = __shfl_sync(0xffffffffu, lpre, src + h);
+#pragma unroll
+                    for (uint32_t j = 0; j < K; ++j) {
+                        const uint32_t bb = __shfl_sync(0xffffffffu, mw[j], src + h);
+                        d[h * K + j] = 0xffffffffu;
+                        if ((bb >> lane) & 1u) {
+                            const uint32_t q = ((src + h) * K + j) * 32 + lane;
+                            v[h * K + j] = ldg_cur(gcur + q);
+                            d[h * K + j] = o + __popc(bb & lt);
+                            if (imode) islot[d[h * K + j]] = static_cast<uint16_t>((I.p0 + q) & tmask);
+                        }
+                        o += __popc(bb);
+                    }
+                }
+#pragma unroll
+                for (uint32_t x = 0; x < kSrc * K; ++x)
+                    if (d[x] != 0xffffffffu) slot[d[x]] = v[x];
+            }
+        }
+    }
+    // index mode, dense block: its mask words go to the staging area (kernel B packs from them)
+    if (imode && !sparse) {
+        uint4* st = reinterpret_cast<uint4*>(P.mstage + I.b * kMaskStageWords + lane * K);
+#pragma unroll
+        for (uint32_t v = 0; v < K / 4; ++v) st[v] = make_uint4(mw[4 * v], mw[4 * v + 1], mw[4 * v + 2], mw[4 * v + 3]);
+    }
+    // record start of the chunk (prefetched by lane 0 at ticket time)
+    if (lane == 0 && !(rs & 1ull)) rs = wait_rstart(P, I.chunk) | 1ull;
+    rs = __shfl_sync(0xffffffffu, rs, 0) & ~1ull;
+
+    const uint64_t fixed = imode ? index_idx_off(I.m, P.T) : record_fixed_bytes(I.m, P.T);
+    if (rs + fixed > P.out_cap) {
+        if (lane == 0) tc_set_err(P.err, TC_ERR_CAPACITY);
+    } else {
+        uint8_t* rec = P.out + rs;
+        const uint64_t n_mask = cdiv(I.m, 32);
+        uint32_t* gmask = reinterpret_cast<uint32_t*>(rec + kHdrBytes) + (I.p0 >> 5) + lane * K;
+        uint32_t* gtoff = reinterpret_cast<uint32_t*>(rec + (imode ? index_toff_off() : kHdrBytes + pad16(4 * n_mask)));
+        const bool full = (lane + 1) * K <= nmw;
+        if (!imode && full) {
+#pragma unroll
+            for (uint32_t v = 0; v < K / 4; ++v)
+                reinterpret_cast<uint4*>(gmask)[v] = make_uint4(mw[4 * v], mw[4 * v + 1], mw[4 * v + 2], mw[4 * v + 3]);
+        }
+        uint32_t pre = lpre;
+#pragma unroll
+        for (uint32_t j = 0; j < K; ++j) {
+            const uint32_t p = I.p0 + (lane * K + j) * 32;
+            if (p < I.m) {
+                if (!imode && !full) gmask[j] = mw[j];
+                if ((p & tmask) == 0) gtoff[p / P.T] = pre;  // kernel B adds the block prefix
+            }
+            pre += __popc(mw[j]);
+        }
+    }
+    if (lane == 0) note_block(P, I.b, total, sparse);
+    *rs_out = rs;
+    return total;
+}
+
+// A warp claims kMaskinBatch consecutive blocks per ticket and counts each run of them that
+// lies in one chunk with one chunk atomic: the ticket and the chunk counter are the two
+// same-address atomics every block would otherwise return through (they serialised the kernel).
+// Deadlock-free as in kernel A: a run is counted before the warp moves to the next chunk, and a
+// block only ever waits for earlier chunks.
+constexpr uint32_t kMaskinBatch = 4;
+
+__device__ __noinline__ void count_run(const EncParams& P, const BlockInfo& R, uint32_t n, unsigned long long cnt,
+                                       unsigned long long rs) {
+    if (R.w == 4)
+        count_blocks<4>(P, R, n, cnt, rs);
+    else
+        count_blocks<2>(P, R, n, cnt, rs);
+}
+
+__global__ void __launch_bounds__(kEncThreads, 3) encode_maskin_kernel(const __grid_constant__ EncParams P) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        unsigned long long t = 0;
+        if (lane == 0) t = atomicAdd(P.ticket, 1ull);
+        const unsigned long long b0 = __shfl_sync(0xffffffffu, t, 0) * kMaskinBatch;
+        if (b0 >= P.total_blocks) return;
+        const unsigned long long b1 = b0 + kMaskinBatch < P.total_blocks ? b0 + kMaskinBatch : P.total_blocks;
+        BlockInfo R{};  // the pending run: blocks of chunk R.chunk not yet counted
+        uint32_t run_n = 0;
+        unsigned long long run_cnt = 0, run_rs = 0;
+        for (unsigned long long b = b0; b < b1; ++b) {
+            const BlockInfo I = decode_block(P, b);
+            if (run_n && I.chunk != R.chunk) {
+                if (lane == 0) count_run(P, R, run_n, run_cnt, run_rs);
+                run_n = 0;
+                run_cnt = 0;
+            }
+            unsigned long long rs = 0;
+            if (lane == 0) rs = I.chunk == 0 ? 1ull : ld_relaxed(&P.rstart[I.chunk]);  // value | 1 once published
+            const uint32_t total = I.w == 4 ? maskin_block<4>(P, I, rs, lane, &run_rs)
+                                            : maskin_block<2>(P, I, rs, lane, &run_rs);
+            R = I;
+            ++run_n;
+            run_cnt += total;
+        }
+        if (lane == 0) count_run(P, R, run_n, run_cnt, run_rs);
+    }
 }
 
 // ------------------------------------------------------------------ kernel P ------------
@@ -631,15 +832,25 @@ constexpr size_t kEncDynSmem = 2 * 16384 + 1024;  // ref | cur | mask words
 cudaError_t launch_encode(const EncParams& p, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(encode_mask_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaFuncSetAttribute(encode_mask_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(encode_mask_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr_set = true;
     }
     if (p.total_blocks == 0) return cudaSuccess;
-    if (p.seg[0].mask_in)
-        encode_mask_kernel<true><<<static_cast<unsigned>(p.total_blocks), kEncThreads, 0, s>>>(p);  // no tile to stage
-    else
-        encode_mask_kernel<false><<<static_cast<unsigned>(p.total_blocks), kEncThreads, kEncDynSmem, s>>>(p);
+    if (p.seg[0].mask_in) {
+        // persistent warps: as many CTAs as fit, never more than one warp per block
+        static int per_sm = 0;
+        if (!per_sm && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, encode_maskin_kernel, kEncThreads, 0) !=
+                           cudaSuccess)
+            return cudaGetLastError();
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const uint64_t want = (p.total_blocks + kWarps * kMaskinBatch - 1) / (kWarps * kMaskinBatch);
+        const uint64_t cap = static_cast<uint64_t>(sms) * (per_sm > 0 ? per_sm : 1);
+        encode_maskin_kernel<<<static_cast<unsigned>(want < cap ? want : cap), kEncThreads, 0, s>>>(p);
+    } else {
+        encode_mask_kernel<<<static_cast<unsigned>(p.total_blocks), kEncThreads, kEncDynSmem, s>>>(p);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     encode_prefix_kernel<<<1, 1024, 0, s>>>(p);

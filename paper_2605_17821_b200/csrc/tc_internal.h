@@ -56,7 +56,7 @@ struct EncSeg {
     uint32_t seg_id;        // segment_id written in the headers
     uint32_t pad_;
     uint64_t word_base;     // added to chunk offsets in the headers (range encodes)
-    const uint32_t* mask_in;  // precomputed change mask of the segment (MASK_IN encode), else nullptr
+    const uint32_t* mask_in;  // precomputed change mask of the segment (kernel A', encode_maskin_kernel), else nullptr
 };
 
 struct EncParams {

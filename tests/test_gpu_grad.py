@@ -173,7 +173,15 @@ def test_replay_corrupt_payload(ctx):
 
 @pytest.mark.parametrize("index_mode", [False, True])
 @pytest.mark.parametrize("n,T,C,zero_frac", [(1, 4096, 1 << 28, 0.0), (1000, 4096, 1 << 28, 0.5),
-                                             (70_001, 256, 8192, 0.9), (300_000, 4096, 1 << 28, 0.99)])
+                                             (70_001, 256, 8192, 0.9), (300_000, 4096, 1 << 28, 0.99),
+                                             # ~20 % changed in the moment segments' second half: sparse
+                                             # blocks with many changes per lane (the word-by-word gather)
+                                             (200_000, 4096, 1 << 28, 0.8),
+                                             # chunks of 96 words: a chunk's mask words start at any
+                                             # 4-byte offset (no 16-byte mask loads there)
+                                             (50_003, 32, 96, 0.9),
+                                             # many chunks: record starts chained across the warps
+                                             (3_000_000, 4096, 1 << 20, 0.99)])
 def test_adam_step_encode_matches_oracle(ctx, tco_lossless, n, T, C, zero_frac, index_mode):
     """NEXT row 2: the fused Adam step + lossless diff == oracle adam_step, then oracle encode of
     (state before -> state after), byte for byte; the state equals the oracle's."""
