@@ -654,13 +654,14 @@ struct ReplayParams {
     unsigned* err;
 };
 
-// one CTA of 1024 threads per tile of kGB elements, 4 per thread: (master, m, v) stay in
-// registers for all fused steps (full occupancy; the IEEE-rounded divisions and square root of
-// every step make this kernel issue-bound, so latency hiding matters more than per-thread work)
-constexpr uint32_t kRThreads = 1024;
+// one CTA of 512 threads per tile of kGB elements, 8 per thread, two CTAs per SM: (master, m, v)
+// stay in registers for all fused steps.  Each tile passes several CTA barriers (entry staging,
+// dense gradient tiles); with one CTA of 1024 threads per SM every barrier idled the whole SM
+// (ncu: a third of the stall samples), with two the other CTA computes through it.
+constexpr uint32_t kRThreads = 512;
 constexpr uint32_t kRPer = kGB / kRThreads;
 constexpr uint32_t kRStage = 2048;  // staged sparse entries of one tile (all fused steps)
-constexpr uint32_t kRGroup = 8;     // fused steps whose dense gradient tiles share two barriers
+constexpr uint32_t kRGroup = 2;     // fused steps whose dense gradient tiles share two barriers
 constexpr size_t kRDynSmem = sizeof(float) * (kRGroup + 3) * kGB;
 
 struct ReplayStep {                 // per fused step, in shared memory
@@ -673,7 +674,7 @@ struct ReplayStep {                 // per fused step, in shared memory
     uint32_t variant;
 };
 
-__global__ void __launch_bounds__(kRThreads) adam_replay_kernel(const __grid_constant__ ReplayParams P) {
+__global__ void __launch_bounds__(kRThreads, 2) adam_replay_kernel(const __grid_constant__ ReplayParams P) {
     extern __shared__ float s_gd[];  // [kRGroup][kGB] dense gradient tiles | [3][kGB] next tile's state
     float* s_next = s_gd + kRGroup * kGB;
     __shared__ uint64_t s_bar;
