@@ -282,7 +282,11 @@ def run_ours(args):
     n_ops = {"encode": [], "fold": [], "stage": [], "replicate": []}
     host_t = {"stage": [], "fold": []}
 
-    def step(k, timed):
+    # The host runs one step ahead of the device: step k issues encode(k), then finishes step
+    # k-1 (reads its record length — encode(k-1) is done by then or about to be —, stages it,
+    # folds it, replicates it).  The device queue never waits for the host's length round trip;
+    # the format choice for encode(k) therefore comes from record k-2 (one step of lag).
+    def issue(k, timed):
         slot = k % 2
         cur = Y if state["content"] == "X" else X
         v = state["ref_version"] + 1
@@ -301,13 +305,19 @@ def run_ours(args):
         tc.diff_encode(ctx, A, cur, recs[slot], obytes[slot], v, v - 1, T, C, True, stream=s_comp,
                        index_mode=use_index)
         e1.record(s_comp)
+        state["ref_version"] = v
+        state["content"] = "Y" if state["content"] == "X" else "X"
+        return {"slot": slot, "v": v, "e0": e0, "e1": e1, "use_index": use_index, "timed": timed}
+
+    def finish(p):
+        slot, v, e0, e1, timed = p["slot"], p["v"], p["e0"], p["e1"], p["timed"]
         e1.synchronize()
         nbytes = int(ob_view[slot].item())
         if nbytes > min(rec_cap, host_cap):
             raise RuntimeError("record exceeds the staging buffers")
-        state["index"] = next_mode(nbytes, use_index)
+        state["index"] = next_mode(nbytes, p["use_index"])
         if timed:
-            state["modes"].append("index" if use_index else "mask")
+            state["modes"].append("index" if p["use_index"] else "mask")
         # Tier-1: D2H into the pinned ring on the copy stream
         s_copy.wait_event(e1)
         c0, c1 = ev(), ev()
@@ -347,14 +357,26 @@ def run_ours(args):
             r1.record(s_comm)
             fut = _Done((r0, r1, nbytes))
         state["rest_version"] = v
-        state["ref_version"] = v
-        state["content"] = "Y" if state["content"] == "X" else "X"
         done_ev[slot] = ([c1], fut, timed)
         if timed:
             n_ops["encode"].append((e0, e1))
             n_ops["fold"].append((f0, f1))
             n_ops["stage"].append((c0, c1))
         return nbytes
+
+    pending = [None]
+
+    def step(k, timed):
+        """Issue step k and finish step k-1; returns step k-1's record bytes (None for the first)."""
+        p = issue(k, timed)
+        out = finish(pending[0]) if pending[0] is not None else None
+        pending[0] = p
+        return out
+
+    def flush():
+        out = finish(pending[0]) if pending[0] is not None else None
+        pending[0] = None
+        return out
 
     def sync_all():
         for s in (s_comp, s_copy, s_comm):
@@ -370,6 +392,7 @@ def run_ours(args):
 
     for k in range(args.warmup):
         step(k, False)
+    flush()
     drain()
     sync_all()
     ctx.check(s_comp)
@@ -384,7 +407,10 @@ def run_ours(args):
     t_start.record(s_comp)
     sizes_seen = []
     for k in range(args.warmup, args.warmup + args.steps):
-        sizes_seen.append(step(k, True))
+        nb = step(k, True)
+        if nb is not None:
+            sizes_seen.append(nb)
+    sizes_seen.append(flush())
     drain()
     for s in (s_copy, s_comm):
         e = torch.cuda.Event()

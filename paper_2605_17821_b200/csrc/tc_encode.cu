@@ -830,10 +830,12 @@ __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __gri
 constexpr size_t kEncDynSmem = 2 * 16384 + 1024;  // ref | cur | mask words
 
 cudaError_t launch_encode(const EncParams& p, cudaStream_t s) {
-    static bool attr_set = false;
-    if (!attr_set) {
+    static bool attr_set[TC_MAX_DEVICES] = {};  // a function attribute is per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= TC_MAX_DEVICES || !attr_set[dev]) {
         cudaFuncSetAttribute(encode_mask_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        attr_set = true;
+        if (dev >= 0 && dev < TC_MAX_DEVICES) attr_set[dev] = true;
     }
     if (p.total_blocks == 0) return cudaSuccess;
     if (p.seg[0].mask_in) {
@@ -842,8 +844,7 @@ cudaError_t launch_encode(const EncParams& p, cudaStream_t s) {
         if (!per_sm && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, encode_maskin_kernel, kEncThreads, 0) !=
                            cudaSuccess)
             return cudaGetLastError();
-        int dev = 0, sms = 0;
-        cudaGetDevice(&dev);
+        int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const uint64_t want = (p.total_blocks + kWarps * kMaskinBatch - 1) / (kWarps * kMaskinBatch);
         const uint64_t cap = static_cast<uint64_t>(sms) * (per_sm > 0 ? per_sm : 1);

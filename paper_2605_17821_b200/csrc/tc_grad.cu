@@ -1053,11 +1053,12 @@ tc_status tc_adam_replay(tc_ctx* ctx, const tc_adam_state* stt, const void* cons
         for (int j = 0; j < nf; ++j) bias(hp, first_step + j, &R.ss[j], &R.ic[j]);
         R.pay = P;
         R.err = tc::ctx_err(ctx);
-        static bool attr = false;
-        if (!attr) {
+        static bool attr[tc::TC_MAX_DEVICES] = {};  // a function attribute is per device
+        const int dev = tc::ctx_device(ctx);
+        if (dev < 0 || dev >= tc::TC_MAX_DEVICES || !attr[dev]) {
             cudaFuncSetAttribute(adam_replay_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(kRDynSmem));
-            attr = true;
+            if (dev >= 0 && dev < tc::TC_MAX_DEVICES) attr[dev] = true;
         }
         adam_replay_kernel<<<grid_for(ctx, R.tiles * kRThreads, kRThreads), kRThreads, kRDynSmem, s>>>(R);
         cudaError_t e = cudaGetLastError();

@@ -15,6 +15,7 @@ constexpr uint32_t kHdrBytes = 64;
 constexpr uint64_t kMaxChunkWords = 2147483647ull;  // 2^31-1 (PAPER.md:203 chunk + rebase)
 
 // Encode block ("scan unit") sizes: one CTA stages ref+cur of one block in 32 KB of smem.
+constexpr int TC_MAX_DEVICES = 64;          // per-device caches (function attributes)
 constexpr uint32_t kEncThreads = 256;
 constexpr uint32_t kEncBlockWords4 = 4096;  // 4-byte words
 constexpr uint32_t kEncBlockWords2 = 8192;  // 2-byte words
