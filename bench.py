@@ -282,7 +282,7 @@ def run_ours(args):
     n_ops = {"encode": [], "fold": [], "stage": [], "replicate": []}
     host_t = {"stage": [], "fold": []}
 
-    # The host runs one step ahead of the device: step k issues encode(k), then finishes step
+    # At N = 1 the host runs one step ahead of the device: step k issues encode(k), then finishes step
     # k-1 (reads its record length — encode(k-1) is done by then or about to be —, stages it,
     # folds it, replicates it).  The device queue never waits for the host's length round trip;
     # the format choice for encode(k) therefore comes from record k-2 (one step of lag).
@@ -365,10 +365,17 @@ def run_ours(args):
         return nbytes
 
     pending = [None]
+    # With a ring neighbour the record slot written by encode(k) is the one Tier-2 still reads for
+    # record k-2; running one step ahead would make encode(k) wait for that push (measured at N = 2:
+    # 5.65 -> 6.14 ms per step), so at N > 1 each step finishes before the next is issued.
+    ahead = world == 1
 
     def step(k, timed):
-        """Issue step k and finish step k-1; returns step k-1's record bytes (None for the first)."""
+        """Issue step k and finish step k-1 (N = 1) or k itself (N > 1); returns the finished
+        step's record bytes (None when nothing finished)."""
         p = issue(k, timed)
+        if not ahead:
+            return finish(p)
         out = finish(pending[0]) if pending[0] is not None else None
         pending[0] = p
         return out
@@ -410,7 +417,9 @@ def run_ours(args):
         nb = step(k, True)
         if nb is not None:
             sizes_seen.append(nb)
-    sizes_seen.append(flush())
+    nb = flush()
+    if nb is not None:
+        sizes_seen.append(nb)
     drain()
     for s in (s_copy, s_comm):
         e = torch.cuda.Event()
