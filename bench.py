@@ -200,9 +200,14 @@ def run_ours(args):
     s_comp = torch.cuda.Stream(device=dev)
     s_copy = torch.cuda.Stream(device=dev, priority=0)
     s_comm = torch.cuda.Stream(device=dev, priority=-1)  # NCCL CTAs get SM slots ahead of the encode
+    # --overlap-fold: the latency-bound fold of record k-1 on its own high-priority stream, beside
+    # the HBM-bound encode of record k (N = 1, one step ahead only)
+    s_fold = torch.cuda.Stream(device=dev, priority=-1) if args.overlap_fold else s_comp
     ctx = tc.Ctx(local)
+    ctx_f = tc.Ctx(local) if s_fold is not s_comp else ctx  # a tc_ctx serves one stream at a time
     if args.fold_dense_permille is not None:
         ctx.set_fold_dense_permille(args.fold_dense_permille)
+        ctx_f.set_fold_dense_permille(args.fold_dense_permille)
     comm = tc.Comm(rank, world, local) if world > 1 else None
     rep_pool = None
     if comm is not None:
@@ -341,9 +346,11 @@ def run_ours(args):
         # restore: fold the record onto the replica
         f0, f1 = ev(), ev()
         th0 = time.perf_counter()
-        f0.record(s_comp)
-        tc.diff_apply(ctx, R, state["rest_version"], [recs[slot]], [nbytes], stream=s_comp)
-        f1.record(s_comp)
+        if s_fold is not s_comp:
+            s_fold.wait_event(e1)
+        f0.record(s_fold)
+        tc.diff_apply(ctx_f, R, state["rest_version"], [recs[slot]], [nbytes], stream=s_fold)
+        f1.record(s_fold)
         host_t["fold"].append(time.perf_counter() - th0)
         if push is not None:
             # Tier-2 push: kernels only (no host synchronization, no helper thread), started after
@@ -357,7 +364,7 @@ def run_ours(args):
             r1.record(s_comm)
             fut = _Done((r0, r1, nbytes))
         state["rest_version"] = v
-        done_ev[slot] = ([c1], fut, timed)
+        done_ev[slot] = ([c1, f1] if s_fold is not s_comp else [c1], fut, timed)
         if timed:
             n_ops["encode"].append((e0, e1))
             n_ops["fold"].append((f0, f1))
@@ -386,7 +393,7 @@ def run_ours(args):
         return out
 
     def sync_all():
-        for s in (s_comp, s_copy, s_comm):
+        for s in (s_comp, s_copy, s_comm, s_fold):
             s.synchronize()
 
     def drain():
@@ -403,13 +410,14 @@ def run_ours(args):
     drain()
     sync_all()
     ctx.check(s_comp)
+    ctx_f.check(s_fold)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = Clocks(local)
     clocks.start()
     time.sleep(0.3)
-    launches0 = ctx.launches + (push["ctx"].launches if push else 0)
+    launches0 = ctx.launches + (push["ctx"].launches if push else 0) + (ctx_f.launches if ctx_f is not ctx else 0)
     t_start, t_end = ev(), ev()
     t_start.record(s_comp)
     sizes_seen = []
@@ -421,18 +429,20 @@ def run_ours(args):
     if nb is not None:
         sizes_seen.append(nb)
     drain()
-    for s in (s_copy, s_comm):
+    for s in (s_copy, s_comm, s_fold):
         e = torch.cuda.Event()
         e.record(s)
         s_comp.wait_event(e)
     t_end.record(s_comp)
     sync_all()
     torch.cuda.synchronize()
-    launches = ctx.launches + (push["ctx"].launches if push else 0) - launches0
+    launches = (ctx.launches + (push["ctx"].launches if push else 0) + (ctx_f.launches if ctx_f is not ctx else 0) -
+                launches0)
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
     ctx.check(s_comp)
+    ctx_f.check(s_fold)
     if push:
         push["ctx"].check(s_comm)
     ms = t_start.elapsed_time(t_end)
@@ -1371,6 +1381,8 @@ def main():
     ap.add_argument("--tile-words", type=int, default=4096)
     ap.add_argument("--chunk-words", type=int, default=1 << 28)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--overlap-fold", type=int, default=0,
+                    help="N = 1: fold record k-1 on a high-priority stream beside encode k")
     ap.add_argument("--timeline", action="store_true")
     ap.add_argument("--format", default="adaptive", choices=["mask", "index", "adaptive"],
                     help="record format: mask, index (u16 positions), or adaptive per step from density")
