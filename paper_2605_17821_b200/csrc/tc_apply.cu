@@ -908,8 +908,8 @@ __global__ void __launch_bounds__(kDenseThreads, kDenseBlocksPerSM) fold_dense_k
 // partial-sector writes).  Running counts carry from unit to unit within a run of consecutive
 // units, and the next tile's end entries are loaded one unit ahead.
 constexpr uint32_t kListThreads = 128;
-constexpr uint32_t kListBlocksPerSM = 8;
-constexpr uint32_t kListStage = 8192;
+constexpr uint32_t kListBlocksPerSM = 10;
+constexpr uint32_t kListStage = 4096;
 
 struct ListSmem {
     uint4 tile[kListT * 4 / 16];     // the unit's state (16 KB for fp32)
