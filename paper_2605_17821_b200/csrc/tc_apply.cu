@@ -158,11 +158,11 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
                 // streaming the whole chunk through shared memory beats scattered writes
                 uint64_t sum = 0;
                 for (int k = 0; k < P.nrec; ++k) sum += P.desc[static_cast<size_t>(k) * P.cap + r].count;
-                // strategy (measured): chains of index-mode records at T = 4096 are
+                // strategy (measured): chains of <= kListMaxRec index-mode records at T = 4096 are
                 // streamed by the list kernel when they are long (N >= 4, >= 0.5 % of the words in
                 // total) or dense (> dense_permille); everything else is scattered.  0 = stream
                 // every chunk (mask-mode chunks through fold_dense_kernel), UINT32_MAX = scatter all.
-                bool all_idx = a.T == kListT;
+                bool all_idx = a.T == kListT && P.nrec <= static_cast<int>(kListMaxRec);
                 for (int k = 0; k < P.nrec && all_idx; ++k) all_idx = P.desc[static_cast<size_t>(k) * P.cap + r].idx != nullptr;
                 const uint64_t mm = a.m;
                 if (P.dense_permille == 0u) {
@@ -914,16 +914,16 @@ constexpr uint32_t kListStage = 4096;
 struct ListSmem {
     uint4 tile[kListT * 4 / 16];     // the unit's state (16 KB for fp32)
     uint4 stage[kListStage / 16];    // position / value runs of a round
-    const uint8_t* pos[TC_MAX_FOLD];
-    const uint8_t* val[TC_MAX_FOLD];
-    const uint32_t* toff[TC_MAX_FOLD];
-    uint32_t count[TC_MAX_FOLD];
-    uint32_t carry[TC_MAX_FOLD];     // first entry of the tile, per record
-    uint32_t tend[TC_MAX_FOLD];      // end entry of the tile, per record
-    uint32_t touched[kListT / 32];   // per 32-word line: written
-    uint32_t pb[TC_MAX_FOLD];        // per record: position-run bytes, total run bytes, stage offset
-    uint32_t sz[TC_MAX_FOLD];
-    uint32_t soff[TC_MAX_FOLD];
+    const uint8_t* pos[kListMaxRec];
+    const uint8_t* val[kListMaxRec];
+    const uint32_t* toff[kListMaxRec];
+    uint32_t count[kListMaxRec];
+    uint32_t carry[kListMaxRec];     // first entry of the tile, per record
+    uint32_t tend[kListMaxRec];      // end entry of the tile, per record
+    uint8_t touched[kListT / 32];    // per 32-word line: written
+    uint32_t pb[kListMaxRec];        // per record: position-run bytes, total run bytes, stage offset
+    uint32_t sz[kListMaxRec];
+    uint32_t soff[kListMaxRec];
     uint32_t fits;                   // every record's runs fit the stage at once
     uint64_t bar;
 };
@@ -991,7 +991,7 @@ __device__ __forceinline__ void list_unit(ListSmem& S, uint4* tile, uint64_t* ba
                     continue;
                 }
                 tw[x] = pv[k];
-                S.touched[x >> 5] = 1u;
+                S.touched[x >> 5] = 1;
             }
             __syncthreads();  // this record's writes before the next (newer) record's
         }
@@ -1033,7 +1033,7 @@ __device__ __forceinline__ void list_unit(ListSmem& S, uint4* tile, uint64_t* ba
                             continue;
                         }
                         tw[x] = pv[k];
-                        S.touched[x >> 5] = 1u;
+                        S.touched[x >> 5] = 1;
                     }
                     if (bb > aa) lastx = px[bb - aa - 1];
                     __syncthreads();  // this record's writes before the next (newer) record's
@@ -1142,7 +1142,7 @@ __global__ void __launch_bounds__(kListThreads, kListBlocksPerSM) fold_list_kern
             for (uint32_t i = bulk; i < bytes; ++i) reinterpret_cast<uint8_t*>(S.tile)[i] = st[i];
         }
         const bool next = u + 1 < u1 && u + 1 < P.unit_first[lo + 1];
-        if (tid < kListT / 32) S.touched[tid] = 0u;
+        if (tid < kListT / 32) S.touched[tid] = 0;
         __syncthreads();  // the record table is in place
         if (tid < N) {  // this tile's entry range per record; the next tile's end, one unit ahead
             if (te_valid) {

@@ -22,6 +22,7 @@ constexpr uint32_t kEncBlockWords2 = 8192;  // 2-byte words
 // Fold: one warp per unit of max(T, kFoldWords) words.
 constexpr uint32_t kFoldThreads = 256;
 constexpr uint32_t kFoldWords = 4096;  // minimum fold unit (one warp: 128 mask words)
+constexpr uint32_t kListMaxRec = 32;    // longest chain fold_list_kernel takes (its per-record tables)
 constexpr uint32_t kListT = 4096;      // tile size of the chains fold_list_kernel takes (one tile = one unit)
 
 __host__ __device__ inline uint64_t pad16(uint64_t x) { return (x + 15) & ~uint64_t(15); }

@@ -472,3 +472,20 @@ def test_index_mode_range_encode(ctx, tco):
             ctx.check()
             parts.append(out[: int(ob.item())].cpu().numpy())
     assert np.array_equal(np.concatenate(parts), full)
+
+
+@pytest.mark.parametrize("N", [32, 33])
+def test_index_list_fold_chain_length_limit(fctx, tco, N):
+    """All-index T = 4096 chains at the list kernel's record-table limit (kListMaxRec = 32) and one
+    past it (such chunks go to the other fold paths): both restore the chain head."""
+    sizes, wb, T = [20000, 9001], [4, 2], 4096
+    states = [synth.state(sizes, wb, 43, v, 0.02) for v in range(N + 1)]
+    ref = [a.copy() for a in states[0]]
+    diffs = []
+    for v in range(1, N + 1):
+        rc, d = tco.encode(ref, states[v], tile_words=T, version=v, ref_version=v - 1, index_mode=True)
+        assert rc == 0
+        diffs.append(d)
+    rc, st_g = gpu_fold(fctx, states[0], 0, diffs)
+    assert rc == tc.OK
+    assert all(np.array_equal(a, b) for a, b in zip(st_g, states[N]))
