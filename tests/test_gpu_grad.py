@@ -172,7 +172,7 @@ def test_replay_corrupt_payload(ctx):
 
 
 @pytest.mark.parametrize("index_mode", [False, True])
-@pytest.mark.parametrize("n,T,C,zero_frac", [(1, 4096, 1 << 28, 0.0), (1000, 4096, 1 << 28, 0.5),
+@pytest.mark.parametrize("n,T,C,zero_frac", [(0, 4096, 1 << 28, 0.0), (1, 4096, 1 << 28, 0.0), (1000, 4096, 1 << 28, 0.5),
                                              (70_001, 256, 8192, 0.9), (300_000, 4096, 1 << 28, 0.99),
                                              # ~20 % changed in the moment segments' second half: sparse
                                              # blocks with many changes per lane (the word-by-word gather)
