@@ -17,7 +17,8 @@
 //                              first winner masks, popcount warp scans for the value offsets,
 //                              scatter of the winning words (a sparse single index record
 //                              straight from its entry ranges); tile_off checked on the way.
-//   fold_list_kernel  (a CTA per 4096-word tile) streaming fold of all-index T = 4096 chains:
+//   fold_list_kernel  (a CTA per 4096-word tile, 10 per SM) streaming fold of all-index T = 4096
+//                              chains of <= 32 records:
 //                              tile in shared memory, records' runs staged, oldest -> newest.
 //   fold_dense_kernel (one warp per CTA) streaming fold of any other chain (opt-in).
 #include <cuda_runtime.h>
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
 // warp scans give every mask word's in-chunk value offset, winners = mask & rem (rem = words
 // no newer record covers), and the winners are scattered: for each lane whose mask word has
 // winners, the warp broadcasts (win, mask, offset) and lane b copies word 32*src+b.  No
-// barriers and no shared-memory staging; latency is hidden by 64 resident warps per SM.
+// barriers and no shared-memory staging; latency is hidden by 32 resident warps per SM (4 CTAs of 8).
 constexpr uint32_t kFoldWarps = kFoldThreads / 32;
 constexpr uint32_t kSubGroups = 4;
 constexpr uint32_t kSub = kSubGroups * 1024;
