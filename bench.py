@@ -476,7 +476,8 @@ def run_ours(args):
     changed = sum(r[4] for r in recs_info)
 
     scatter_ref = None
-    if world == 1:  # writes Y's values at the X/Y differences into R (R == Y after), then puts R back
+    # (sparse steps only: at high f the position lists alone outgrow the memory the step leaves)
+    if world == 1 and args.f <= 0.05:  # writes Y's values at the X/Y differences into R, then puts R back
         scatter_ref = scatter_reference(X, Y, R, s_comp)
         if state["content"] == "X":
             with torch.cuda.stream(s_comp):
