@@ -474,6 +474,22 @@ def run_ours(args):
     peak, peak_src = peaks()
     rec_bytes = sizes_seen[-1]
     changed = sum(r[4] for r in recs_info)
+    # Tier-1 denominator, measured live after the timed region: a plain cudaMemcpyAsync (torch) of
+    # the same record into the same pinned ring slot, all ranks at once as in the step; best of 3
+    pcie = None
+    if rec_bytes:
+        hv = host_ring[0].view(torch.uint8)[:rec_bytes]
+        best = None
+        for _ in range(3):
+            p0, p1 = ev(), ev()
+            p0.record(s_copy)
+            with torch.cuda.stream(s_copy):
+                hv.copy_(recs[0][:rec_bytes], non_blocking=True)
+            p1.record(s_copy)
+            s_copy.synchronize()
+            t_ = p0.elapsed_time(p1)
+            best = t_ if best is None else min(best, t_)
+        pcie = rec_bytes / best / 1e6
 
     scatter_ref = None
     # (sparse steps only: at high f the position lists alone outgrow the memory the step leaves)
@@ -574,7 +590,11 @@ def run_ours(args):
                          "traffic": traffic.get("fold"),
                          "dram_gbs": round(traffic["fold"] / fold_ms / 1e6, 1) if traffic.get("fold") else None,
                          "scatter_reference": scatter_ref},
-                "stage_d2h": {"ms": round(stage_ms, 4), "gbs": round(rec_bytes / stage_ms / 1e6, 2)},
+                "stage_d2h": {"ms": round(stage_ms, 4), "gbs": round(rec_bytes / stage_ms / 1e6, 2),
+                              "pcie_copy_gbs": round(pcie, 2) if pcie else None,
+                              "frac_pcie": round(rec_bytes / stage_ms / 1e6 / pcie, 4) if pcie else None,
+                              "pcie_note": "denominator: a plain D2H cudaMemcpyAsync of the same record into "
+                                           "the same pinned slot, measured after the timed region"},
                 "replicate_in_step": None if rep_ms is None else {
                     "ms": round(rep_ms, 4), "gbs_per_direction": round(rec_bytes / rep_ms / 1e6, 1),
                     "note": "inside the pipelined step: shares HBM with encode/fold, PCIe with the "
