@@ -55,6 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     common = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", inc,
                      "-I", os.path.join(ROOT, "include")]
+    common += os.environ.get("TC_NVCC_DEFS", "").split()  # experiments only, e.g. -DTC_DENSE_RUN=8
     if verbose:
         common += ["-Xptxas", "-v"]
     procs = []

@@ -492,7 +492,10 @@ constexpr uint32_t kDenseThreads = 32;
 constexpr uint32_t kDSub = 4096;
 constexpr uint32_t kMW = kDSub / 1024;  // mask words per lane
 constexpr uint32_t kDenseBlocksPerSM = 9;
-constexpr uint64_t kDenseRun = 16;  // consecutive units per CTA visit (running counts carry over)
+#ifndef TC_DENSE_RUN
+#define TC_DENSE_RUN 16
+#endif
+constexpr uint64_t kDenseRun = TC_DENSE_RUN;  // consecutive units per CTA visit (running counts carry over)
 constexpr int kDBatch = 8;
 constexpr uint32_t kWin = 512;
 static_assert(kFoldWords % kDSub == 0, "fold units are whole dense sub-units");
