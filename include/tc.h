@@ -230,7 +230,8 @@ tc_status tc_ipc_close(void* dev_ptr);
  * peer slot `peer_dst` (capacity peer_cap) with NVLink stores from every SM, then publish
  * {bytes, version} to `peer_mailbox` with a system-scope release.  A record larger than
  * peer_cap is not copied; the mailbox then carries bytes = UINT64_MAX (the receiver's
- * tc_peer_wait reports TC_ERR_CAPACITY).  version >= 1.  Stream-ordered on `stream`; the
+ * tc_peer_wait reports TC_ERR_CAPACITY).  Any length: the last bytes % 16 are copied byte by
+ * byte (src and peer_dst themselves must be 16-byte aligned).  version >= 1.  Stream-ordered on `stream`; the
  * caller orders reuse of a slot (e.g. one slot per in-flight version). */
 tc_status tc_push_peer(tc_ctx* ctx, const void* src, const uint64_t* src_bytes, void* peer_dst,
                        uint64_t peer_cap, void* peer_mailbox, uint64_t version, tc_stream stream);

@@ -251,13 +251,18 @@ class BaseReplicator:
     into a flat device payload (§3.2 "in-memory byte payloads", no write-then-read)
     and stages it to Tier-1 (pinned host); `pump` (once per training iteration) pushes the next
     paced chunk into the ring neighbour's staging buffer with NVLink stores (tc_push_peer); the
-    replica becomes visible (its commit mailbox carries the version) only when every byte has
-    arrived — all-or-nothing; `flush` sends the remainder at once (the sync flush on
-    spillover).  Collective at construction (IPC handle exchange); one per rank."""
+    replica becomes visible only when every byte has arrived — all-or-nothing (SPEC.md:291);
+    `flush` sends the remainder at once (the sync flush on spillover).
+
+    The receiver keeps TWO staging slots, sized by the previous rank's shard (the rank it receives
+    from).  Successive bases alternate slots, and the commit mailbox names the slot:
+    {bytes, 2·version + slot}.  While base k+1 streams into one slot, the commit still points at
+    base k in the other, so a recovering rank never reads a torn replica.  The sender checks on
+    the host that its payload fits the neighbour's slot before it pushes anything.
+    Collective at construction (IPC handle exchange over torch.distributed); one per rank.  With
+    world == 1 the ring of one is this GPU itself: no handle exchange, local slots."""
 
     def __init__(self, shard_bytes: int, rank: int, world: int, device: int, stream=None):
-        import torch.distributed as dist
-
         from . import tc
 
         self.tc = tc
@@ -267,59 +272,79 @@ class BaseReplicator:
         self.s = stream or torch.cuda.Stream(self.dev)
         self.ctx = tc.Ctx(device)
         self.ctx.set_push_ctas(16)
-        self.payload = torch.empty(max(16, (self.n + 15) // 16 * 16), dtype=torch.uint8, device=self.dev)
+        self.payload = torch.empty(_pad16(self.n), dtype=torch.uint8, device=self.dev)
         self.host = tc.HostBuffer(max(1, self.n))
-        # this GPU receives the previous rank's base here; progress mailbox per chunk, commit mailbox
-        self.stage = tc.IpcBuffer(max(16, (self.n + 15) // 16 * 16))
+        if world > 1:
+            import torch.distributed as dist
+
+            sizes = [None] * world
+            dist.all_gather_object(sizes, self.n)
+        else:
+            sizes = [self.n]
+        nxt, prv = ring_peers(rank, world)
+        self.prev_n, self.peer_n = int(sizes[prv]), int(sizes[nxt])
+        # this GPU receives the previous rank's bases here (two slots), plus the mailboxes
+        self.stage = [tc.IpcBuffer(_pad16(self.prev_n)) for _ in range(2)]
         self.progress = tc.IpcBuffer(16)
         self.commit = tc.IpcBuffer(16)
-        hs = [None] * world
-        dist.all_gather_object(hs, [self.stage.handle, self.progress.handle, self.commit.handle, self.n])
-        nx = hs[(rank + 1) % world]
-        self.peer_n = int(nx[3])
-        self.peer_stage = tc.PeerMapping(nx[0], self.peer_n)
-        self.peer_progress = tc.PeerMapping(nx[1], 16)
-        self.peer_commit = tc.PeerMapping(nx[2], 16)
+        if world > 1:
+            hs = [None] * world
+            dist.all_gather_object(hs, [b.handle for b in self.stage] + [self.progress.handle, self.commit.handle])
+            nx = hs[nxt]
+            self._maps = [tc.PeerMapping(nx[0], _pad16(self.peer_n)), tc.PeerMapping(nx[1], _pad16(self.peer_n)),
+                          tc.PeerMapping(nx[2], 16), tc.PeerMapping(nx[3], 16)]
+            self.peer_stage, self.peer_progress, self.peer_commit = self._maps[:2], self._maps[2], self._maps[3]
+        else:  # the ring of one: the neighbour is this GPU
+            self._maps = []
+            self.peer_stage, self.peer_progress, self.peer_commit = self.stage, self.progress, self.commit
         self.len_dev = torch.zeros(1, dtype=torch.int64, device=self.dev)
         self.zero_dev = torch.zeros(1, dtype=torch.int64, device=self.dev)
         self.plan = None
         self.sent = 0
         self.version = 0
+        self.slot = 1      # the slot of the base in flight (the first base goes to slot 0)
         self.seq = 0
         self.log = []   # (iteration, kind, bytes): chunk | sync_flush | commit
 
     def intercept(self, segments, version: int, interval: int, margin: int | None = None, cap: int = 256 * MiB):
         """Serialize the shard (device segments, in order) once, stage it to Tier-1, plan the pacing."""
         if self.plan is not None and self.sent < self.plan.total_bytes:
-            self.flush(version)  # the previous base must be complete before it is overwritten
+            self.flush(version)  # the previous base must be complete before the next one starts
+        if int(version) < 1:
+            raise ValueError("base versions are >= 1")
+        o = sum(t.numel() * t.element_size() for t in segments)
+        if o != self.n:
+            raise ValueError(f"shard is {o} bytes, replicator built for {self.n}")
+        if self.n > self.peer_n:  # the neighbour sized its slots for the shard it expects from us
+            raise ValueError(f"shard of {self.n} bytes does not fit the neighbour's {self.peer_n}-byte slot")
         with torch.cuda.stream(self.s):
             o = 0
             for t in segments:
                 b = t.contiguous().view(torch.uint8).reshape(-1)
                 self.payload[o:o + b.numel()].copy_(b)
                 o += b.numel()
-        if o != self.n:
-            raise ValueError(f"shard is {o} bytes, replicator built for {self.n}")
         self.tc.stage_host(self.host, self.payload, self.n, self.tc.D2H, stream=self.s)
         self.plan = plan_chunks(self.n, interval, margin, cap)
         self.sent, self.version = 0, int(version)
+        self.slot ^= 1  # the other slot: the committed base stays intact until this one commits
         return self.plan
 
     def _push(self, nbytes: int):
-        # 16-byte aligned cover of [sent, sent + nbytes) (payload and stage are padded to 16 bytes;
+        # 16-byte aligned cover of [sent, sent + nbytes) (payload and slots are padded to 16 bytes;
         # an overlap re-sends bytes the peer already holds, with the same values)
         a0 = self.sent & ~15
-        end = min((self.n + 15) // 16 * 16, (self.sent + nbytes + 15) // 16 * 16)
+        end = min(_pad16(self.n), (self.sent + nbytes + 15) // 16 * 16)
         self.len_dev.fill_(end - a0)
         self.seq += 1
-        self.tc.push_peer(self.ctx, self.payload[a0:], self.len_dev, _Offset(self.peer_stage, a0),
-                          (self.peer_n + 15) // 16 * 16 - a0, self.peer_progress, self.seq, stream=self.s)
+        self.tc.push_peer(self.ctx, self.payload[a0:], self.len_dev, _Offset(self.peer_stage[self.slot], a0),
+                          _pad16(self.peer_n) - a0, self.peer_progress, self.seq, stream=self.s)
         self.sent += nbytes
 
     def _commit(self, it: int):
-        self.seq += 1
-        self.tc.push_peer(self.ctx, self.payload, self.zero_dev, self.peer_stage, 0, self.peer_commit, self.version,
-                          stream=self.s)
+        # stream-ordered after every chunk push of this base (same stream, each push fences at
+        # system scope before its CTAs count out): {0, 2·version + slot} with a release store
+        self.tc.push_peer(self.ctx, self.payload, self.zero_dev, self.peer_stage[self.slot], 0, self.peer_commit,
+                          2 * self.version + self.slot, stream=self.s)
         self.log.append((it, "commit", 0))
 
     def pump(self, it: int):
@@ -344,17 +369,28 @@ class BaseReplicator:
             self._commit(it)
         self.s.synchronize()
 
-    def committed_version(self) -> int:
-        """Version of the previous rank's base held complete in this GPU's staging buffer (0: none)."""
+    def _commit_word(self) -> int:
         return int(self.commit.tensor[8:16].view(torch.int64).item())
 
+    def committed_version(self) -> int:
+        """Version of the previous rank's base held complete in this GPU's staging slots (0: none)."""
+        return self._commit_word() >> 1
+
     def received(self) -> torch.Tensor:
-        return self.stage.tensor[: self.peer_n]
+        """The previous rank's committed base (its slot; empty if none is committed)."""
+        w = self._commit_word()
+        if w == 0:
+            return self.stage[0].tensor[:0]
+        return self.stage[w & 1].tensor[: self.prev_n]
 
     def close(self):
-        for p_ in (self.peer_stage, self.peer_progress, self.peer_commit):
+        for p_ in self._maps:
             p_.close()
         torch.cuda.synchronize(self.dev)
+
+
+def _pad16(n: int) -> int:
+    return max(16, (int(n) + 15) // 16 * 16)
 
 
 class _Offset:

@@ -74,7 +74,10 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
                     err = TC_ERR_CORRUPT;
                     break;
                 }
-                if (r >= P.cap) { err = TC_ERR_CAPACITY; break; }
+                if (r >= P.cap) {  // below the ABI limit the table is sized by the shortest diff:
+                    err = P.cap < TC_MAX_RECORDS_PER_DIFF ? TC_ERR_INVALID : TC_ERR_CAPACITY;  // layouts differ
+                    break;
+                }
                 if (imode && T > kIndexMaxT) { err = TC_ERR_INVALID; break; }  // unsupported here
                 FoldRec R;
                 if (imode) {
@@ -258,6 +261,12 @@ __device__ __forceinline__ void build_mask_from_index(const FoldRec& R, uint32_t
                 continue;
             }
             if (k > a && __ldg(reinterpret_cast<const unsigned short*>(idx) + k - 1) >= x) bad = true;
+            // a tampered (non-increasing) position list can make the binary search above return
+            // entries outside the sub-unit: never let them index the warp's mask words
+            if (ts + x < sub || ts + x >= send) {
+                bad = true;
+                continue;
+            }
             const uint32_t pos = ts + x - sub;
             atomicOr(&imask[pos >> 5], 1u << (pos & 31));
         }

@@ -141,7 +141,13 @@ tc_status tc_replicate_peer(tc_comm* c, const void* send, const uint64_t* send_b
             tc::set_error("payload larger than recv_cap");
             return TC_ERR_CAPACITY;
         }
-        if (n && cudaMemcpyAsync(recv, send, n, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return TC_ERR_CUDA;
+        if (n) {
+            e = cudaMemcpyAsync(recv, send, n, cudaMemcpyDeviceToDevice, s);
+            if (e != cudaSuccess) {
+                tc::set_error(std::string("ring-of-one copy: ") + cudaGetErrorString(e));
+                return TC_ERR_CUDA;
+            }
+        }
         *recv_bytes = n;
         return TC_OK;
     }

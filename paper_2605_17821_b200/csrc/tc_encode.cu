@@ -237,7 +237,17 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
                 bits = (d0 & 1u) | ((d0 >> 15) & 2u) | ((d1 & 1u) << 2) | ((d1 >> 13) & 8u) |
                        ((d2 & 1u) << 4) | ((d2 >> 11) & 32u) | ((d3 & 1u) << 6) | ((d3 >> 9) & 128u);
             }
-            if (adv && bits) g4[vi] = v;  // new ref = cur on the whole vector (equal where unchanged)
+            if (adv && bits) {
+                if ((vi + 1) * VW <= I.nb) {
+                    g4[vi] = v;  // new ref = cur on the whole vector (equal where unchanged)
+                } else {
+                    // the vector straddling the segment end: only its in-range words (the ref may
+                    // be a view into a larger buffer; nothing past n_words is written)
+                    const word_t* cv = scur + vi * VW;
+                    for (uint32_t k = 0; k < VW; ++k)
+                        if ((bits >> k) & 1u) gref[vi * VW + k] = cv[k];
+                }
+            }
             uint32_t x = bits << (VW * (lane & (LPM - 1)));
 #pragma unroll
             for (uint32_t d = 1; d < LPM; d <<= 1) x |= __shfl_xor_sync(0xffffffffu, x, d);

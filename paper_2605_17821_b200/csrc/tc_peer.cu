@@ -16,8 +16,8 @@
 namespace {
 
 constexpr uint32_t kPushThreads = 512;
-constexpr int kPushDepth = 8;
-constexpr int kPushCtas = 32;        // enough stores in flight for NVLink; leaves the SMs to the encode / fold        // 16-byte loads in flight per thread before their remote stores
+constexpr int kPushDepth = 8;  // 16-byte loads in flight per thread before their remote stores
+constexpr int kPushCtas = 32;  // enough stores in flight for NVLink; leaves the SMs to the encode / fold
 constexpr uint32_t kWaitSpinLimit = 1u << 22;  // x ~2 us sleep: ~10 s watchdog
 
 tc_status fail(tc_status s, const std::string& msg) {
@@ -67,6 +67,10 @@ __global__ void __launch_bounds__(kPushThreads) push_kernel(const uint4* __restr
             for (int q = 0; q < kPushDepth; ++q) dst[i + q * stride] = v[q];
         }
         for (; i < n; i += stride) dst[i] = __ldg(src + i);
+        // the last nb % 16 bytes (records are 16-byte padded, but a caller's payload need not be)
+        const uint32_t tail = static_cast<uint32_t>(nb & 15u);
+        if (tail && blockIdx.x == gridDim.x - 1 && threadIdx.x < tail)
+            reinterpret_cast<uint8_t*>(dst + n)[threadIdx.x] = reinterpret_cast<const uint8_t*>(src + n)[threadIdx.x];
     }
     __threadfence_system();
     __syncthreads();

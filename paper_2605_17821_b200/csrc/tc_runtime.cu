@@ -418,6 +418,11 @@ tc_status tc_diff_apply(tc_ctx* ctx, void* const* state, const uint64_t* n_words
             return fail(TC_ERR_INVALID, "record pointers must be 16-byte aligned device pointers");
         P.rec[j] = static_cast<const uint8_t*>(records[j]);
         P.rec_bytes[j] = record_bytes_[j];
+        // a record is at least 80 bytes (header + tile_off), and every diff of one fold must
+        // hold the same number of records: the shortest diff bounds the descriptor table (a diff
+        // with more records than that fails the walker's layout check anyway)
+        const uint64_t by_bytes = record_bytes_[j] / 80 + 1;
+        if (by_bytes < cap) cap = by_bytes;
     }
     P.nseg = nseg;
     P.nrec = n_records;

@@ -137,3 +137,29 @@ def shard_layout(cfg: str, rank: int = 0):
     if bf16:
         return [m, m, m, m], [2, 4, 4, 4]
     return [m, m, m], [4, 4, 4]
+
+
+def segment_versions(n: int, word_bytes: int, seed: int, seg: int, versions, f: float,
+                     structure: int = S1_IID, start: int = 0, block: int = 1 << 23, threads: int | None = None):
+    """Words [start, start+n) of segment ``seg`` at each version in ``versions`` (ascending), made
+    block by block on a thread pool (numpy releases the GIL): the same words as ``state``, for
+    full-size (2^28-word) chunks where one thread would take minutes.  Returns {version: array}."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    versions = sorted(set(int(v) for v in versions))
+    out = {v: np.empty(n, dtype=_dtype(word_bytes)) for v in versions}
+
+    def one(b0):
+        m = min(block, n - b0)
+        a = base(m, word_bytes, seed, seg, start + b0)
+        t = 0
+        for v in versions:
+            while t < v:
+                t += 1
+                a = step(a, seed, seg, t, f, structure, start + b0)
+            out[v][b0:b0 + m] = a
+
+    with ThreadPoolExecutor(threads or os.cpu_count() or 1) as ex:
+        list(ex.map(one, range(0, n, block)))
+    return out

@@ -489,3 +489,58 @@ def test_index_list_fold_chain_length_limit(fctx, tco, N):
     rc, st_g = gpu_fold(fctx, states[0], 0, diffs)
     assert rc == tc.OK
     assert all(np.array_equal(a, b) for a, b in zip(st_g, states[N]))
+
+
+# ------------------------------------------------------- ADVICE r1 regressions -------------
+@pytest.mark.parametrize("n,w", [(4099, 4), (4097, 4), (8195, 2), (8193, 2), (13, 2), (3, 4)])
+def test_advance_ref_view_keeps_bytes_past_the_segment(ctx, tco, n, w):
+    """The fused ref advance writes nothing past n_words: the ref is a view into a larger buffer
+    whose trailing bytes are sentinels (include/tc.h tc_segment: only the first n_words words are
+    the caller's segment).  The last vector straddles the segment end and its tail word changed."""
+    dt = torch.int16 if w == 2 else torch.int32
+    ref_np, cur_np = rand_pair(n, w, 0.0)
+    cur_np[-1] ^= 1  # the straddling vector holds a change
+    cur_np[0] ^= 1
+    buf = torch.full((n + 64,), -0x5A5A if w == 2 else -0x5A5A5A5A, dtype=dt, device="cuda")
+    buf[:n] = to_dev(ref_np)
+    ref = buf[:n]
+    cur = to_dev(cur_np)
+    cap = tc.diff_bound([n], [w])
+    out = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    ob = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tc.diff_encode(ctx, [ref], [cur], out, ob, 1, 0, advance_ref=True)
+    ctx.check()
+    rc, exp = tco.encode([ref_np.copy()], [cur_np], version=1, ref_version=0)
+    assert rc == 0 and np.array_equal(out[: int(ob.item())].cpu().numpy(), exp)
+    assert np.array_equal(to_np(buf[:n]), cur_np)
+    tail = buf[n:].cpu()
+    assert bool((tail == (-0x5A5A if w == 2 else -0x5A5A5A5A)).all()), "bytes past the segment were written"
+
+
+def test_index_tamper_t8192_chain(fctx, tco):
+    """Index mode at T = 8192 (tiles span two 4096-word fold units), N = 2: a non-increasing
+    position list in the second record must surface as CORRUPT, never as out-of-range shared
+    memory writes (tc_apply.cu build_mask_from_index)."""
+    n, T = 40000, 8192
+    states = [synth.state([n], [4], 77, v, 0.05) for v in range(3)]
+    ref = [states[0][0].copy()]
+    recs = []
+    for v in (1, 2):
+        rc, d = tco.encode(ref, [states[v][0]], tile_words=T, version=v, ref_version=v - 1, index_mode=True)
+        assert rc == 0
+        recs.append(d)
+    nt = -(-n // T)
+    p = 64 + ((4 * (nt + 1) + 15) // 16) * 16
+    toff = np.frombuffer(recs[1][64: 64 + 4 * (nt + 1)].tobytes(), np.uint32)
+    k0, k1 = int(toff[0]), int(toff[1])
+    assert k1 - k0 > 4
+    for lo, hi in ((k0, k1 - 1), (k0 + 1, k1 - 2)):  # swap entries: the list is no longer increasing
+        bad = recs[1].copy()
+        a = bad[p + 2 * lo: p + 2 * lo + 2].copy()
+        bad[p + 2 * lo: p + 2 * lo + 2] = bad[p + 2 * hi: p + 2 * hi + 2]
+        bad[p + 2 * hi: p + 2 * hi + 2] = a
+        assert tco.fold([states[0][0].copy()], 0, [recs[0], bad])[0] == tc.ERR_CORRUPT
+        rc, _ = gpu_fold(fctx, states[0], 0, [recs[0], bad])
+        assert rc == tc.ERR_CORRUPT
+    rc, st = gpu_fold(fctx, states[0], 0, recs)
+    assert rc == tc.OK and np.array_equal(st[0], states[2][0])

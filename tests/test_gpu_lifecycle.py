@@ -112,3 +112,127 @@ def test_fullsize_cfg2_sampled_parity_and_round_trip(tco):
     ctx.check()
     assert all(torch.equal(a, b) for a, b in zip(X, Y))
     ctx.close()
+
+
+def _idx_record(buf, pos):
+    """Sections of one index-mode record (header | tile_off u32[nt+1] | idx u16[count] |
+    values), parsed from the layout table, not from either implementation."""
+    h = buf[pos: pos + 64]
+    w, flags = int(h[6]), int(h[7])
+    T = int(h[8:12].view("<u4")[0])
+    seg = int(h[12:16].view("<u4")[0])
+    off, m, count = (int(h[a:a + 8].view("<u8")[0]) for a in (16, 24, 32))
+    total = int(h[56:64].view("<u8")[0])
+    nt = -(-m // T)
+    p = pos + 64
+    toff = buf[p: p + 4 * (nt + 1)].view("<u4")
+    p += -(-4 * (nt + 1) // 16) * 16
+    idx = buf[p: p + 2 * count].view("<u2")
+    p += -(-2 * count // 16) * 16
+    vals = buf[p: p + w * count].view("<u2" if w == 2 else "<u4")
+    return dict(w=w, flags=flags, T=T, seg=seg, off=off, m=m, count=count, total=total, toff=toff, idx=idx,
+                vals=vals, pos=pos)
+
+
+def test_fullsize_cfg2_bench_config_chain_parity(tco):
+    """BASELINE configs[1] (cfg2, 21.8 GB) in exactly the configuration bench.py times: index-mode
+    records, advance_ref = 1, T = 4096, C = 2^28, two chained versions (v0 -> v1 -> v2, the second
+    encoded against the advanced reference).  Per segment, the first and the last chunk record are
+    byte-compared whole with oracle.encode of that chunk; every other chunk is compared on 8
+    random 256-tile windows (tile_off differences, positions and values of the window == the
+    oracle's record of the window) — SURVEY §8(d) sampled-chunk rule; the oracle's inputs come from
+    synth (numpy), never from the device.  Then the chain folds onto the base bit-exactly."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    sizes, wb = synth.shard_layout("cfg2")
+    seed, f, T, C = synth.SEED0, 0.01, 4096, 1 << 28
+    W = sum(n * w for n, w in zip(sizes, wb))
+    if torch.cuda.mem_get_info()[0] < 3.3 * W:
+        pytest.skip("not enough device memory for the full-size case")
+    ref = _dev_state(sizes, wb, seed, 0, f)
+    cur = [r.clone() for r in ref]
+    ctx = tc.Ctx(0)
+    recs = []
+    for v in (1, 2):
+        for s, t in enumerate(cur):
+            tc.synth_step(t, seed, s, v, synth.p53_of(f))
+        cap = tc.diff_bound(sizes, wb, T, C, index_mode=True)
+        out = torch.empty(cap, dtype=torch.uint8, device="cuda")
+        ob = torch.zeros(1, dtype=torch.int64, device="cuda")
+        tc.diff_encode(ctx, ref, cur, out, ob, v, v - 1, T, C, True, index_mode=True)
+        ctx.check()
+        assert all(torch.equal(a, b) for a, b in zip(ref, cur)), "advance_ref: ref != cur after the encode"
+        n = int(ob.item())
+        recs.append((out, n))
+    host = [o[:n].cpu().numpy() for o, n in recs]
+    per = []  # (version, record dict)
+    for v, buf in zip((1, 2), host):
+        pos = 0
+        while pos < buf.size:
+            r = _idx_record(buf, pos)
+            assert r["flags"] == 3 and r["T"] == T
+            per.append((v, r))
+            pos += r["total"]
+        assert pos == buf.size
+    rng = np.random.default_rng(2026)
+    full_jobs, win_jobs = [], []
+    for s in range(4):
+        chunks = sorted({r["off"] for v, r in per if r["seg"] == s})
+        assert chunks == list(range(0, sizes[s], C))
+        for c0 in chunks:
+            if c0 in (chunks[0], chunks[-1]):
+                full_jobs.append((s, c0))
+            else:
+                m = min(C, sizes[s] - c0)
+                nt = -(-m // T)
+                for t0 in rng.choice(nt - 256, size=8, replace=False):
+                    win_jobs.append((s, c0, int(t0)))
+
+    def rec_of(v, s, c0):
+        return next(r for vv, r in per if vv == v and r["seg"] == s and r["off"] == c0)
+
+    def check_full(job):
+        s, c0 = job
+        m = min(C, sizes[s] - c0)
+        st = synth.segment_versions(m, wb[s], seed, s, [0, 1, 2], f, start=c0, threads=4)
+        bad = []
+        for v in (1, 2):
+            rc, exp = tco.encode([st[v - 1].copy()], [st[v]], tile_words=T, chunk_words=C, advance_ref=True,
+                                 version=v, ref_version=v - 1, index_mode=True)
+            exp = exp.copy()
+            exp[12:16] = np.frombuffer(np.uint32(s).tobytes(), np.uint8)  # the one-segment oracle run
+            exp[16:24] = np.frombuffer(np.uint64(c0).tobytes(), np.uint8)  # names segment 0, offset 0
+            r = rec_of(v, s, c0)
+            buf = host[v - 1]
+            if rc != 0 or not np.array_equal(buf[r["pos"]: r["pos"] + r["total"]], exp):
+                bad.append((v, s, c0))
+        return bad
+
+    def check_window(job):
+        s, c0, t0 = job
+        a = c0 + t0 * T
+        st = synth.segment_versions(256 * T, wb[s], seed, s, [0, 1, 2], f, start=a, threads=1)
+        bad = []
+        for v in (1, 2):
+            rc, exp = tco.encode([st[v - 1].copy()], [st[v]], tile_words=T, chunk_words=C, advance_ref=True,
+                                 version=v, ref_version=v - 1, index_mode=True)
+            e = _idx_record(exp, 0)
+            r = rec_of(v, s, c0)
+            k0, k1 = int(r["toff"][t0]), int(r["toff"][t0 + 256])
+            ok = rc == 0 and np.array_equal(r["toff"][t0: t0 + 257] - np.uint32(k0), e["toff"]) \
+                and np.array_equal(r["idx"][k0:k1], e["idx"]) and np.array_equal(r["vals"][k0:k1], e["vals"])
+            if not ok:
+                bad.append((v, s, c0, t0))
+        return bad
+
+    with ThreadPoolExecutor(4) as ex:
+        bad = sum(ex.map(check_full, full_jobs), []) + sum(ex.map(check_window, win_jobs), [])
+    assert not bad, f"records differ from the oracle: {bad[:8]}"
+    assert len(full_jobs) == 8 and len(win_jobs) == 8 * (sum(-(-n // C) for n in sizes) - 8)
+    # the chain folds onto the base bit-exactly (index-mode chain, default strategy)
+    for s, t in enumerate(ref):
+        tc.synth_base(t, seed, s)
+    tc.diff_apply(ctx, ref, 0, [o for o, _ in recs], [n for _, n in recs])
+    ctx.check()
+    assert all(torch.equal(a, b) for a, b in zip(ref, cur))
+    ctx.close()

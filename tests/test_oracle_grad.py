@@ -199,3 +199,29 @@ def test_replay_is_the_sequential_application():
         M, Mm, Mv = adam_f64(M, Mm, Mv, g, 3 + j)
     assert np.allclose(a[0], M, rtol=1e-6, atol=1e-6)
     assert math.isfinite(float(a[0].sum()))
+
+
+def test_adam_eps_placement_pinned():
+    """Where ε sits (DESIGN G8: denom = √v̂ + ε, ε added after the bias correction, outside the
+    square root).  With v = 0 and m ≠ 0 the step is exactly lr·m̂/ε; with √v̂ comparable to ε the
+    two terms are summed.  ε inside the root (√(v̂+ε)) or ahead of the correction ((√v + ε)/√(1−β2ᵗ))
+    changes these steps by orders of magnitude."""
+    lr, b1, b2, eps = 1e-3, 0.9, 0.999, 1e-8
+    m0 = np.array([1e-9, -3e-9, 2e-10, 5e-9, 1e-9, -1e-9], np.float32)
+    # v0 = 0 (pure ε), then v̂ = ε², 4ε², ε²/4 at step t (√v̂ = ε, 2ε, ε/2)
+    for t in (1, 2, 7):
+        c2 = 1 - b2 ** t
+        vh_target = np.array([0, 0, 0, eps ** 2, 4 * eps ** 2, 0.25 * eps ** 2])
+        v0 = (vh_target * c2 / b2).astype(np.float32)  # g = 0: v = β2·v0
+        master = np.zeros(6, np.float32)  # the update itself, at full fp32 relative precision
+        m, v = m0.copy(), v0.copy()
+        oracle.adam_step(master, m, v, np.zeros(6, np.uint16), np.zeros(6, np.float32), t, lr=lr, b1=b1, b2=b2,
+                         eps=eps)
+        mh = b1 * m0.astype(np.float64) / (1 - b1 ** t)
+        vh = b2 * v0.astype(np.float64) / c2
+        expect = -lr * mh / (np.sqrt(vh) + eps)
+        assert np.allclose(master, expect, rtol=1e-5, atol=0), (t, master, expect)
+        wrong_in_root = -lr * mh / np.sqrt(vh + eps)
+        wrong_before_corr = -lr * mh / ((np.sqrt(b2 * v0.astype(np.float64)) + eps) / np.sqrt(c2))
+        assert not np.allclose(master, wrong_in_root, rtol=1e-2)
+        assert not np.allclose(master, wrong_before_corr, rtol=1e-2)

@@ -60,6 +60,8 @@ rep.s.synchronize()
 dist.barrier()
 if rep.committed_version() != 10:
     fails.append("spillover base visible before its flush")
+if not torch.equal(rep.received(), flat(shard(prv, 1))):  # base 2 streams into the other slot
+    fails.append("committed base 1 torn while base 2 was in flight")
 dist.barrier()
 rep.intercept(shard(rank, 3), version=30, interval=10, margin=2, cap=1 << 30)  # flushes base 2 first
 rep.s.synchronize()
