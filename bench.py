@@ -238,15 +238,34 @@ def run_ours(args):
     free = torch.cuda.mem_get_info(dev)[0]
     est = int(min(cap, (args.f * 1.1 + 0.05) * W + (64 << 20)))
     spill_need = (sum(sizes) // 4096 + 1) * (8192 + 1024)  # encode scratch (index mode: 8 KB spill + mask stage)
-    rec_cap = cap if 2 * cap + est + spill_need + (8 << 30) < free else est
-    recs = [torch.empty(rec_cap, dtype=torch.uint8, device=dev) for _ in range(2)]
+    # the step runs through the product lifecycle (paper_2605_17821_b200.checkpoint.Checkpointer) —
+    # encode, Tier-1 staging, Tier-2 NVLink push, hot-standby fold, the version chain — except
+    # with --tier2 nccl (kept as the NCCL baseline, driven here)
+    use_ck = comm is None or args.tier2 == "push"
+    ck = None
+    if use_ck:
+        from paper_2605_17821_b200.checkpoint import Checkpointer
+
+        ck = Checkpointer(Y, rank, world, tier2="push" if world > 1 else None, expected_f=args.f,
+                          record_format=args.format if allow_index else "mask", dev_slots=2, t1_bytes=3 * est,
+                          t2_slots=2, standby=R, tile_words=T, chunk_words=C, ahead=world == 1,
+                          stage_base=False, ref=A, stream=s_comp, push_ctas=args.push_ctas, timing=True)
+        rec_cap = ck.rec_cap
+        recs = ck.dev
+        s_copy, s_comm = ck.s_copy, ck.s_comm  # the step's side streams are the lifecycle's
+    else:
+        rec_cap = cap if 2 * cap + est + spill_need + (8 << 30) < free else est
+        recs = [torch.empty(rec_cap, dtype=torch.uint8, device=dev) for _ in range(2)]
     # the Tier-2 receive buffer: the neighbour's record (its capacity is exchanged by
     # tc_replicate_peer, so it need not be the worst-case bound)
     recv = torch.empty(est, dtype=torch.uint8, device=dev) if comm else None
     # NCCL-free Tier-2 (--tier2 push): two IPC slots + mailboxes on this GPU receive the previous
     # rank's records; the next rank's are mapped here and written with NVLink stores
     push = None
-    if comm is not None and args.tier2 == "push":
+    if ck is not None and world > 1:
+        push = {"mine": {"slots": ck.rx, "mail": ck.rx_mail}, "cap": ck.next_cap, "ctx": ck.pctx,
+                "ctas": args.push_ctas, "peer_slots": ck.tx, "peer_mail": ck.tx_mail}
+    elif comm is not None and args.tier2 == "push":
         import torch.distributed as dist
 
         mine = {"slots": [tc.IpcBuffer(est) for _ in range(2)], "mail": [tc.IpcBuffer(16) for _ in range(2)]}
@@ -261,7 +280,7 @@ def run_ours(args):
     # the encode kernel writes each record's length straight into mapped pinned memory, so the
     # host learns it without a copy-engine round trip
     ob_host = tc.HostBuffer(64)
-    ob_view = ob_host.view(torch.int64)
+    ob_view = ob_host.view(torch.int64) if ck is None else ck.lens_v
     obytes = [ob_view[i: i + 1] for i in range(2)]
     host_cap = est  # Tier-1 ring slots sized to the expected record, not the state
     host_ring = [tc.HostBuffer(host_cap) for _ in range(2)]  # libtc-pinned Tier-1 ring
@@ -404,11 +423,42 @@ def run_ours(args):
                     n_ops["replicate"].append((r0p, r1p, nbp))
                 done_ev[sl] = (done_ev[sl][0], None, False)
 
+    if ck is not None:
+        # the product path: one save_step per version (the Checkpointer runs one step ahead at
+        # N = 1 and finishes each step before the next at N > 1, as above); the records older
+        # than the last one are reclaimed every step, so the Tier-1 arena
+        # is a ring, as a deployment that takes a base every I iterations would keep it
+        ck_done = []  # (version, bytes, index mode) of every finished save
+
+        def ck_finished(nb):
+            if nb is not None:
+                ck_done.append((ck.chain.head, nb, ck.where[ck.chain.head]["index"]))
+                ck.reclaim(max(ck.chain.base_version, ck.chain.head - 1))
+            return nb
+
+        def step(k, timed):  # noqa: F811
+            cur = Y if state["content"] == "X" else X
+            v = state["ref_version"] + 1
+            nb = ck.save_step(v, segments=cur)
+            state["ref_version"] = v
+            state["content"] = "Y" if state["content"] == "X" else "X"
+            return ck_finished(nb)
+
+        def flush():  # noqa: F811
+            return ck_finished(ck.flush())
+
+        def drain():  # noqa: F811
+            pass
+
     for k in range(args.warmup):
         step(k, False)
     flush()
     drain()
     sync_all()
+    if ck is not None:
+        for v_ in ck.times.values():
+            v_.clear()
+        v_timed0 = state["ref_version"] + 1
     ctx.check(s_comp)
     ctx_f.check(s_fold)
     if world > 1:
@@ -417,7 +467,12 @@ def run_ours(args):
     clocks = Clocks(local)
     clocks.start()
     time.sleep(0.3)
-    launches0 = ctx.launches + (push["ctx"].launches if push else 0) + (ctx_f.launches if ctx_f is not ctx else 0)
+    def n_launch():
+        if ck is not None:
+            return ck.ctx.launches + (ck.pctx.launches if world > 1 else 0)
+        return ctx.launches + (push["ctx"].launches if push else 0) + (ctx_f.launches if ctx_f is not ctx else 0)
+
+    launches0 = n_launch()
     t_start, t_end = ev(), ev()
     t_start.record(s_comp)
     sizes_seen = []
@@ -436,8 +491,7 @@ def run_ours(args):
     t_end.record(s_comp)
     sync_all()
     torch.cuda.synchronize()
-    launches = (ctx.launches + (push["ctx"].launches if push else 0) + (ctx_f.launches if ctx_f is not ctx else 0) -
-                launches0)
+    launches = n_launch() - launches0
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -445,6 +499,14 @@ def run_ours(args):
     ctx_f.check(s_fold)
     if push:
         push["ctx"].check(s_comm)
+    if ck is not None:
+        ck.ctx.check(s_comp)
+        n_ops["encode"] = ck.times["encode"]
+        n_ops["fold"] = ck.times["fold"]
+        n_ops["stage"] = ck.times["stage"]
+        timed_done = [d for d in ck_done if d[0] >= v_timed0]
+        n_ops["replicate"] = [(a, b, d[1]) for (a, b), d in zip(ck.times["push"], timed_done)]
+        state["modes"] = ["index" if d[2] else "mask" for d in timed_done]
     ms = t_start.elapsed_time(t_end)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -467,7 +529,11 @@ def run_ours(args):
     ok = all(torch.equal(a, r) for a, r in zip(A, R))
     last_cur = Y if state["content"] == "Y" else X
     ok = ok and all(torch.equal(a, c) for a, c in zip(A, last_cur))
-    host_last = host_ring[(args.warmup + args.steps - 1) % 2].numpy()
+    if ck is not None:
+        w_last = ck.where[ck.chain.head]
+        host_last = ck.t1.view(w_last["t1"], w_last["n"]).numpy()
+    else:
+        host_last = host_ring[(args.warmup + args.steps - 1) % 2].numpy()
     recs_info = record_counts(host_last, sizes_seen[-1])
     enc_b, fold_b = algorithmic_bytes(recs_info)
     enc_bs, fold_bs = algorithmic_bytes(recs_info, sector=True)

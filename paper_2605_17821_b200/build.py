@@ -46,16 +46,18 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defs: str = "") -> str:
+    """Compile every csrc/*.cu and link libtc.so (or `out`, with extra -D `defs`: experiment builds)."""
+    lib = out or LIB
+    if out is None and not force and not needs_build():
         return LIB
     inc, libdir = nccl_dirs()
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build") if out is None else out + ".objs"
     os.makedirs(objdir, exist_ok=True)
     objs = []
     common = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", inc,
                      "-I", os.path.join(ROOT, "include")]
-    common += os.environ.get("TC_NVCC_DEFS", "").split()  # experiments only, e.g. -DTC_DENSE_RUN=8
+    common += (os.environ.get("TC_NVCC_DEFS", "") + " " + defs).split()  # experiments only, e.g. -DTC_DENSE_RUN=8
     if verbose:
         common += ["-Xptxas", "-v"]
     procs = []
@@ -66,11 +68,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for p in procs:
         if p.wait() != 0:
             raise RuntimeError("nvcc failed")
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L", libdir, "-l:libnccl.so.2",
                            "-Xlinker", "-rpath," + libdir, "-cudart", "static"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

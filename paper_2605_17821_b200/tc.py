@@ -14,7 +14,8 @@ import re
 import torch
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libtc.so")
+# TC_LIB_PATH: an experiment build of the same sources (tools/, A/B runs); default the in-tree one
+LIB_PATH = os.environ.get("TC_LIB_PATH") or os.path.join(PKG, "libtc.so")
 INCLUDE = os.path.join(os.path.dirname(PKG), "include")
 
 OK, ERR_INVALID, ERR_NOMEM, ERR_CUDA, ERR_NCCL = 0, 1, 2, 3, 4

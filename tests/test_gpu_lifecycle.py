@@ -29,22 +29,20 @@ def _dev_state(sizes, wb, seed, version, f):
     return segs
 
 
-@pytest.mark.parametrize("source", ["t1", "device"])
+@pytest.mark.parametrize("source", ["t1", "t2", None])
 def test_chain_of_8_restore_after_failure(source):
     sizes, wb, seed, f = [70001, 70001, 70001, 70001], [2, 4, 4, 4], synth.SEED0 + 4, 0.01
     live = _dev_state(sizes, wb, seed, 0, f)
     base_host = [to_np(s) for s in live]  # the base checkpoint (version 0)
-    ck = Checkpointer(live, tile_words=4096, chunk_words=1 << 14)
+    ck = Checkpointer(live, tile_words=4096, chunk_words=1 << 14, tier2="push", expected_f=f)
     for v in range(1, 9):
         for s, t in enumerate(live):  # one training step changes a fraction f of the words
             tc.synth_step(t, seed, s, v, synth.p53_of(f))
         ck.save_step(v)
+    ck.flush()
     torch.cuda.synchronize()
     expect = synth.state(sizes, wb, seed, 8, f)
     assert all(np.array_equal(to_np(a), b) for a, b in zip(live, expect))
-    # simulated GPU failure: the device state and the reference are gone
-    for t in live + ck.ref:
-        t.zero_()
     restored = [to_dev(b) for b in base_host]  # base fetched back (Tier-1/2/3)
     ver = ck.restore(restored, source=source, batch=8)
     assert ver == 8
@@ -57,6 +55,81 @@ def test_chain_of_8_restore_after_failure(source):
     assert all(np.array_equal(to_np(a), b) for a, b in zip(mid, exp6))
     ck.reclaim(6)
     assert ck.chain.base_version == 6 and [e.version for e in ck.chain.entries] == [7, 8]
+    ck.close()
+
+
+@pytest.mark.parametrize("lose_t1", [False, True])
+def test_recover_after_gpu_failure_ring_of_one(lose_t1):
+    """The lifecycle end to end on one GPU (the ring of one is this GPU): base staged to Tier-1 and
+    streamed to the (local) Tier-2 neighbour, 7 saves through the one-step-ahead pipeline with the
+    adaptive record format and a hot standby replica, then a GPU failure (state + reference
+    wiped) — and optionally a node failure (Tier-1 lost too) — and recover(): consensus, the
+    cascade Tier-1 -> Tier-2 for the base and every record, one fold per batch
+    of 5.  The recovered state, the reference and the standby equal the seeded chain head."""
+    sizes, wb, seed = [90001, 90001, 90001, 90001], [2, 4, 4, 4], synth.SEED0 + 9
+    fs = [0.002, 0.3, 0.01, 0.0, 1.0, 0.02, 0.05]  # mixes index / mask records
+    live = _dev_state(sizes, wb, seed, 0, 0.0)
+    standby = [t.clone() for t in live]
+    ck = Checkpointer(live, tier2="push", expected_f=1.0, standby=standby, t2_slots=8, chunk_words=1 << 15)
+    expect = [to_np(t) for t in live]
+    for v, f in enumerate(fs, start=1):
+        for s, t in enumerate(live):
+            tc.synth_step(t, seed, s, v, synth.p53_of(f))
+        ck.save_step(v)
+        expect = [synth.step(e, seed, s, v, f) for s, e in enumerate(expect)]
+    ck.base_rep.flush(100)  # the paced base stream completes (sync flush, P:209)
+    ck.flush()
+    ck.base_rep.s.synchronize()
+    torch.cuda.synchronize()
+    assert all(np.array_equal(to_np(a), b) for a, b in zip(standby, expect))
+    formats = {ck.where[e.version]["count"] * 16 < sum(sizes) for e in ck.chain.entries}
+    assert len(formats) == 2, "the adaptive format should have produced both record modes"
+    ck.drop_tier("hbm")
+    if lose_t1:
+        ck.drop_tier("t1")
+    assert ck.recover(batch=5) == len(fs)
+    for t in (live, ck.ref):
+        assert all(np.array_equal(to_np(a), b) for a, b in zip(t, expect))
+    # the chain continues after the recovery
+    for s, t in enumerate(live):
+        tc.synth_step(t, seed, s, 8, synth.p53_of(0.01))
+    ck.save_step(8)
+    ck.flush()
+    torch.cuda.synchronize()
+    assert all(torch.equal(a, b) for a, b in zip(standby, live))
+    ck.close()
+
+
+def test_checkpointer_cfg2_saves_without_reallocation():
+    """BASELINE configs[1] (cfg2, 21.8 GB) through the product path: 12 saves with every buffer
+    allocated once (record slots sized to the expected change fraction, mapped-pinned lengths,
+    one Tier-1 arena), no host synchronization on the encode it just issued, a hot standby folded
+    behind every record; device memory does not grow after the first save."""
+    sizes, wb = synth.shard_layout("cfg2")
+    seed, f = synth.SEED0, 0.01
+    W = sum(n * w for n, w in zip(sizes, wb))
+    if torch.cuda.mem_get_info()[0] < 3.4 * W:
+        pytest.skip("not enough device memory for the full-size case")
+    live = _dev_state(sizes, wb, seed, 0, f)
+    standby = [t.clone() for t in live]
+    ck = Checkpointer(live, expected_f=f, standby=standby, stage_base=False, t1_bytes=16 * (1 << 30))
+    torch.cuda.synchronize()
+    mem0 = None
+    for v in range(1, 13):
+        for s, t in enumerate(live):
+            tc.synth_step(t, seed, s, v, synth.p53_of(f))
+        ck.save_step(v)
+        if v == 2:
+            torch.cuda.synchronize()
+            mem0 = torch.cuda.memory_allocated()
+    ck.flush()
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated() == mem0
+    assert [e.version for e in ck.chain.entries] == list(range(1, 13))
+    assert all("t1" in e.tiers for e in ck.chain.entries)
+    assert all(torch.equal(a, b) for a, b in zip(standby, live))
+    assert all(torch.equal(a, b) for a, b in zip(ck.ref, live))
+    ck.close()
 
 
 def test_fullsize_cfg2_sampled_parity_and_round_trip(tco):

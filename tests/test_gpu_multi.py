@@ -42,3 +42,15 @@ def test_paced_base_replication_world2():
     p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     assert p.stdout.count("OK") >= n
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_lifecycle_recover_from_tier2_world2():
+    """Product lifecycle: rank 0 loses HBM + Tier-1, recover() pulls base + chain from the ring
+    neighbour's Tier-2 over NVLink, the other ranks from Tier-1; consensus over the group."""
+    n = min(torch.cuda.device_count(), 4)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29536", os.path.join(ROOT, "tools", "lifecycle_check.py")]
+    p = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert p.stdout.count("OK") >= n

@@ -174,13 +174,13 @@ def test_base_replicator_ring_of_one():
     b1, b2, b3 = shard(1), shard(2), shard(3)
     n = flat(b1).numel()
     rep = BaseReplicator(n, 0, 1, 0)
-    assert rep.committed_version() == 0 and rep.received().numel() == 0
+    assert rep.committed_version() == -1 and rep.received().numel() == 0
     plan = rep.intercept(b1, version=10, interval=10, margin=2, cap=1 << 30)
     assert not plan.spillover and plan.iters == 8
     for it in range(1, 11):
         rep.pump(it)
         rep.s.synchronize()
-        assert rep.committed_version() == (10 if it >= plan.iters else 0), it
+        assert rep.committed_version() == (10 if it >= plan.iters else -1), it
     assert torch.equal(rep.received(), flat(b1))
     assert torch.equal(rep.host.tensor[:n], flat(b1).cpu())
     # base 2 spills over (small chunk cap): while it streams, base 1 stays committed and intact
