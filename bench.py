@@ -249,7 +249,8 @@ def run_ours(args):
         ck = Checkpointer(Y, rank, world, tier2="push" if world > 1 else None, expected_f=args.f,
                           record_format=args.format if allow_index else "mask", dev_slots=2, t1_bytes=3 * est,
                           t2_slots=2, standby=R, tile_words=T, chunk_words=C, ahead=world == 1,
-                          stage_base=False, ref=A, stream=s_comp, push_ctas=args.push_ctas, timing=True)
+                          stage_base=False, ref=A, stream=s_comp, push_ctas=args.push_ctas, timing=True,
+                          fused_t2=bool(args.t2_fused))
         rec_cap = ck.rec_cap
         recs = ck.dev
         s_copy, s_comm = ck.s_copy, ck.s_comm  # the step's side streams are the lifecycle's
@@ -504,6 +505,8 @@ def run_ours(args):
         n_ops["encode"] = ck.times["encode"]
         n_ops["fold"] = ck.times["fold"]
         n_ops["stage"] = ck.times["stage"]
+        state["rest_version"] = ck.chain.head  # the standby replica (R) and the reference (A)
+        state["index"] = bool(ck.next_index)    # the format the next record would take
         timed_done = [d for d in ck_done if d[0] >= v_timed0]
         n_ops["replicate"] = [(a, b, d[1]) for (a, b), d in zip(ck.times["push"], timed_done)]
         state["modes"] = ["index" if d[2] else "mask" for d in timed_done]
@@ -624,9 +627,13 @@ def run_ours(args):
                 "record_format": args.format,
                 "record_modes_timed": sorted(set(state["modes"])),
                 "l2": f"no flush: every step streams {W / 1e9:.1f} GB of state per rank (> 126 MB L2)",
-                "step": "encode(advance_ref) + D2H stage + " + (
-                    ("NVLink push to the ring neighbour's IPC slot + " if push else "NCCL ring replicate + ")
-                    if world > 1 else "") + "fold onto restore replica",
+                "step": ("Checkpointer.save_step: " if ck is not None else "") + (
+                    "encode(advance_ref) writing the record over NVLink into the ring neighbour's IPC slot "
+                    "(fused Tier-2 emit) + D2H stage + fold onto restore replica"
+                    if (ck is not None and world > 1 and args.t2_fused)
+                    else "encode(advance_ref) + D2H stage + " + (
+                        ("NVLink push to the ring neighbour's IPC slot + " if push else "NCCL ring replicate + ")
+                        if world > 1 else "") + "fold onto restore replica"),
                 "parallelism": f"dp{world} (independent ZeRO shards; Tier-2 ring r->r+1)" if world > 1 else "1 GPU",
             },
             "roofline": {
@@ -661,7 +668,11 @@ def run_ours(args):
                               "frac_pcie": round(rec_bytes / stage_ms / 1e6 / pcie, 4) if pcie else None,
                               "pcie_note": "denominator: a plain D2H cudaMemcpyAsync of the same record into "
                                            "the same pinned slot, measured after the timed region"},
-                "replicate_in_step": None if rep_ms is None else {
+                "replicate_in_step": ({"fused": "Tier-2 written by the encode kernels into the neighbour's "
+                                                "IPC slot over NVLink (tc_diff_encode_push): no separate copy in "
+                                                "the step; see 'replicate' for the isolated push"}
+                                      if (ck is not None and world > 1 and args.t2_fused) else None)
+                if rep_ms is None else {
                     "ms": round(rep_ms, 4), "gbs_per_direction": round(rec_bytes / rep_ms / 1e6, 1),
                     "note": "inside the pipelined step: shares HBM with encode/fold, PCIe with the "
                             "Tier-1 D2H, and waits for the slower neighbour's encode"},
@@ -689,13 +700,18 @@ def run_ours(args):
 
 
 def run_streaming(args, rank, world, local, dev):
-    """cfg5 (the paper's 40B: h 5120, inter 20480, L 128; shard r of 8 = 70.9 GB per rank): the
-    record bound (73.5 GB) does not fit beside the state and its reference (141.8 GB), so the
-    checkpoint is encoded in runs of whole chunks (tc_diff_encode_range) through a 2-slot device
-    ring, each run staged to a pinned host buffer (Tier-1) — and at N > 1 sent to the ring
-    neighbour (Tier-2) — while the next run is encoded.  Reference = the base (advance_ref = 0: a
-    third 70.9 GB copy for an advancing reference does not fit).  One step = one full per-rank
-    checkpoint; ms_per_step is the end-to-end per-rank checkpoint time of the north star."""
+    """cfg5 (the paper's 40B: h 5120, inter 20480, L 128; shard r of 8 = 70.9 GB per rank),
+    checkpointing EVERY step (BASELINE configs[4]): the state evolves by one synthetic training
+    step per version (untimed), and each version is checkpointed against the advancing reference
+    (advance_ref = 1: state + reference = 141.9 GB of HBM).  The record bound (73.5 GB) does not fit
+    beside them, so the checkpoint is encoded in runs of whole chunks (tc_diff_encode_range)
+    through a 2-slot device ring, each run staged to the rank's pinned Tier-1 arena — and at N > 1
+    pushed into the ring neighbour's slot over NVLink (Tier-2) — while the next run is encoded.
+    ms_per_step = the end-to-end per-rank checkpoint of one version (the north star's "well under
+    10 s").  After the timed steps the whole chain is verified: the reference equals the state, the
+    base is regenerated and every version's diff is folded back from Tier-1 (bit-exact against the
+    live state), and one 256-tile window per segment of the last version is byte-compared with the
+    oracle on inputs from synth."""
     import torch
     import torch.distributed as dist
 
@@ -709,18 +725,16 @@ def run_streaming(args, rank, world, local, dev):
     T, C, K = args.tile_words, args.chunk_words, args.stream_chunks
     s_comp = torch.cuda.Stream(device=dev)
     s_copy = torch.cuda.Stream(device=dev)
-    s_comm = torch.cuda.Stream(device=dev)
+    s_comm = torch.cuda.Stream(device=dev, priority=-1)
     ctx = tc.Ctx(local)
     if args.fold_dense_permille is not None:
         ctx.set_fold_dense_permille(args.fold_dense_permille)
-    comm = tc.Comm(rank, world, local) if world > 1 else None
-    X = [torch.empty(n, dtype=torch.int16 if w == 2 else torch.int32, device=dev) for n, w in zip(sizes, wb)]
-    Y = [torch.empty(n, dtype=torch.int16 if w == 2 else torch.int32, device=dev) for n, w in zip(sizes, wb)]
+    S = [torch.empty(n, dtype=torch.int16 if w == 2 else torch.int32, device=dev) for n, w in zip(sizes, wb)]
+    R = [torch.empty(n, dtype=torch.int16 if w == 2 else torch.int32, device=dev) for n, w in zip(sizes, wb)]
     with torch.cuda.stream(s_comp):
         for i in range(len(sizes)):
-            tc.synth_base(X[i], seed, i, stream=s_comp)
-            Y[i].copy_(X[i])
-            tc.synth_step(Y[i], seed, i, 1, p53, args.structure, stream=s_comp)
+            tc.synth_base(S[i], seed, i, stream=s_comp)
+            R[i].copy_(S[i])
     s_comp.synchronize()
     runs = []
     for i, n in enumerate(sizes):
@@ -737,14 +751,31 @@ def run_streaming(args, rank, world, local, dev):
     fixed_idx = tc.diff_bound(sizes, wb, T, C, index_mode=True) - (2 + w_avg) * total_words
     mode = {"index": args.format == "index" and allow_index}
     slots = [torch.empty(slot_cap, dtype=torch.uint8, device=dev) for _ in range(2)]
-    rslots = [torch.empty(slot_cap, dtype=torch.uint8, device=dev) for _ in range(2)] if comm else None
+    push = None
+    if world > 1:  # Tier-2: two IPC slots + mailboxes on this GPU for the previous rank's runs
+        mine = {"slots": [tc.IpcBuffer(slot_cap) for _ in range(2)], "mail": [tc.IpcBuffer(16) for _ in range(2)]}
+        hs = [None] * world
+        dist.all_gather_object(hs, [b_.handle for b_ in mine["slots"]] + [m.handle for m in mine["mail"]])
+        nx = hs[(rank + 1) % world]
+        pctx = tc.Ctx(local)
+        pctx.set_push_ctas(args.push_ctas)
+        push = {"mine": mine, "ctx": pctx, "slots": [tc.PeerMapping(h, slot_cap) for h in nx[:2]],
+                "mail": [tc.PeerMapping(h, 16) for h in nx[2:]]}
     lens_h = tc.HostBuffer(8 * max(2, len(runs)))
     lens = lens_h.view(torch.int64)
-    host = tc.HostBuffer(int((args.f * 1.1 + 0.05) * W) + (256 << 20))
+    n_versions = args.warmup + args.steps
+    # Tier-1 keeps every version's diff (for the round trip): the first is a mask-mode record, the
+    # adaptive format then takes index mode below 1/16 changed
+    mask_est = int(fixed_mask + 1.1 * args.f * W) + (64 << 20)
+    idx_est = int(fixed_idx + 1.1 * args.f * (2 + w_avg) * total_words) + (64 << 20)
+    later = idx_est if (allow_index and args.f < 1 / 16) else mask_est
+    host = tc.HostBuffer((mask_est if args.format != "index" else idx_est) + (n_versions - 1) * later)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    diffs = []  # (version, host offset, bytes)
+    seq = [0]
 
-    def step(times):
-        pos = 0
+    def checkpoint(v, times, pos0):
+        pos = pos0
         done = [None, None]
         for r_i, (i, c0, k) in enumerate(runs):
             sl = r_i % 2
@@ -752,7 +783,7 @@ def run_streaming(args, rank, world, local, dev):
                 s_comp.wait_event(e)
             e0, e1 = ev(), ev()
             e0.record(s_comp)
-            tc.diff_encode_range(ctx, X[i], Y[i], i, c0, k, slots[sl], lens[r_i: r_i + 1], 1, 0, T, C, False,
+            tc.diff_encode_range(ctx, R[i], S[i], i, c0, k, slots[sl], lens[r_i: r_i + 1], v, v - 1, T, C, True,
                                  stream=s_comp, index_mode=mode["index"])
             e1.record(s_comp)
             e1.synchronize()
@@ -764,9 +795,11 @@ def run_streaming(args, rank, world, local, dev):
             c1 = torch.cuda.Event()
             c1.record(s_copy)
             done[sl] = [c1]
-            if comm is not None:
+            if push is not None:
                 s_comm.wait_event(e1)
-                comm.replicate_peer(slots[sl], lens[r_i: r_i + 1], rslots[sl], tc.TO_NEXT, stream=s_comm)
+                seq[0] += 1
+                tc.push_peer(push["ctx"], slots[sl], lens[r_i: r_i + 1], push["slots"][sl], slot_cap,
+                             push["mail"][sl], seq[0], stream=s_comm)
                 r1 = torch.cuda.Event()
                 r1.record(s_comm)
                 done[sl].append(r1)
@@ -774,15 +807,25 @@ def run_streaming(args, rank, world, local, dev):
             if times is not None:
                 times.append((e0, e1))
         if args.format == "adaptive" and allow_index:  # density of this checkpoint picks the next format
+            nb = pos - pos0
             if mode["index"]:
-                count = max(0.0, pos - fixed_idx) / (2 + w_avg)
+                count = max(0.0, nb - fixed_idx) / (2 + w_avg)
             else:
-                count = max(0.0, pos - fixed_mask) / w_avg
+                count = max(0.0, nb - fixed_mask) / w_avg
             mode["index"] = count * 16 < total_words
         return pos
 
-    for _ in range(args.warmup):
-        step(None)
+    def train_step(v):  # the synthetic optimizer step producing version v (untimed)
+        with torch.cuda.stream(s_comp):
+            for i in range(len(sizes)):
+                tc.synth_step(S[i], seed, i, v, p53, args.structure, stream=s_comp)
+
+    pos = 0
+    for v in range(1, args.warmup + 1):
+        train_step(v)
+        p1 = checkpoint(v, None, pos)
+        diffs.append((v, pos, p1 - pos))
+        pos = p1
     for st in (s_comp, s_copy, s_comm):
         st.synchronize()
     ctx.check(s_comp)
@@ -791,32 +834,62 @@ def run_streaming(args, rank, world, local, dev):
     clocks = Clocks(local)
     clocks.start()
     time.sleep(0.3)
-    launches0 = ctx.launches
-    t0, t1 = ev(), ev()
-    t0.record(s_comp)
-    enc_times = []
-    total = 0
-    for _ in range(args.steps):
-        total = step(enc_times)
-    for st in (s_copy, s_comm):
-        e = torch.cuda.Event()
-        e.record(st)
-        s_comp.wait_event(e)
-    t1.record(s_comp)
+    launches0 = ctx.launches + (push["ctx"].launches if push else 0)
+    enc_times, step_ms, modes = [], [], []
+    for v in range(args.warmup + 1, n_versions + 1):
+        train_step(v)
+        t0, t1 = ev(), ev()
+        t0.record(s_comp)
+        modes.append("index" if mode["index"] else "mask")
+        p1 = checkpoint(v, enc_times, pos)
+        for st in (s_copy, s_comm):
+            e = torch.cuda.Event()
+            e.record(st)
+            s_comp.wait_event(e)
+        t1.record(s_comp)
+        diffs.append((v, pos, p1 - pos))
+        pos = p1
+        step_ms.append((t0, t1))
     for st in (s_comp, s_copy, s_comm):
         st.synchronize()
-    launches = ctx.launches - launches0
+    launches = ctx.launches + (push["ctx"].launches if push else 0) - launches0
     clk = clocks.stop()
     ctx.check(s_comp)
-    tt = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=dev)
+    if push is not None:
+        push["ctx"].check(s_comm)
+    ms_sum = sum(a.elapsed_time(b) for a, b in step_ms)
+    tt = torch.tensor([ms_sum], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     ms_step = float(tt.item()) / args.steps
     enc_ms = sum(a.elapsed_time(b) for a, b in enc_times) / args.steps
-    recs_info = record_counts(host.numpy(), total)
+    last_v, last_pos, last_n = diffs[-1]
+    recs_info = record_counts(host.numpy()[last_pos:], last_n)
     enc_b, _ = algorithmic_bytes(recs_info)
-    enc_b -= sum(r[4] * r[2] for r in recs_info)  # advance_ref = 0: no ref writes
+    enc_bs, _ = algorithmic_bytes(recs_info, sector=True)
     peak, peak_src = peaks()
+    # ---- verification (untimed): advance, full round trip from Tier-1, oracle windows ----
+    ok_adv = all(torch.equal(r, s_) for r, s_ in zip(R, S))
+    with torch.cuda.stream(s_comp):
+        for i in range(len(sizes)):
+            tc.synth_base(R[i], seed, i, stream=s_comp)
+    del slots
+    big = max(max(16, n) for _, _, n in diffs)
+    stage = [torch.empty(big, dtype=torch.uint8, device=dev) for _ in range(min(5, len(diffs)))]
+    tr0, tr1 = ev(), ev()
+    tr0.record(s_comp)
+    for j in range(0, len(diffs), len(stage)):
+        batch = diffs[j: j + len(stage)]
+        for (v, off, n), buf in zip(batch, stage):
+            tc.stage_host(buf, host.tensor[off:], n, tc.H2D, stream=s_comp)
+        tc.diff_apply(ctx, R, batch[0][0] - 1, stage[:len(batch)], [n for _, _, n in batch], stream=s_comp)
+    tr1.record(s_comp)
+    ctx.check(s_comp)
+    ok_rt = all(torch.equal(r, s_) for r, s_ in zip(R, S))
+    restore_ms = tr0.elapsed_time(tr1)
+    del stage
+    ok_or = _cfg5_oracle_windows(host.numpy(), last_pos, last_n, sizes, wb, seed, args.f, last_v, T, C)
+    ok = ok_adv and ok_rt and ok_or
     if rank == 0:
         res = {
             "metric": METRIC, "value": round(world * W / (ms_step * 1e-3) / 1e9, 2), "unit": "GB/s",
@@ -824,31 +897,94 @@ def run_streaming(args, rank, world, local, dev):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16+u32 (bitwise)",
             "data": "synthetic (seeded splitmix64 state shards, DESIGN.md §6)",
             "config": {"workload": "cfg5: paper's 40B (h5120 inter20480 L128) ZeRO shard r of 8 per rank, "
-                                   "checkpoint every step, streamed encode + async host staging",
+                                   "checkpoint every step of an evolving state, streamed encode + async host staging",
                        "phi": synth.CONFIGS["cfg5"][0], "segments": [[n, w] for n, w in zip(sizes, wb)],
                        "state_bytes_per_rank": W, "f": args.f, "tile_words": T, "chunk_words": C,
-                       "chunks_per_run": K, "runs": len(runs), "advance_ref": 0,
-                       "record_format": args.format, "record_mode_timed": "index" if mode["index"] else "mask",
+                       "chunks_per_run": K, "runs": len(runs), "advance_ref": 1, "versions": n_versions,
+                       "record_format": args.format, "record_modes_timed": sorted(set(modes)),
+                       "tier2": "NVLink push into the ring neighbour's IPC slot" if push else None,
                        "l2": f"no flush: {W / 1e9:.1f} GB of state per rank per step",
                        "parallelism": f"dp{world} shards of the 8-way split" if world > 1 else "1 GPU (shard 0 of 8)"},
             "end_to_end_checkpoint_s": round(ms_step / 1e3, 4),
             "paper_context": "TierCheck reports < 10 s end-to-end checkpointing for up to 40B on 16x A800 (P:16)",
             "roofline": {"kernel": "tc_diff_encode_range x runs (encode_mask + prefix + emit)", "bound": "hbm",
-                         "achieved": round(enc_b / (enc_ms * 1e-3) / 1e9, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(enc_b / (enc_ms * 1e-3) / 1e9 / peak, 4), "traffic": None,
-                         "algorithmic_bytes": enc_b, "peak_source": peak_src, "encode_ms_per_step": round(enc_ms, 3)},
-            "breakdown": {"record_bytes": total, "changed_words": sum(r[4] for r in recs_info),
-                          "tier1_gbs": round(total / ms_step / 1e6, 2)},
+                         "achieved": round(enc_bs / (enc_ms * 1e-3) / 1e9, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(enc_bs / (enc_ms * 1e-3) / 1e9 / peak, 4), "traffic": None,
+                         "algorithmic_bytes": int(enc_bs), "bytes_basis": "sector-granular (SURVEY §8(d))",
+                         "frac_word": round(enc_b / (enc_ms * 1e-3) / 1e9 / peak, 4),
+                         "peak_source": peak_src, "encode_ms_per_step": round(enc_ms, 3)},
+            "breakdown": {"record_bytes_last": last_n, "changed_words_last": sum(r[4] for r in recs_info),
+                          "tier1_gbs": round(last_n / ms_step / 1e6, 2),
+                          "verify": {"reference_equals_state": bool(ok_adv),
+                                     "chain_round_trip_from_tier1": bool(ok_rt),
+                                     "restore_ms_all_versions": round(restore_ms, 2),
+                                     "oracle_windows_last_version": bool(ok_or)}},
             "gpu_launches": launches, "clocks": clk,
             "e2e": None, "e2e_note": "not measured for cfg5: a per-step H2D of the 70.9 GB state would only "
                                      "measure PCIe (see the cfg2 line for the e2e contract)",
         }
         emit(res)
-    if comm is not None:
-        comm.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    if not ok:
+        sys.exit(1)
+
+
+def _cfg5_oracle_windows(buf, pos0, nbytes, sizes, wb, seed, f, v, T, C):
+    """One 256-tile window per segment (chunk 0, tiles 1000..1255) of version v's diff, byte-
+    compared with the oracle's record of that window — inputs from synth (numpy), never the GPU."""
+    import oracle
+
+    pos, ok = pos0, True
+    seen = set()
+    while pos < pos0 + nbytes:
+        h = buf[pos: pos + 64]
+        w, flags = int(h[6]), int(h[7])
+        seg = int(h[12:16].view("<u4")[0])
+        off, m, count = (int(h[a: a + 8].view("<u8")[0]) for a in (16, 24, 32))
+        total = int(h[56:64].view("<u8")[0])
+        if off == 0 and seg not in seen and m >= 1300 * T:
+            seen.add(seg)
+            t0 = 1000
+            st = synth.segment_versions(256 * T, w, seed, seg, [v - 1, v], f, start=t0 * T, threads=4)
+            rc, exp = oracle.encode([st[v - 1].copy()], [st[v]], tile_words=T, chunk_words=C, advance_ref=True,
+                                    version=v, ref_version=v - 1, index_mode=bool(flags & 2))
+            nt = -(-m // T)
+            p = pos + 64
+            if flags & 2:
+                toff = buf[p: p + 4 * (nt + 1)].view("<u4")
+                pi = p + (-(-4 * (nt + 1) // 16) * 16)
+                idx = buf[pi: pi + 2 * count].view("<u2")
+                pv = pi + (-(-2 * count // 16) * 16)
+            else:
+                pm = p
+                p = pm + (-(-4 * (-(-m // 32)) // 16) * 16)
+                toff = buf[p: p + 4 * (nt + 1)].view("<u4")
+                pv = p + (-(-4 * (nt + 1) // 16) * 16)
+            vals = buf[pv: pv + w * count].view("<u2" if w == 2 else "<u4")
+            k0, k1 = int(toff[t0]), int(toff[t0 + 256])
+            e = exp
+            eh_m = 256 * T
+            ep = 64
+            if flags & 2:
+                et = e[ep: ep + 4 * 257].view("<u4")
+                ei = ep + (-(-4 * 257 // 16) * 16)
+                ecount = int(e[32:40].view("<u8")[0])
+                eidx = e[ei: ei + 2 * ecount].view("<u2")
+                ev_ = e[ei + (-(-2 * ecount // 16) * 16):].view("<u2" if w == 2 else "<u4")[:ecount]
+                ok = ok and rc == 0 and np.array_equal(toff[t0: t0 + 257] - np.uint32(k0), et) and \
+                    np.array_equal(idx[k0:k1], eidx) and np.array_equal(vals[k0:k1], ev_)
+            else:
+                emask = e[ep: ep + 4 * (eh_m // 32)].view("<u4")
+                ok = ok and rc == 0 and np.array_equal(buf[pm + 4 * (t0 * T // 32): pm + 4 * ((t0 + 256) * T // 32)].view("<u4"), emask)
+                ecount = int(e[32:40].view("<u8")[0])
+                et0 = ep + (-(-4 * (eh_m // 32) // 16) * 16)
+                et = e[et0: et0 + 4 * 257].view("<u4")
+                ev_ = e[et0 + (-(-4 * 257 // 16) * 16):].view("<u2" if w == 2 else "<u4")[:ecount]
+                ok = ok and np.array_equal(toff[t0: t0 + 257] - np.uint32(k0), et) and np.array_equal(vals[k0:k1], ev_)
+        pos += total
+    return ok and len(seen) == len(sizes)
 
 
 def scatter_reference(X, Y, R, s):
@@ -1157,6 +1293,14 @@ def replicate_probe(tc, comm, rec, obytes, recv, rec_bytes, dev, s_comm, push=No
             tc.peer_wait(pc, push["mine"]["mail"][0], base + i, None, stream=s_comm)
 
         ms_prec = timed(push_rec)
+        # the record-size push by CTA count (the step uses few CTAs so as not to slow the encode
+        # beside it; alone, more stores in flight reach more of the link)
+        by_ctas = {}
+        for ctas in (16, 64, 148, 296, 592):
+            pc.set_push_ctas(ctas)
+            by_ctas[ctas] = timed(push_rec)
+        pc.set_push_ctas(push["ctas"])
+        best_ctas = min(by_ctas, key=by_ctas.get)
         land, lmail = tc.IpcBuffer(G), tc.IpcBuffer(16)
         hs = [None] * dist.get_world_size()
         dist.all_gather_object(hs, [land.handle, lmail.handle])
@@ -1179,6 +1323,10 @@ def replicate_probe(tc, comm, rec, obytes, recv, rec_bytes, dev, s_comm, push=No
         lmail.free()
         out["push"] = {"ms": round(ms_prec, 4), **frac(rec_bytes / ms_prec / 1e6),
                        "ctas": push["ctas"],
+                       "record_by_ctas": {str(c): {"ms": round(t_, 4), **frac(rec_bytes / t_ / 1e6)}
+                                          for c, t_ in by_ctas.items()},
+                       "record_best": {"ctas": best_ctas, "ms": round(by_ctas[best_ctas], 4),
+                                       **frac(rec_bytes / by_ctas[best_ctas] / 1e6)},
                        "ring_shift_1GiB": {"ms": round(ms_p1g, 4), **frac(G / ms_p1g / 1e6)},
                        "ring_shift_1GiB_all_sms": {"ms": round(ms_p1g_max, 4), **frac(G / ms_p1g_max / 1e6)},
                        "note": "tc_push_peer (NVLink stores from every SM into the neighbour's IPC-mapped slot, "
@@ -1455,12 +1603,50 @@ def time_oracle(workload, f, sample_words, steps):
     return W, times, sizes
 
 
+def time_oracle_parallel(workload, f, sample_words, steps, threads):
+    """The same oracle calls on all host cores: the sample's segments are cut into `threads` slices
+    per segment (whole 4096-word tiles), and each thread encodes + restores its slices as their own
+    one-segment shards (the oracle as it stands; ctypes releases the GIL around each C call)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+
+    sizes, wb, X, Y = oracle_sample(workload, f, sample_words)
+    W = sum(n * w for n, w in zip(sizes, wb))
+    jobs = []
+    for s, n in enumerate(sizes):
+        step_ = -(-n // threads + 4095) // 4096 * 4096
+        for a in range(0, n, step_):
+            b = min(n, a + step_)
+            jobs.append({"X": X[s][a:b], "Y": Y[s][a:b], "ref": X[s][a:b].copy(), "rest": X[s][a:b].copy()})
+
+    def one(j, k):
+        cur = j["Y"] if k % 2 == 0 else j["X"]
+        rc, rec = oracle.encode([j["ref"]], [cur], version=k + 1, ref_version=k)
+        rc2, _ = oracle.apply([j["rest"]], k, rec)
+        assert rc == 0 and rc2 == 0
+
+    times = []
+    with ThreadPoolExecutor(threads) as ex:
+        for k in range(steps):
+            t0 = time.perf_counter()
+            list(ex.map(lambda j: one(j, k), jobs))
+            times.append(time.perf_counter() - t0)
+    return W, times, sizes, len(jobs)
+
+
 def cpu_baseline(workload, args):
     W, times, sizes = time_oracle(workload, args.f, args.sample_words, args.oracle_steps)
     t = statistics.median(times)
+    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    Wp, times_p, _, njobs = time_oracle_parallel(workload, args.f, args.sample_words, args.oracle_steps + 1, ncpu)
+    tp = statistics.median(times_p[1:])
     return {"value": round(W / t / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
             "sample": f"words [0, {sizes[0]}) of each of {len(sizes)} segments of the {workload} shard "
                       f"({W / 1e6:.0f} MB of state); encode + restore per step; median of {len(times)}",
+            "all_cores": {"value": round(Wp / tp / 1e9, 4), "unit": "GB/s", "cores": ncpu, "kind": "oracle",
+                          "sample": f"the same sample cut into {njobs} slices (whole tiles), one thread per core; "
+                                    f"median of {len(times_p) - 1} after one warm-up"},
             "host": host_desc()}
 
 
@@ -1478,7 +1664,9 @@ def run_reference(args):
     if rank != 0:
         return
     workload = args.workload or ("cfg2" if world == 1 else "cfg3")
-    W, times, sizes = time_oracle(workload, args.f, args.sample_words, args.warmup + args.steps)
+    # the oracle on all of the box's host cores (slices of the sample, one thread per core)
+    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    W, times, sizes, njobs = time_oracle_parallel(workload, args.f, args.sample_words, args.warmup + args.steps, ncpu)
     times = times[args.warmup:]
     ms = 1e3 * sum(times) / len(times)
     v = round(W / (ms * 1e-3) / 1e9, 4)
@@ -1488,8 +1676,9 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "u16+u32 (bitwise)", "data": "synthetic",
         "config": {"workload": WORKLOADS.get(workload, workload), "f": args.f,
                    "sample": f"words [0, {sizes[0]}) of each segment ({W / 1e6:.0f} MB of state) per step"},
-        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
-                         "sample": f"words [0, {sizes[0]}) of each of {len(sizes)} segments; encode + restore",
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": ncpu, "kind": "oracle",
+                         "sample": f"words [0, {sizes[0]}) of each of {len(sizes)} segments, cut into {njobs} "
+                                   f"slices over {ncpu} threads; encode + restore",
                          "host": host_desc()},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -1521,6 +1710,9 @@ def main():
                     help="N=1: also measure the paper's lossy differential (NEXT row 3) in the step's buffers")
     ap.add_argument("--push-ctas", type=int, default=16,
                     help="CTAs of the Tier-2 NVLink push inside the step (fewer = less interference)")
+    ap.add_argument("--t2-fused", type=int, default=1,
+                    help="push mode: 1 = the encoder writes the record into the neighbour's slot (fused), "
+                         "0 = a separate push kernel after the encode")
     ap.add_argument("--tier2", default="push", choices=["push", "nccl"],
                     help="Tier-2 replication: NVLink stores into the neighbour's IPC slot, or NCCL send/recv")
     ap.add_argument("--recovery", type=int, default=None,

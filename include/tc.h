@@ -235,9 +235,13 @@ tc_status tc_ipc_close(void* dev_ptr);
  * caller orders reuse of a slot (e.g. one slot per in-flight version). */
 tc_status tc_push_peer(tc_ctx* ctx, const void* src, const uint64_t* src_bytes, void* peer_dst,
                        uint64_t peer_cap, void* peer_mailbox, uint64_t version, tc_stream stream);
-/* Encode (as tc_diff_encode) and push the record to the peer slot in one stream-ordered call:
- * the Tier-2 copy leaves as soon as the record is complete, with no host synchronization and
- * no NCCL. */
+/* Encode (as tc_diff_encode) with the Tier-2 copy FUSED into the encoder (SURVEY.md §8(f) NEXT
+ * row 1): every record byte the encode kernels write into `out` is also stored, over NVLink, at the
+ * same offset of `peer_dst` — the record is never re-read from HBM and there is no separate copy
+ * launch, host synchronization or NCCL; the last emitting CTA then publishes {bytes, version} into
+ * `peer_mailbox` with a system-scope release (as tc_push_peer).  A record larger than peer_cap (or
+ * an encode that reports an error) is published as refused (bytes = UINT64_MAX: the receiver's
+ * tc_peer_wait reports TC_ERR_CAPACITY); bytes below peer_cap may then hold a partial record. */
 tc_status tc_diff_encode_push(tc_ctx* ctx, const tc_segment* segs, int nseg, const tc_encode_opts* opts,
                               uint64_t version, uint64_t ref_version, void* out, uint64_t out_cap,
                               uint64_t* out_bytes, void* peer_dst, uint64_t peer_cap,

@@ -186,10 +186,11 @@ class Checkpointer:
       - Tier-2 (`tier2="push"`): `t2_slots` slots + mailboxes on this GPU for the previous rank's
         records, the next rank's mapped here (CUDA IPC, one exchange) — NVLink stores, no NCCL;
         the paced base stream to the same neighbour (BaseReplicator).  world == 1 is the ring of one.
-    save_step(v): encode v on the caller's stream (fused ref advance) and, one step behind (the
-      host never waits for the encode it just issued), finish v-1: read its length, stage it to
-      Tier-1 on the copy stream, push it to the neighbour on the comm stream, fold it onto the
-      optional hot `standby` replica, append it to the chain, pick the next record format (R19).
+    save_step(v): encode v on the caller's stream (fused ref advance; with Tier-2 the encoder also
+      writes the record into the neighbour's slot over NVLink and publishes its mailbox — the
+      fused emit, NEXT row 1) and, one step behind (the host never waits for the encode it just
+      issued), finish v-1: read its length, stage it to Tier-1 on the copy stream, fold it onto
+      the optional hot `standby` replica, append it to the chain, pick the next format (R19).
     recover(): consensus on (base, replay end) over the group, the cascade
       Tier-1 -> Tier-2 per item (plan_loading), the base fetched into the live state
       and the chain folded onto it in batches of N; the reference follows.
@@ -200,7 +201,7 @@ class Checkpointer:
                  t1_bytes: int | None = None, t2_slots: int = 8, standby=None, tile_words: int = 4096,
                  chunk_words: int = 1 << 28, ahead: bool = True, stage_base: bool = True, ref=None,
                  stream=None, base_version: int = 0, push_ctas: int = 16, timing: bool = False,
-                 base_interval: int = 50):
+                 base_interval: int = 50, fused_t2: bool = True):
         from . import tc
 
         self.tc = tc
@@ -255,6 +256,7 @@ class Checkpointer:
             raise ValueError("tier2 must be None or 'push'")
         self.stage_base = stage_base
         self.base_interval = base_interval
+        self.fused_t2 = fused_t2  # Tier-2 written by the encoder itself (else a push kernel after it)
         if stage_base:
             self._stage_base_t1(base_version)
             if self.base_rep is not None:
@@ -271,7 +273,8 @@ class Checkpointer:
             caps = [None] * self.world
             dist.all_gather_object(caps, self.rec_cap, group=self.group)
         nxt, prv = ring_peers(self.rank, self.world)
-        self.prev_cap, self.next_cap = int(caps[prv]), int(caps[nxt])
+        # my slots receive the previous rank's records; the next rank sized its slots for mine
+        self.prev_cap, self.next_cap = int(caps[prv]), self.rec_cap
         self.rx = [tc.IpcBuffer(self.prev_cap) for _ in range(slots)]    # previous rank's records land here
         self.rx_mail = [tc.IpcBuffer(16) for _ in range(slots)]
         self.pctx = tc.Ctx(self.device.index)
@@ -329,8 +332,16 @@ class Checkpointer:
         ref_version = self.pending[-1]["v"] if self.pending else self.chain.head
         e0 = self._ev(self.s_comp) if self.timing else None
         index_mode = bool(self.next_index) and self.cap_idx > 0
-        tc.diff_encode(self.ctx, self.ref, self.seg, self.dev[slot], self.lens_v[slot: slot + 1], version, ref_version,
-                       self.T, self.C, True, stream=self.s_comp, index_mode=index_mode)
+        if self.tier2 == "push" and self.fused_t2:
+            # Tier-2 fused into the encode: the record is written locally and, over NVLink, into
+            # the neighbour's slot version % t2_slots; the encoder publishes its mailbox
+            t2 = version % self.t2_slots
+            tc.diff_encode_push(self.ctx, self.ref, self.seg, self.dev[slot], self.lens_v[slot: slot + 1], version,
+                                ref_version, self.tx[t2], self.next_cap, self.tx_mail[t2], self.T, self.C, True,
+                                stream=self.s_comp, index_mode=index_mode)
+        else:
+            tc.diff_encode(self.ctx, self.ref, self.seg, self.dev[slot], self.lens_v[slot: slot + 1], version,
+                           ref_version, self.T, self.C, True, stream=self.s_comp, index_mode=index_mode)
         e1 = self._ev(self.s_comp)
         self.pending.append({"v": version, "ref_v": ref_version, "slot": slot, "e0": e0, "e1": e1,
                              "index": index_mode})
@@ -377,19 +388,21 @@ class Checkpointer:
             tiers.add("t1")
             if self.timing:
                 self.times["stage"].append((c0, d2h))
-        # Tier-2: NVLink push into the neighbour's slot v % t2_slots (mailbox {bytes, v})
+        # Tier-2: the encode already wrote the record into the neighbour's slot v % t2_slots and
+        # published its mailbox {bytes, v} (fused emit) — or, unfused, a push kernel copies it now
         t2 = None
-        if self.tier2 == "push":
+        if self.tier2 == "push" and n <= self.next_cap:
             t2 = v % self.t2_slots
-            self.s_comm.wait_event(e1)
-            r0 = self._ev(self.s_comm) if self.timing else None
-            tc.push_peer(self.pctx, self.dev[slot], self.lens_v[slot: slot + 1], self.tx[t2], self.next_cap,
-                         self.tx_mail[t2], v, stream=self.s_comm)
-            r1 = self._ev(self.s_comm)
-            busy.append(r1)
+            if not self.fused_t2:
+                self.s_comm.wait_event(e1)
+                r0 = self._ev(self.s_comm) if self.timing else None
+                tc.push_peer(self.pctx, self.dev[slot], self.lens_v[slot: slot + 1], self.tx[t2], self.next_cap,
+                             self.tx_mail[t2], v, stream=self.s_comm)
+                r1 = self._ev(self.s_comm)
+                busy.append(r1)
+                if self.timing:
+                    self.times["push"].append((r0, r1))
             tiers.add("t2")
-            if self.timing:
-                self.times["push"].append((r0, r1))
             # the record that used this neighbour slot before is no longer on Tier-2
             for e in self.chain.entries:
                 if e.version != v and self.where.get(e.version, {}).get("t2") == t2:
@@ -699,7 +712,8 @@ class BaseReplicator:
         else:
             sizes = [self.n]
         nxt, prv = ring_peers(rank, world)
-        self.prev_n, self.peer_n = int(sizes[prv]), int(sizes[nxt])
+        # my slots hold the previous rank's base; the next rank sized its slots for mine
+        self.prev_n, self.peer_n = int(sizes[prv]), self.n
         # this GPU receives the previous rank's bases here (two slots), plus the mailboxes
         self.stage = [tc.IpcBuffer(_pad16(self.prev_n)) for _ in range(2)]
         self.progress = tc.IpcBuffer(16)

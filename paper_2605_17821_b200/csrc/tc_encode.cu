@@ -127,6 +127,17 @@ __device__ __forceinline__ uint16_t ldg_cur(const uint16_t* p) {
     return static_cast<uint16_t>(__ldg(reinterpret_cast<const unsigned short*>(p)));
 }
 
+// Every record write goes through rec_store: with the fused Tier-2 emit on (P.peer_out), the same
+// bytes are also stored at the same offset of the ring neighbour's slot over NVLink — where they fit
+// its capacity (§3.2).  The record is never re-read.
+template <bool PEER, typename T>
+__device__ __forceinline__ void rec_store(const EncParams& P, T* local, T v) {
+    *local = v;
+    if (PEER) {
+        const uint64_t o = static_cast<uint64_t>(reinterpret_cast<const uint8_t*>(local) - P.out);
+        if (o + sizeof(T) <= P.peer_cap) *reinterpret_cast<T*>(P.peer_out + o) = v;
+    }
+}
 // Block / chunk bookkeeping (one thread, after its own stores; nobody waits for it): one packed
 // atomic {done blocks : 24 | changed words : 40} per chunk tells the block that completes the
 // chunk, which writes the header and publishes the next record start.  `nblocks` blocks of chunk
@@ -136,7 +147,7 @@ __device__ __forceinline__ void note_block(const EncParams& P, unsigned long lon
     atomicAdd(&P.group_sum[b / kEmitGroup], static_cast<unsigned long long>(total));
 }
 
-template <int W>
+template <int W, bool PEER>
 __device__ __forceinline__ void count_blocks(const EncParams& P, const BlockInfo& I, uint32_t nblocks,
                                              unsigned long long total, unsigned long long rs) {
     const bool imode = P.index_mode != 0;
@@ -152,38 +163,38 @@ __device__ __forceinline__ void count_blocks(const EncParams& P, const BlockInfo
         else {
         uint8_t* rec = P.out + rs;
         uint64_t* h = reinterpret_cast<uint64_t*>(rec);
-        h[0] = 0x31444354ull /* "TCD1" */ | (1ull << 32) | (static_cast<uint64_t>(W) << 48) |
-               ((imode ? 3ull : 1ull) << 56);
-        h[1] = static_cast<uint64_t>(P.T) | (static_cast<uint64_t>(P.seg[I.seg].seg_id) << 32);
-        h[2] = P.seg[I.seg].word_base + I.chunk_off;
-        h[3] = I.m;
-        h[4] = count;
-        h[5] = P.version;
-        h[6] = P.ref_version;
-        h[7] = rec_total;
+        rec_store<PEER, uint64_t>(P, h + 0, 0x31444354ull /* "TCD1" */ | (1ull << 32) | (static_cast<uint64_t>(W) << 48) |
+                                          ((imode ? 3ull : 1ull) << 56));
+        rec_store<PEER, uint64_t>(P, h + 1, static_cast<uint64_t>(P.T) | (static_cast<uint64_t>(P.seg[I.seg].seg_id) << 32));
+        rec_store<PEER, uint64_t>(P, h + 2, P.seg[I.seg].word_base + I.chunk_off);
+        rec_store<PEER, uint64_t>(P, h + 3, I.m);
+        rec_store<PEER, uint64_t>(P, h + 4, count);
+        rec_store<PEER, uint64_t>(P, h + 5, P.version);
+        rec_store<PEER, uint64_t>(P, h + 6, P.ref_version);
+        rec_store<PEER, uint64_t>(P, h + 7, rec_total);
         uint32_t* gtoff;
         uint8_t* gval;
         if (imode) {
             gtoff = reinterpret_cast<uint32_t*>(rec + index_toff_off());
             uint8_t* gidx = rec + index_idx_off(I.m, P.T);
-            for (uint64_t x = 2 * count; x < pad16(2 * count); ++x) gidx[x] = 0;
+            for (uint64_t x = 2 * count; x < pad16(2 * count); ++x) rec_store<PEER, uint8_t>(P, gidx + x, 0);
             gval = rec + index_val_off(I.m, P.T, count);
         } else {
             uint32_t* gmask = reinterpret_cast<uint32_t*>(rec + kHdrBytes);
-            for (uint64_t x = n_mask; x < pad16(4 * n_mask) / 4; ++x) gmask[x] = 0;
+            for (uint64_t x = n_mask; x < pad16(4 * n_mask) / 4; ++x) rec_store<PEER, uint32_t>(P, gmask + x, 0u);
             gtoff = reinterpret_cast<uint32_t*>(rec + kHdrBytes + pad16(4 * n_mask));
             gval = rec + record_fixed_bytes(I.m, P.T);
         }
-        gtoff[n_tiles] = static_cast<uint32_t>(count);
-        for (uint64_t x = n_tiles + 1; x < pad16(4 * (n_tiles + 1)) / 4; ++x) gtoff[x] = 0;
-        for (uint64_t x = W * count; x < pad16(W * count); ++x) gval[x] = 0;
+        rec_store<PEER, uint32_t>(P, gtoff + n_tiles, static_cast<uint32_t>(count));
+        for (uint64_t x = n_tiles + 1; x < pad16(4 * (n_tiles + 1)) / 4; ++x) rec_store<PEER, uint32_t>(P, gtoff + x, 0u);
+        for (uint64_t x = W * count; x < pad16(W * count); ++x) rec_store<PEER, uint8_t>(P, gval + x, 0);
         }
         st_relaxed(&P.rstart[I.chunk + 1], next | 1ull);
         if (I.chunk + 1 == P.total_chunks) *P.out_bytes = next;
     }
 }
 
-template <int W>
+template <int W, bool PEER>
 __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_t* tile, int tid) {
     using word_t = typename Word<W>::T;
     constexpr uint32_t B = Word<W>::kBlock;
@@ -341,17 +352,20 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
         uint32_t* gtoff = reinterpret_cast<uint32_t*>(rec + (imode ? index_toff_off() : kHdrBytes + pad16(4 * n_mask)));
         const uint32_t p = I.p0 + (mw0 + lane) * 32;
         if (lane < static_cast<int>(MPW) && p < I.m) {
-            if (!imode) gmask[(I.p0 >> 5) + mw0 + lane] = mine;
+            if (!imode) rec_store<PEER, uint32_t>(P, gmask + (I.p0 >> 5) + mw0 + lane, mine);
             if ((p & (P.T - 1)) == 0) gtoff[p / P.T] = woff + pre;  // kernel B adds the block prefix
         }
     }
 
     if (tid == 0) {
         note_block(P, I.b, total, sparse);
-        count_blocks<W>(P, I, 1, total, rs);
+        count_blocks<W, PEER>(P, I, 1, total, rs);
     }
+    // (kernel A's NVLink stores are ordered before kernel B's publish by the kernel boundary and
+    // B's system-scope fence; a per-CTA fence here cost 2.5x on the encode: r2 measurement)
 }
 
+template <bool PEER>
 __global__ void __launch_bounds__(kEncThreads, 6) encode_mask_kernel(const __grid_constant__ EncParams P) {
     extern __shared__ __align__(128) uint8_t tile[];
     __shared__ SmemA sm;
@@ -377,9 +391,9 @@ __global__ void __launch_bounds__(kEncThreads, 6) encode_mask_kernel(const __gri
     __syncthreads();
     if (tid == 0 && sm.I.chunk != 0) sm.rs = ld_relaxed(&P.rstart[sm.I.chunk]);  // value | 1 once published
     if (sm.I.w == 4)
-        mask_block<4>(P, sm, tile, tid);
+        mask_block<4, PEER>(P, sm, tile, tid);
     else
-        mask_block<2>(P, sm, tile, tid);
+        mask_block<2, PEER>(P, sm, tile, tid);
 }
 
 // ------------------------------------------------------------------ kernel A' -----------
@@ -522,7 +536,7 @@ __device__ __forceinline__ uint32_t maskin_block(const EncParams& P, const Block
         for (uint32_t j = 0; j < K; ++j) {
             const uint32_t p = I.p0 + (lane * K + j) * 32;
             if (p < I.m) {
-                if (!imode && !full) gmask[j] = mw[j];
+                if (!imode && !full) rec_store<false, uint32_t>(P, gmask + j, mw[j]);
                 if ((p & tmask) == 0) gtoff[p / P.T] = pre;  // kernel B adds the block prefix
             }
             pre += __popc(mw[j]);
@@ -543,9 +557,9 @@ constexpr uint32_t kMaskinBatch = 4;
 __device__ __noinline__ void count_run(const EncParams& P, const BlockInfo& R, uint32_t n, unsigned long long cnt,
                                        unsigned long long rs) {
     if (R.w == 4)
-        count_blocks<4>(P, R, n, cnt, rs);
+        count_blocks<4, false>(P, R, n, cnt, rs);
     else
-        count_blocks<2>(P, R, n, cnt, rs);
+        count_blocks<2, false>(P, R, n, cnt, rs);
 }
 
 __global__ void __launch_bounds__(kEncThreads, 3) encode_maskin_kernel(const __grid_constant__ EncParams P) {
@@ -623,7 +637,7 @@ __device__ __forceinline__ uint16_t ldg_word(const uint16_t* p) {
 
 // Dense block (more than 4 KB of changed words, not spilled): re-read its mask words from the
 // record and the changed words from cur, pack them in index order (a warp per block).
-template <int W>
+template <int W, bool PEER>
 __device__ __forceinline__ void emit_dense(const EncParams& P, const BlockInfo& I, uint32_t info,
                                            unsigned long long prefix, int lane) {
     using word_t = typename Word<W>::T;
@@ -670,26 +684,29 @@ __device__ __forceinline__ void emit_dense(const EncParams& P, const BlockInfo& 
                     if ((bb >> lane) & 1u) {
                         v[q] = ldg_word(gcur + (q0 + src) * 32 + lane);
                         d[q] = o + __popc(bb & lt);
-                        if (imode) gidx[d[q]] = static_cast<uint16_t>((I.p0 + (q0 + src) * 32 + lane) & tmask);
+                        if (imode) rec_store<PEER, uint16_t>(P, gidx + d[q], static_cast<uint16_t>((I.p0 + (q0 + src) * 32 + lane) & tmask));
                     }
                 }
             }
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-                if (d[q] != 0xffffffffu) gval[d[q]] = v[q];
+                if (d[q] != 0xffffffffu) rec_store<PEER, word_t>(P, gval + d[q], v[q]);
         }
     }
 }
 
 // Copy one batch of up to 4 spilled blocks (<= 64 words each handled here; the rest of a longer
 // block in the caller's loop): loads of the whole batch are issued before any store.
-__device__ __forceinline__ void copy_words(uint8_t* dst, const uint8_t* src, uint32_t w, uint32_t i) {
+template <bool PEER>
+__device__ __forceinline__ void copy_words(const EncParams& P, uint8_t* dst, const uint8_t* src, uint32_t w, uint32_t i) {
     if (w == 4)
-        reinterpret_cast<uint32_t*>(dst)[i] = __ldg(reinterpret_cast<const uint32_t*>(src) + i);
+        rec_store<PEER, uint32_t>(P, reinterpret_cast<uint32_t*>(dst) + i, __ldg(reinterpret_cast<const uint32_t*>(src) + i));
     else
-        reinterpret_cast<uint16_t*>(dst)[i] = __ldg(reinterpret_cast<const unsigned short*>(src) + i);
+        rec_store<PEER, uint16_t>(P, reinterpret_cast<uint16_t*>(dst) + i,
+                            static_cast<uint16_t>(__ldg(reinterpret_cast<const unsigned short*>(src) + i)));
 }
 
+template <bool PEER>
 __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __grid_constant__ EncParams P) {
     __shared__ uint32_t s_warp[kWarps];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -732,10 +749,10 @@ __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __gri
         const uint32_t B = I.w == 4 ? kEncBlockWords4 : kEncBlockWords2;
         if (I.nb && fits) {  // kernel A wrote the tile_off entries of the block block-relative
             if (P.T >= B) {
-                if ((I.p0 & (P.T - 1)) == 0) gtoff[I.p0 / P.T] += pr;
+                if ((I.p0 & (P.T - 1)) == 0) rec_store<PEER, uint32_t>(P, gtoff + I.p0 / P.T, gtoff[I.p0 / P.T] + pr);
             } else {
                 const uint32_t n_t = (I.nb + P.T - 1) / P.T;
-                for (uint32_t t = 0; t < n_t; ++t) gtoff[I.p0 / P.T + t] += pr;
+                for (uint32_t t = 0; t < n_t; ++t) rec_store<PEER, uint32_t>(P, gtoff + I.p0 / P.T + t, gtoff[I.p0 / P.T + t] + pr);
             }
         }
         if (imode) {
@@ -784,14 +801,14 @@ __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __gri
                 const uint32_t i = lane + 32 * k;
                 if (i < cn[q]) {
                     if (wq[q] == 4)
-                        reinterpret_cast<uint32_t*>(dq[q])[i] = v[q][k];
+                        rec_store<PEER, uint32_t>(P, reinterpret_cast<uint32_t*>(dq[q]) + i, v[q][k]);
                     else
-                        reinterpret_cast<uint16_t*>(dq[q])[i] = static_cast<uint16_t>(v[q][k]);
+                        rec_store<PEER, uint16_t>(P, reinterpret_cast<uint16_t*>(dq[q]) + i, static_cast<uint16_t>(v[q][k]));
                 }
             }
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-            for (uint32_t i = 64 + lane; i < cn[q]; i += 32) copy_words(dq[q], sq[q], wq[q], i);
+            for (uint32_t i = 64 + lane; i < cn[q]; i += 32) copy_words<PEER>(P, dq[q], sq[q], wq[q], i);
         if (imode) {  // the u16 in-tile positions, same batching
             uint16_t iv[4][2];
             uint8_t* iq[4];
@@ -810,11 +827,11 @@ __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __gri
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
                     const uint32_t i = lane + 32 * k;
-                    if (i < cn[q]) reinterpret_cast<uint16_t*>(iq[q])[i] = iv[q][k];
+                    if (i < cn[q]) rec_store<PEER, uint16_t>(P, reinterpret_cast<uint16_t*>(iq[q]) + i, iv[q][k]);
                 }
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                for (uint32_t i = 64 + lane; i < cn[q]; i += 32) copy_words(iq[q], sq[q] + kSpillBytes, 2, i);
+                for (uint32_t i = 64 + lane; i < cn[q]; i += 32) copy_words<PEER>(P, iq[q], sq[q] + kSpillBytes, 2, i);
         }
     }
 
@@ -829,9 +846,27 @@ __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __gri
             P.gpre[g] + __shfl_sync(0xffffffffu, wp + inc - c, t) - P.cbase[I.chunk];
         const uint32_t inf = __shfl_sync(0xffffffffu, info, t);
         if (I.w == 4)
-            emit_dense<4>(P, I, inf, prefix, lane);
+            emit_dense<4, PEER>(P, I, inf, prefix, lane);
         else
-            emit_dense<2>(P, I, inf, prefix, lane);
+            emit_dense<2, PEER>(P, I, inf, prefix, lane);
+    }
+    // fused Tier-2 emit: every CTA's peer stores are fenced at system scope; the last CTA publishes
+    // {bytes, version} into the neighbour's mailbox (a refused record: bytes = UINT64_MAX)
+    if (PEER) {
+        __threadfence_system();
+        __syncthreads();
+        if (tid == 0) {
+            const unsigned prev = atomicAdd(P.peer_counter, 1u);
+            if (prev == gridDim.x - 1) {
+                *P.peer_counter = 0u;  // ready for the next push on this ctx (stream-ordered)
+                __threadfence_system();
+                const unsigned long long nb = *reinterpret_cast<const volatile unsigned long long*>(P.out_bytes);
+                const bool ok = nb <= P.peer_cap && *reinterpret_cast<const volatile unsigned int*>(P.err) == 0u;
+                asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(P.peer_mail), "l"(ok ? nb : ~0ull) : "memory");
+                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(P.peer_mail + 1),
+                             "l"(static_cast<unsigned long long>(P.peer_version)) : "memory");
+            }
+        }
     }
 }
 
@@ -844,7 +879,8 @@ cudaError_t launch_encode(const EncParams& p, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= TC_MAX_DEVICES || !attr_set[dev]) {
-        cudaFuncSetAttribute(encode_mask_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(encode_mask_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(encode_mask_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (dev >= 0 && dev < TC_MAX_DEVICES) attr_set[dev] = true;
     }
     if (p.total_blocks == 0) return cudaSuccess;
@@ -860,14 +896,20 @@ cudaError_t launch_encode(const EncParams& p, cudaStream_t s) {
         const uint64_t cap = static_cast<uint64_t>(sms) * (per_sm > 0 ? per_sm : 1);
         encode_maskin_kernel<<<static_cast<unsigned>(want < cap ? want : cap), kEncThreads, 0, s>>>(p);
     } else {
-        encode_mask_kernel<<<static_cast<unsigned>(p.total_blocks), kEncThreads, kEncDynSmem, s>>>(p);
+        if (p.peer_out)
+            encode_mask_kernel<true><<<static_cast<unsigned>(p.total_blocks), kEncThreads, kEncDynSmem, s>>>(p);
+        else
+            encode_mask_kernel<false><<<static_cast<unsigned>(p.total_blocks), kEncThreads, kEncDynSmem, s>>>(p);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     encode_prefix_kernel<<<1, 1024, 0, s>>>(p);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    encode_emit_kernel<<<static_cast<unsigned>(p.n_groups), kEncThreads, 0, s>>>(p);
+    if (p.peer_out)
+        encode_emit_kernel<true><<<static_cast<unsigned>(p.n_groups), kEncThreads, 0, s>>>(p);
+    else
+        encode_emit_kernel<false><<<static_cast<unsigned>(p.n_groups), kEncThreads, 0, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -87,6 +87,14 @@ struct EncParams {
     uint32_t* mstage;                 // index mode: [total_blocks][kMaskStageWords] mask words
     int advance_ref;
     int index_mode;
+    // fused Tier-2 emit (tc_diff_encode_push): every record byte is also stored at the same offset
+    // of the ring neighbour's slot (NVLink), where it fits peer_cap; the last emit CTA publishes
+    // {bytes | UINT64_MAX if refused, peer_version} into peer_mail.  peer_out == nullptr: off.
+    uint8_t* peer_out;
+    uint64_t peer_cap;
+    unsigned long long* peer_mail;
+    uint64_t peer_version;
+    unsigned int* peer_counter;
 };
 
 constexpr uint32_t kMaskStageWords = 256;  // mask words of one block (8192 16-bit words max)
@@ -144,6 +152,9 @@ int ctx_num_sms(tc_ctx* c);
 void ctx_add_launches(tc_ctx* c, uint64_t n);
 uint32_t ctx_push_ctas(tc_ctx* c);
 tc_status ctx_grad_scratch(tc_ctx* c, size_t bytes, cudaStream_t s, void** out);
+tc_status encode_push(tc_ctx* ctx, const tc_segment* segs, int nseg, const tc_encode_opts* opts, uint64_t version,
+                      uint64_t ref_version, void* out, uint64_t out_cap, uint64_t* out_bytes, void* peer_dst,
+                      uint64_t peer_cap, void* peer_mailbox, cudaStream_t s);
 tc_status encode_from_masks(tc_ctx* ctx, const tc_segment* segs, const uint32_t* const* masks, int nseg,
                             const tc_encode_opts* opts, uint64_t version, uint64_t ref_version, void* out,
                             uint64_t out_cap, uint64_t* out_bytes, cudaStream_t s);

@@ -174,9 +174,8 @@ tc_status tc_diff_encode_push(tc_ctx* ctx, const tc_segment* segs, int nseg, con
     if (!peer_dst || !aligned16(peer_dst) || !peer_mailbox || !aligned16(peer_mailbox))
         return fail(TC_ERR_INVALID, "peer_dst / peer_mailbox must be 16-byte aligned device pointers");
     if (version == 0) return fail(TC_ERR_INVALID, "version must be >= 1");
-    tc_status st = tc_diff_encode(ctx, segs, nseg, opts, version, ref_version, out, out_cap, out_bytes, stream);
-    if (st != TC_OK) return st;
-    return tc_push_peer(ctx, out, out_bytes, peer_dst, peer_cap, peer_mailbox, version, stream);
+    return tc::encode_push(ctx, segs, nseg, opts, version, ref_version, out, out_cap, out_bytes, peer_dst, peer_cap,
+                           peer_mailbox, static_cast<cudaStream_t>(stream));
 }
 
 tc_status tc_peer_wait(tc_ctx* ctx, const void* mailbox, uint64_t version, uint64_t* bytes_out, tc_stream stream) {

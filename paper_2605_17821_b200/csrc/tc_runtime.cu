@@ -236,13 +236,26 @@ struct SegSpec {
 };
 }  // namespace
 
+struct PeerEmit {  // fused Tier-2 emit target (tc_diff_encode_push)
+    void* dst = nullptr;
+    uint64_t cap = 0;
+    void* mailbox = nullptr;
+};
+
 static tc_status encode_impl(tc_ctx* ctx, const SegSpec* specs, int nseg, const tc_encode_opts& o,
                              uint64_t version, uint64_t ref_version, void* out, uint64_t out_cap,
-                             uint64_t* out_bytes, cudaStream_t s) {
+                             uint64_t* out_bytes, cudaStream_t s, const PeerEmit* peer = nullptr) {
     cudaSetDevice(ctx->device);
     tc_status st = TC_OK;
     EncParams P;
     memset(&P, 0, sizeof(P));
+    if (peer) {
+        P.peer_out = static_cast<uint8_t*>(peer->dst);
+        P.peer_cap = peer->cap;
+        P.peer_mail = static_cast<unsigned long long*>(peer->mailbox);
+        P.peer_version = version;
+        P.peer_counter = ctx->err + 1;
+    }
     uint64_t blocks = 0, chunks = 0;
     for (int i = 0; i < nseg; ++i) {
         const SegSpec& g = specs[i];
@@ -498,6 +511,31 @@ tc_status ctx_grad_scratch(tc_ctx* c, size_t bytes, cudaStream_t s, void** out) 
 }  // namespace tc
 
 namespace tc {
+// tc_diff_encode with the fused Tier-2 emit: the encoder writes the record into `out` and, over
+// NVLink, into the peer slot; its last emit CTA publishes the mailbox (tc_peer.cu).
+tc_status encode_push(tc_ctx* ctx, const tc_segment* segs, int nseg, const tc_encode_opts* opts, uint64_t version,
+                      uint64_t ref_version, void* out, uint64_t out_cap, uint64_t* out_bytes, void* peer_dst,
+                      uint64_t peer_cap, void* peer_mailbox, cudaStream_t s) {
+    if (!ctx) return fail(TC_ERR_INVALID, "ctx is NULL");
+    tc_encode_opts o;
+    default_opts(opts, &o);
+    tc_status st = check_opts(o);
+    if (st != TC_OK) return st;
+    st = check_segs(segs, nseg, true);
+    if (st != TC_OK) return st;
+    if (!out || !aligned16(out)) return fail(TC_ERR_INVALID, "out must be a 16-byte aligned device pointer");
+    if (!out_bytes) return fail(TC_ERR_INVALID, "out_bytes is NULL");
+    SegSpec sp[TC_MAX_SEGMENTS];
+    for (int i = 0; i < nseg; ++i)
+        sp[i] = {static_cast<uint8_t*>(segs[i].ref), static_cast<const uint8_t*>(segs[i].cur), segs[i].n_words,
+                 segs[i].word_bytes, static_cast<uint32_t>(i), 0};
+    PeerEmit pe;
+    pe.dst = peer_dst;
+    pe.cap = peer_cap;
+    pe.mailbox = peer_mailbox;
+    return encode_impl(ctx, sp, nseg, o, version, ref_version, out, out_cap, out_bytes, s, &pe);
+}
+
 // Encode `cur` against the change masks `masks[s]` (bit i of u32 word i/32 = word i of segment s
 // changed) instead of a reference: the records tc_diff_encode(ref, cur) would produce for any ref
 // with those differences (tc_adam_step_encode).  No reference is read or advanced.

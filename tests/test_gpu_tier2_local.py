@@ -203,3 +203,38 @@ def test_base_replicator_ring_of_one():
         rep.intercept(b1[:1], version=40, interval=10)
     rep.ctx.check(rep.s)
     rep.close()
+
+
+@pytest.mark.parametrize("index_mode", [False, True])
+def test_fused_encode_push_capacity_and_ranges(ctx, tco, index_mode):
+    """tc_diff_encode_push (the encoder writes the record into the peer slot itself): a slot too
+    small for the record -> the mailbox reports refusal (tc_peer_wait: CAPACITY) while the local
+    record is still exact; several chunks and tile sizes land byte-exact in a slot that fits."""
+    sizes, wb = [70001, 9000, 40000], [4, 2, 4]
+    states = [synth.state(sizes, wb, 91, v, 0.2) for v in range(3)]
+    for T, C, ok in ((4096, 1 << 28, False), (256, 8192, True), (1024, 4096 * 3, True)):
+        ref = [to_dev(a) for a in states[0]]
+        cur = [to_dev(a) for a in states[1]]
+        rc, exp = tco.encode([a.copy() for a in states[0]], states[1], tile_words=T, chunk_words=C, version=1,
+                             ref_version=0, index_mode=index_mode)
+        cap = tc.diff_bound(sizes, wb, T, C, index_mode)
+        slot_cap = exp.size if ok else exp.size // 2
+        slot = tc.IpcBuffer(max(16, slot_cap))
+        mail = tc.IpcBuffer(16)
+        out = torch.zeros(cap, dtype=torch.uint8, device="cuda")
+        ob = torch.zeros(1, dtype=torch.int64, device="cuda")
+        got = torch.zeros(1, dtype=torch.int64, device="cuda")
+        s = torch.cuda.Stream()
+        tc.diff_encode_push(ctx, ref, cur, out, ob, 1, 0, slot, slot_cap, mail, T, C, True, stream=s,
+                            index_mode=index_mode)
+        tc.peer_wait(ctx, mail, 1, got, stream=s)
+        rc = ctx.check_status(s)
+        n = int(ob.item())
+        assert n == exp.size and np.array_equal(out[:n].cpu().numpy(), exp)
+        if ok:
+            assert rc == tc.OK and int(got.item()) == n
+            assert np.array_equal(slot.tensor[:n].cpu().numpy(), exp)
+        else:
+            assert rc == tc.ERR_CAPACITY and int(got.item()) == 0
+        slot.free()
+        mail.free()
