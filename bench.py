@@ -644,6 +644,8 @@ def run_ours(args):
                 "unit": "GB/s",
                 "frac": round(enc_bs / (enc_ms * 1e-3) / 1e9 / peak, 4),
                 "traffic": traffic.get("encode"),
+                "traffic_source": (f"stored ncu capture {traffic.get('source')} ({traffic.get('round', 'r6')}), "
+                                   "same kernels and workload; not measured in this run") if traffic else None,
                 "algorithmic_bytes": int(enc_bs),
                 "bytes_basis": "sector-granular (SURVEY §8(d): a scattered 4-byte ref-advance write moves its "
                                "32-byte sector); word-granular below",

@@ -189,47 +189,85 @@ __device__ __forceinline__ uint32_t flags16(const float* x, uint64_t n, uint64_t
     return f;
 }
 
-// pass 1: thread t of block b takes elements [b*kGB + 16t, +16): per-thread counts, a block scan
-// in index order, the group sums; sparse blocks pack their entries into the spill slot
-__global__ void __launch_bounds__(kGThreads) grad_count_kernel(const __grid_constant__ SparseParams P) {
-    __shared__ uint32_t s_warp[kGThreads / 32];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint64_t b = blockIdx.x;
-    const uint64_t i0 = b * kGB + 16ull * tid;
-    const float thr = *P.thr;
-    float v[16];
-    const uint32_t f = flags16(P.x, P.n, i0, thr, v);
-    const uint32_t c = __popc(f);
-    uint32_t inc = c;
+// the 16 elements [i0, i0 + 16) of one thread as four 16-byte loads (issued, not consumed)
+__device__ __forceinline__ void load16(const float* x, uint64_t n, uint64_t i0, float4 (&q)[4]) {
+    if (i0 + 16 <= n) {
+        const float4* p = reinterpret_cast<const float4*>(x + i0);
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += y;
-    }
-    if (lane == 31) s_warp[wid] = inc;
-    __syncthreads();
-    uint32_t wp = 0, total = 0;
+        for (int k = 0; k < 4; ++k) q[k] = __ldg(p + k);
+    } else {
 #pragma unroll
-    for (int k = 0; k < static_cast<int>(kGThreads / 32); ++k) {
-        wp += k < wid ? s_warp[k] : 0u;
-        total += s_warp[k];
-    }
-    if (tid == 0) {
-        P.bcount[b] = total | (total > kGSpill ? kDenseBit : 0u);
-        if (total) atomicAdd(&P.gsum[b / kGGroup], static_cast<unsigned long long>(total));
-    }
-    if (total == 0 || total > kGSpill || f == 0) return;
-    uint16_t* sv = reinterpret_cast<uint16_t*>(P.spill + b * (kGSpill * 6));
-    int32_t* si = reinterpret_cast<int32_t*>(P.spill + b * (kGSpill * 6) + kGSpill * 2);
-    uint32_t k = wp + inc - c;
-#pragma unroll
-    for (int e = 0; e < 16; ++e)
-        if ((f >> e) & 1u) {
-            const uint64_t i = i0 + e;
-            sv[k] = __half_as_ushort(__float2half_rn(v[e]));
-            si[k] = static_cast<int32_t>(i - i / P.chunk * P.chunk);
-            ++k;
+        for (int k = 0; k < 4; ++k) {
+            const uint64_t j = i0 + 4 * k;
+            q[k] = make_float4(j < n ? x[j] : 0.0f, j + 1 < n ? x[j + 1] : 0.0f, j + 2 < n ? x[j + 2] : 0.0f,
+                               j + 3 < n ? x[j + 3] : 0.0f);
         }
+    }
+}
+
+// pass 1 (persistent, grid-stride over blocks): thread t of block b takes elements [b*kGB + 16t,
+// +16); the loads of the CTA's next block are issued before the current one is scanned, so the
+// HBM stream never waits on a block's scan and spill (one block per CTA ran at 4.2 TB/s, r2 ncu):
+// per-thread counts, a block scan in index order, the group sums; sparse blocks pack their
+// entries into the spill slot
+__global__ void __launch_bounds__(kGThreads) grad_count_kernel(const __grid_constant__ SparseParams P) {
+    __shared__ uint32_t s_warp[2][kGThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const float thr = *P.thr;
+    float4 q[4], qn[4];
+    uint64_t b = blockIdx.x;
+    if (b < P.nblocks) load16(P.x, P.n, b * kGB + 16ull * tid, q);
+    for (uint32_t it = 0; b < P.nblocks; b += gridDim.x, ++it) {
+        const uint64_t bn = b + gridDim.x;
+        if (bn < P.nblocks) load16(P.x, P.n, bn * kGB + 16ull * tid, qn);
+        const uint64_t i0 = b * kGB + 16ull * tid;
+        float v[16];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            v[4 * k] = q[k].x;
+            v[4 * k + 1] = q[k].y;
+            v[4 * k + 2] = q[k].z;
+            v[4 * k + 3] = q[k].w;
+        }
+        uint32_t f = 0;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) f |= keep(v[e], thr) ? (1u << e) : 0u;
+        const uint32_t c = __popc(f);
+        uint32_t inc = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += y;
+        }
+        uint32_t* sw = s_warp[it & 1];  // alternating: no second barrier per block
+        if (lane == 31) sw[wid] = inc;
+        __syncthreads();
+        uint32_t wp = 0, total = 0;
+#pragma unroll
+        for (int k = 0; k < static_cast<int>(kGThreads / 32); ++k) {
+            wp += k < wid ? sw[k] : 0u;
+            total += sw[k];
+        }
+        if (tid == 0) {
+            P.bcount[b] = total | (total > kGSpill ? kDenseBit : 0u);
+            if (total) atomicAdd(&P.gsum[b / kGGroup], static_cast<unsigned long long>(total));
+        }
+        if (total != 0 && total <= kGSpill && f != 0) {
+            uint16_t* sv = reinterpret_cast<uint16_t*>(P.spill + b * (kGSpill * 6));
+            int32_t* si = reinterpret_cast<int32_t*>(P.spill + b * (kGSpill * 6) + kGSpill * 2);
+            uint32_t k = wp + inc - c;
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+                if ((f >> e) & 1u) {
+                    const uint64_t i = i0 + e;
+                    sv[k] = __half_as_ushort(__float2half_rn(v[e]));
+                    si[k] = static_cast<int32_t>(i - i / P.chunk * P.chunk);
+                    ++k;
+                }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) q[k] = qn[k];
+    }
 }
 
 // group prefix, chunk starts, payload length + capacity, header, chunk table and pads (1 CTA)
@@ -937,7 +975,13 @@ tc_status tc_grad_compress(tc_ctx* ctx, const float* grad, uint64_t n, const tc_
     cudaError_t e0 = cudaMemsetAsync(P.gsum, 0, 8 * P.ngroups, s);
     if (e0 != cudaSuccess) return cuda_fail(e0, "cudaMemsetAsync(group sums)");
     grad_sample_kernel<<<1, 1024, 0, s>>>(P);
-    grad_count_kernel<<<static_cast<unsigned>(P.nblocks), kGThreads, 0, s>>>(P);
+    {  // persistent: as many CTAs as fit, never more than blocks
+        static int per_sm = 0;
+        if (!per_sm && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grad_count_kernel, kGThreads, 0) != cudaSuccess)
+            per_sm = 4;
+        const uint64_t cap = static_cast<uint64_t>(tc::ctx_num_sms(ctx)) * (per_sm > 0 ? per_sm : 1);
+        grad_count_kernel<<<static_cast<unsigned>(P.nblocks < cap ? P.nblocks : cap), kGThreads, 0, s>>>(P);
+    }
     grad_prefix_kernel<<<1, 1024, 0, s>>>(P);
     grad_emit_kernel<<<static_cast<unsigned>(P.ngroups), kGThreads, 0, s>>>(P);
     cudaError_t e = cudaGetLastError();
