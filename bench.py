@@ -173,6 +173,42 @@ class Clocks:
 
 
 # ------------------------------------------------------------- the GPU arm --------------
+S3_ADAM = 2  # --structure 2: the state before / after one real Adam step
+
+
+def adam_pair(X, Y, seed, s):
+    """S3 "Adam-realistic" inputs (input preparation only — torch ops, untimed): X =
+    a mid-training state (bf16 weights = RNE of the fp32 master ~ N(0, 0.02²), moments ~ 1e-3
+    scale), Y = X after ONE bias-corrected Adam step (lr 1e-4, betas 0.9 / 0.999, eps 1e-8, step
+    100) with a random gradient ~ N(0, 1e-3²).  Every fp32 word of master / m / v changes; the bf16
+    words change where the update moves the master across a bf16 rounding boundary (~half)."""
+    import torch
+
+    g = torch.Generator(device=X[1].device).manual_seed(int(seed))
+    lr, b1, b2, eps, t = 1e-4, 0.9, 0.999, 1e-8, 100
+    n = X[1].numel()
+    step = 1 << 26
+    with torch.cuda.stream(s):
+        for a in range(0, n, step):
+            b = min(n, a + step)
+            master = X[1].view(torch.float32)[a:b]
+            m = X[2].view(torch.float32)[a:b]
+            v = X[3].view(torch.float32)[a:b]
+            master.normal_(0.0, 0.02, generator=g)
+            m.normal_(0.0, 1e-3, generator=g)
+            v.normal_(0.0, 1e-3, generator=g)
+            v.mul_(v)
+            X[0][a:b].copy_(master.to(torch.bfloat16).view(torch.int16))
+            grad = torch.empty_like(master).normal_(0.0, 1e-3, generator=g)
+            m2 = m * b1 + grad * (1 - b1)
+            v2 = v * b2 + grad * grad * (1 - b2)
+            upd = (m2 / (1 - b1 ** t)) / ((v2 / (1 - b2 ** t)).sqrt() + eps)
+            master2 = master - lr * upd
+            Y[1].view(torch.float32)[a:b].copy_(master2)
+            Y[2].view(torch.float32)[a:b].copy_(m2)
+            Y[3].view(torch.float32)[a:b].copy_(v2)
+            Y[0][a:b].copy_(master2.to(torch.bfloat16).view(torch.int16))
+    s.synchronize()
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -220,13 +256,22 @@ def run_ours(args):
     Y = [alloc(n, w) for n, w in zip(sizes, wb)]
     A = [alloc(n, w) for n, w in zip(sizes, wb)]  # the advancing reference (chain state)
     R = [alloc(n, w) for n, w in zip(sizes, wb)]  # the restore replica (fold target)
-    with torch.cuda.stream(s_comp):
-        for s in range(len(sizes)):
-            tc.synth_base(X[s], seed, s, stream=s_comp)
-            Y[s].copy_(X[s])
-            tc.synth_step(Y[s], seed, s, 1, p53, args.structure, stream=s_comp)
-            A[s].copy_(X[s])
-            R[s].copy_(X[s])
+    if args.structure == S3_ADAM:
+        if wb != [2, 4, 4, 4]:
+            raise SystemExit("--structure 2 needs the bf16 + fp32 master/m/v layout")
+        adam_pair(X, Y, seed, s_comp)
+        with torch.cuda.stream(s_comp):
+            for s in range(len(sizes)):
+                A[s].copy_(X[s])
+                R[s].copy_(X[s])
+    else:
+        with torch.cuda.stream(s_comp):
+            for s in range(len(sizes)):
+                tc.synth_base(X[s], seed, s, stream=s_comp)
+                Y[s].copy_(X[s])
+                tc.synth_step(Y[s], seed, s, 1, p53, args.structure, stream=s_comp)
+                A[s].copy_(X[s])
+                R[s].copy_(X[s])
     s_comp.synchronize()
     cap = tc.diff_bound(sizes, wb, T, C)
     cap_idx = tc.diff_bound(sizes, wb, T, C, index_mode=True)
@@ -433,7 +478,7 @@ def run_ours(args):
 
         def ck_finished(nb):
             if nb is not None:
-                ck_done.append((ck.chain.head, nb, ck.where[ck.chain.head]["index"]))
+                ck_done.append((ck.chain.head, nb, ck.where[ck.chain.head]["fmt"]))
                 ck.reclaim(max(ck.chain.base_version, ck.chain.head - 1))
             return nb
 
@@ -506,10 +551,10 @@ def run_ours(args):
         n_ops["fold"] = ck.times["fold"]
         n_ops["stage"] = ck.times["stage"]
         state["rest_version"] = ck.chain.head  # the standby replica (R) and the reference (A)
-        state["index"] = bool(ck.next_index)    # the format the next record would take
+        state["index"] = ck.next_fmt == "index"  # the format the next record would take
         timed_done = [d for d in ck_done if d[0] >= v_timed0]
         n_ops["replicate"] = [(a, b, d[1]) for (a, b), d in zip(ck.times["push"], timed_done)]
-        state["modes"] = ["index" if d[2] else "mask" for d in timed_done]
+        state["modes"] = [d[2] for d in timed_done]
     ms = t_start.elapsed_time(t_end)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -572,14 +617,18 @@ def run_ours(args):
     restore = None
     if args.restore_chain > 0:
         restore = restore_bench(tc, ctx, X, Y, A, R, recs[0], sizes, wb, seed, p53, T, C, s_comp,
-                                args.restore_chain, args.structure, peak, dev, state["index"], comm=comm,
+                                args.restore_chain, args.structure if args.structure != S3_ADAM else 0, peak, dev,
+                                state["index"], comm=comm,
                                 spare=recs[1] if len(recs) > 1 else None,
                                 recovery=args.recovery if args.recovery is not None else workload == "cfg4")
         # put the step buffers back to the X / Y pair (X intact; Y, A, R were reused)
+        if args.structure == S3_ADAM:
+            adam_pair(X, Y, seed, s_comp)
         with torch.cuda.stream(s_comp):
             for i in range(len(sizes)):
-                Y[i].copy_(X[i])
-                tc.synth_step(Y[i], seed, i, 1, p53, args.structure, stream=s_comp)
+                if args.structure != S3_ADAM:
+                    Y[i].copy_(X[i])
+                    tc.synth_step(Y[i], seed, i, 1, p53, args.structure, stream=s_comp)
                 A[i].copy_(X[i])
                 R[i].copy_(X[i])
         s_comp.synchronize()
@@ -620,7 +669,7 @@ def run_ours(args):
                 "segments": [[n, w] for n, w in zip(sizes, wb)],
                 "state_bytes_per_rank": W,
                 "f": args.f,
-                "structure": "S1 iid" if args.structure == 0 else "S2 runs",
+                "structure": {0: "S1 iid", 1: "S2 runs", S3_ADAM: "S3 Adam step (torch, lr 1e-4)"}[args.structure],
                 "tile_words": T,
                 "chunk_words": C,
                 "fold_records_per_step": 1,
@@ -1704,7 +1753,7 @@ def main():
     ap.add_argument("--overlap-fold", type=int, default=0,
                     help="N = 1: fold record k-1 on a high-priority stream beside encode k")
     ap.add_argument("--timeline", action="store_true")
-    ap.add_argument("--format", default="adaptive", choices=["mask", "index", "adaptive"],
+    ap.add_argument("--format", default="adaptive", choices=["mask", "index", "full", "adaptive"],
                     help="record format: mask, index (u16 positions), or adaptive per step from density")
     ap.add_argument("--restore-chain", type=int, default=8, help="records in the chained-restore probe (0: off)")
     ap.add_argument("--e2e-steps", type=int, default=6)

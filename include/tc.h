@@ -92,18 +92,24 @@ typedef struct tc_segment {
     uint32_t reserved;    /* must be 0 */
 } tc_segment;
 
+enum { TC_FORMAT_MASK = 0, TC_FORMAT_INDEX = 1, TC_FORMAT_FULL = 2 };
+
 typedef struct tc_encode_opts {
     uint32_t tile_words;  /* T: power of two in [32, 65536]; default 4096 (reading R7)          */
     uint32_t advance_ref; /* 1 (default): ref[i] <- cur[i] for every changed word, so the next
                              record is incremental (reading R2); 0: ref untouched             */
     uint64_t chunk_words; /* C: multiple of T, <= 2^31-1; default 2^28 (PAPER.md:203 chunking,
                              reading R8)                                                      */
-    uint32_t index_mode;  /* 0 (default): mask section (4 bytes per 32 words).  1: index mode —
-                             the mask is replaced by u16[count] in-tile positions after tile_off
-                             (flags bit1; 2 bytes per changed word), smaller when f < 1/16: the
-                             lossless analog of the paper's "FP16 values and INT32 indices"
-                             sparse payload (§3.2).  Records of both modes fold
-                             together.  Requires T <= 8192 (restore stages a tile's mask words). */
+    uint32_t index_mode;  /* record format (TC_FORMAT_*).  0 (default): mask section (4 bytes per
+                             32 words).  1: index mode — the mask is replaced by u16[count] in-tile
+                             positions after tile_off (flags bit1; 2 bytes per changed word),
+                             smaller when f < 1/16: the lossless analog of the paper's "FP16
+                             values and INT32 indices" sparse payload (§3.2);
+                             requires T <= 8192.  2: full records (flags 5, reading R21) — every
+                             word of the chunk, no mask / tile_off (count = m); smaller than a mask
+                             record when more than 1 - 1/(8w) of the words changed (the dense
+                             regime of a real optimizer step) and encoded by one streaming copy.
+                             Records of all three formats fold together. */
     uint32_t reserved;    /* must be 0 */
 } tc_encode_opts;
 

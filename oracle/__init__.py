@@ -46,6 +46,8 @@ def lib():
         L.tco_record_bytes.argtypes = [u64, u32, u32, u64]
         L.tco_record_bytes_index.restype = u64
         L.tco_record_bytes_index.argtypes = [u64, u32, u32, u64]
+        L.tco_record_bytes_full.restype = u64
+        L.tco_record_bytes_full.argtypes = [u64, u32]
         L.tco_encode.restype = ctypes.c_int
         L.tco_encode.argtypes = [
             vp, vp, vp, vp, ctypes.c_int, u32, u64, ctypes.c_int, ctypes.c_int, u64, u64, vp, u64,
@@ -88,18 +90,22 @@ def _seg_arrays(segs):
     return n, w
 
 
-def record_bytes(m: int, tile_words: int, word_bytes: int, count: int, index_mode: bool = False) -> int:
+def record_bytes(m: int, tile_words: int, word_bytes: int, count: int, index_mode: bool = False,
+                 full: bool = False) -> int:
+    if full:
+        return int(lib().tco_record_bytes_full(m, word_bytes))
     f = lib().tco_record_bytes_index if index_mode else lib().tco_record_bytes
     return int(f(m, tile_words, word_bytes, count))
 
 
-def worst_case_bytes(sizes, word_bytes, tile_words: int, chunk_words: int, index_mode: bool = False) -> int:
+def worst_case_bytes(sizes, word_bytes, tile_words: int, chunk_words: int, index_mode: bool = False,
+                     full: bool = False) -> int:
     tot = 0
     for n, w in zip(sizes, word_bytes):
         off = 0
         while True:
             m = min(n - off, chunk_words)
-            tot += record_bytes(m, tile_words, w, m, index_mode)
+            tot += record_bytes(m, tile_words, w, m, index_mode, full)
             off += m
             if off >= n:
                 break
@@ -107,21 +113,23 @@ def worst_case_bytes(sizes, word_bytes, tile_words: int, chunk_words: int, index
 
 
 def encode(ref, cur, tile_words=4096, chunk_words=1 << 28, advance_ref=True, version=1,
-           ref_version=0, cap=None, index_mode=False):
+           ref_version=0, cap=None, index_mode=False, full=False):
     """Encode lists of per-segment numpy arrays (uint16 / uint32).  Returns (rc, bytes).
+    Record format: mask (default), index (``index_mode``) or full (``full``: every word).
 
     ``ref`` arrays are modified in place when ``advance_ref`` is true."""
     n, w = _seg_arrays(ref)
     n2, w2 = _seg_arrays(cur)
     assert (n == n2).all() and (w == w2).all()
     if cap is None:
-        cap = worst_case_bytes([int(x) for x in n], [int(x) for x in w], tile_words, chunk_words, index_mode)
+        cap = worst_case_bytes([int(x) for x in n], [int(x) for x in w], tile_words, chunk_words, index_mode, full)
     out = np.zeros(max(cap, 1), dtype=np.uint8)
     rp = (ctypes.c_void_p * len(ref))(*[_ptr(a) for a in ref])
     cp = (ctypes.c_void_p * len(cur))(*[_ptr(a) for a in cur])
     ob = ctypes.c_uint64(0)
     rc = lib().tco_encode(rp, cp, _ptr(n), _ptr(w), len(ref), tile_words, chunk_words,
-                          1 if advance_ref else 0, 1 if index_mode else 0, version, ref_version, _ptr(out), cap,
+                          1 if advance_ref else 0, 2 if full else (1 if index_mode else 0), version, ref_version,
+                          _ptr(out), cap,
                           ctypes.byref(ob))
     return rc, out[: ob.value].copy()
 

@@ -53,10 +53,47 @@ uint64_t tco_record_bytes_index(uint64_t m, uint32_t T, uint32_t w, uint64_t cou
     return HDR_BYTES + pad16(4 * (ceil_div(m, T) + 1)) + pad16(2 * count) + pad16((uint64_t)w * count);
 }
 
+/* Full record (flags bit2 FULL, reading R21): 64 + pad16(w*m) — every word of
+ * the chunk, no mask, no tile_off. */
+uint64_t tco_record_bytes_full(uint64_t m, uint32_t w) { return HDR_BYTES + pad16((uint64_t)w * m); }
+
+/* Full-format chunk: header (count = m) | values = cur[0..m) in index order.  The reference
+ * still advances only at the changed words (the same result as copying all of cur). */
+static int encode_chunk_full(void* ref, const void* cur, uint64_t chunk_off, uint64_t m, uint32_t w,
+                             uint32_t T, uint32_t seg, int advance_ref, uint64_t version, uint64_t ref_version,
+                             uint8_t* out, uint64_t cap, uint64_t* written) {
+    uint64_t total = tco_record_bytes_full(m, w);
+    if (total > cap) return TCO_ERR_CAPACITY;
+    memset(out, 0, total);
+    for (uint64_t i = 0; i < m; i++) {
+        uint32_t a = load_word(ref, chunk_off + i, w);
+        uint32_t b = load_word(cur, chunk_off + i, w);
+        store_word(out + HDR_BYTES, i, w, b);
+        if (advance_ref && a != b) store_word(ref, chunk_off + i, w, b);
+    }
+    out[0] = 'T'; out[1] = 'C'; out[2] = 'D'; out[3] = '1';
+    put_u16(out + 4, 1);
+    out[6] = (uint8_t)w;
+    out[7] = 5; /* REPLACE | FULL */
+    put_u32(out + 8, T);
+    put_u32(out + 12, seg);
+    put_u64(out + 16, chunk_off);
+    put_u64(out + 24, m);
+    put_u64(out + 32, m);
+    put_u64(out + 40, version);
+    put_u64(out + 48, ref_version);
+    put_u64(out + 56, total);
+    *written = total;
+    return TCO_OK;
+}
+
 /* one chunk [chunk_off, chunk_off+m) of one segment. */
 static int encode_chunk(void* ref, const void* cur, uint64_t chunk_off, uint64_t m, uint32_t w,
                         uint32_t T, uint32_t seg, int advance_ref, int index_mode, uint64_t version,
                         uint64_t ref_version, uint8_t* out, uint64_t cap, uint64_t* written) {
+    if (index_mode == 2)
+        return encode_chunk_full(ref, cur, chunk_off, m, w, T, seg, advance_ref, version, ref_version, out, cap,
+                                 written);
     /* 1. count the changed words: unsigned bitwise compare of each word (reading R5). */
     uint64_t count = 0;
     for (uint64_t i = 0; i < m; i++)
@@ -146,6 +183,7 @@ int tco_encode(void* const* ref, const void* const* cur, const uint64_t* n, cons
                uint64_t ref_version, uint8_t* out, uint64_t out_cap, uint64_t* out_bytes) {
     *out_bytes = 0;
     if (nseg < 0 || !is_pow2(T) || T < 32 || T > 65536) return TCO_ERR_INVALID;
+    if (index_mode < 0 || index_mode > 2) return TCO_ERR_INVALID;
     if (C == 0 || C % T != 0 || C > MAX_CHUNK_WORDS) return TCO_ERR_INVALID;
     uint64_t pos = 0;
     for (int s = 0; s < nseg; s++) {
@@ -170,7 +208,7 @@ int tco_encode(void* const* ref, const void* const* cur, const uint64_t* n, cons
 /* ---------------------------------------------------------------- restore ---- */
 
 typedef struct {
-    uint32_t w, T, seg, index_mode;
+    uint32_t w, T, seg, index_mode, full;
     uint64_t chunk_off, m, count, version, ref_version, total;
     const uint8_t* mask; /* mask mode */
     const uint8_t* toff;
@@ -185,8 +223,9 @@ static int parse_header(const uint8_t* p, uint64_t avail, rec_view* r) {
     if (get_u16(p + 4) != 1) return TCO_ERR_CORRUPT;
     r->w = p[6];
     if (r->w != 2 && r->w != 4) return TCO_ERR_CORRUPT;
-    if (p[7] != 1 && p[7] != 3) return TCO_ERR_CORRUPT;
+    if (p[7] != 1 && p[7] != 3 && p[7] != 5) return TCO_ERR_CORRUPT;
     r->index_mode = p[7] == 3;
+    r->full = p[7] == 5;
     r->T = get_u32(p + 8);
     if (!is_pow2(r->T) || r->T < 32 || r->T > 65536) return TCO_ERR_CORRUPT;
     r->seg = get_u32(p + 12);
@@ -197,11 +236,18 @@ static int parse_header(const uint8_t* p, uint64_t avail, rec_view* r) {
     r->ref_version = get_u64(p + 48);
     r->total = get_u64(p + 56);
     if (r->m > MAX_CHUNK_WORDS || r->count > r->m) return TCO_ERR_CORRUPT;
-    uint64_t want = r->index_mode ? tco_record_bytes_index(r->m, r->T, r->w, r->count)
-                                   : tco_record_bytes(r->m, r->T, r->w, r->count);
+    if (r->full && r->count != r->m) return TCO_ERR_CORRUPT; /* a full record holds every word */
+    uint64_t want = r->full ? tco_record_bytes_full(r->m, r->w)
+                    : r->index_mode ? tco_record_bytes_index(r->m, r->T, r->w, r->count)
+                                    : tco_record_bytes(r->m, r->T, r->w, r->count);
     if (r->total != want) return TCO_ERR_CORRUPT;
     if (r->total > avail) return TCO_ERR_CORRUPT;
-    if (!r->index_mode) {
+    if (r->full) {
+        r->mask = NULL;
+        r->toff = NULL;
+        r->idx = NULL;
+        r->values = p + HDR_BYTES;
+    } else if (!r->index_mode) {
         r->mask = p + HDR_BYTES;
         r->toff = r->mask + pad16(4 * ceil_div(r->m, 32));
         r->idx = NULL;
@@ -218,6 +264,7 @@ static int parse_header(const uint8_t* p, uint64_t avail, rec_view* r) {
 /* Body check: tile_off[0] = 0, per-tile popcount equals
  * tile_off[t+1]-tile_off[t], tile_off[n_tiles] = count, mask bits >= m are zero. */
 static int check_body(const rec_view* r) {
+    if (r->full) return TCO_OK; /* no mask, no tile_off: every word is a value */
     uint64_t n_tiles = ceil_div(r->m, r->T);
     uint64_t n_mask = ceil_div(r->m, 32);
     if (get_u32(r->toff) != 0) return TCO_ERR_CORRUPT;
@@ -303,7 +350,11 @@ int tco_apply(void* const* state, const uint64_t* n, const uint32_t* w, int nseg
     for (uint64_t k = 0; k < n_rec; k++) {
         rec_view r;
         parse_header(diff + pos, diff_bytes - pos, &r);
-        if (r.index_mode) {
+        if (r.full) {
+            /* every word of the chunk takes its value */
+            for (uint64_t i = 0; i < r.m; i++)
+                store_word(state[r.seg], r.chunk_off + i, r.w, load_word(r.values, i, r.w));
+        } else if (r.index_mode) {
             /* the k-th value goes to word t*T + idx[k] of the chunk, t = the tile holding k */
             uint64_t n_tiles = ceil_div(r.m, r.T);
             for (uint64_t t = 0; t < n_tiles; t++)

@@ -27,7 +27,8 @@
  *     4     2 format_version = 1
  *     6     1 word_bytes (2 | 4)
  *     7     1 flags (bit0 REPLACE = 1; bit1 INDEX: the mask section is replaced by u16[count]
- *               in-tile positions after tile_off — DESIGN.md §4)
+ *               in-tile positions after tile_off — DESIGN.md §4; bit2 FULL: flags = 5, every
+ *               word of the chunk, count = m, no mask and no tile_off — reading R21)
  *     8     4 tile_words T (power of two, 32..65536)
  *    12     4 segment_id
  *    16     8 chunk_word_offset
@@ -38,6 +39,7 @@
  *    56     8 total_bytes of this record
  *    64       mask u32[ceil(m/32)]  | tile_off u32[ceil(m/T)+1] | values (w*count)      (mask mode)
  *    64       tile_off u32[ceil(m/T)+1] | idx u16[count] | values (w*count)            (index mode)
+ *    64       values (w*m)                                                            (full)
  *
  * Parity status: every function here is pinned by tests/test_oracle_*.py against
  * numpy library special cases, closed forms, invariants, brute force and the
@@ -62,10 +64,12 @@ enum {
 /* Closed-form byte size of one record (Appendix A), mask mode and index mode. */
 uint64_t tco_record_bytes(uint64_t m, uint32_t tile_words, uint32_t word_bytes, uint64_t count);
 uint64_t tco_record_bytes_index(uint64_t m, uint32_t tile_words, uint32_t word_bytes, uint64_t count);
+uint64_t tco_record_bytes_full(uint64_t m, uint32_t word_bytes);
 
 /* Encode one shard (nseg segments, segment s = n[s] words of w[s] bytes) into the
  * concatenation of its records, segment 0..nseg-1, chunks ascending.
  * chunk_words must be a positive multiple of tile_words and <= 2^31-1.
+ * index_mode: 0 mask records, 1 index records, 2 full records (every word).
  * If advance_ref != 0, ref[s][i] is overwritten with cur[s][i] for every changed
  * word (after the compare).  Returns TCO_OK or an error; *out_bytes = bytes written. */
 int tco_encode(void* const* ref, const void* const* cur, const uint64_t* n, const uint32_t* w,

@@ -219,10 +219,14 @@ class Checkpointer:
         self.cap_mask = tc.diff_bound(self.sizes, self.wb, tile_words, chunk_words)
         self.cap_idx = tc.diff_bound(self.sizes, self.wb, tile_words, chunk_words, index_mode=True) \
             if tile_words <= 8192 else 0
-        worst = max(self.cap_mask, self.cap_idx)
+        self.cap_full = tc.diff_bound(self.sizes, self.wb, tile_words, chunk_words, full=True)
+        worst = max(self.cap_mask, self.cap_idx, self.cap_full)
         self.rec_cap = int(min(worst, (expected_f * 1.1 + 0.05) * self.W + (64 << 20)))
+        if record_format not in ("adaptive", "mask", "index", "full"):
+            raise ValueError("record_format: adaptive | mask | index | full")
         self.format = record_format
-        self.next_index = record_format == "index"
+        self.next_fmt = record_format if record_format != "adaptive" else "mask"
+        self.full_run = 0  # consecutive full records (adaptive: every 8th is a mask probe of the density)
         self.dev = [torch.empty(self.rec_cap, dtype=torch.uint8, device=self.device) for _ in range(dev_slots)]
         self.lens = tc.HostBuffer(8 * dev_slots)
         self.lens_v = self.lens.view(torch.int64)
@@ -331,20 +335,21 @@ class Checkpointer:
         self.slot_busy[slot] = []
         ref_version = self.pending[-1]["v"] if self.pending else self.chain.head
         e0 = self._ev(self.s_comp) if self.timing else None
-        index_mode = bool(self.next_index) and self.cap_idx > 0
+        fmt = self.next_fmt if (self.next_fmt != "index" or self.cap_idx > 0) else "mask"
+        index_mode, full = fmt == "index", fmt == "full"
         if self.tier2 == "push" and self.fused_t2:
             # Tier-2 fused into the encode: the record is written locally and, over NVLink, into
             # the neighbour's slot version % t2_slots; the encoder publishes its mailbox
             t2 = version % self.t2_slots
             tc.diff_encode_push(self.ctx, self.ref, self.seg, self.dev[slot], self.lens_v[slot: slot + 1], version,
                                 ref_version, self.tx[t2], self.next_cap, self.tx_mail[t2], self.T, self.C, True,
-                                stream=self.s_comp, index_mode=index_mode)
+                                stream=self.s_comp, index_mode=index_mode, full=full)
         else:
             tc.diff_encode(self.ctx, self.ref, self.seg, self.dev[slot], self.lens_v[slot: slot + 1], version,
-                           ref_version, self.T, self.C, True, stream=self.s_comp, index_mode=index_mode)
+                           ref_version, self.T, self.C, True, stream=self.s_comp, index_mode=index_mode, full=full)
         e1 = self._ev(self.s_comp)
         self.pending.append({"v": version, "ref_v": ref_version, "slot": slot, "e0": e0, "e1": e1,
-                             "index": index_mode})
+                             "index": index_mode, "fmt": fmt})
         out = None
         while self.pending and (not self.ahead or len(self.pending) > 1):
             out = self._finish(self.pending.popleft())
@@ -371,9 +376,9 @@ class Checkpointer:
             self.needs_base = True
             self.pending.clear()
             return n
-        count = self._count_of(n, p["index"])
+        count = self._count_of(n, p["fmt"])
         if self.format == "adaptive":
-            self.next_index = count * 16 < self.words
+            self.next_fmt = self._choose(count, p["fmt"])
         tiers = set()
         busy = []
         # Tier-1: D2H into the arena on the copy stream
@@ -418,14 +423,33 @@ class Checkpointer:
                 self.times["fold"].append((f0, f1))
         self.slot_busy[slot] = busy
         self.chain.append(v, p["ref_v"], n, tiers)
-        self.where[v] = {"t1": off, "t2": t2, "n": n, "d2h": d2h, "count": count, "index": p["index"]}
+        self.where[v] = {"t1": off, "t2": t2, "n": n, "d2h": d2h, "count": count, "index": p["index"],
+                         "fmt": p["fmt"]}
         return n
 
-    def _count_of(self, n: int, index_mode: bool) -> float:
+    def _count_of(self, n: int, fmt: str):
+        """Changed words of a record of n bytes (None for a full record: it holds every word)."""
         w_avg = self.W / max(1, self.words)
-        if index_mode:
+        if fmt == "full":
+            return None
+        if fmt == "index":
             return max(0.0, n - (self.cap_idx - (2 + w_avg) * self.words)) / (2 + w_avg)
         return max(0.0, n - (self.cap_mask - self.W)) / w_avg
+
+    def _choose(self, count, fmt: str) -> str:
+        """Adaptive record format (R19; the paper adapts its payload format per tensor):
+        the smallest record for the last density — index below 1/16 changed, full when a mask
+        record would be within 2 % of it (full records encode in one streaming pass).  After a
+        full record the density is unknown: stay full, with a mask record every 8th as a probe."""
+        if count is None:
+            self.full_run += 1
+            return "mask" if self.full_run % 8 == 0 else "full"
+        self.full_run = 0
+        w_avg = self.W / max(1, self.words)
+        if self.cap_idx > 0 and count * 16 < self.words:
+            return "index"
+        mask_bytes = (self.cap_mask - self.W) + count * w_avg
+        return "full" if self.cap_full <= 1.02 * mask_bytes else "mask"
 
     def save_base(self, version: int):
         """A new base at `version` (§3.1 base stream; P:209 paced): the live state

@@ -64,12 +64,13 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
                 const uint32_t seg = static_cast<uint32_t>(h1 >> 32);
                 const uint64_t coff = ld_u64(h + 16), m = ld_u64(h + 24), count = ld_u64(h + 32);
                 const uint64_t version = ld_u64(h + 40), ref_version = ld_u64(h + 48), total = ld_u64(h + 56);
-                const bool imode = flags == 3;
-                if (magic != 0x31444354u || fmt != 1 || (w != 2 && w != 4) || (flags != 1 && flags != 3) ||
+                const bool imode = flags == 3, full = flags == 5;
+                if (magic != 0x31444354u || fmt != 1 || (w != 2 && w != 4) || (flags != 1 && flags != 3 && flags != 5) ||
                     !is_pow2(T) || T < 32 || T > 65536 || seg != static_cast<uint32_t>(s) || w != P.w[s] ||
-                    coff != off || coff % T != 0 || m > kMaxChunkWords || count > m ||
+                    coff != off || coff % T != 0 || m > kMaxChunkWords || count > m || (full && count != m) ||
                     (m == 0 && P.n[s] != 0) || off + m > P.n[s] ||
-                    total != (imode ? record_bytes_index(m, T, w, count) : record_bytes(m, T, w, count)) ||
+                    total != (full ? record_bytes_full(m, w)
+                              : imode ? record_bytes_index(m, T, w, count) : record_bytes(m, T, w, count)) ||
                     total > bytes - pos) {
                     err = TC_ERR_CORRUPT;
                     break;
@@ -80,7 +81,13 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
                 }
                 if (imode && T > kIndexMaxT) { err = TC_ERR_INVALID; break; }  // unsupported here
                 FoldRec R;
-                if (imode) {
+                R.full = full ? 1u : 0u;
+                if (full) {  // every word of the chunk, in index order
+                    R.mask = nullptr;
+                    R.idx = nullptr;
+                    R.toff = nullptr;
+                    R.values = h + kHdrBytes;
+                } else if (imode) {
                     R.mask = nullptr;
                     R.toff = h + index_toff_off();
                     R.idx = h + index_idx_off(m, T);
@@ -168,8 +175,12 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
                 // every chunk (mask-mode chunks through fold_dense_kernel), UINT32_MAX = scatter all.
                 bool all_idx = a.T == kListT && P.nrec <= static_cast<int>(kListMaxRec);
                 for (int k = 0; k < P.nrec && all_idx; ++k) all_idx = P.desc[static_cast<size_t>(k) * P.cap + r].idx != nullptr;
+                bool any_full = false;  // chains with a full record are scattered (fold_unit handles them)
+                for (int k = 0; k < P.nrec; ++k) any_full = any_full || P.desc[static_cast<size_t>(k) * P.cap + r].full;
                 const uint64_t mm = a.m;
-                if (P.dense_permille == 0u) {
+                if (any_full) {
+                    a.dense = 0u;
+                } else if (P.dense_permille == 0u) {
                     a.dense = all_idx ? 2u : 1u;
                 } else if (P.dense_permille == 0xffffffffu || !all_idx) {
                     a.dense = 0u;
@@ -298,9 +309,17 @@ __device__ void fold_unit(const FoldParams& P, uint64_t r, uint64_t ku, uint32_t
             const uint32_t* toff = reinterpret_cast<const uint32_t*>(R.toff);
             const word_t* vals = reinterpret_cast<const word_t*>(R.values);
             const uint32_t count = static_cast<uint32_t>(R.count);
+            const bool full = R.full != 0;
             // all mask words of the sub-unit first (independent read-only loads)
             uint32_t mk[kSubGroups];
-            if (R.idx) {
+            if (full) {
+                // a full record: every word of the chunk is a value (its implicit mask is all ones)
+#pragma unroll
+                for (uint32_t g = 0; g < kSubGroups; ++g) {
+                    const uint32_t p = sub + (32 * g + lane) * 32;
+                    mk[g] = p >= send ? 0u : (p + 32 > send ? (1u << (send - p)) - 1u : 0xffffffffu);
+                }
+            } else if (R.idx) {
                 // index-mode record: build this sub-unit's mask words from the in-tile positions
                 build_mask_from_index(R, sub, send, imask, lane, bad);
 #pragma unroll
@@ -312,7 +331,7 @@ __device__ void fold_unit(const FoldParams& P, uint64_t r, uint64_t ku, uint32_t
                     mk[g] = p < send ? ldg_u32(mask + (p >> 5)) : 0u;
                 }
             }
-            uint32_t run = sub == ustart ? ldg_u32(toff + ustart / T) : carry[j];
+            uint32_t run = sub == ustart ? (full ? ustart : ldg_u32(toff + ustart / T)) : carry[j];
             if (sub == ustart && ku == 0 && run != 0) bad = true;
 #pragma unroll
             for (uint32_t g = 0; g < kSubGroups; ++g) {
@@ -331,7 +350,7 @@ __device__ void fold_unit(const FoldParams& P, uint64_t r, uint64_t ku, uint32_t
                 }
                 const uint32_t pre = run + inc - c;  // in-chunk offset of this mask word's values
                 run += __shfl_sync(0xffffffffu, inc, 31);
-                if (T < kSub && p < send && p != ustart && (p & (T - 1)) == 0 && ldg_u32(toff + p / T) != pre)
+                if (!full && T < kSub && p < send && p != ustart && (p & (T - 1)) == 0 && ldg_u32(toff + p / T) != pre)
                     bad = true;
                 const uint32_t win = mk[g] & rem[g];
                 rem[g] &= ~mk[g];
@@ -390,7 +409,7 @@ __device__ void fold_unit(const FoldParams& P, uint64_t r, uint64_t ku, uint32_t
             }
             carry[j] = run;
             if (send == uend) {  // unit end: the next unit's first entry, or the final entry
-                const uint32_t want = uend < m ? ldg_u32(toff + uend / T) : ldg_u32(toff + (m + T - 1) / T);
+                const uint32_t want = full ? uend : (uend < m ? ldg_u32(toff + uend / T) : ldg_u32(toff + (m + T - 1) / T));
                 if (want != run || (uend == m && count != run)) bad = true;
             }
         }

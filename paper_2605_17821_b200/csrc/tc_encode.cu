@@ -396,6 +396,97 @@ __global__ void __launch_bounds__(kEncThreads, 6) encode_mask_kernel(const __gri
         mask_block<2, PEER>(P, sm, tile, tid);
 }
 
+// ------------------------------------------------------------------ kernel F -------------
+// Full records (tc_encode_opts.index_mode = 2; reading R21): every word of the chunk, no mask —
+// the dense-regime format (every fp32 word of a real Adam step changes).  Record
+// sizes do not depend on the data, so every block knows its output position up front: one
+// streaming pass, cur -> record values (+ ref <- cur with advance_ref), 3 W of HBM traffic and no
+// compare, no prefix, no spill.  A CTA per scan block; the chunk's first block writes the header,
+// its last the padding; block 0 the diff's length.  With the fused Tier-2 emit (PEER) the same
+// bytes also go to the neighbour's slot and the last CTA publishes the mailbox.
+template <bool PEER>
+__global__ void __launch_bounds__(kEncThreads) encode_full_kernel(const __grid_constant__ EncParams P) {
+    const int tid = threadIdx.x;
+    const BlockInfo I = decode_block(P, blockIdx.x);
+    const EncSeg& S = P.seg[I.seg];
+    const unsigned long long cl = I.chunk - S.first_chunk;
+    const unsigned long long rs = S.full_base + cl * record_bytes_full(P.C, I.w);  // earlier chunks are full
+    const uint64_t total = record_bytes_full(I.m, I.w);
+    if (rs + total > P.out_cap) {
+        if (tid == 0 && I.k == 0) tc_set_err(P.err, TC_ERR_CAPACITY);  // this record is not written
+    } else {
+        uint8_t* rec = P.out + rs;
+        const uint32_t nbytes = I.nb * I.w;
+        const uint4* src = reinterpret_cast<const uint4*>(S.cur + (I.chunk_off + I.p0) * I.w);
+        uint4* dst = reinterpret_cast<uint4*>(rec + kHdrBytes + static_cast<uint64_t>(I.p0) * I.w);
+        uint4* ref = reinterpret_cast<uint4*>(S.ref + (I.chunk_off + I.p0) * I.w);
+        const uint32_t nv = nbytes / 16;
+        const bool adv = P.advance_ref != 0;
+        constexpr uint32_t kV = 16384 / 16 / kEncThreads;  // 4 vectors per thread per block
+        uint4 v[kV];
+#pragma unroll
+        for (uint32_t q = 0; q < kV; ++q) {
+            const uint32_t i = tid + q * kEncThreads;
+            if (i < nv) v[q] = __ldg(src + i);
+        }
+#pragma unroll
+        for (uint32_t q = 0; q < kV; ++q) {
+            const uint32_t i = tid + q * kEncThreads;
+            if (i < nv) {
+                rec_store<PEER, uint4>(P, dst + i, v[q]);
+                if (adv) ref[i] = v[q];
+            }
+        }
+        // the segment's last block: the words past the last whole 16-byte vector
+        for (uint32_t x = nv * 16 + tid * I.w; x < nbytes; x += kEncThreads * I.w) {
+            const uint8_t* sb = reinterpret_cast<const uint8_t*>(src) + x;
+            uint8_t* db = reinterpret_cast<uint8_t*>(dst) + x;
+            uint8_t* rb = reinterpret_cast<uint8_t*>(ref) + x;
+            if (I.w == 4) {
+                const uint32_t wv = *reinterpret_cast<const uint32_t*>(sb);
+                rec_store<PEER, uint32_t>(P, reinterpret_cast<uint32_t*>(db), wv);
+                if (adv) *reinterpret_cast<uint32_t*>(rb) = wv;
+            } else {
+                const uint16_t wv = *reinterpret_cast<const uint16_t*>(sb);
+                rec_store<PEER, uint16_t>(P, reinterpret_cast<uint16_t*>(db), wv);
+                if (adv) *reinterpret_cast<uint16_t*>(rb) = wv;
+            }
+        }
+        if (tid == 0 && I.k == 0) {
+            uint64_t* h = reinterpret_cast<uint64_t*>(rec);
+            rec_store<PEER, uint64_t>(P, h + 0, 0x31444354ull /* "TCD1" */ | (1ull << 32) |
+                                                    (static_cast<uint64_t>(I.w) << 48) | (5ull << 56));
+            rec_store<PEER, uint64_t>(P, h + 1, static_cast<uint64_t>(P.T) | (static_cast<uint64_t>(S.seg_id) << 32));
+            rec_store<PEER, uint64_t>(P, h + 2, S.word_base + I.chunk_off);
+            rec_store<PEER, uint64_t>(P, h + 3, I.m);
+            rec_store<PEER, uint64_t>(P, h + 4, I.m);  // count: every word
+            rec_store<PEER, uint64_t>(P, h + 5, P.version);
+            rec_store<PEER, uint64_t>(P, h + 6, P.ref_version);
+            rec_store<PEER, uint64_t>(P, h + 7, total);
+        }
+        if (I.k + 1 == I.nblk)
+            for (uint64_t x = kHdrBytes + static_cast<uint64_t>(I.w) * I.m + tid; x < total; x += kEncThreads)
+                rec_store<PEER, uint8_t>(P, rec + x, 0);
+    }
+    if (blockIdx.x == 0 && tid == 0) *reinterpret_cast<volatile uint64_t*>(P.out_bytes) = P.full_total;
+    if (PEER) {
+        __threadfence_system();
+        __syncthreads();
+        if (tid == 0) {
+            const unsigned prev = atomicAdd(P.peer_counter, 1u);
+            if (prev == gridDim.x - 1) {
+                *P.peer_counter = 0u;
+                __threadfence_system();
+                const unsigned long long nb = P.full_total;
+                const bool ok = nb <= P.peer_cap && *reinterpret_cast<const volatile unsigned int*>(P.err) == 0u;
+                asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(P.peer_mail), "l"(ok ? nb : ~0ull) : "memory");
+                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(P.peer_mail + 1),
+                             "l"(static_cast<unsigned long long>(P.peer_version)) : "memory");
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------ kernel A' -----------
 // Mask-input variant of kernel A (EncSeg::mask_in: the change mask comes precomputed, e.g. from
 // the fused Adam step, tc_adam_step_encode; `cur` is the only state: no ref, no compare, no ref
@@ -884,6 +975,13 @@ cudaError_t launch_encode(const EncParams& p, cudaStream_t s) {
         if (dev >= 0 && dev < TC_MAX_DEVICES) attr_set[dev] = true;
     }
     if (p.total_blocks == 0) return cudaSuccess;
+    if (p.index_mode == kFormatFull) {  // full records: one streaming pass (kernel F)
+        if (p.peer_out)
+            encode_full_kernel<true><<<static_cast<unsigned>(p.total_blocks), kEncThreads, 0, s>>>(p);
+        else
+            encode_full_kernel<false><<<static_cast<unsigned>(p.total_blocks), kEncThreads, 0, s>>>(p);
+        return cudaGetLastError();
+    }
     if (p.seg[0].mask_in) {
         // persistent warps: as many CTAs as fit, never more than one warp per block
         static int per_sm = 0;

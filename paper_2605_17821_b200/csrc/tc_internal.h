@@ -43,6 +43,9 @@ __host__ __device__ inline uint64_t record_bytes_index(uint64_t m, uint32_t T, u
     return index_val_off(m, T, count) + pad16(uint64_t(w) * count);
 }
 constexpr uint32_t kIndexMaxT = 8192;
+// full record (flags 5, reading R21): header | values (w * m), every word of the chunk
+__host__ __device__ inline uint64_t record_bytes_full(uint64_t m, uint32_t w) { return kHdrBytes + pad16(uint64_t(w) * m); }
+constexpr int kFormatFull = 2;  // tc_encode_opts.index_mode value of full records
 
 // ---- per-segment launch description of one encode (kernel parameter, no table) ----
 struct EncSeg {
@@ -59,6 +62,7 @@ struct EncSeg {
     uint32_t pad_;
     uint64_t word_base;     // added to chunk offsets in the headers (range encodes)
     const uint32_t* mask_in;  // precomputed change mask of the segment (kernel A', encode_maskin_kernel), else nullptr
+    uint64_t full_base;       // full records (index_mode 2): byte offset of the segment's first record in out
 };
 
 struct EncParams {
@@ -95,6 +99,7 @@ struct EncParams {
     unsigned long long* peer_mail;
     uint64_t peer_version;
     unsigned int* peer_counter;
+    uint64_t full_total;         // full records: the diff's length (known up front)
 };
 
 constexpr uint32_t kMaskStageWords = 256;  // mask words of one block (8192 16-bit words max)
@@ -118,7 +123,7 @@ struct FoldRec {           // one record of one diff, as located by the walker
     uint32_t seg;
     uint32_t w;
     uint32_t dense;        // desc[r] of diff 0 only: 0 fold_kernel, 1 fold_dense_kernel, 2 fold_list_kernel
-    uint32_t pad_;
+    uint32_t full;         // a full record (every word of the chunk; mask / idx / toff are nullptr)
 };
 
 struct FoldParams {

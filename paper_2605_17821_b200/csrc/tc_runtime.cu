@@ -68,8 +68,8 @@ static tc_status check_opts(const tc_encode_opts& o) {
         return fail(TC_ERR_INVALID, "tile_words must be a power of two in [32, 65536]");
     if (o.chunk_words == 0 || o.chunk_words % o.tile_words != 0 || o.chunk_words > kMaxChunkWords)
         return fail(TC_ERR_INVALID, "chunk_words must be a positive multiple of tile_words and <= 2^31-1");
-    if (o.index_mode > 1 || o.reserved != 0) return fail(TC_ERR_INVALID, "index_mode must be 0 or 1, reserved 0");
-    if (o.index_mode && o.tile_words > kIndexMaxT) return fail(TC_ERR_INVALID, "index mode requires tile_words <= 8192");
+    if (o.index_mode > 2 || o.reserved != 0) return fail(TC_ERR_INVALID, "index_mode must be 0, 1 or 2, reserved 0");
+    if (o.index_mode == 1 && o.tile_words > kIndexMaxT) return fail(TC_ERR_INVALID, "index mode requires tile_words <= 8192");
     return TC_OK;
 }
 
@@ -215,8 +215,9 @@ tc_status tc_diff_bound(const tc_segment* segs, int nseg, const tc_encode_opts* 
         uint64_t off = 0;
         do {
             const uint64_t m = n - off < o.chunk_words ? n - off : o.chunk_words;
-            tot += o.index_mode ? record_bytes_index(m, o.tile_words, static_cast<uint32_t>(w), m)
-                                : record_bytes(m, o.tile_words, static_cast<uint32_t>(w), m);
+            tot += o.index_mode == kFormatFull ? record_bytes_full(m, static_cast<uint32_t>(w))
+                   : o.index_mode ? record_bytes_index(m, o.tile_words, static_cast<uint32_t>(w), m)
+                                  : record_bytes(m, o.tile_words, static_cast<uint32_t>(w), m);
             off += m;
         } while (off < n);
     }
@@ -256,7 +257,7 @@ static tc_status encode_impl(tc_ctx* ctx, const SegSpec* specs, int nseg, const 
         P.peer_version = version;
         P.peer_counter = ctx->err + 1;
     }
-    uint64_t blocks = 0, chunks = 0;
+    uint64_t blocks = 0, chunks = 0, full_bytes = 0;
     for (int i = 0; i < nseg; ++i) {
         const SegSpec& g = specs[i];
         EncSeg& E = P.seg[i];
@@ -277,6 +278,8 @@ static tc_status encode_impl(tc_ctx* ctx, const SegSpec* specs, int nseg, const 
         const uint64_t last_blocks = m_last ? cdiv(m_last, E.block_words) : 1;
         blocks += (E.n_chunks - 1) * E.blocks_per_chunk + last_blocks;
         chunks += E.n_chunks;
+        E.full_base = full_bytes;  // full records: their sizes are known up front (no count)
+        full_bytes += (E.n_chunks - 1) * record_bytes_full(full, g.w) + record_bytes_full(m_last, g.w);
     }
     P.nseg = nseg;
     P.T = o.tile_words;
@@ -289,7 +292,7 @@ static tc_status encode_impl(tc_ctx* ctx, const SegSpec* specs, int nseg, const 
     P.out_cap = out_cap;
     P.out_bytes = out_bytes;
     P.advance_ref = o.advance_ref ? 1 : 0;
-    P.index_mode = o.index_mode ? 1 : 0;
+    P.index_mode = static_cast<int>(o.index_mode);
     P.err = ctx->err;
 
     const uint64_t groups = cdiv(blocks, kEmitGroup);
@@ -306,9 +309,11 @@ static tc_status encode_impl(tc_ctx* ctx, const SegSpec* specs, int nseg, const 
     const size_t need = w_cbase + 8 * chunks;
     st = ensure(&ctx->enc, &ctx->enc_bytes, need, s);
     if (st != TC_OK) return st;
-    st = ensure(&ctx->spill, &ctx->spill_bytes, blocks * static_cast<size_t>(kSpillBytes) * (o.index_mode ? 2 : 1), s);
-    if (st != TC_OK) return st;
-    if (o.index_mode) {
+    if (o.index_mode != kFormatFull) {
+        st = ensure(&ctx->spill, &ctx->spill_bytes, blocks * static_cast<size_t>(kSpillBytes) * (o.index_mode ? 2 : 1), s);
+        if (st != TC_OK) return st;
+    }
+    if (o.index_mode == 1) {
         st = ensure(&ctx->mstage, &ctx->mstage_bytes, blocks * static_cast<size_t>(kMaskStageWords) * 4, s);
         if (st != TC_OK) return st;
         P.mstage = static_cast<uint32_t*>(ctx->mstage);
@@ -324,9 +329,10 @@ static tc_status encode_impl(tc_ctx* ctx, const SegSpec* specs, int nseg, const 
     P.spill = static_cast<uint8_t*>(ctx->spill);
     cudaError_t e = cudaMemsetAsync(base, 0, z_end, s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(scratch)");
+    P.full_total = full_bytes;
     e = launch_encode(P, s);
     if (e != cudaSuccess) return cuda_fail(e, "encode launch");
-    ctx->launches += 3;
+    ctx->launches += o.index_mode == kFormatFull ? 1 : 3;
     return TC_OK;
 }
 
@@ -336,7 +342,8 @@ static uint64_t range_bound(uint64_t n, uint32_t w, const tc_encode_opts& o, uin
     for (uint64_t c = c0; c < c0 + nc && c < total_chunks; ++c) {
         const uint64_t off = c * o.chunk_words;
         const uint64_t m = n > off ? (n - off < o.chunk_words ? n - off : o.chunk_words) : 0;
-        tot += o.index_mode ? record_bytes_index(m, o.tile_words, w, m) : record_bytes(m, o.tile_words, w, m);
+        tot += o.index_mode == kFormatFull ? record_bytes_full(m, w)
+               : o.index_mode ? record_bytes_index(m, o.tile_words, w, m) : record_bytes(m, o.tile_words, w, m);
     }
     return tot;
 }

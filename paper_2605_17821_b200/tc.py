@@ -154,8 +154,12 @@ def _stream(stream) -> int | None:
     return int(stream)
 
 
-def _opts(tile_words=4096, chunk_words=1 << 28, advance_ref=True, index_mode=False) -> EncodeOpts:
-    return EncodeOpts(tile_words, 1 if advance_ref else 0, chunk_words, 1 if index_mode else 0, 0)
+FORMAT_MASK, FORMAT_INDEX, FORMAT_FULL = 0, 1, 2  # tc_encode_opts.index_mode (include/tc.h)
+
+
+def _opts(tile_words=4096, chunk_words=1 << 28, advance_ref=True, index_mode=False, full=False) -> EncodeOpts:
+    fmt = FORMAT_FULL if full else (FORMAT_INDEX if index_mode else FORMAT_MASK)
+    return EncodeOpts(tile_words, 1 if advance_ref else 0, chunk_words, fmt, 0)
 
 
 def _wb(t: torch.Tensor) -> int:
@@ -184,9 +188,9 @@ def layout_segments(sizes, word_bytes):
     return arr
 
 
-def diff_bound(sizes, word_bytes, tile_words=4096, chunk_words=1 << 28, index_mode=False) -> int:
+def diff_bound(sizes, word_bytes, tile_words=4096, chunk_words=1 << 28, index_mode=False, full=False) -> int:
     segs = layout_segments(sizes, word_bytes)
-    o = _opts(tile_words, chunk_words, True, index_mode)
+    o = _opts(tile_words, chunk_words, True, index_mode, full)
     out = u64(0)
     _check(LIB.tc_diff_bound(segs, len(sizes), ctypes.byref(o), ctypes.byref(out)), "tc_diff_bound")
     return out.value
@@ -234,10 +238,11 @@ class Ctx:
 
 
 def diff_encode(ctx: Ctx, ref, cur, out: torch.Tensor, out_bytes: torch.Tensor, version: int, ref_version: int,
-                tile_words=4096, chunk_words=1 << 28, advance_ref=True, stream=None, index_mode=False):
-    """Enqueue tc_diff_encode.  ``out`` uint8 CUDA tensor, ``out_bytes`` int64 CUDA tensor [1]."""
+                tile_words=4096, chunk_words=1 << 28, advance_ref=True, stream=None, index_mode=False, full=False):
+    """Enqueue tc_diff_encode.  ``out`` uint8 CUDA tensor, ``out_bytes`` int64 CUDA tensor [1].
+    Record format: mask (default), index (``index_mode``) or full (``full``: every word)."""
     segs = segments(ref, cur)
-    o = _opts(tile_words, chunk_words, advance_ref, index_mode)
+    o = _opts(tile_words, chunk_words, advance_ref, index_mode, full)
     _check(LIB.tc_diff_encode(ctx.h, segs, len(ref), ctypes.byref(o), version, ref_version, out.data_ptr(),
                               out.numel() * out.element_size(), out_bytes.data_ptr(), _stream(stream)),
            "tc_diff_encode")
@@ -302,10 +307,11 @@ def push_peer(ctx: Ctx, src: torch.Tensor, src_bytes, peer_dst, peer_cap: int, p
 
 def diff_encode_push(ctx: Ctx, ref, cur, out: torch.Tensor, out_bytes, version: int, ref_version: int, peer_dst,
                      peer_cap: int, peer_mailbox, tile_words=4096, chunk_words=1 << 28, advance_ref=True,
-                     stream=None, index_mode=False):
-    """Enqueue tc_diff_encode_push: encode, then push the record into the ring neighbour's slot."""
+                     stream=None, index_mode=False, full=False):
+    """Enqueue tc_diff_encode_push: the encoder writes the record into `out` AND the ring
+    neighbour's slot (fused Tier-2 emit) and publishes its mailbox."""
     segs = segments(ref, cur)
-    o = _opts(tile_words, chunk_words, advance_ref, index_mode)
+    o = _opts(tile_words, chunk_words, advance_ref, index_mode, full)
     _check(LIB.tc_diff_encode_push(ctx.h, segs, len(ref), ctypes.byref(o), version, ref_version, out.data_ptr(),
                                    out.numel() * out.element_size(), out_bytes.data_ptr(), peer_dst.data_ptr(),
                                    int(peer_cap), peer_mailbox.data_ptr(), _stream(stream)), "tc_diff_encode_push")
@@ -318,9 +324,9 @@ def peer_wait(ctx: Ctx, mailbox, version: int, bytes_out=None, stream=None):
 
 
 def diff_bound_range(n_words: int, word_bytes: int, first_chunk: int, n_chunks: int, tile_words=4096,
-                     chunk_words=1 << 28, index_mode=False) -> int:
+                     chunk_words=1 << 28, index_mode=False, full=False) -> int:
     seg = Segment(None, None, int(n_words), int(word_bytes), 0)
-    o = _opts(tile_words, chunk_words, True, index_mode)
+    o = _opts(tile_words, chunk_words, True, index_mode, full)
     out = u64(0)
     _check(LIB.tc_diff_bound_range(ctypes.byref(seg), ctypes.byref(o), first_chunk, n_chunks, ctypes.byref(out)),
            "tc_diff_bound_range")
@@ -329,11 +335,12 @@ def diff_bound_range(n_words: int, word_bytes: int, first_chunk: int, n_chunks: 
 
 def diff_encode_range(ctx: Ctx, ref: torch.Tensor, cur: torch.Tensor, segment_id: int, first_chunk: int,
                       n_chunks: int, out: torch.Tensor, out_bytes: torch.Tensor, version: int, ref_version: int,
-                      tile_words=4096, chunk_words=1 << 28, advance_ref=True, stream=None, index_mode=False):
+                      tile_words=4096, chunk_words=1 << 28, advance_ref=True, stream=None, index_mode=False,
+                      full=False):
     """Enqueue tc_diff_encode_range (the records of chunks [first_chunk, first_chunk+n_chunks) of
     one segment, byte-identical to that part of the full encode)."""
     seg = segments([ref], [cur])
-    o = _opts(tile_words, chunk_words, advance_ref, index_mode)
+    o = _opts(tile_words, chunk_words, advance_ref, index_mode, full)
     _check(LIB.tc_diff_encode_range(ctx.h, seg, segment_id, ctypes.byref(o), first_chunk, n_chunks, version,
                                     ref_version, out.data_ptr(), out.numel() * out.element_size(),
                                     out_bytes.data_ptr(), _stream(stream)), "tc_diff_encode_range")

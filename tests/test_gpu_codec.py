@@ -544,3 +544,78 @@ def test_index_tamper_t8192_chain(fctx, tco):
         assert rc == tc.ERR_CORRUPT
     rc, st = gpu_fold(fctx, states[0], 0, recs)
     assert rc == tc.OK and np.array_equal(st[0], states[2][0])
+
+
+# ------------------------------------------------------------ full records (R21) ------------
+@pytest.mark.parametrize("sizes,wb,f,T,C", CASES)
+@pytest.mark.parametrize("advance", [True, False])
+def test_full_encode_matches_oracle_bytes(ctx, tco, sizes, wb, f, T, C, advance):
+    """Full-format records (every word, kernel F): byte-exact vs the oracle, ref advanced."""
+    pairs = [rand_pair(n, w, f) for n, w in zip(sizes, wb)]
+    ref = [p[0] for p in pairs]
+    cur = [p[1] for p in pairs]
+    ref_o = [r.copy() for r in ref]
+    rc, exp = tco.encode(ref_o, cur, tile_words=T, chunk_words=C, advance_ref=advance, version=9, ref_version=8,
+                         full=True)
+    assert rc == 0
+    refd = [to_dev(a) for a in ref]
+    curd = [to_dev(a) for a in cur]
+    cap = tc.diff_bound([a.size for a in ref], [a.itemsize for a in ref], T, C, full=True)
+    assert cap == exp.size
+    out = torch.full((cap + 64,), 0xAB, dtype=torch.uint8, device="cuda")
+    ob = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tc.diff_encode(ctx, refd, curd, out, ob, 9, 8, T, C, advance, full=True)
+    ctx.check()
+    assert int(ob.item()) == exp.size
+    got = out.cpu().numpy()
+    assert np.array_equal(got[: exp.size], exp) and (got[exp.size:] == 0xAB).all()
+    assert all(np.array_equal(to_np(a), b) for a, b in zip(refd, ref_o))
+
+
+@pytest.mark.parametrize("N", [1, 3, 6])
+def test_full_mask_index_chain_fold_matches_oracle(fctx, tco, N):
+    """Chains mixing full, mask and index records fold bit-exactly under every restore strategy."""
+    sizes, wb, T, C = [70001, 9000, 33333], [4, 2, 4], 4096, 4096 * 5
+    fs = [0.02, 1.0, 0.3, 0.001, 0.99, 0.05]
+    states = [synth.state(sizes, wb, 61, 0, 0.0)]
+    for v in range(1, N + 1):
+        states.append([synth.step(a, 61, s, v, fs[v - 1]) for s, a in enumerate(states[-1])])
+    ref = [a.copy() for a in states[0]]
+    diffs = []
+    for v in range(1, N + 1):
+        rc, d = tco.encode(ref, states[v], tile_words=T, chunk_words=C, version=v, ref_version=v - 1,
+                           index_mode=v % 3 == 1, full=v % 3 == 2)
+        assert rc == 0
+        diffs.append(d)
+    rc, st_g = gpu_fold(fctx, states[0], 0, diffs)
+    assert rc == tc.OK
+    assert all(np.array_equal(a, b) for a, b in zip(st_g, states[N]))
+
+
+def test_full_range_encode_and_tamper(ctx, tco):
+    """Range encodes of full records concatenate to the full encode; a full record whose count is
+    not m, or whose flags say FULL|INDEX, is CORRUPT with the state untouched."""
+    sizes, wb, T, C = [40001, 70003], [2, 4], 256, 8192
+    ref_np, cur_np = zip(*[rand_pair(n, w, 0.9) for n, w in zip(sizes, wb)])
+    rc, exp = tco.encode([a.copy() for a in ref_np], list(cur_np), tile_words=T, chunk_words=C, advance_ref=False,
+                         version=2, ref_version=1, full=True)
+    parts = []
+    for i, (n, w) in enumerate(zip(sizes, wb)):
+        nch = -(-n // C)
+        for c0 in range(0, nch, 3):
+            k = min(3, nch - c0)
+            cap = tc.diff_bound_range(n, w, c0, k, T, C, full=True)
+            out = torch.zeros(cap, dtype=torch.uint8, device="cuda")
+            ob = torch.zeros(1, dtype=torch.int64, device="cuda")
+            tc.diff_encode_range(ctx, to_dev(ref_np[i]), to_dev(cur_np[i]), i, c0, k, out, ob, 2, 1, T, C, False,
+                                 full=True)
+            ctx.check()
+            parts.append(out[: int(ob.item())].cpu().numpy())
+    assert np.array_equal(np.concatenate(parts), exp)
+    for byte, val in ((32, 1), (7, 7)):
+        bad = exp.copy()
+        bad[byte] = (int(bad[byte]) + val) & 0xFF if byte == 32 else val
+        rc, st = gpu_fold(ctx, list(ref_np), 1, [bad])
+        assert rc == tc.ERR_CORRUPT and all(np.array_equal(a, b) for a, b in zip(st, ref_np))
+    rc, st = gpu_fold(ctx, list(ref_np), 1, [exp])
+    assert rc == tc.OK and all(np.array_equal(a, b) for a, b in zip(st, cur_np))

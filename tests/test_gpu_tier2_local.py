@@ -238,3 +238,25 @@ def test_fused_encode_push_capacity_and_ranges(ctx, tco, index_mode):
             assert rc == tc.ERR_CAPACITY and int(got.item()) == 0
         slot.free()
         mail.free()
+
+
+def test_fused_encode_push_full_records(ctx, tco):
+    """The fused Tier-2 emit of full records (kernel F writes both copies, publishes the mailbox)."""
+    states = [_shard(0, 0.0), _shard(1, 1.0)]
+    ref = [to_dev(a) for a in states[0]]
+    cur = [to_dev(a) for a in states[1]]
+    rc, exp = tco.encode([a.copy() for a in states[0]], states[1], version=1, ref_version=0, full=True)
+    cap = tc.diff_bound(SIZES, WB, full=True)
+    slot, mail = tc.IpcBuffer(cap), tc.IpcBuffer(16)
+    out = torch.zeros(cap, dtype=torch.uint8, device="cuda")
+    ob = torch.zeros(1, dtype=torch.int64, device="cuda")
+    got = torch.zeros(1, dtype=torch.int64, device="cuda")
+    s = torch.cuda.Stream()
+    tc.diff_encode_push(ctx, ref, cur, out, ob, 1, 0, slot, cap, mail, stream=s, full=True)
+    tc.peer_wait(ctx, mail, 1, got, stream=s)
+    ctx.check(s)
+    n = int(got.item())
+    assert n == exp.size == int(ob.item())
+    assert np.array_equal(out[:n].cpu().numpy(), exp) and np.array_equal(slot.tensor[:n].cpu().numpy(), exp)
+    slot.free()
+    mail.free()

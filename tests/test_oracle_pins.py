@@ -501,3 +501,77 @@ def test_index_tamper_flags_is_corrupt(tco):
     bad = rec.copy()
     bad[7] = 2  # INDEX without REPLACE
     _expect(tco, base, bad, tco.ERR_CORRUPT)
+
+
+# --------------------------------------------------------------- full records (R21) -------
+def _parse_full(rec, pos=0):
+    """Full-format record sections from the layout table: header | values (w*m)."""
+    h = rec[pos: pos + 64]
+    w, flags = int(h[6]), int(h[7])
+    m, count, total = (int(h[a: a + 8].view("<u8")[0]) for a in (24, 32, 56))
+    vals = rec[pos + 64: pos + 64 + w * m].view("<u2" if w == 2 else "<u4")
+    return dict(w=w, flags=flags, m=m, count=count, total=total, values=vals,
+                pad=rec[pos + 64 + w * m: pos + total])
+
+
+@pytest.mark.parametrize("n,w,f,C", [(0, 4, 0.0, 4096), (1, 2, 1.0, 4096), (7, 2, 0.5, 4096), (300, 4, 0.97, 4096),
+                                     (5000, 4, 1.0, 1024), (9001, 2, 0.2, 2048)])
+def test_full_records_equal_cur(tco, n, w, f, C):
+    """A full record is the chunk of `cur` itself (identity special case): flags 5, count = m, values =
+    cur[chunk], size 64 + pad16(w m) with zero padding; chunks rebased like the other formats; the
+    reference advances to cur; apply(ref, full) == cur."""
+    ref, cur = _rand_pair(n, w, f)
+    r0 = ref.copy()
+    rc, rec = tco.encode([ref], [cur], tile_words=64, chunk_words=C, version=3, ref_version=2, full=True)
+    assert rc == 0
+    assert np.array_equal(ref, cur), "advance_ref: ref != cur"
+    pos, off = 0, 0
+    while True:
+        r = _parse_full(rec, pos)
+        m = min(n - off, C)
+        assert r["flags"] == 5 and r["m"] == m and r["count"] == m and r["w"] == w
+        assert r["total"] == 64 + recfmt.pad16(w * m) == tco.record_bytes(m, 64, w, m, full=True)
+        assert int(rec[pos + 16: pos + 24].view("<u8")[0]) == off
+        assert np.array_equal(r["values"], cur[off: off + m]) and not r["pad"].any()
+        pos += r["total"]
+        off += m
+        if off >= n:
+            break
+    assert pos == rec.size
+    st = r0.copy()
+    rc, v = tco.apply([st], 2, rec)
+    assert rc == 0 and v == 3 and np.array_equal(st, cur)
+
+
+def test_full_mask_index_chain_fold(tco):
+    """A chain mixing the three formats folds to the final state == sequential applies; a full
+    record hides every older change of its chunk (newest wins)."""
+    sizes, wb = [3000, 5000], [2, 4]
+    s = [synth.state(sizes, wb, 23, v, 0.3) for v in range(7)]
+    ref = [a.copy() for a in s[0]]
+    ds = []
+    for v in range(1, 7):
+        rc, d = tco.encode(ref, s[v], tile_words=64, chunk_words=1024, version=v, ref_version=v - 1,
+                           index_mode=v % 3 == 1, full=v % 3 == 2)
+        assert rc == 0
+        ds.append(d)
+    st = [a.copy() for a in s[0]]
+    rc, ver = tco.fold(st, 0, ds)
+    assert rc == 0 and ver == 6 and all(np.array_equal(a, b) for a, b in zip(st, s[6]))
+    # from the base, a single full record of version 5 followed by record 6 gives the same state
+    ref5 = [a.copy() for a in s[0]]
+    rc, d5 = tco.encode(ref5, s[5], tile_words=64, chunk_words=1024, version=5, ref_version=0, full=True)
+    st = [a.copy() for a in s[0]]
+    assert tco.fold(st, 0, [d5, ds[5]])[0] == 0 and all(np.array_equal(a, b) for a, b in zip(st, s[6]))
+
+
+@pytest.mark.parametrize("byte,val", [(7, 7), (32, 1), (56, 3)])
+def test_full_tamper_is_corrupt(tco, byte, val):
+    """flags FULL|INDEX, count != m, total != 64 + pad16(w m) -> CORRUPT, state untouched."""
+    ref, cur = _rand_pair(300, 4, 0.9)
+    base = ref.copy()
+    rc, rec = tco.encode([ref], [cur], tile_words=64, version=5, ref_version=4, full=True)
+    bad = rec.copy()
+    bad[byte] = (int(bad[byte]) + val) & 0xFF if byte != 7 else val
+    _expect(tco, base, bad, tco.ERR_CORRUPT)
+    _expect(tco, base, rec[:-16], tco.ERR_CORRUPT)

@@ -37,6 +37,9 @@ def enc_bytes(recs, advance):
     b = 0
     for m, w, T, count, flags in recs:
         W = m * w
+        if flags == 5:  # full record: read cur, write the values (+ ref <- cur): no compare
+            b += 64 + 2 * W + (W if advance else 0)
+            continue
         meta = 64 + 4 * (-(-m // T) + 1) + (2 * count if flags & 2 else 4 * -(-m // 32))
         b += 2 * W + meta + w * count
         if advance and m:
@@ -52,6 +55,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--advance", type=int, default=1)
     ap.add_argument("--index", action="store_true")
+    ap.add_argument("--full", action="store_true", help="full records (every word, kernel F)")
     ap.add_argument("--structure", type=int, default=synth.S1_IID)
     a = ap.parse_args()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
@@ -65,7 +69,7 @@ def main():
     X = [alloc(n, w) for n, w in zip(sizes, wb)]
     Y = [alloc(n, w) for n, w in zip(sizes, wb)]
     R = [alloc(n, w) for n, w in zip(sizes, wb)] if a.advance else X
-    cap = tc.diff_bound(sizes, wb, T, C, a.index)
+    cap = tc.diff_bound(sizes, wb, T, C, a.index, full=a.full)
     out = torch.empty(cap, dtype=torch.uint8, device=dev)
     first = torch.empty(cap, dtype=torch.uint8, device=dev)
     ob = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -87,7 +91,7 @@ def main():
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                tc.diff_encode(ctx, R, Y, out, ob, 1, 0, T, C, bool(a.advance), index_mode=a.index)
+                tc.diff_encode(ctx, R, Y, out, ob, 1, 0, T, C, bool(a.advance), index_mode=a.index, full=a.full)
                 e1.record()
                 ctx.check()
                 if r:
@@ -105,7 +109,7 @@ def main():
                 same = same_ref if same is None else (same and same_ref)
             t = statistics.median(ms)
             b = enc_bytes(recs, a.advance)
-            print(json.dumps({"f": f, "defer": d, "index": a.index, "advance": a.advance, "ms": round(t, 3),
+            print(json.dumps({"f": f, "defer": d, "index": a.index, "full": a.full, "advance": a.advance, "ms": round(t, 3),
                               "ms_all": [round(x, 3) for x in ms], "record_bytes": n,
                               "alg_bytes": int(b), "gbs": round(b / t / 1e6, 1), "frac": round(b / t / 1e6 / peak, 3),
                               "state_gbs": round(W / t / 1e6, 1), "identical_to_first": same}), flush=True)
