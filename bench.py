@@ -108,6 +108,10 @@ def algorithmic_bytes(recs, sector=False):
     enc = fold = 0
     for seg, m, w, T, count, total, flags in recs:
         W = m * w
+        if flags == 5:  # full record: read cur, write every word (+ ref <- cur); fold: read + write all
+            enc += 64 + 3 * W
+            fold += 64 + 2 * W
+            continue
         if flags & 2:  # index mode: tile_off + u16 position per changed word instead of the mask
             meta = 64 + 4 * (-(-m // T) + 1) + 2 * count
         else:
@@ -281,7 +285,8 @@ def run_ours(args):
     fixed_mask = tc.diff_bound(sizes, [w for w in wb], T, C) - sum(n * w for n, w in zip(sizes, wb))
     # records: the bound at f is ~ (f + 0.036) W; allocate the bound only when it fits
     free = torch.cuda.mem_get_info(dev)[0]
-    est = int(min(cap, (args.f * 1.1 + 0.05) * W + (64 << 20)))
+    f_exp = 1.0 if args.structure == S3_ADAM else args.f  # S3: every fp32 word changes
+    est = int(min(max(cap, tc.diff_bound(sizes, wb, T, C, full=True)), (f_exp * 1.1 + 0.05) * W + (64 << 20)))
     spill_need = (sum(sizes) // 4096 + 1) * (8192 + 1024)  # encode scratch (index mode: 8 KB spill + mask stage)
     # the step runs through the product lifecycle (paper_2605_17821_b200.checkpoint.Checkpointer) —
     # encode, Tier-1 staging, Tier-2 NVLink push, hot-standby fold, the version chain — except
@@ -291,7 +296,8 @@ def run_ours(args):
     if use_ck:
         from paper_2605_17821_b200.checkpoint import Checkpointer
 
-        ck = Checkpointer(Y, rank, world, tier2="push" if world > 1 else None, expected_f=args.f,
+        ck = Checkpointer(Y, rank, world, tier2="push" if world > 1 else None,
+                          expected_f=1.0 if args.structure == S3_ADAM else args.f,
                           record_format=args.format if allow_index else "mask", dev_slots=2, t1_bytes=3 * est,
                           t2_slots=2, standby=R, tile_words=T, chunk_words=C, ahead=world == 1,
                           stage_base=False, ref=A, stream=s_comp, push_ctas=args.push_ctas, timing=True,
@@ -477,6 +483,8 @@ def run_ours(args):
         ck_done = []  # (version, bytes, index mode) of every finished save
 
         def ck_finished(nb):
+            if nb is not None and ck.needs_base:
+                raise RuntimeError(f"a {nb}-byte record outgrew the {ck.rec_cap}-byte record slot (R20)")
             if nb is not None:
                 ck_done.append((ck.chain.head, nb, ck.where[ck.chain.head]["fmt"]))
                 ck.reclaim(max(ck.chain.base_version, ck.chain.head - 1))
@@ -607,7 +615,7 @@ def run_ours(args):
 
     scatter_ref = None
     # (sparse steps only: at high f the position lists alone outgrow the memory the step leaves)
-    if world == 1 and args.f <= 0.05:  # writes Y's values at the X/Y differences into R, then puts R back
+    if world == 1 and args.f <= 0.05 and args.structure != S3_ADAM:  # writes Y's values at the X/Y differences into R, then puts R back
         scatter_ref = scatter_reference(X, Y, R, s_comp)
         if state["content"] == "X":
             with torch.cuda.stream(s_comp):
