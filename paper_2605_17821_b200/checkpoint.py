@@ -201,7 +201,7 @@ class Checkpointer:
                  t1_bytes: int | None = None, t2_slots: int = 8, standby=None, tile_words: int = 4096,
                  chunk_words: int = 1 << 28, ahead: bool = True, stage_base: bool = True, ref=None,
                  stream=None, base_version: int = 0, push_ctas: int = 16, timing: bool = False,
-                 base_interval: int = 50, fused_t2: bool = True):
+                 base_interval: int = 50, fused_t2: bool = True, rec_cap: int | None = None):
         from . import tc
 
         self.tc = tc
@@ -221,7 +221,8 @@ class Checkpointer:
             if tile_words <= 8192 else 0
         self.cap_full = tc.diff_bound(self.sizes, self.wb, tile_words, chunk_words, full=True)
         worst = max(self.cap_mask, self.cap_idx, self.cap_full)
-        self.rec_cap = int(min(worst, (expected_f * 1.1 + 0.05) * self.W + (64 << 20)))
+        self.rec_cap = int(rec_cap) if rec_cap is not None else \
+            int(min(worst, (expected_f * 1.1 + 0.05) * self.W + (64 << 20)))
         if record_format not in ("adaptive", "mask", "index", "full"):
             raise ValueError("record_format: adaptive | mask | index | full")
         self.format = record_format
@@ -372,9 +373,12 @@ class Checkpointer:
             self.times["encode"].append((p["e0"], e1))
         if n > self.rec_cap:
             # the record outgrew its slot (R20): the reference has advanced, so this version can only
-            # be recovered from a base — the next save takes one (§3.1 base stream)
+            # be recovered from a base — the next save takes one (§3.1 base stream).
+            # Records issued after it are useless (they link to it) and dropped; the device's sticky
+            # TC_ERR_CAPACITY of the refused record is consumed here.
             self.needs_base = True
             self.pending.clear()
+            self.ctx.check_status(self.s_comp)
             return n
         count = self._count_of(n, p["fmt"])
         if self.format == "adaptive":

@@ -287,12 +287,12 @@ __device__ __forceinline__ void mask_block(const EncParams& P, SmemA& sm, uint8_
         woff += k < wid ? v : 0u;
         total += v;
     }
-    const bool sparse = total * W <= kSpillBytes;
+    const bool imode = P.index_mode != 0;
+    const bool sparse = total * W <= (imode ? kSpillBytes : kSpillMask);
 
     // ---- sparse block: pack the new words into the block's spill slot now (index mode: and
     //      their u16 in-tile positions in the second half of the slot) ----
-    const bool imode = P.index_mode != 0;
-    const size_t slot_bytes = imode ? 2 * kSpillBytes : kSpillBytes;
+    const size_t slot_bytes = imode ? 2 * kSpillBytes : kSpillMask;
     if (sparse && total) {
         word_t* slot = reinterpret_cast<word_t*>(P.spill + I.b * slot_bytes) + woff;
         uint16_t* islot = reinterpret_cast<uint16_t*>(P.spill + I.b * slot_bytes + kSpillBytes) + woff;
@@ -531,12 +531,12 @@ __device__ __forceinline__ uint32_t maskin_block(const EncParams& P, const Block
     }
     const uint32_t lpre = inc - c;  // changed words of the block before this lane's mask words
     const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-    const bool sparse = total * W <= kSpillBytes;
     const bool imode = P.index_mode != 0;
+    const bool sparse = total * W <= (imode ? kSpillBytes : kSpillMask);
     const uint32_t tmask = P.T - 1;
 
     if (sparse && total) {
-        const size_t slot_bytes = imode ? 2 * kSpillBytes : kSpillBytes;
+        const size_t slot_bytes = imode ? 2 * kSpillBytes : kSpillMask;
         word_t* slot = reinterpret_cast<word_t*>(P.spill + I.b * slot_bytes);
         uint16_t* islot = reinterpret_cast<uint16_t*>(P.spill + I.b * slot_bytes + kSpillBytes);
         const uint32_t maxc = __reduce_max_sync(0xffffffffu, c);
@@ -852,7 +852,7 @@ __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __gri
             src = P.spill + b * (2 * kSpillBytes);
         } else {
             dst = rec + record_fixed_bytes(I.m, P.T) + prefix * I.w;
-            src = P.spill + b * kSpillBytes;
+            src = P.spill + b * kSpillMask;
         }
         dense = (info & kDenseFlag) != 0 && c != 0 && fits;
     }

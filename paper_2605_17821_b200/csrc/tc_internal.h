@@ -106,6 +106,10 @@ constexpr uint32_t kMaskStageWords = 256;  // mask words of one block (8192 16-b
 
 constexpr uint32_t kEmitGroup = 256;        // blocks per emit CTA / per group sum
 constexpr uint32_t kSpillBytes = 4096;      // per-block spill slot (1/4 of a block's words)
+#ifndef TC_SPILL_MASK
+#define TC_SPILL_MASK 4096
+#endif
+constexpr uint32_t kSpillMask = TC_SPILL_MASK;  // mask mode: spill slot per block (experiment knob)
 constexpr uint32_t kDenseFlag = 0x80000000u;
 constexpr int kAccDoneShift = 40;  // chunk_acc: blocks counted above bit 40 (a chunk has <= 2^19 blocks)
 constexpr unsigned long long kAccCountMask = (1ull << kAccDoneShift) - 1;

@@ -310,7 +310,7 @@ static tc_status encode_impl(tc_ctx* ctx, const SegSpec* specs, int nseg, const 
     st = ensure(&ctx->enc, &ctx->enc_bytes, need, s);
     if (st != TC_OK) return st;
     if (o.index_mode != kFormatFull) {
-        st = ensure(&ctx->spill, &ctx->spill_bytes, blocks * static_cast<size_t>(kSpillBytes) * (o.index_mode ? 2 : 1), s);
+        st = ensure(&ctx->spill, &ctx->spill_bytes, blocks * static_cast<size_t>(o.index_mode ? 2 * kSpillBytes : kSpillMask), s);
         if (st != TC_OK) return st;
     }
     if (o.index_mode == 1) {

@@ -309,3 +309,33 @@ def test_fullsize_cfg2_bench_config_chain_parity(tco):
     ctx.check()
     assert all(torch.equal(a, b) for a, b in zip(ref, cur))
     ctx.close()
+
+
+def test_record_overflow_forces_a_base_and_the_chain_recovers():
+    """R20: record slots sized for a sparse job; a dense step's record does not fit — refused on the
+    device, so the next save is a base (§3.1 base stream): the reference becomes the
+    live state, Tier-1 holds the new base, the neighbour (ring of one) receives it in paced chunks.
+    The chain continues from it and recover() after a GPU failure lands on the chain head."""
+    sizes, wb, seed = [60001, 60001, 60001, 60001], [2, 4, 4, 4], synth.SEED0 + 13
+    live = _dev_state(sizes, wb, seed, 0, 0.0)
+    ck = Checkpointer(live, tier2="push", rec_cap=64 << 10, t2_slots=4, chunk_words=1 << 15, base_interval=4)
+    small = ck.rec_cap
+    expect = [to_np(t) for t in live]
+    fs = {1: 0.001, 2: 0.9, 3: 0.001, 4: 0.002, 5: 0.001}
+    for v in range(1, 6):
+        for s, t in enumerate(live):
+            tc.synth_step(t, seed, s, v, synth.p53_of(fs[v]))
+        expect = [synth.step(e, seed, s, v, fs[v]) for s, e in enumerate(expect)]
+        ck.save_step(v)
+    ck.flush()
+    ck.base_rep.flush(99)
+    torch.cuda.synchronize()
+    assert small < sum(n * w for n, w in zip(sizes, wb)) * 0.9  # the dense record cannot fit
+    # v2 overflowed (found when save 3 finished it; v3, linked to v2, is dropped), so save 4 is a
+    # base: the chain restarts at 4
+    assert ck.chain.base_version == 4 and [e.version for e in ck.chain.entries] == [5]
+    assert ck.base_rep.committed_version() == 4
+    ck.drop_tier("hbm")
+    assert ck.recover(batch=5) == 5
+    assert all(np.array_equal(to_np(a), b) for a, b in zip(live, expect))
+    ck.close()
