@@ -134,10 +134,12 @@ class HostArena:
     entries (records oldest -> newest, reclaimed from the oldest).  `alloc` returns a byte offset,
     or None when the entry does not fit (the caller then keeps that entry off Tier-1)."""
 
-    def __init__(self, nbytes: int):
-        from . import tc
+    def __init__(self, nbytes: int, buffer=None):
+        if buffer is None:
+            from . import tc
 
-        self.buf = tc.HostBuffer(max(16, int(nbytes)))
+            buffer = tc.HostBuffer(max(16, int(nbytes)))
+        self.buf = buffer  # tc.HostBuffer (anything with .nbytes / .tensor / .data_ptr())
         self.cap = self.buf.nbytes
         self.q = deque()  # (key, off, nbytes16)
 

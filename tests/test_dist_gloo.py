@@ -128,3 +128,30 @@ def test_plan_loading_cascade():
 
     assert plan_loading(True, True) == "t1" and plan_loading(True, False) == "t1"
     assert plan_loading(False, True) == "t2" and plan_loading(False, False) == "t3"
+
+
+class _FakeBuf:
+    def __init__(self, n):
+        self.nbytes = n
+
+
+def test_host_arena_ring_allocation():
+    """The Tier-1 arena (checkpoint.HostArena) is a FIFO ring: entries are 16-byte padded, placed
+    after the newest, wrap to offset 0 when the tail is full, never overlap a live entry, and the
+    space of reclaimed (oldest) entries is reused."""
+    from paper_2605_17821_b200.checkpoint import HostArena
+
+    a = HostArena(1000, buffer=_FakeBuf(1000))
+    assert a.alloc("r1", 300) == 0
+    assert a.alloc("r2", 301) == 304          # padded to 16
+    assert a.alloc("r3", 400) is None         # 304 + 304 + 400 > 1000 and no room at the front
+    a.release(lambda k: k != "r1")            # reclaim r1: [0, 304) is free
+    assert a.alloc("r3", 200) == 608          # still fits after r2
+    assert a.alloc("r4", 250) == 0            # wraps into the reclaimed front
+    assert a.alloc("r5", 100) is None         # [256, 304) is too small; r2 and r3 are live
+    a.release(lambda k: k not in ("r2", "r3"))
+    assert a.alloc("r5", 100) == 256          # after r4, in the freed middle
+    live = sorted((o, o + n) for _, o, n in a.q)
+    assert all(b0 <= a1 for (a0, b0), (a1, b1) in zip(live, live[1:])), live
+    a.clear()
+    assert a.alloc("x", 992) == 0 and a.alloc("y", 1) is None  # 1000 bytes hold 992 padded
