@@ -34,6 +34,15 @@ __device__ __forceinline__ bool is_pow2(uint64_t x) { return x && !(x & (x - 1))
 
 __device__ __forceinline__ uint64_t ld_u64(const uint8_t* p) { return *reinterpret_cast<const uint64_t*>(p); }
 
+constexpr uint32_t kEntryTiles = 32;  // fold_entries: tiles a warp takes per unit (one per lane)
+
+// Words per fold unit of a chunk: max(T, kFoldWords); entry-driven chunks (strategy 3) take
+// kEntryTiles tiles of max(T, kFoldWords) words per unit.
+__host__ __device__ inline uint64_t fold_unit_words(uint32_t T, uint32_t strategy) {
+    const uint64_t U = T > kFoldWords ? T : kFoldWords;
+    return strategy == 3u ? U * kEntryTiles : U;
+}
+
 // ------------------------------------------------------------------ walker ----------
 __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_constant__ FoldParams P) {
     __shared__ unsigned s_err[TC_MAX_FOLD];
@@ -157,14 +166,13 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
             P.info[2] = 0;
             P.info[3] = 0;
             P.info[4] = 0;
+            P.info[5] = 0;
         } else {
             const unsigned R = s_nrec[0];
-            uint64_t u = 0, ndense = 0, nlist = 0;
+            uint64_t u = 0, ndense = 0, nlist = 0, nentry = 0;
             for (unsigned r = 0; r < R; ++r) {
                 P.unit_first[r] = u;
                 FoldRec& a = P.desc[r];
-                const uint64_t U = a.T > kFoldWords ? a.T : kFoldWords;
-                u += a.m ? cdiv(a.m, U) : 0;
                 // dense chunk: the changed words of the N records cover enough sectors that
                 // streaming the whole chunk through shared memory beats scattered writes
                 uint64_t sum = 0;
@@ -175,11 +183,20 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
                 // every chunk (mask-mode chunks through fold_dense_kernel), UINT32_MAX = scatter all.
                 bool all_idx = a.T == kListT && P.nrec <= static_cast<int>(kListMaxRec);
                 for (int k = 0; k < P.nrec && all_idx; ++k) all_idx = P.desc[static_cast<size_t>(k) * P.cap + r].idx != nullptr;
+                bool all_index = true;  // every record of the chunk's chain is an index-mode record
+                for (int k = 0; k < P.nrec && all_index; ++k) all_index = P.desc[static_cast<size_t>(k) * P.cap + r].idx != nullptr;
                 bool any_full = false;  // chains with a full record are scattered (fold_unit handles them)
                 for (int k = 0; k < P.nrec; ++k) any_full = any_full || P.desc[static_cast<size_t>(k) * P.cap + r].full;
                 const uint64_t mm = a.m;
                 if (any_full) {
                     a.dense = 0u;
+                } else if (all_index && P.dense_permille != 0u && P.dense_permille != 0xffffffffu &&
+                           (P.nrec == 1 || sum * 400ull <= mm * static_cast<uint64_t>(P.nrec))) {
+                    // index records applied straight from their entries, one pass per record oldest ->
+                    // newest (fold_entries_kernel): always for one record; for a chain while the
+                    // records average <= 0.25 % changed (cfg2 measured: a pass costs 0.38 ms at 0.1 %,
+                    // 2.3 ms at 1 %; the streaming list fold of 8 records 6.6 / 8.1 ms)
+                    a.dense = 3u;
                 } else if (P.dense_permille == 0u) {
                     a.dense = all_idx ? 2u : 1u;
                 } else if (P.dense_permille == 0xffffffffu || !all_idx) {
@@ -190,13 +207,17 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
                 }
                 ndense += a.dense == 1u;
                 nlist += a.dense == 2u;
+                nentry += a.dense == 3u;
+                const uint64_t U = fold_unit_words(a.T, a.dense);
+                u += a.m ? cdiv(a.m, U) : 0;
             }
             P.unit_first[R] = u;
             P.info[0] = R;
             P.info[1] = u;
             P.info[2] = ndense;              // chunks for fold_dense_kernel
-            P.info[3] = R - ndense - nlist;  // chunks for fold_kernel
+            P.info[3] = R - ndense - nlist - nentry;  // chunks for fold_kernel
             P.info[4] = nlist;               // chunks for fold_list_kernel
+            P.info[5] = nentry;              // chunks for fold_entries_kernel
         }
     }
 }
@@ -416,44 +437,83 @@ __device__ void fold_unit(const FoldParams& P, uint64_t r, uint64_t ku, uint32_t
     }
 }
 
-// One sparse index-mode record (N = 1): its positions are explicit, so the unit's tiles are applied
-// straight from their entry ranges [tile_off[t], tile_off[t+1]) — coalesced position / value
-// loads, scattered word stores — without building mask words.  Checks as everywhere: ranges
-// monotone and inside the record, first entry 0, last = count, positions inside the tile and
-// strictly increasing.
+// One index-mode record (N = 1): its positions are explicit, so a unit of kEntryTiles tiles is
+// applied straight from its entries — no mask words.  Lane l holds tile l's entry range
+// [tile_off[t], tile_off[t+1]); the warp walks the group's entries as one flat range, 32 entries
+// per pass and 4 passes in flight (coalesced position / value loads), each lane finding its
+// entry's tile by a 5-step binary search over the lanes' tile starts (shuffles), then storing the
+// word.  Checks as everywhere: ranges monotone and inside the record, first entry 0, last =
+// count, positions inside the tile and strictly increasing within it.  ~20 warp instructions per
+// 32 entries, against ~800 per 32 entries through the mask machinery (r2 ncu: that path issued
+// on 61 % of cycles at 23 % of DRAM bandwidth for the step's 1 % record).
 template <int W>
-__device__ void fold_unit_index1(const FoldParams& P, uint64_t r, uint64_t ku, int lane, bool& bad) {
+__device__ void fold_entries(const FoldParams& P, const FoldRec& R, uint64_t ku, int lane, bool& bad) {
     using word_t = typename Word<W>::T;
-    const FoldRec& R = P.desc[r];
     const uint32_t m = R.m, T = R.T;
-    const uint32_t U = T > kFoldWords ? T : kFoldWords;
-    const uint32_t ustart = static_cast<uint32_t>(ku) * U;
-    const uint32_t uend = ustart + U < m ? ustart + U : m;
+    const uint64_t Uw = fold_unit_words(R.T, 3u);
+    const uint32_t tpu = static_cast<uint32_t>(Uw / T);  // tiles per unit
+    const uint32_t nt = (m + T - 1) / T;
+    const uint32_t tb0 = static_cast<uint32_t>(ku) * tpu;
+    const uint32_t tb1 = tb0 + tpu < nt ? tb0 + tpu : nt;
     word_t* state = reinterpret_cast<word_t*>(P.state[R.seg]) + R.chunk_off;
     const uint32_t* toff = reinterpret_cast<const uint32_t*>(R.toff);
     const uint16_t* idx = reinterpret_cast<const uint16_t*>(R.idx);
     const word_t* vals = reinterpret_cast<const word_t*>(R.values);
     const uint32_t count = static_cast<uint32_t>(R.count);
-    const uint32_t t0 = ustart / T, t1 = (uend + T - 1) / T;  // tiles of the unit (<= 128)
-    // the unit's tile boundaries, one per lane (all loads in flight together)
-    for (uint32_t tb = t0; tb < t1; tb += 32) {
-        const uint32_t t = tb + lane;
-        const bool in = t < t1;
-        const uint32_t a = in ? ldg_u32(toff + t) : 0u, b = in ? ldg_u32(toff + t + 1) : 0u;
-        if (in && (b < a || b > count || (t == 0 && a != 0) || ((t + 1) * T >= m && b != count))) bad = true;
-        const uint32_t nt = t1 - tb < 32 ? t1 - tb : 32;
-        for (uint32_t q = 0; q < nt; ++q) {  // the warp applies tile tb + q
-            const uint32_t k0 = __shfl_sync(0xffffffffu, a, q), k1 = __shfl_sync(0xffffffffu, b, q);
-            if (k1 < k0 || k1 > count) continue;
-            const uint32_t ts = (tb + q) * T;
-            const uint32_t tl = m - ts < T ? m - ts : T;
-            for (uint32_t k = k0 + lane; k < k1; k += 32) {
-                const uint32_t x = __ldg(reinterpret_cast<const unsigned short*>(idx) + k);
-                if (x >= tl || (k > k0 && __ldg(reinterpret_cast<const unsigned short*>(idx) + k - 1) >= x)) {
-                    bad = true;
-                    continue;
+    constexpr int kQ = 4;
+    for (uint32_t tg = tb0; tg < tb1; tg += 32) {
+        const uint32_t ng = tb1 - tg < 32 ? tb1 - tg : 32;  // tiles in this group
+        const uint32_t t = tg + lane;
+        const bool in = static_cast<uint32_t>(lane) < ng;
+        const uint32_t a = in ? ldg_u32(toff + t) : 0xffffffffu;
+        const uint32_t b = in ? ldg_u32(toff + t + 1) : 0u;
+        if (in && (b < a || b > count || (t == 0 && a != 0) || (t + 1 == nt && b != count))) bad = true;
+        const uint32_t A = __shfl_sync(0xffffffffu, a, 0);
+        const uint32_t B = __shfl_sync(0xffffffffu, b, ng - 1);
+        if (B < A || B > count || __any_sync(0xffffffffu, bad)) {
+            bad = true;
+            continue;
+        }
+        uint32_t carry_x = 0xffffffffu;  // position of the entry before this pass's lane 0
+        for (uint32_t kb = A; kb < B; kb += 32 * kQ) {
+            uint32_t x[kQ];
+            word_t v[kQ];
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) {
+                const uint32_t k = kb + q * 32 + lane;
+                x[q] = 0;
+                if (k < B) {
+                    x[q] = __ldg(reinterpret_cast<const unsigned short*>(idx) + k);
+                    v[q] = ldg_word(vals + k);
                 }
-                state[ts + x] = ldg_word(vals + k);
+            }
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) {
+                const uint32_t k = kb + q * 32 + lane;
+                // the tile: the last lane j < ng whose start a_j <= k (empty tiles resolve upward)
+                uint32_t lo = 0, hi = ng;
+#pragma unroll
+                for (int st = 0; st < 5; ++st) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    const uint32_t am = __shfl_sync(0xffffffffu, a, mid);
+                    if (hi - lo > 1) {
+                        if (am <= k) lo = mid;
+                        else hi = mid;
+                    }
+                }
+                const uint32_t aj = __shfl_sync(0xffffffffu, a, lo);
+                const uint32_t up = __shfl_up_sync(0xffffffffu, x[q], 1);
+                const uint32_t prev = lane == 0 ? carry_x : up;
+                carry_x = __shfl_sync(0xffffffffu, x[q], 31);
+                if (k < B) {
+                    const uint32_t ts = (tg + lo) * T;
+                    const uint32_t tl = m - ts < T ? m - ts : T;
+                    if (x[q] >= tl || (k > aj && prev >= x[q])) {
+                        bad = true;
+                        continue;
+                    }
+                    state[ts + x[q]] = v[q];
+                }
             }
         }
     }
@@ -476,24 +536,57 @@ __global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const __grid_cons
             const uint64_t mid = (lo + hi) >> 1;
             if (P.unit_first[mid] <= u) lo = mid; else hi = mid;
         }
-        if (P.desc[lo].dense) {  // folded by fold_dense_kernel: jump past the chunk
+        if (P.desc[lo].dense == 1u || P.desc[lo].dense == 2u) {  // a streaming kernel's chunk: jump past it
             const uint64_t nxt = P.unit_first[lo + 1];
             u += (nxt - u + nwarps - 1) / nwarps * nwarps - nwarps;
             continue;
         }
         const uint64_t ku = u - P.unit_first[lo];
-        // a sparse single index-mode record (< 0.6 % of the chunk; cfg2 measured: 0.75 vs 1.75 ms at
-        // 0.1 %, 1.64 vs 2.04 ms at 0.5 %, crossover near 0.7 %) is applied straight from its entries
-        if (P.nrec == 1 && P.desc[lo].idx && P.desc[lo].count * 1000ull < static_cast<uint64_t>(P.desc[lo].m) * 6ull) {
-            if (P.desc[lo].w == 4)
-                fold_unit_index1<4>(P, lo, ku, lane, bad);
-            else
-                fold_unit_index1<2>(P, lo, ku, lane, bad);
-        } else if (P.desc[lo].w == 4) {
+        if (P.desc[lo].dense == 3u) {  // fold_entries_kernel's chunk: jump past it
+            const uint64_t nxt = P.unit_first[lo + 1];
+            u += (nxt - u + nwarps - 1) / nwarps * nwarps - nwarps;
+            continue;
+        }
+        if (P.desc[lo].w == 4) {
             fold_unit<4>(P, lo, ku, s_carry[wid], s_imask[wid], lane, bad);
         } else {
             fold_unit<2>(P, lo, ku, s_carry[wid], s_imask[wid], lane, bad);
         }
+        if (__any_sync(0xffffffffu, bad)) {  // malformed record: state unspecified
+            if (lane == 0) tc_set_err(P.err, TC_ERR_CORRUPT);
+            return;
+        }
+    }
+}
+
+// Chunks whose chain is index-mode records applied from their entries (walker strategy 3): one
+// launch per record j, oldest first (stream order = newest wins); a warp per unit of kEntryTiles
+// tiles (fold_entries).
+__global__ void __launch_bounds__(kFoldThreads) fold_entries_kernel(const __grid_constant__ FoldParams P, int j) {
+    if (*reinterpret_cast<volatile unsigned*>(P.err) != 0) return;  // sticky error pending
+    if (P.info[5] == 0) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint64_t R = P.info[0];
+    const uint64_t total = P.info[1];
+    const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * kFoldWarps;
+    bool bad = false;
+    for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * kFoldWarps + wid; u < total; u += nwarps) {
+        uint64_t lo = 0, hi = R;
+        while (hi - lo > 1) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (P.unit_first[mid] <= u) lo = mid; else hi = mid;
+        }
+        if (P.desc[lo].dense != 3u) {  // another kernel's chunk: jump past it
+            const uint64_t nxt = P.unit_first[lo + 1];
+            u += (nxt - u + nwarps - 1) / nwarps * nwarps - nwarps;
+            continue;
+        }
+        const uint64_t ku = u - P.unit_first[lo];
+        const FoldRec& Rj = P.desc[static_cast<size_t>(j) * P.cap + lo];  // record j of chunk lo
+        if (Rj.w == 4)
+            fold_entries<4>(P, Rj, ku, lane, bad);
+        else
+            fold_entries<2>(P, Rj, ku, lane, bad);
         if (__any_sync(0xffffffffu, bad)) {  // malformed record: state unspecified
             if (lane == 0) tc_set_err(P.err, TC_ERR_CORRUPT);
             return;
@@ -1238,7 +1331,20 @@ cudaError_t launch_fold(const FoldParams& p, cudaStream_t s, int num_sms, uint64
             occ_l = 1;
     }
     fold_list_kernel<<<num_sms * occ_l, kListThreads, 0, s>>>(p);
-    *launches += 4;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    static int occ_e = 0;
+    if (!occ_e) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_e, fold_entries_kernel, kFoldThreads, 0) != cudaSuccess ||
+            occ_e < 1)
+            occ_e = 4;
+    }
+    for (int j = 0; j < p.nrec; ++j) {  // each returns at once when no chunk takes strategy 3
+        fold_entries_kernel<<<num_sms * occ_e, kFoldThreads, 0, s>>>(p, j);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    *launches += 4 + static_cast<uint64_t>(p.nrec);
     return cudaGetLastError();
 }
 

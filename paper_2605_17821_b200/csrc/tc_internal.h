@@ -143,7 +143,7 @@ struct FoldParams {
     uint32_t dense_permille;  // chunk r is dense when sum_j count_j * 1000 > m * dense_permille
     FoldRec* desc;          // [nrec][cap]
     uint64_t* unit_first;   // [cap + 1]
-    unsigned long long* info;  // [0] records per diff, [1] total units, chunks for [2] fold_dense, [3] fold, [4] fold_list
+    unsigned long long* info;  // [0] records per diff, [1] total units, chunks for [2] fold_dense, [3] fold, [4] fold_list, [5] fold_entries
     unsigned int* err;
 };
 

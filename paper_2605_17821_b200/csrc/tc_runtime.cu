@@ -454,7 +454,7 @@ tc_status tc_diff_apply(tc_ctx* ctx, void* const* state, const uint64_t* n_words
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaSetDevice(ctx->device);
     const size_t desc_bytes = sizeof(FoldRec) * cap * n_records;
-    const size_t need = desc_bytes + 8 * (cap + 1) + 48;
+    const size_t need = desc_bytes + 8 * (cap + 1) + 64;  // desc | unit_first | info[6]
     tc_status st = ensure(&ctx->fold, &ctx->fold_bytes, need, s);
     if (st != TC_OK) return st;
     uint8_t* base = static_cast<uint8_t*>(ctx->fold);

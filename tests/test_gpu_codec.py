@@ -321,7 +321,7 @@ def test_launch_counter(ctx):
     tc.diff_encode(ctx, [ref], [ref.clone()], out, ob, 1, 0)
     tc.diff_apply(ctx, [ref], 0, [out], [int(ob.item())])
     ctx.check()
-    assert ctx.launches == before + 7  # encode (mask, prefix, emit) + fold (walker, scatter, stream, list)
+    assert ctx.launches == before + 8  # encode (mask, prefix, emit) + fold (walker, scatter, stream, list, entries)
 
 
 @pytest.mark.parametrize("advance", [True, False])
@@ -619,3 +619,35 @@ def test_full_range_encode_and_tamper(ctx, tco):
         assert rc == tc.ERR_CORRUPT and all(np.array_equal(a, b) for a, b in zip(st, ref_np))
     rc, st = gpu_fold(ctx, list(ref_np), 1, [exp])
     assert rc == tc.OK and all(np.array_equal(a, b) for a, b in zip(st, cur_np))
+
+
+@pytest.mark.parametrize("N", [1, 2, 5, 9])
+@pytest.mark.parametrize("T", [4096, 256])
+def test_sparse_index_chain_entry_passes(fctx, tco, N, T):
+    """Sparse all-index chains (<= 0.25 % per record on average: walker strategy 3, one entry pass
+    per record oldest first) fold bit-exactly; a non-increasing position list in a middle record is
+    CORRUPT (the fold may have started: the state is then unspecified)."""
+    sizes, wb, C = [300_001, 70_001, 200_003], [4, 2, 4], 4096 * 16
+    states = [synth.state(sizes, wb, 71, v, 0.002) for v in range(N + 1)]
+    ref = [a.copy() for a in states[0]]
+    diffs = []
+    for v in range(1, N + 1):
+        rc, d = tco.encode(ref, states[v], tile_words=T, chunk_words=C, version=v, ref_version=v - 1,
+                           index_mode=True)
+        assert rc == 0
+        diffs.append(d)
+    rc, st_g = gpu_fold(fctx, states[0], 0, diffs)
+    assert rc == tc.OK
+    assert all(np.array_equal(a, b) for a, b in zip(st_g, states[N]))
+    # tamper record (N+1)//2: swap the first two positions of the first tile holding >= 2 entries
+    j = (N + 1) // 2 - 1
+    bad = diffs[j].copy()
+    nt = -(-min(sizes[0], C) // T)
+    toff = bad[64: 64 + 4 * (nt + 1)].view("<u4")
+    t = int(np.nonzero(np.diff(toff.astype(np.int64)) >= 2)[0][0])
+    p = 64 + ((4 * (nt + 1) + 15) // 16) * 16 + 2 * int(toff[t])
+    bad[p: p + 4] = bad[[p + 2, p + 3, p, p + 1]]
+    chain = diffs[:j] + [bad] + diffs[j + 1:]
+    assert tco.fold([a.copy() for a in states[0]], 0, chain)[0] == tc.ERR_CORRUPT
+    rc, _ = gpu_fold(fctx, states[0], 0, chain)
+    assert rc == tc.ERR_CORRUPT
