@@ -682,6 +682,104 @@ __global__ void __launch_bounds__(256) adam_mask_kernel(float* __restrict__ mast
     }
 }
 
+// The Adam step with its FULL-format differential written in the same pass (tc_adam_step_encode with
+// index_mode = 2, reading R21): full records have data-independent sizes, so every element knows
+// where its four words go — record of segment s (w16 | master | m | v), chunk c at
+// base[s] + c * rec_full[s], word i - c*C after the 64-byte header — and the pass writes the new
+// state and the record together: no mask, no second pass over the new state (the mask path's
+// dense case re-read it).  A thread per 4 consecutive parameters (16-byte loads / stores; 8 bytes
+// for the bf16 words); the thread holding a chunk's first quad writes its four headers, the one
+// holding its last quad the padding.
+struct AdamFullLayout {
+    uint64_t base[4];      // byte offset of each segment's first record
+    uint64_t rec_full[4];  // record bytes of a full chunk (m = C)
+    uint64_t C, total, version, ref_version;
+    uint32_t T;
+};
+
+__device__ __forceinline__ void adam_full_header(uint8_t* out, const AdamFullLayout& L, int s, uint64_t c, uint64_t mc) {
+    const uint32_t w = s == 0 ? 2u : 4u;
+    uint64_t* h = reinterpret_cast<uint64_t*>(out + L.base[s] + c * L.rec_full[s]);
+    h[0] = 0x31444354ull /* "TCD1" */ | (1ull << 32) | (static_cast<uint64_t>(w) << 48) | (5ull << 56);
+    h[1] = static_cast<uint64_t>(L.T) | (static_cast<uint64_t>(s) << 32);
+    h[2] = c * L.C;
+    h[3] = mc;
+    h[4] = mc;
+    h[5] = L.version;
+    h[6] = L.ref_version;
+    h[7] = kHdr + pad16u(w * mc);
+}
+
+__global__ void __launch_bounds__(256) adam_full_kernel(float* __restrict__ master, float* __restrict__ m,
+                                                        float* __restrict__ v, uint16_t* __restrict__ w16, uint64_t n,
+                                                        const float* __restrict__ g, AdamC a, float ss, float ic,
+                                                        uint8_t* __restrict__ out, uint64_t out_cap, uint64_t* out_bytes,
+                                                        const AdamFullLayout L, unsigned* err) {
+    const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t0 == 0) {
+        *reinterpret_cast<volatile uint64_t*>(out_bytes) = L.total;
+        if (L.total > out_cap) tc_set_err(err, TC_ERR_CAPACITY);
+        if (n == 0 && L.total <= out_cap)
+            for (int s = 0; s < 4; ++s) adam_full_header(out, L, s, 0, 0);  // four empty records
+    }
+    if (L.total > out_cap) return;  // nothing of the diff is written
+    const uint64_t nq = (n + 3) / 4;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t q = t0; q < nq; q += stride) {
+        const uint64_t i0 = q * 4;
+        const uint64_t c = i0 / L.C, off = i0 - c * L.C;  // C is a multiple of 4: a quad never straddles chunks
+        const uint64_t mc = n - c * L.C < L.C ? n - c * L.C : L.C;
+        uint8_t* r0 = out + L.base[0] + c * L.rec_full[0] + kHdr;
+        uint8_t* r1 = out + L.base[1] + c * L.rec_full[1] + kHdr;
+        uint8_t* r2 = out + L.base[2] + c * L.rec_full[2] + kHdr;
+        uint8_t* r3 = out + L.base[3] + c * L.rec_full[3] + kHdr;
+        if (i0 + 4 <= n) {
+            float4 w = reinterpret_cast<const float4*>(master)[q];
+            float4 mm = reinterpret_cast<const float4*>(m)[q];
+            float4 vv = reinterpret_cast<const float4*>(v)[q];
+            const float4 gg = __ldg(reinterpret_cast<const float4*>(g) + q);
+            adam_update(w.x, mm.x, vv.x, gg.x, a, ss, ic);
+            adam_update(w.y, mm.y, vv.y, gg.y, a, ss, ic);
+            adam_update(w.z, mm.z, vv.z, gg.z, a, ss, ic);
+            adam_update(w.w, mm.w, vv.w, gg.w, a, ss, ic);
+            ushort4 h;
+            h.x = __bfloat16_as_ushort(__float2bfloat16_rn(w.x));
+            h.y = __bfloat16_as_ushort(__float2bfloat16_rn(w.y));
+            h.z = __bfloat16_as_ushort(__float2bfloat16_rn(w.z));
+            h.w = __bfloat16_as_ushort(__float2bfloat16_rn(w.w));
+            reinterpret_cast<float4*>(master)[q] = w;
+            reinterpret_cast<float4*>(m)[q] = mm;
+            reinterpret_cast<float4*>(v)[q] = vv;
+            reinterpret_cast<ushort4*>(w16)[q] = h;
+            *reinterpret_cast<ushort4*>(r0 + 2 * off) = h;
+            *reinterpret_cast<float4*>(r1 + 4 * off) = w;
+            *reinterpret_cast<float4*>(r2 + 4 * off) = mm;
+            *reinterpret_cast<float4*>(r3 + 4 * off) = vv;
+        } else {
+            for (uint64_t i = i0; i < n; ++i) {  // the last, partial quad
+                float w = master[i], mm = m[i], vv = v[i];
+                adam_update(w, mm, vv, g[i], a, ss, ic);
+                const uint16_t h = __bfloat16_as_ushort(__float2bfloat16_rn(w));
+                master[i] = w;
+                m[i] = mm;
+                v[i] = vv;
+                w16[i] = h;
+                const uint64_t o = i - c * L.C;
+                *reinterpret_cast<uint16_t*>(r0 + 2 * o) = h;
+                *reinterpret_cast<float*>(r1 + 4 * o) = w;
+                *reinterpret_cast<float*>(r2 + 4 * o) = mm;
+                *reinterpret_cast<float*>(r3 + 4 * o) = vv;
+            }
+        }
+        if (off == 0)
+            for (int s = 0; s < 4; ++s) adam_full_header(out, L, s, c, mc);
+        if (off + 4 >= mc) {  // the chunk's last quad: zero the padding of its four records
+            for (uint64_t x = 2 * mc; x < pad16u(2 * mc); ++x) r0[x] = 0;
+            for (uint64_t x = 4 * mc; x < pad16u(4 * mc); ++x) r1[x] = r2[x] = r3[x] = 0;
+        }
+    }
+}
+
 struct ReplayParams {
     float* master;
     float* m;
@@ -1111,6 +1209,10 @@ tc_status tc_adam_replay(tc_ctx* ctx, const tc_adam_state* stt, const void* cons
     return tc_adam_step(ctx, stt, scratch, hp, first_step + nf, stream);
 }
 
+static tc_status adam_step_encode_full(tc_ctx* ctx, const tc_adam_state* stt, const float* grad, const tc_adam_hp* hp,
+                                       uint64_t step, const tc_encode_opts& o, void* out, uint64_t out_cap,
+                                       uint64_t* out_bytes, cudaStream_t s);
+
 tc_status tc_adam_step_encode(tc_ctx* ctx, const tc_adam_state* stt, const float* grad, const tc_adam_hp* hp,
                               uint64_t step, const tc_encode_opts* opts, void* out, uint64_t out_cap,
                               uint64_t* out_bytes, tc_stream stream) {
@@ -1121,6 +1223,15 @@ tc_status tc_adam_step_encode(tc_ctx* ctx, const tc_adam_state* stt, const float
     if (stt->n && (!grad || !aligned16(grad))) return fail(TC_ERR_INVALID, "grad is NULL or not 16-byte aligned");
     cudaSetDevice(tc::ctx_device(ctx));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (opts && opts->index_mode == 2) {  // full records: one pass (the options are checked as usual)
+        tc_encode_opts o = *opts;
+        uint64_t bound = 0;
+        tc_segment lay[4] = {{nullptr, nullptr, stt->n, 2, 0}, {nullptr, nullptr, stt->n, 4, 0},
+                             {nullptr, nullptr, stt->n, 4, 0}, {nullptr, nullptr, stt->n, 4, 0}};
+        st = tc_diff_bound(lay, 4, &o, &bound);  // validates T, C, the format
+        if (st != TC_OK) return st;
+        return adam_step_encode_full(ctx, stt, grad, hp, step, o, out, out_cap, out_bytes, s);
+    }
     const uint64_t n = stt->n, words = (n + 31) / 32;
     const size_t per = pad16u(4 * (words ? words : 1));
     void* scratch = nullptr;
@@ -1142,6 +1253,37 @@ tc_status tc_adam_step_encode(tc_ctx* ctx, const tc_adam_state* stt, const float
                           {nullptr, stt->m, n, 4, 0}, {nullptr, stt->v, n, 4, 0}};
     const uint32_t* const masks[4] = {mk[0], mk[1], mk[2], mk[3]};
     return tc::encode_from_masks(ctx, segs, masks, 4, opts, step, step - 1, out, out_cap, out_bytes, s);
+}
+
+// full-format records: the state and the record in one pass (adam_full_kernel)
+static tc_status adam_step_encode_full(tc_ctx* ctx, const tc_adam_state* stt, const float* grad, const tc_adam_hp* hp,
+                                       uint64_t step, const tc_encode_opts& o, void* out, uint64_t out_cap,
+                                       uint64_t* out_bytes, cudaStream_t s) {
+    const uint64_t n = stt->n, C = o.chunk_words;
+    AdamFullLayout L;
+    uint64_t pos = 0;
+    for (int k = 0; k < 4; ++k) {
+        const uint64_t w = k == 0 ? 2 : 4;
+        L.base[k] = pos;
+        L.rec_full[k] = kHdr + pad16u(w * C);
+        const uint64_t chunks = n ? (n + C - 1) / C : 1;
+        const uint64_t mlast = n ? n - (chunks - 1) * C : 0;
+        pos += (chunks - 1) * L.rec_full[k] + kHdr + pad16u(w * mlast);
+    }
+    L.C = C;
+    L.total = pos;
+    L.version = step;
+    L.ref_version = step - 1;
+    L.T = o.tile_words;
+    float ss, ic;
+    bias(hp, step, &ss, &ic);
+    adam_full_kernel<<<grid_for(ctx, (n + 3) / 4 + 1, 256), 256, 0, s>>>(
+        stt->master, stt->m, stt->v, stt->w16, n, grad, adam_consts(hp), ss, ic, static_cast<uint8_t*>(out), out_cap,
+        out_bytes, L, tc::ctx_err(ctx));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "adam full launch");
+    tc::ctx_add_launches(ctx, 1);
+    return TC_OK;
 }
 
 }  // extern "C"

@@ -505,11 +505,11 @@ def adam_replay(ctx: Ctx, master, m, v, w16, payloads, payload_bytes, first_step
 
 
 def adam_step_encode(ctx: Ctx, master, m, v, w16, grad, step: int, out: torch.Tensor, out_bytes, tile_words=4096,
-                     chunk_words=1 << 28, index_mode=False, stream=None, **hp):
+                     chunk_words=1 << 28, index_mode=False, stream=None, full=False, **hp):
     """Enqueue tc_adam_step_encode: the Adam step + the lossless diff of its update (segments w16,
-    master, m, v) into ``out``."""
+    master, m, v) into ``out``; ``full`` = full records written in the Adam pass itself."""
     st, h = _adam(master, m, v, w16), _hp(**hp)
-    o = _opts(tile_words, chunk_words, False, index_mode)
+    o = _opts(tile_words, chunk_words, False, index_mode, full)
     _check(LIB.tc_adam_step_encode(ctx.h, ctypes.byref(st), grad.data_ptr(), ctypes.byref(h), int(step), ctypes.byref(o),
                                    out.data_ptr(), out.numel() * out.element_size(), out_bytes.data_ptr(),
                                    _stream(stream)), "tc_adam_step_encode")

@@ -171,7 +171,7 @@ def test_replay_corrupt_payload(ctx):
     assert ctx.check_status() == tc.ERR_CORRUPT
 
 
-@pytest.mark.parametrize("index_mode", [False, True])
+@pytest.mark.parametrize("index_mode", [False, True, "full"])
 @pytest.mark.parametrize("n,T,C,zero_frac", [(0, 4096, 1 << 28, 0.0), (1, 4096, 1 << 28, 0.0), (1000, 4096, 1 << 28, 0.5),
                                              (70_001, 256, 8192, 0.9), (300_000, 4096, 1 << 28, 0.99),
                                              # ~20 % changed in the moment segments' second half: sparse
@@ -196,14 +196,16 @@ def test_adam_step_encode_matches_oracle(ctx, tco_lossless, n, T, C, zero_frac, 
     oracle.adam_step(st[0], st[1], st[2], st[3], g, 5)
     ref = [before[3], before[0].view(np.uint32), before[1].view(np.uint32), before[2].view(np.uint32)]
     cur = [st[3], st[0].view(np.uint32), st[1].view(np.uint32), st[2].view(np.uint32)]
+    full = index_mode == "full"  # full records: written by the Adam pass itself (adam_full_kernel)
+    index_mode = index_mode is True
     rc, exp = tco_lossless.encode([a.copy() for a in ref], cur, tile_words=T, chunk_words=C, advance_ref=False,
-                                  version=5, ref_version=4, index_mode=index_mode)
+                                  version=5, ref_version=4, index_mode=index_mode, full=full)
     assert rc == 0
     gs = to_gpu_state(before)
-    cap = tc.diff_bound([n] * 4, [2, 4, 4, 4], T, C, index_mode)
+    cap = tc.diff_bound([n] * 4, [2, 4, 4, 4], T, C, index_mode, full=full)
     out = torch.full((cap,), 0xAB, dtype=torch.uint8, device="cuda")
     ob = torch.zeros(1, dtype=torch.int64, device="cuda")
-    tc.adam_step_encode(ctx, *gs, dev(g), 5, out, ob, T, C, index_mode)
+    tc.adam_step_encode(ctx, *gs, dev(g), 5, out, ob, T, C, index_mode, full=full)
     ctx.check()
     nb = int(ob.item())
     assert nb == exp.size and np.array_equal(out[:nb].cpu().numpy(), exp)

@@ -37,12 +37,15 @@ def main():
     w16 = torch.empty(n, dtype=torch.int16, device=dev)
     g = torch.empty_like(master)
     refs = [torch.empty_like(w16), torch.empty_like(master), torch.empty_like(master), torch.empty_like(master)]
-    cap = max(tc.diff_bound([n] * 4, [2, 4, 4, 4], 4096, 1 << 28, index_mode=im) for im in (False, True))
+    cap = max(max(tc.diff_bound([n] * 4, [2, 4, 4, 4], 4096, 1 << 28, index_mode=im) for im in (False, True)),
+              tc.diff_bound([n] * 4, [2, 4, 4, 4], 4096, 1 << 28, full=True))
     out = torch.empty(cap, dtype=torch.uint8, device=dev)
     ob = torch.zeros(1, dtype=torch.int64, device=dev)
     W = 14 * n
     res = {"n": n, "state_bytes": W}
-    for regime, imode in (("sparse", False), ("sparse_index", True), ("dense", False)):
+    for regime, imode in (("sparse", False), ("sparse_index", True), ("dense", False), ("dense_full", "full")):
+        full = imode == "full"
+        imode = imode is True
         gen = torch.Generator(device=dev).manual_seed(1)
         with torch.cuda.stream(s):
             torch.randn(n, out=master, generator=gen)
@@ -77,7 +80,7 @@ def main():
             reset()
             e0, e1 = ev(), ev()
             e0.record(s)
-            tc.adam_step_encode(ctx, master, m, v, w16, g, 7, out, ob, stream=s, index_mode=imode)
+            tc.adam_step_encode(ctx, master, m, v, w16, g, 7, out, ob, stream=s, index_mode=imode, full=full)
             e1.record(s)
             s.synchronize()
             fused.append(e0.elapsed_time(e1))
@@ -89,7 +92,7 @@ def main():
             tc.adam_step(ctx, master, m, v, w16, g, 7, stream=s)
             e1.record(s)
             tc.diff_encode(ctx, refs, [w16, master.view(torch.int32), m.view(torch.int32), v.view(torch.int32)],
-                           out, ob, 7, 6, stream=s, index_mode=imode)
+                           out, ob, 7, 6, stream=s, index_mode=imode, full=full)
             e2.record(s)
             s.synchronize()
             unfused.append((e0.elapsed_time(e1), e1.elapsed_time(e2)))
@@ -111,6 +114,8 @@ def main():
                        "unfused_ms": round(am + em, 3), "speedup": round((am + em) / fm, 3),
                        "changed_bytes": changed_bytes,
                        "fused_frac_hbm_min_bytes": round((4 * n + W + changed_bytes + nb) / fm / 1e6 / peak, 4)}
+        if full:  # the full path writes every state word and every record word: grad + 2 W + record
+            res[regime]["fused_frac_hbm"] = round((4 * n + 2 * W + nb) / fm / 1e6 / peak, 4)
     res["note"] = ("NEXT row 2 (DESIGN.md §13): tc_adam_step_encode vs tc_adam_step + tc_diff_encode(ref copy); "
                    "fused_frac_hbm_min_bytes counts grad + state read + changed words written + record")
     print(json.dumps(res))
