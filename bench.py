@@ -842,9 +842,14 @@ def run_streaming(args, rank, world, local, dev):
     seq = [0]
 
     def checkpoint(v, times, pos0):
-        pos = pos0
+        """One version: the runs' encodes issued one run ahead of the host, which learns each run's
+        length (mapped pinned memory) only after issuing the next encode — the device never idles
+        for the host's round trip — then stages it to Tier-1 and pushes it to the neighbour."""
+        pos = [pos0]
         done = [None, None]
-        for r_i, (i, c0, k) in enumerate(runs):
+
+        def issue(r_i):
+            i, c0, k = runs[r_i]
             sl = r_i % 2
             for e in done[sl] or []:
                 s_comp.wait_event(e)
@@ -853,12 +858,16 @@ def run_streaming(args, rank, world, local, dev):
             tc.diff_encode_range(ctx, R[i], S[i], i, c0, k, slots[sl], lens[r_i: r_i + 1], v, v - 1, T, C, True,
                                  stream=s_comp, index_mode=mode["index"])
             e1.record(s_comp)
+            return e0, e1
+
+        def finish(r_i, e0, e1):
+            sl = r_i % 2
             e1.synchronize()
             n = int(lens[r_i].item())
-            if pos + n > host.nbytes:
+            if pos[0] + n > host.nbytes:
                 raise RuntimeError("host Tier-1 buffer too small")
             s_copy.wait_event(e1)
-            tc.stage_host(host.tensor[pos:], slots[sl], n, tc.D2H, stream=s_copy)
+            tc.stage_host(host.tensor[pos[0]:], slots[sl], n, tc.D2H, stream=s_copy)
             c1 = torch.cuda.Event()
             c1.record(s_copy)
             done[sl] = [c1]
@@ -870,17 +879,26 @@ def run_streaming(args, rank, world, local, dev):
                 r1 = torch.cuda.Event()
                 r1.record(s_comm)
                 done[sl].append(r1)
-            pos += n
+            pos[0] += n
             if times is not None:
                 times.append((e0, e1))
+
+        pend = None
+        for r_i in range(len(runs)):
+            # the slot of run r_i was last used by run r_i - 2, finished (its copy enqueued) by now
+            cur = (r_i,) + issue(r_i)
+            if pend is not None:
+                finish(*pend)
+            pend = cur
+        finish(*pend)
         if args.format == "adaptive" and allow_index:  # density of this checkpoint picks the next format
-            nb = pos - pos0
+            nb = pos[0] - pos0
             if mode["index"]:
                 count = max(0.0, nb - fixed_idx) / (2 + w_avg)
             else:
                 count = max(0.0, nb - fixed_mask) / w_avg
             mode["index"] = count * 16 < total_words
-        return pos
+        return pos[0]
 
     def train_step(v):  # the synthetic optimizer step producing version v (untimed)
         with torch.cuda.stream(s_comp):
