@@ -247,7 +247,10 @@ tc_status tc_push_peer(tc_ctx* ctx, const void* src, const uint64_t* src_bytes, 
  * launch, host synchronization or NCCL; the last emitting CTA then publishes {bytes, version} into
  * `peer_mailbox` with a system-scope release (as tc_push_peer).  A record larger than peer_cap (or
  * an encode that reports an error) is published as refused (bytes = UINT64_MAX: the receiver's
- * tc_peer_wait reports TC_ERR_CAPACITY); bytes below peer_cap may then hold a partial record. */
+ * tc_peer_wait reports TC_ERR_CAPACITY); bytes below peer_cap may then hold a partial record.
+ * peer_dst / peer_mailbox may also be mapped page-locked host memory (tc_host_alloc): the
+ * encoder then emits the record straight into Tier-1 over PCIe (the host polls the mailbox).
+ * Measured slower than encode + copy engine (tools/t1_emit_bench.py). */
 tc_status tc_diff_encode_push(tc_ctx* ctx, const tc_segment* segs, int nseg, const tc_encode_opts* opts,
                               uint64_t version, uint64_t ref_version, void* out, uint64_t out_cap,
                               uint64_t* out_bytes, void* peer_dst, uint64_t peer_cap,

@@ -260,3 +260,29 @@ def test_fused_encode_push_full_records(ctx, tco):
     assert np.array_equal(out[:n].cpu().numpy(), exp) and np.array_equal(slot.tensor[:n].cpu().numpy(), exp)
     slot.free()
     mail.free()
+
+
+@pytest.mark.parametrize("fmt", ["mask", "index", "full"])
+def test_fused_encode_emit_into_mapped_host_memory(ctx, tco, fmt):
+    """The fused emit with a page-locked mapped host buffer as the destination (the Tier-1 emit
+    option, tools/t1_emit_bench.py): host bytes == oracle record, host mailbox == {n, version}."""
+    kw = {"index_mode": fmt == "index", "full": fmt == "full"}
+    states = [_shard(0, 0.0), _shard(1, 0.02)]
+    ref = [to_dev(a) for a in states[0]]
+    cur = [to_dev(a) for a in states[1]]
+    rc, exp = tco.encode([a.copy() for a in states[0]], states[1], version=1, ref_version=0, **kw)
+    assert rc == 0
+    cap = tc.diff_bound(SIZES, WB, **kw)
+    host, mail = tc.HostBuffer(cap), tc.HostBuffer(16)
+    mail.tensor.zero_()
+    out = torch.zeros(cap, dtype=torch.uint8, device="cuda")
+    ob = torch.zeros(1, dtype=torch.int64, device="cuda")
+    s = torch.cuda.Stream()
+    tc.diff_encode_push(ctx, ref, cur, out, ob, 1, 0, host, cap, mail, stream=s, **kw)
+    ctx.check(s)
+    n = exp.size
+    assert int(ob.item()) == n
+    assert mail.tensor.view(torch.int64).tolist() == [n, 1]
+    assert np.array_equal(host.tensor[:n].numpy(), exp)
+    host.free()
+    mail.free()
