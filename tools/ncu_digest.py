@@ -21,8 +21,8 @@ PROF = os.path.join(ROOT, "profiles")
 
 
 def short(name):
-    for k in ("encode_mask_kernel", "encode_prefix_kernel", "encode_emit_kernel", "fold_walk_kernel",
-              "fold_dense_kernel", "fold_list_kernel", "fold_kernel", "synth_base_kernel", "synth_step_kernel", "stage_sizes_kernel"):
+    for k in ("encode_mask_kernel", "encode_prefix_kernel", "encode_emit_kernel", "encode_full_kernel",
+              "fold_walk_kernel", "fold_dense_kernel", "fold_list_kernel", "fold_entries_kernel", "fold_kernel", "synth_base_kernel", "synth_step_kernel", "stage_sizes_kernel"):
         if k in name:
             return k
     return name.split("(")[0][-60:]
@@ -53,6 +53,7 @@ def main():
     ap.add_argument("--tag", required=True)
     ap.add_argument("--workload", default="cfg2")
     ap.add_argument("--f", type=float, default=0.01)
+    ap.add_argument("--label", default="", help="what the capture is (stored with the traffic, shown by bench.py)")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     traffic_path = os.path.join(PROF, "ncu_traffic.json")
@@ -64,7 +65,7 @@ def main():
         ours = {i: d for i, d in per.items() if d["name"].startswith(("encode", "fold"))}
         # a step whose chunks all go one way launches the other fold kernel to exit at once
         ours = {i: d for i, d in ours.items()
-                if d.get("ns", 0) > 20e3 or not d["name"].startswith(("fold_dense", "fold_list"))}
+                if d.get("ns", 0) > 20e3 or not d["name"].startswith(("fold_dense", "fold_list", "fold_entries"))}
         agg = defaultdict(lambda: [0, 0.0, 0.0])
         for d in ours.values():
             g = agg[d["name"]]
@@ -82,9 +83,12 @@ def main():
             out.append(f"| {n} | {c} | {ns / c / 1e6:.3f} | {ns / tot:.3f} | {by / c / 1e9:.3f} |")
         open(os.path.join(PROF, f"{a.tag}_launch_summary.md"), "w").write("\n".join(out) + "\n")
         enc = sum(agg[k][2] / max(1, agg[k][0]) for k in ("encode_mask_kernel", "encode_prefix_kernel",
-                                                           "encode_emit_kernel") if k in agg)
-        fold = sum(agg[k][2] / max(1, agg[k][0]) for k in ("fold_walk_kernel", "fold_kernel", "fold_dense_kernel", "fold_list_kernel") if k in agg)
+                                                           "encode_emit_kernel", "encode_full_kernel") if k in agg)
+        fold = sum(agg[k][2] / max(1, agg[k][0]) for k in ("fold_walk_kernel", "fold_kernel", "fold_dense_kernel", "fold_list_kernel",
+                                                         "fold_entries_kernel") if k in agg)
         traffic[key] = {"encode": int(enc), "fold": int(fold), "source": f"profiles/{a.tag}_launches.csv"}
+        if a.label:
+            traffic[key]["round"] = a.label
         json.dump(traffic, open(traffic_path, "w"), indent=1)
         print("\n".join(out))
     if a.full:
