@@ -929,13 +929,17 @@ __global__ void __launch_bounds__(kRThreads, 2) adam_replay_kernel(const __grid_
                 __syncthreads();
                 for (int s = g0; s < g1; ++s) {
                     const ReplayStep& R = s_step[s];
+                    // the step's gradients first (loads in flight together), then the updates
+                    float g[kRPer];
 #pragma unroll
                     for (uint32_t j = 0; j < kRPer; ++j) {
                         const uint64_t i = base + j * kRThreads + tid;
-                        const float g = R.variant == 1 ? (i < P.n ? __fmul_rn(R.scale, static_cast<float>(R.q[i])) : 0.0f)
-                                                       : s_gd[(s - g0) * kGB + j * kRThreads + tid];
-                        adam_update(w[j], mm[j], vv[j], g, P.a, P.ss[s], P.ic[s]);
+                        g[j] = R.variant == 1 ? (i < P.n ? __fmul_rn(R.scale, static_cast<float>(R.q[i])) : 0.0f)
+                                              : s_gd[(s - g0) * kGB + j * kRThreads + tid];
                     }
+                    const float ss = P.ss[s], ic = P.ic[s];
+#pragma unroll
+                    for (uint32_t j = 0; j < kRPer; ++j) adam_update(w[j], mm[j], vv[j], g[j], P.a, ss, ic);
                 }
                 __syncthreads();  // before the next group's tiles
                 continue;

@@ -145,7 +145,10 @@ def test_adam_step_matches_oracle(ctx, hp):
 
 @pytest.mark.parametrize("N", [1, 2, 5, 10])
 @pytest.mark.parametrize("n,kind,opts", [(50_000, "normal", {}), (300_001, "normal", {}),
-                                          (200_000, "zeros_mixed", {"k": 0.05, "chunk_elems": 4096 * 7})])
+                                          (200_000, "zeros_mixed", {"k": 0.05, "chunk_elems": 4096 * 7}),
+                                          # ~1230 entries per 4096-element tile and step: past the
+                                          # replay's shared stage (2048 per tile) from N = 3 on
+                                          (150_001, "normal", {"k": 0.3, "small_threshold": 1000})])
 def test_fused_replay_matches_sequential_oracle(ctx, N, n, kind, opts):
     """fused replay of N payloads == sequential decompress + adam_step, bit-exact."""
     st = state(n, N)
@@ -210,3 +213,75 @@ def test_adam_step_encode_matches_oracle(ctx, tco_lossless, n, T, C, zero_frac, 
     nb = int(ob.item())
     assert nb == exp.size and np.array_equal(out[:nb].cpu().numpy(), exp)
     assert same_state(gs, st)
+
+
+def _idx_offset(p):
+    """Byte offset of the INT32 index array of a sparse payload (oracle/tco_grad.h layout)."""
+    h = p[:64]
+    chunks = int(h[8:12].view("<u4")[0])
+    kept = int(h[24:32].view("<u8")[0])
+    return 64 + 16 * chunks + (2 * kept + 15) // 16 * 16, kept
+
+
+@pytest.mark.parametrize("k,N", [(0.01, 3), (0.3, 4)])
+@pytest.mark.parametrize("tamper", ["order", "range"])
+def test_replay_corrupt_indices(ctx, k, N, tamper):
+    """An index out of order within a tile, or pointing past the tile's chunk span, is CORRUPT in
+    the fused replay (both the staged path and, at k = 0.3, the path past the stage)."""
+    n = 150_001
+    st = state(n, N)
+    opts = {"k": k, "small_threshold": 1000}
+    pays = [oracle.grad_compress(grad_of("normal", n), seed=40 + j, **opts)[1] for j in range(N)]
+    bad = pays[0].copy()
+    off, kept = _idx_offset(bad)
+    idx = bad[off: off + 4 * kept].view("<i4")
+    j = kept // 2
+    if tamper == "order":
+        idx[j], idx[j + 1] = idx[j + 1], idx[j]
+    else:
+        idx[j] = idx[j] + 5 * 4096
+    gs = to_gpu_state(st)
+    dp = [dev(np.concatenate([p, np.zeros(16, np.uint8)])) for p in [bad] + pays[1:]]
+    tc.adam_replay(ctx, *gs, dp, [p.size for p in [bad] + pays[1:]], 1, torch.empty(n, device="cuda"))
+    assert ctx.check_status() == tc.ERR_CORRUPT
+
+
+def _wide_floats(r, n, lo_exp, hi_exp, zeros=0.05, denormals=0.05, signed=True):
+    """fp32 values with exponents uniform in [lo_exp, hi_exp], plus exact zeros and denormals."""
+    assert -126 <= lo_exp <= hi_exp <= 127  # normal exponents (no inf / NaN)
+    mant = r.integers(0, 1 << 23, n, dtype=np.uint32)
+    ex = r.integers(lo_exp + 127, hi_exp + 128, n).astype(np.uint32)
+    bits = (ex << 23) | mant
+    u = r.random(n)
+    bits[u < zeros] = 0
+    den = (u >= zeros) & (u < zeros + denormals)
+    bits[den] = mant[den] | 1
+    if signed:
+        bits |= (r.random(n) < 0.5).astype(np.uint32) << 31
+    return bits.view(np.float32)
+
+
+@pytest.mark.parametrize("variant", ["int8", "sparse"])
+def test_fused_replay_wide_state(ctx, variant):
+    """The replay's branch-free Adam update (fast sqrt / quotient sequences, ranges checked per
+    element, the rest redone with the intrinsics) against the oracle over m, v spanning the whole
+    fp32 range — tiny, huge, denormal and zero moments — bit for bit."""
+    n = 60_000 if variant == "int8" else 300_001
+    r = np.random.default_rng(77)
+    st = [r.standard_normal(n).astype(np.float32) * 10,
+          _wide_floats(r, n, -126, 60),
+          _wide_floats(r, n, -126, 120, signed=False),
+          np.zeros(n, np.uint16)]
+    N = 4
+    # FP16-representable gradients (a "wide" one would hold infinities, and NaN payload bits are
+    # not comparable across the two implementations)
+    pays = [oracle.grad_compress(grad_of("normal", n) * np.float32(10.0 ** (j - 2)), seed=200 + j)[1]
+            for j in range(N)]
+    gs = to_gpu_state(st)
+    for hp in ({}, {"eps": 1e-30, "beta2": 0.99999}):
+        o = {"lr": 1e-3, "b1": 0.9, "b2": 0.999, "eps": 1e-8, **{"b2" if k == "beta2" else k: v for k, v in hp.items()}}
+        assert oracle.adam_replay(st[0], st[1], st[2], st[3], pays, first_step=3, **o) == 0
+        dp = [dev(np.concatenate([p, np.zeros(16, np.uint8)])) for p in pays]
+        tc.adam_replay(ctx, *gs, dp, [p.size for p in pays], 3, torch.empty(n, device="cuda"), **hp)
+        ctx.check()
+        assert same_state(gs, st)

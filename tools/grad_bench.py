@@ -35,6 +35,9 @@ def main():
     ap.add_argument("--N", type=int, default=5)              # P:395 batch of N = 5 diffs
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--k", type=float, default=0.01)
+    ap.add_argument("--state", default="zero", choices=["zero", "mid"],
+                    help="Adam moments before the replay: zero (a fresh optimizer) or mid-training "
+                         "(m ~ N(0, 1e-3), v ~ |N(0, 1)| 1e-6 everywhere)")
     a = ap.parse_args()
     n, N = a.n, a.N
     dev = torch.device("cuda", 0)
@@ -70,6 +73,9 @@ def main():
     master = torch.randn(n, dtype=torch.float32, device=dev)
     m = torch.zeros(n, dtype=torch.float32, device=dev)
     v = torch.zeros(n, dtype=torch.float32, device=dev)
+    if a.state == "mid":
+        m.normal_(0.0, 1e-3)
+        v.normal_(0.0, 1.0).abs_().mul_(1e-6)
     w16 = torch.zeros(n, dtype=torch.int16, device=dev)
     snap = [x.clone() for x in (master, m, v, w16)]
 
@@ -105,7 +111,7 @@ def main():
     st = 12 * n
     f_bytes = 2 * st + sum(nbytes[:-1]) + (4 * n + nbytes[-1]) + (4 * n + 2 * st + 2 * n)
     s_bytes = N * ((4 * n + nbytes[0]) + (4 * n + 2 * st + 2 * n))
-    out = {"n": n, "N": N, "k": a.k, "payload_bytes": nbytes[0], "kept": kept,
+    out = {"n": n, "N": N, "k": a.k, "state": a.state, "payload_bytes": nbytes[0], "kept": kept,
            "compress": {"ms": round(ms_c, 3), "gbs": round(c_bytes / ms_c / 1e6, 1),
                         "frac_hbm": round(c_bytes / ms_c / 1e6 / peak, 4), "bytes": c_bytes},
            "decompress": {"ms": round(ms_d, 3), "gbs": round(d_bytes / ms_d / 1e6, 1),
