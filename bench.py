@@ -1443,8 +1443,12 @@ def lossy_probe(tc, ctx, X, Y, A, R, rec, s, dev, peak, N=5, k=0.01, reps=3):
     dense = R[1].view(torch.float32)
     slot = (rec.numel() // N) & ~15
     cap = tc.grad_bound(n, k=k)
-    if slot < min(cap, int(6.5 * k * 3 * n)):
-        return {"skipped": "record buffer too small for the payloads"}
+    need = (min(cap, int(6.5 * k * 3 * n)) + 15) & ~15
+    if slot < need:  # the step's record slots are sized for its records: payload slots of their own
+        if torch.cuda.mem_get_info(dev)[0] < N * need + (2 << 30):
+            return {"skipped": "no device memory for the payload slots"}
+        rec = torch.empty(N * need, dtype=torch.uint8, device=dev)
+        slot = need
     pays = [rec[j * slot:(j + 1) * slot] for j in range(N)]
     ob = torch.zeros(N, dtype=torch.int64, device=dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731

@@ -3,6 +3,8 @@ records, a simulated GPU failure that wipes the live state and the reference, re
 Tier-1 (H2D of the staged records) with one fold of the chain — bit-exact against the state the
 seeded generator defines; plus the full-size (cfg2) parity of the bench launch configuration on
 sampled chunks and a full-size round trip."""
+import gc
+
 import numpy as np
 import pytest
 
@@ -108,6 +110,8 @@ def test_checkpointer_cfg2_saves_without_reallocation():
     sizes, wb = synth.shard_layout("cfg2")
     seed, f = synth.SEED0, 0.01
     W = sum(n * w for n, w in zip(sizes, wb))
+    gc.collect()
+    torch.cuda.empty_cache()  # blocks cached by earlier tests count as used
     if torch.cuda.mem_get_info()[0] < 3.4 * W:
         pytest.skip("not enough device memory for the full-size case")
     live = _dev_state(sizes, wb, seed, 0, f)
@@ -138,6 +142,8 @@ def test_fullsize_cfg2_sampled_parity_and_round_trip(tco):
     full record reproduces the current state exactly."""
     sizes, wb = synth.shard_layout("cfg2")
     seed, f = synth.SEED0, 0.01
+    gc.collect()
+    torch.cuda.empty_cache()  # blocks cached by earlier tests count as used
     free = torch.cuda.mem_get_info()[0]
     W = sum(n * w for n, w in zip(sizes, wb))
     if free < 4.5 * W:
@@ -207,8 +213,10 @@ def _idx_record(buf, pos):
                 vals=vals, pos=pos)
 
 
-def test_fullsize_cfg2_bench_config_chain_parity(tco):
-    """BASELINE configs[1] (cfg2, 21.8 GB) in exactly the configuration bench.py times: index-mode
+@pytest.mark.parametrize("workload,shard", [("cfg2", 0), ("cfg3", 7)])
+def test_fullsize_bench_config_chain_parity(tco, workload, shard):
+    """BASELINE configs[1] (cfg2, 21.8 GB; and the last cfg3 shard of 8, 11.6 GB, as a rank of the
+    N > 1 bench lines holds it, seed SEED0 + shard) in exactly the configuration bench.py times: index-mode
     records, advance_ref = 1, T = 4096, C = 2^28, two chained versions (v0 -> v1 -> v2, the second
     encoded against the advanced reference).  Per segment, the first and the last chunk record are
     byte-compared whole with oracle.encode of that chunk; every other chunk is compared on 8
@@ -217,9 +225,11 @@ def test_fullsize_cfg2_bench_config_chain_parity(tco):
     synth (numpy), never from the device.  Then the chain folds onto the base bit-exactly."""
     from concurrent.futures import ThreadPoolExecutor
 
-    sizes, wb = synth.shard_layout("cfg2")
-    seed, f, T, C = synth.SEED0, 0.01, 4096, 1 << 28
+    sizes, wb = synth.shard_layout(workload, shard)
+    seed, f, T, C = synth.SEED0 + shard, 0.01, 4096, 1 << 28
     W = sum(n * w for n, w in zip(sizes, wb))
+    gc.collect()
+    torch.cuda.empty_cache()  # blocks cached by earlier tests count as used
     if torch.cuda.mem_get_info()[0] < 3.3 * W:
         pytest.skip("not enough device memory for the full-size case")
     ref = _dev_state(sizes, wb, seed, 0, f)
