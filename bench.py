@@ -222,6 +222,13 @@ def run_ours(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    numa = None
+    if world > 1 and args.numa_bind:
+        # every rank stages into host memory at once: pin each rank (and so its pinned Tier-1
+        # buffers, first touch) to its GPU's NUMA node (N = 1 keeps every core for the oracle arm)
+        from paper_2605_17821_b200.checkpoint import bind_local_numa
+
+        numa = bind_local_numa(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     workload = args.workload or ("cfg2" if world == 1 else "cfg3")
@@ -699,6 +706,7 @@ def run_ours(args):
                         ("NVLink push to the ring neighbour's IPC slot + " if push else "NCCL ring replicate + ")
                         if world > 1 else "") + "fold onto restore replica"),
                 "parallelism": f"dp{world} (independent ZeRO shards; Tier-2 ring r->r+1)" if world > 1 else "1 GPU",
+                "numa": numa,
             },
             "roofline": {
                 "kernel": "tc_diff_encode = encode_mask_kernel + encode_prefix_kernel + encode_emit_kernel",
@@ -1819,6 +1827,8 @@ def main():
     ap.add_argument("--fold-dense-permille", type=int, default=None,
                     help="restore strategy threshold (tc_ctx_set_fold_dense_permille); default: libtc's")
     ap.add_argument("--cpu-baseline", type=int, default=1)
+    ap.add_argument("--numa-bind", type=int, default=1,
+                    help="N > 1: bind each rank to its GPU's NUMA node before the pinned buffers are allocated")
     ap.add_argument("--sample-words", type=int, default=1 << 25)
     ap.add_argument("--oracle-steps", type=int, default=3)
     args = ap.parse_args()
