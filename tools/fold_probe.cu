@@ -8,6 +8,9 @@
 //              stored whole (explicit read-modify-write of the touched sectors only)
 //   stream   : read every line, store the 128-byte lines that hold a change (round 1 list fold)
 //   copy     : read all, write all (the streaming ceiling)
+//   scatter  : the pure scattered store of an index record's entries — sorted u32 positions and
+//              values read coalesced, one 4-byte store per entry (no record parsing): the floor of
+//              an N = 1 fold at that density (positions: one per stride 1/p, jittered in it)
 // The change pattern is a splitmix64 hash of the word index (i.i.d. Bernoulli(p)).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fold_probe tools/fold_probe.cu
 #include <cuda_runtime.h>
@@ -120,6 +123,18 @@ __global__ void k_copy(const uint4* a, uint4* b, uint64_t nv) {
     for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += stride) b[v] = a[v];
 }
 
+__global__ void k_gen_entries(uint32_t* pos, uint32_t* val, uint64_t ne, uint64_t stride) {
+    const uint64_t st = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ne; i += st) {
+        pos[i] = (uint32_t)(i * stride + h64(i) % stride);
+        val[i] = (uint32_t)i;
+    }
+}
+__global__ void k_scatter(uint32_t* s, const uint32_t* pos, const uint32_t* val, uint64_t ne) {
+    const uint64_t st = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ne; i += st) s[__ldg(pos + i)] = __ldg(val + i);
+}
+
 // hash-only pass (ALU cost of the pattern generator, no memory)
 __global__ void k_hash(uint64_t n, uint64_t thr, uint32_t* sink) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -181,6 +196,21 @@ int main(int argc, char** argv) {
         printf("  rmw16   : %8.3f ms  touched-sector RMW %7.1f GB/s\n", tr, 2 * ts_b / tr / 1e6);
         printf("  wsect   : %8.3f ms  touched-sector W   %7.1f GB/s\n", tw, ts_b / tw / 1e6);
         printf("  stream  : %8.3f ms  R all + W lines    %7.1f GB/s\n", ts, (W + line * W) / ts / 1e6);
+    }
+    // the pure scatter of an index record's entries (u32 positions: n < 2^32 words)
+    if (n < (1ull << 32)) {
+        for (double p : {0.001, 0.01, 0.03}) {
+            const uint64_t stride = (uint64_t)(1.0 / p + 0.5), ne = n / stride;
+            uint32_t *pos, *val;
+            if (cudaMalloc(&pos, ne * 4) != cudaSuccess || cudaMalloc(&val, ne * 4) != cudaSuccess) break;
+            k_gen_entries<<<grid, block>>>(pos, val, ne, stride);
+            cudaDeviceSynchronize();
+            float tsc = timeit([&] { k_scatter<<<grid, block>>>(s, pos, val, ne); });
+            printf("scatter p=%.3f: %llu entries %8.3f ms  %6.2f G entries/s  (entries 8 B read + 32-B sector fill + write-back each: %7.1f GB/s)\n",
+                   p, (unsigned long long)ne, tsc, ne / tsc / 1e6, ne * 72.0 / tsc / 1e6);
+            cudaFree(pos);
+            cudaFree(val);
+        }
     }
     cudaError_t e = cudaDeviceSynchronize();
     printf("%s\n", cudaGetErrorString(e));
