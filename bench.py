@@ -736,7 +736,8 @@ def run_ours(args):
                          "frac_hbm_sector": round(fold_bs / fold_ms / 1e6 / peak, 4),
                          "traffic": traffic.get("fold"),
                          "dram_gbs": round(traffic["fold"] / fold_ms / 1e6, 1) if traffic.get("fold") else None,
-                         "scatter_reference": scatter_ref},
+                         "scatter_reference": scatter_ref,
+                         "scatter_roofline": scatter_roofline(changed, fold_ms, args.f)},
                 "stage_d2h": {"ms": round(stage_ms, 4), "gbs": round(rec_bytes / stage_ms / 1e6, 2),
                               "pcie_copy_gbs": round(pcie, 2) if pcie else None,
                               "frac_pcie": round(rec_bytes / stage_ms / 1e6 / pcie, 4) if pcie else None,
@@ -1665,6 +1666,22 @@ def run_e2e(args, tc, ctx, dev, sizes, wb, X, Y, A, R, recs, obytes, host_ring, 
             "frac_h2d": round(W / (ms * 1e-3) / 1e9 / h2d_gbs, 3),
             "note": "H2D of the new state version from pinned host (copy stream, one step ahead, two landing "
                     "buffers) + encode + D2H record + fold (compute stream)"}
+
+
+# the measured floor of a scattered fold: the pure scatter of sorted (position, value) entries into a
+# 16 GB fp32 state (tools/fold_probe.cu, profiles/rd4e_fold_probe_scatter.txt), G entries/s by density
+SCATTER_FLOOR = {0.001: 20.43, 0.01: 23.61, 0.03: 33.80}
+
+
+def scatter_roofline(changed, fold_ms, f):
+    """The step's N = 1 fold against the random-store roofline, where measured."""
+    peak = SCATTER_FLOOR.get(f)
+    if not changed or not fold_ms or peak is None:
+        return None
+    got = changed / fold_ms / 1e6
+    return {"unit": "G entries/s", "achieved": round(got, 2), "peak": peak, "frac": round(got / peak, 3),
+            "peak_source": "pure scatter of sorted u32 positions + values, one 4-byte store each, at this "
+                           "density (tools/fold_probe.cu, profiles/rd4e_fold_probe_scatter.txt)"}
 
 
 def load_traffic(workload, f):
