@@ -820,34 +820,82 @@ __device__ __forceinline__ void emit_dense(const EncParams& P, const BlockInfo& 
     }
 }
 
-// Words [start, n) of a spilled run, lane-strided with 4 loads in flight per lane before the
-// stores (a block with > 64 changed words; one word in flight per lane made kernel B's copy run
-// at 2.1 TB/s at f = 10 %, r2 ncu)
+// Bytes [0, nbytes) of a 16-byte aligned spill run -> the record at `dst` (any 2-byte alignment k),
+// with 16-byte loads and 16-byte stores: in the 16-byte aligned window starting at dst - k, vector
+// u holds source bytes [16u - k, 16u - k + 16) = the tail of source vector u - 1 and the head of
+// vector u, joined by funnel shifts (source vector u - 1 comes from the neighbouring lane).  The
+// window's first and last vectors are stored in 2-byte pieces (the bytes around the run belong to
+// other blocks).  Four vectors per lane in flight.  (Kernel B copied spilled runs with one 2- or
+// 4-byte word per lane: 64-128 bytes per warp instruction, long-scoreboard bound at 22 % issue,
+// f = 10 %, ncu rd4h.)
+__device__ __forceinline__ uint4 funnel16(uint4 p, uint4 c, uint32_t s) {
+    const uint32_t r = (s & 3u) * 8u;
+    uint32_t w0, w1, w2, w3, w4;
+    switch (s >> 2) {
+        case 0: w0 = p.x; w1 = p.y; w2 = p.z; w3 = p.w; w4 = c.x; break;
+        case 1: w0 = p.y; w1 = p.z; w2 = p.w; w3 = c.x; w4 = c.y; break;
+        case 2: w0 = p.z; w1 = p.w; w2 = c.x; w3 = c.y; w4 = c.z; break;
+        default: w0 = p.w; w1 = c.x; w2 = c.y; w3 = c.z; w4 = c.w; break;
+    }
+    return make_uint4(__funnelshift_r(w0, w1, r), __funnelshift_r(w1, w2, r), __funnelshift_r(w2, w3, r),
+                      __funnelshift_r(w3, w4, r));
+}
+
+// window vector u (bytes [16u, 16u + 16) from D) of a run occupying window bytes [k, k + nbytes)
 template <bool PEER>
-__device__ __forceinline__ void copy_run(const EncParams& P, uint8_t* dst, const uint8_t* src, uint32_t w,
-                                         uint32_t start, uint32_t n, int lane) {
-    for (uint32_t i0 = start + lane; i0 < n; i0 += 128) {
-        uint32_t v[4];
+__device__ __forceinline__ void store_window_vec(const EncParams& P, uint8_t* D, uint32_t u, uint4 o, uint32_t k,
+                                                 uint32_t nbytes) {
+    const uint32_t lo = 16 * u;
+    if (lo >= k && lo + 16 <= k + nbytes) {
+        rec_store<PEER, uint4>(P, reinterpret_cast<uint4*>(D) + u, o);
+        return;
+    }
+    const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t i = i0 + 32 * q;
-            if (i < n)
-                v[q] = w == 4 ? __ldg(reinterpret_cast<const uint32_t*>(src) + i)
-                              : static_cast<uint32_t>(__ldg(reinterpret_cast<const unsigned short*>(src) + i));
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t i = i0 + 32 * q;
-            if (i < n) {
-                if (w == 4)
-                    rec_store<PEER, uint32_t>(P, reinterpret_cast<uint32_t*>(dst) + i, v[q]);
-                else
-                    rec_store<PEER, uint16_t>(P, reinterpret_cast<uint16_t*>(dst) + i, static_cast<uint16_t>(v[q]));
-            }
-        }
+    for (int e = 0; e < 8; ++e) {
+        const uint32_t x = lo + 2 * e;
+        if (x >= k && x < k + nbytes)
+            rec_store<PEER, uint16_t>(P, reinterpret_cast<uint16_t*>(D + x), static_cast<uint16_t>(ow[e >> 1] >> (16 * (e & 1))));
     }
 }
 
+template <bool PEER>
+__device__ __forceinline__ void copy_vec(const EncParams& P, uint8_t* dst, const uint8_t* src, uint32_t nbytes,
+                                         int lane) {
+    if (nbytes == 0) return;
+    const uint32_t k = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst) & 15u);
+    uint8_t* D = dst - k;
+    const uint32_t nd = (k + nbytes + 15) >> 4;  // window vectors
+    const uint32_t ns = (nbytes + 15) >> 4;      // source vectors (the slot is 16-byte padded)
+    const uint4* S = reinterpret_cast<const uint4*>(src);
+    const uint32_t sh = 16 - k;
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    uint4 carry = z;  // source vector (first vector of this pass) - 1, for lane 0
+    for (uint32_t u0 = 0; u0 < nd; u0 += 128) {
+        uint4 c[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t u = u0 + 32 * q + lane;
+            c[q] = u < ns ? __ldg(S + u) : z;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t u = u0 + 32 * q + lane;
+            uint4 pv;
+            pv.x = __shfl_up_sync(0xffffffffu, c[q].x, 1);
+            pv.y = __shfl_up_sync(0xffffffffu, c[q].y, 1);
+            pv.z = __shfl_up_sync(0xffffffffu, c[q].z, 1);
+            pv.w = __shfl_up_sync(0xffffffffu, c[q].w, 1);
+            if (lane == 0) pv = carry;
+            carry.x = __shfl_sync(0xffffffffu, c[q].x, 31);
+            carry.y = __shfl_sync(0xffffffffu, c[q].y, 31);
+            carry.z = __shfl_sync(0xffffffffu, c[q].z, 31);
+            carry.w = __shfl_sync(0xffffffffu, c[q].w, 31);
+            if (u < nd) store_window_vec<PEER>(P, D, u, k ? funnel16(pv, c[q], sh) : c[q], k, nbytes);
+            if (u0 + 32 * q + 32 >= nd) break;  // (warp-uniform) the run ends in this group
+        }
+    }
+}
 
 template <bool PEER>
 __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __grid_constant__ EncParams P) {
@@ -909,8 +957,23 @@ __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __gri
         dense = (info & kDenseFlag) != 0 && c != 0 && fits;
     }
 
-    // ---- sparse blocks of this warp: packed words spill slot -> record, 4 blocks per batch ----
-    uint32_t todo = __ballot_sync(0xffffffffu, valid && fits && !dense && c != 0);
+    // ---- sparse blocks of this warp: packed words spill slot -> record.  Runs of <= 64 words: 4
+    //      blocks per batch, a word per lane; longer runs: whole, in 16-byte vectors (copy_vec) ----
+    uint32_t todo = __ballot_sync(0xffffffffu, valid && fits && !dense && c != 0 && c <= 64);
+    uint32_t longr = __ballot_sync(0xffffffffu, valid && fits && !dense && c > 64);
+    while (longr) {
+        const int sl = __ffs(longr) - 1;
+        longr &= longr - 1;
+        const uint32_t cn = __shfl_sync(0xffffffffu, c, sl);
+        const uint32_t wq = __shfl_sync(0xffffffffu, w, sl);
+        uint8_t* dq = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst), sl));
+        const uint8_t* sq = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(src), sl));
+        copy_vec<PEER>(P, dq, sq, cn * wq, lane);
+        if (imode) {
+            uint8_t* iq = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(idst), sl));
+            copy_vec<PEER>(P, iq, sq + kSpillBytes, cn * 2, lane);
+        }
+    }
     while (todo) {
         int bl[4];
         uint32_t cn[4], wq[4];
@@ -949,9 +1012,6 @@ __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __gri
                         rec_store<PEER, uint16_t>(P, reinterpret_cast<uint16_t*>(dq[q]) + i, static_cast<uint16_t>(v[q][k]));
                 }
             }
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            if (cn[q] > 64) copy_run<PEER>(P, dq[q], sq[q], wq[q], 64, cn[q], lane);
         if (imode) {  // the u16 in-tile positions, same batching
             uint16_t iv[4][2];
             uint8_t* iq[4];
@@ -972,9 +1032,6 @@ __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __gri
                     const uint32_t i = lane + 32 * k;
                     if (i < cn[q]) rec_store<PEER, uint16_t>(P, reinterpret_cast<uint16_t*>(iq[q]) + i, iv[q][k]);
                 }
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (cn[q] > 64) copy_run<PEER>(P, iq[q], sq[q] + kSpillBytes, 2, 64, cn[q], lane);
         }
     }
 
