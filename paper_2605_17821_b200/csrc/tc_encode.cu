@@ -15,8 +15,9 @@
 //                           ref+cur are staged by two 1-D TMA bulk copies into shared memory;
 //                           lane l of a warp tests word 32q+l so __ballot_sync IS the mask word;
 //                           __popc + warp scans give counts; ref advance is fused.  A sparse
-//                           block (<= 4 KB of changed words) packs its new words into its spill
-//                           slot; a dense one leaves them for kernel B.  The mask and the
+//                           block (<= 8 KB of changed words in mask records, <= 4 KB in index
+//                           records) packs its new words into its spill slot; a dense one leaves
+//                           them for kernel B.  The mask and the
 //                           block-relative tile_off entries go straight to their final place once
 //                           the chunk's record start is known (chunk c waits only for chunk c-1's
 //                           counts, i.e. only at chunk boundaries); the block completing a chunk
@@ -28,8 +29,8 @@
 //   B  encode_emit_kernel   one CTA per 256 blocks: block-wide scan of the block counts -> each
 //                           block's in-chunk prefix (a thread per block, which also adds it to
 //                           the block's tile_off entries); each warp then moves its blocks'
-//                           spilled words into place, 4 blocks per batch with all loads in
-//                           flight before the stores, and packs dense blocks from mask + cur.
+//                           spilled words into place (runs of <= 64 words 4 blocks per batch,
+//                           longer ones in 16-byte vectors) and packs dense blocks from mask + cur.
 #include <cuda_runtime.h>
 
 #include "tc_internal.h"
@@ -752,7 +753,7 @@ __global__ void __launch_bounds__(1024) encode_prefix_kernel(const __grid_consta
 
 // ------------------------------------------------------------------ kernel B ------------
 
-// Dense block (more than 4 KB of changed words, not spilled): re-read its mask words from the
+// Dense block (more changed words than its spill slot holds): re-read its mask words from the
 // record and the changed words from cur, pack them in index order (a warp per block).
 template <int W, bool PEER>
 __device__ __forceinline__ void emit_dense(const EncParams& P, const BlockInfo& I, uint32_t info,

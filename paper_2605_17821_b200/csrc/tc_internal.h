@@ -106,10 +106,14 @@ constexpr uint32_t kMaskStageWords = 256;  // mask words of one block (8192 16-b
 
 constexpr uint32_t kEmitGroup = 256;        // blocks per emit CTA / per group sum
 constexpr uint32_t kSpillBytes = 4096;      // per-block spill slot (1/4 of a block's words)
+// mask mode: spill slot per block.  8 KB = the index mode's slot (2 x kSpillBytes: values and
+// positions), so a context that encodes both formats holds one buffer; with kernel B's vector
+// copy it beats re-reading cur for blocks of up to 2048 fp32 / 4096 bf16 changed words
+// (f = 30 % 16.3 -> 14.2 ms).  Experiment builds override it.
 #ifndef TC_SPILL_MASK
-#define TC_SPILL_MASK 4096
+#define TC_SPILL_MASK 8192
 #endif
-constexpr uint32_t kSpillMask = TC_SPILL_MASK;  // mask mode: spill slot per block (experiment knob)
+constexpr uint32_t kSpillMask = TC_SPILL_MASK;
 constexpr uint32_t kDenseFlag = 0x80000000u;
 constexpr int kAccDoneShift = 40;  // chunk_acc: blocks counted above bit 40 (a chunk has <= 2^19 blocks)
 constexpr unsigned long long kAccCountMask = (1ull << kAccDoneShift) - 1;
