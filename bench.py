@@ -309,7 +309,7 @@ def run_ours(args):
                           t1_bytes=(args.dev_slots + 1) * est,
                           t2_slots=2, standby=R, tile_words=T, chunk_words=C, ahead=world == 1,
                           stage_base=False, ref=A, stream=s_comp, push_ctas=args.push_ctas, timing=True,
-                          fused_t2=bool(args.t2_fused))
+                          fused_t2=bool(args.t2_fused), overlap_standby=bool(args.overlap_standby))
         rec_cap = ck.rec_cap
         recs = ck.dev
         s_copy, s_comm = ck.s_copy, ck.s_comm  # the step's side streams are the lifecycle's
@@ -472,7 +472,7 @@ def run_ours(args):
         return out
 
     def sync_all():
-        for s in (s_comp, s_copy, s_comm, s_fold):
+        for s in (s_comp, s_copy, s_comm, s_fold) + ((ck.s_stby,) if ck is not None else ()):
             s.synchronize()
 
     def drain():
@@ -531,7 +531,8 @@ def run_ours(args):
     time.sleep(0.3)
     def n_launch():
         if ck is not None:
-            return ck.ctx.launches + (ck.pctx.launches if world > 1 else 0)
+            return ck.ctx.launches + (ck.pctx.launches if world > 1 else 0) + \
+                (ck.sctx.launches if ck.sctx is not ck.ctx else 0)
         return ctx.launches + (push["ctx"].launches if push else 0) + (ctx_f.launches if ctx_f is not ctx else 0)
 
     launches0 = n_launch()
@@ -546,7 +547,7 @@ def run_ours(args):
     if nb is not None:
         sizes_seen.append(nb)
     drain()
-    for s in (s_copy, s_comm, s_fold):
+    for s in (s_copy, s_comm, s_fold) + ((ck.s_stby,) if ck is not None else ()):
         e = torch.cuda.Event()
         e.record(s)
         s_comp.wait_event(e)
@@ -563,6 +564,8 @@ def run_ours(args):
         push["ctx"].check(s_comm)
     if ck is not None:
         ck.ctx.check(s_comp)
+        if ck.sctx is not ck.ctx:
+            ck.sctx.check(ck.s_stby)
         n_ops["encode"] = ck.times["encode"]
         n_ops["fold"] = ck.times["fold"]
         n_ops["stage"] = ck.times["stage"]
@@ -1821,6 +1824,8 @@ def main():
     ap.add_argument("--tile-words", type=int, default=4096)
     ap.add_argument("--chunk-words", type=int, default=1 << 28)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--overlap-standby", type=int, default=0,
+                    help="Checkpointer: the standby fold of record k-1 on its own stream beside encode k")
     ap.add_argument("--overlap-fold", type=int, default=0,
                     help="N = 1: fold record k-1 on a high-priority stream beside encode k")
     ap.add_argument("--timeline", action="store_true")

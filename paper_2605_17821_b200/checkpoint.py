@@ -203,7 +203,8 @@ class Checkpointer:
                  t1_bytes: int | None = None, t2_slots: int = 8, standby=None, tile_words: int = 4096,
                  chunk_words: int = 1 << 28, ahead: bool = True, stage_base: bool = True, ref=None,
                  stream=None, base_version: int = 0, push_ctas: int = 16, timing: bool = False,
-                 base_interval: int = 50, fused_t2: bool = True, rec_cap: int | None = None):
+                 base_interval: int = 50, fused_t2: bool = True, rec_cap: int | None = None,
+                 overlap_standby: bool = False):
         from . import tc
 
         self.tc = tc
@@ -238,6 +239,12 @@ class Checkpointer:
         self.s_copy = torch.cuda.Stream(self.device, priority=0)
         self.s_comm = torch.cuda.Stream(self.device, priority=-1)
         self.standby = list(standby) if standby is not None else None
+        # the standby fold of record k-1 on a stream (and context) of its own, beside the encode of
+        # record k — or behind it on the compute stream
+        self.s_stby, self.sctx = self.s_comp, self.ctx
+        if overlap_standby and self.standby is not None:
+            self.s_stby = torch.cuda.Stream(self.device, priority=-1)
+            self.sctx = tc.Ctx(dev)
         self.ahead = ahead
         self.timing = timing
         self.times = {"encode": [], "stage": [], "push": [], "fold": []}
@@ -421,9 +428,11 @@ class Checkpointer:
                     self.where[e.version]["t2"] = None
         # hot standby: fold the record onto the replica right behind the encode
         if self.standby is not None:
-            f0 = self._ev(self.s_comp) if self.timing else None
-            tc.diff_apply(self.ctx, self.standby, p["ref_v"], [self.dev[slot]], [n], stream=self.s_comp)
-            f1 = self._ev(self.s_comp)
+            if self.s_stby is not self.s_comp:
+                self.s_stby.wait_event(e1)
+            f0 = self._ev(self.s_stby) if self.timing else None
+            tc.diff_apply(self.sctx, self.standby, p["ref_v"], [self.dev[slot]], [n], stream=self.s_stby)
+            f1 = self._ev(self.s_stby)
             busy.append(f1)
             if self.timing:
                 self.times["fold"].append((f0, f1))
@@ -573,6 +582,9 @@ class Checkpointer:
             for r, t in zip(self.ref, self.seg):
                 r.copy_(t)
         if self.standby is not None:
+            s.wait_stream(self.s_stby)  # a standby fold still in flight finishes before the copy
+            if self.sctx is not self.ctx:
+                self.sctx.check(self.s_stby)
             with torch.cuda.stream(s):
                 for r, t in zip(self.standby, self.seg):
                     r.copy_(t)
