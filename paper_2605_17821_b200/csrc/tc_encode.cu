@@ -757,7 +757,7 @@ __global__ void __launch_bounds__(1024) encode_prefix_kernel(const __grid_consta
 // record and the changed words from cur, pack them in index order (a warp per block).
 template <int W, bool PEER>
 __device__ __forceinline__ void emit_dense(const EncParams& P, const BlockInfo& I, uint32_t info,
-                                           unsigned long long prefix, int lane) {
+                                           unsigned long long prefix, int lane, uint8_t* ring) {
     using word_t = typename Word<W>::T;
     const bool imode = P.index_mode != 0;
     const unsigned long long rs = ld_relaxed(&P.rstart[I.chunk]) & ~1ull;
@@ -784,6 +784,74 @@ __device__ __forceinline__ void emit_dense(const EncParams& P, const BlockInfo& 
     constexpr uint32_t MPG = 32 / LPM; // mask words per group of 32 vectors
     const uint4* gcur4 = reinterpret_cast<const uint4*>(gcur);
     uint32_t base = 0;
+    if (!imode && ring) {
+        // mask records: the packed words go through a 2 KB warp-private ring in shared memory
+        // indexed by their DESTINATION address mod 2 KB, and leave it as 16-byte aligned vectors
+        // (the run's first and last vectors in 2-byte pieces: their other bytes are the
+        // neighbouring blocks').  r2 ncu: the word-per-lane stores made this loop store-issue bound.
+        const uintptr_t g0a = reinterpret_cast<uintptr_t>(gval);  // run start (any W alignment)
+        uintptr_t done = g0a;                                       // written up to here
+        auto flush = [&](uintptr_t upto, bool last) {
+            // the vectors [done & ~15, upto) (last: including upto's partial vector)
+            const uintptr_t v0 = done & ~uintptr_t(15);
+            const uintptr_t v1 = last ? ((upto + 15) & ~uintptr_t(15)) : (upto & ~uintptr_t(15));
+            for (uintptr_t va = v0 + 16 * static_cast<uintptr_t>(lane); va < v1; va += 512) {
+                const uint4 o = *reinterpret_cast<const uint4*>(ring + (va & 2047));
+                uint8_t* dstv = reinterpret_cast<uint8_t*>(va);
+                if (va >= done && va + 16 <= upto) {
+                    rec_store<PEER, uint4>(P, reinterpret_cast<uint4*>(dstv), o);
+                } else {
+                    const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const uintptr_t x = va + 2 * e;
+                        if (x >= done && x < upto)
+                            rec_store<PEER, uint16_t>(P, reinterpret_cast<uint16_t*>(x),
+                                                      static_cast<uint16_t>(ow[e >> 1] >> (16 * (e & 1))));
+                    }
+                }
+            }
+            done = v1 < upto ? v1 : upto;
+        };
+        for (uint32_t g0 = 0; g0 < nmw; g0 += 2 * MPG) {
+            uint32_t bits[2];
+            uint4 vec[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const uint32_t mwi = g0 + u * MPG + lane / LPM;
+                const uint32_t mw = mwi < nmw ? gmask[(I.p0 >> 5) + mwi] : 0u;
+                bits[u] = (mw >> ((lane % LPM) * VW)) & ((1u << VW) - 1u);
+                if (bits[u]) vec[u] = __ldg(gcur4 + (g0 + u * MPG) * LPM + lane);
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const uint32_t c = __popc(bits[u]);
+                uint32_t inc = c;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+                    if (lane >= d) inc += t;
+                }
+                uint32_t o = base + inc - c;
+                base += __shfl_sync(0xffffffffu, inc, 31);
+                if (bits[u]) {
+                    const word_t* vw = reinterpret_cast<const word_t*>(&vec[u]);
+#pragma unroll
+                    for (uint32_t k = 0; k < VW; ++k)
+                        if ((bits[u] >> k) & 1u) {
+                            *reinterpret_cast<word_t*>(ring + ((g0a + static_cast<uintptr_t>(o) * W) & 2047)) = vw[k];
+                            ++o;
+                        }
+                }
+            }
+            __syncwarp();
+            flush(g0a + static_cast<uintptr_t>(base) * W, false);
+            __syncwarp();
+        }
+        flush(g0a + static_cast<uintptr_t>(base) * W, true);
+        __syncwarp();
+        return;
+    }
     for (uint32_t g0 = 0; g0 < nmw; g0 += 2 * MPG) {
         uint32_t bits[2];
         uint4 vec[2];
@@ -901,6 +969,7 @@ __device__ __forceinline__ void copy_vec(const EncParams& P, uint8_t* dst, const
 template <bool PEER>
 __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __grid_constant__ EncParams P) {
     __shared__ uint32_t s_warp[kWarps];
+    __shared__ __align__(16) uint8_t s_ring[kWarps][2048];  // dense blocks: per-warp output ring
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const unsigned long long g = blockIdx.x;
     const unsigned long long b = g * kEmitGroup + tid;
@@ -1047,9 +1116,9 @@ __global__ void __launch_bounds__(kEncThreads, 4) encode_emit_kernel(const __gri
             P.gpre[g] + __shfl_sync(0xffffffffu, wp + inc - c, t) - P.cbase[I.chunk];
         const uint32_t inf = __shfl_sync(0xffffffffu, info, t);
         if (I.w == 4)
-            emit_dense<4, PEER>(P, I, inf, prefix, lane);
+            emit_dense<4, PEER>(P, I, inf, prefix, lane, s_ring[wid]);
         else
-            emit_dense<2, PEER>(P, I, inf, prefix, lane);
+            emit_dense<2, PEER>(P, I, inf, prefix, lane, s_ring[wid]);
     }
     // fused Tier-2 emit: every CTA's peer stores are fenced at system scope; the last CTA publishes
     // {bytes, version} into the neighbour's mailbox (a refused record: bytes = UINT64_MAX)
