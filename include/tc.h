@@ -122,7 +122,11 @@ const char* tc_last_error(void);
 int tc_abi_version(void);
 
 /* Create a context on CUDA device `device` (the device is made current on the calling
- * thread).  Scratch grows on demand, stream-ordered.  *out receives the handle. */
+ * thread).  Scratch grows on demand, stream-ordered, and is kept until tc_ctx_destroy; its
+ * largest part is the encoders' per-block spill area: 8 KB per scan block of 4096 4-byte /
+ * 8192 2-byte words (mask and index records alike) = half the bytes of the largest state
+ * encoded, plus ~1 % bookkeeping (index records: + 1 KB per block of staged mask words).
+ * *out receives the handle. */
 tc_status tc_ctx_create(int device, tc_ctx** out);
 tc_status tc_ctx_destroy(tc_ctx* ctx);
 /* Synchronize `stream`, then return and clear the sticky device error (TC_OK if none). */
