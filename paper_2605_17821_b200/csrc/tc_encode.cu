@@ -753,6 +753,10 @@ __global__ void __launch_bounds__(1024) encode_prefix_kernel(const __grid_consta
 
 // ------------------------------------------------------------------ kernel B ------------
 
+__device__ __forceinline__ uint32_t word4(const uint4& o, int i) {  // i: compile-time after unrolling
+    return i == 0 ? o.x : i == 1 ? o.y : i == 2 ? o.z : o.w;
+}
+
 // Dense block (more changed words than its spill slot holds): re-read its mask words from the
 // record and the changed words from cur, pack them in index order (a warp per block).
 template <int W, bool PEER>
@@ -801,13 +805,12 @@ __device__ __forceinline__ void emit_dense(const EncParams& P, const BlockInfo& 
                 if (va >= done && va + 16 <= upto) {
                     rec_store<PEER, uint4>(P, reinterpret_cast<uint4*>(dstv), o);
                 } else {
-                    const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
                         const uintptr_t x = va + 2 * e;
                         if (x >= done && x < upto)
                             rec_store<PEER, uint16_t>(P, reinterpret_cast<uint16_t*>(x),
-                                                      static_cast<uint16_t>(ow[e >> 1] >> (16 * (e & 1))));
+                                                      static_cast<uint16_t>(word4(o, e >> 1) >> (16 * (e & 1))));
                     }
                 }
             }
@@ -919,12 +922,11 @@ __device__ __forceinline__ void store_window_vec(const EncParams& P, uint8_t* D,
         rec_store<PEER, uint4>(P, reinterpret_cast<uint4*>(D) + u, o);
         return;
     }
-    const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
         const uint32_t x = lo + 2 * e;
         if (x >= k && x < k + nbytes)
-            rec_store<PEER, uint16_t>(P, reinterpret_cast<uint16_t*>(D + x), static_cast<uint16_t>(ow[e >> 1] >> (16 * (e & 1))));
+            rec_store<PEER, uint16_t>(P, reinterpret_cast<uint16_t*>(D + x), static_cast<uint16_t>(word4(o, e >> 1) >> (16 * (e & 1))));
     }
 }
 
