@@ -820,6 +820,10 @@ def run_streaming(args, rank, world, local, dev):
         nch = max(1, -(-n // C))
         for c0 in range(0, nch, K):
             runs.append((i, c0, min(K, nch - c0)))
+    # the checkpoint's last run is one chunk: its Tier-1 copy is the only one nothing overlaps
+    if runs and runs[-1][2] > 1:
+        i, c0, k = runs.pop()
+        runs += [(i, c0, k - 1), (i, c0 + k - 1, 1)]
     allow_index = args.format in ("index", "adaptive") and T <= 8192
     slot_cap = max(max(tc.diff_bound_range(sizes[i], wb[i], c0, k, T, C),
                        tc.diff_bound_range(sizes[i], wb[i], c0, k, T, C, index_mode=True) if allow_index else 0)
