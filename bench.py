@@ -1343,11 +1343,10 @@ def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nre
             "fold_ms": round(fm, 4), "state_gbs": round(W / fm / 1e6, 1),
             "hbm_gbs_word": round(fold_b / fm / 1e6, 1), "frac_hbm_word": round(fold_b / fm / 1e6 / peak, 4),
             "hbm_gbs_sector": round(fold_bs / fm / 1e6, 1), "frac_hbm_sector": round(fold_bs / fm / 1e6 / peak, 4),
-            "stream_bytes": stream_b, "hbm_gbs_stream": round(stream_b / fm / 1e6, 1),
-            "frac_hbm_stream": round(stream_b / fm / 1e6 / peak, 4),
-            "floor_note": "profiles/rd2_fold_floor_probe.md: at the N = 8 chain's union density a kernel that "
-                          "reads and writes only the touched sectors still reads 0.96 of the state from DRAM "
-                          "(128-byte lines) and runs at 3.7 TB/s - about 8.5 ms at cfg2's size",
+            "streaming_model": {"bytes": stream_b, "gbs": round(stream_b / fm / 1e6, 1),
+                                "note": "NOT SURVEY §8(d) bytes: the whole state read + touched lines written + "
+                                        "records (what the streaming fold moves)"},
+            "touched_sector_floor": touched_floor(fu, W, fm),
             "tier1_restore_ms": round(statistics.median(t1_ms), 3),
             "restored_equals_head": bool(ok),
             "failure_recovery": rec_out}
@@ -1678,6 +1677,24 @@ def run_e2e(args, tc, ctx, dev, sizes, wb, X, Y, A, R, recs, obytes, host_ring, 
 # the measured floor of a scattered fold: the pure scatter of sorted (position, value) entries into a
 # 16 GB fp32 state (tools/fold_probe.cu, profiles/rd4e_fold_probe_scatter.txt), G entries/s by density
 SCATTER_FLOOR = {0.001: 20.43, 0.01: 23.61, 0.03: 33.80}
+
+
+# the measured floor of a chained fold: read-modify-write of ONLY the touched 32-byte sectors of a
+# 16 GB fp32 state (tools/fold_probe.cu rmw16, profiles/rd4e_fold_probe_scatter.txt), ms per GB of
+# state by union density
+RMW_FLOOR_MS_PER_GB = {0.0773: 6.272 / 16.0}
+
+
+def touched_floor(union_frac, state_bytes, fold_ms):
+    """The chain fold against the best valid touched-sector pattern measured at its density."""
+    for p, msgb in RMW_FLOOR_MS_PER_GB.items():
+        if abs(union_frac - p) < 0.005:
+            floor = msgb * state_bytes / 1e9
+            return {"floor_ms": round(floor, 3), "frac_of_floor": round(floor / fold_ms, 3),
+                    "source": "tools/fold_probe.cu rmw16 at p = %.4f (profiles/rd4e_fold_probe_scatter.txt, "
+                              "profiles/rd2_fold_floor_probe.md): at this density the touched sectors span 92 %% "
+                              "of the 128-byte lines, so DRAM reads ~0.96 of the state" % p}
+    return None
 
 
 def scatter_roofline(changed, fold_ms, f):
