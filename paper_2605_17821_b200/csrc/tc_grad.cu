@@ -347,21 +347,61 @@ __global__ void __launch_bounds__(kGThreads) grad_emit_kernel(const __grid_const
     for (int k = 0; k < static_cast<int>(kGThreads / 32); ++k) wp += k < wid ? s_warp[k] : 0u;
     const unsigned long long off = P.gpre[g] + wp + inc - c;
     const float thr = *P.thr;
-    for (int i = 0; i < 32; ++i) {  // the warp's blocks, one at a time
+    // spilled blocks: 4 per batch, the first 64 entries of each loaded before any is stored (one
+    // round trip per 4 blocks instead of one per block; the rest of a longer run after the batch)
+    uint32_t sp = __ballot_sync(0xffffffffu, (info & ~kDenseBit) != 0 && !(info & kDenseBit));
+    while (sp) {
+        uint32_t cn[4];
+        unsigned long long oq[4];
+        uint64_t bq[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int i = sp ? __ffs(sp) - 1 : -1;
+            if (sp) sp &= sp - 1;
+            const int sl = i < 0 ? 0 : i;
+            cn[q] = i < 0 ? 0u : __shfl_sync(0xffffffffu, info, sl) & ~kDenseBit;
+            oq[q] = __shfl_sync(0xffffffffu, off, sl);
+            bq[q] = g * kGGroup + wid * 32 + static_cast<uint32_t>(sl);
+        }
+        uint16_t v[4][2];
+        int32_t x[4][2];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint8_t* slot = P.spill + bq[q] * (kGSpill * 6);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t k = lane + 32 * h;
+                if (k < cn[q]) {
+                    v[q][h] = reinterpret_cast<const uint16_t*>(slot)[k];
+                    x[q][h] = reinterpret_cast<const int32_t*>(slot + kGSpill * 2)[k];
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t k = lane + 32 * h;
+                if (k < cn[q]) {
+                    gv[oq[q] + k] = v[q][h];
+                    gi[oq[q] + k] = x[q][h];
+                }
+            }
+            if (cn[q] > 64) {
+                const uint8_t* slot = P.spill + bq[q] * (kGSpill * 6);
+                for (uint32_t k = 64 + lane; k < cn[q]; k += 32) {
+                    gv[oq[q] + k] = reinterpret_cast<const uint16_t*>(slot)[k];
+                    gi[oq[q] + k] = reinterpret_cast<const int32_t*>(slot + kGSpill * 2)[k];
+                }
+            }
+        }
+    }
+    for (int i = 0; i < 32; ++i) {  // the warp's dense blocks, one at a time
         const uint32_t ci = __shfl_sync(0xffffffffu, info, i);
         const uint32_t cnt = ci & ~kDenseBit;
-        if (cnt == 0) continue;
+        if (cnt == 0 || !(ci & kDenseBit)) continue;
         const unsigned long long o = __shfl_sync(0xffffffffu, off, i);
         const uint64_t bb = g * kGGroup + wid * 32 + i;
-        if (!(ci & kDenseBit)) {
-            const uint16_t* sv = reinterpret_cast<const uint16_t*>(P.spill + bb * (kGSpill * 6));
-            const int32_t* si = reinterpret_cast<const int32_t*>(P.spill + bb * (kGSpill * 6) + kGSpill * 2);
-            for (uint32_t k = lane; k < cnt; k += 32) {
-                gv[o + k] = sv[k];
-                gi[o + k] = si[k];
-            }
-            continue;
-        }
         // dense block: the count kernel's order (16-element runs of threads 0..255), 32 runs a pass
         unsigned long long run = o;
         for (uint32_t t0 = 0; t0 < kGThreads; t0 += 32) {
