@@ -137,31 +137,68 @@ struct SparseParams {
 constexpr uint32_t kGGroup = 256;  // blocks per emit CTA (a thread per block)
 constexpr uint32_t kDenseBit = 0x80000000u;
 
-// the threshold: rank-th smallest magnitude of `sample` seeded draws (bitonic sort in smem)
+// the threshold: rank-th smallest magnitude of `sample` seeded draws.  A radix select over the
+// magnitudes' bits (non-negative floats order as their bit patterns): four 8-bit passes, each a
+// shared-memory histogram of the candidates that share the bits chosen so far and one warp's scan
+// for the bin holding the rank — 12 barriers instead of a bitonic sort's 91 (the same value: the
+// rank-th order statistic is unique).
 __global__ void __launch_bounds__(1024) grad_sample_kernel(const __grid_constant__ SparseParams P) {
-    __shared__ float s[kSampleMax];
-    const int tid = threadIdx.x;
-    uint32_t S2 = 1;
-    while (S2 < P.sample) S2 <<= 1;
-    for (uint32_t j = tid; j < S2; j += 1024)
-        s[j] = j < P.sample ? fabsf(P.x[splitmix64(P.seed + j) % P.n]) : __int_as_float(0x7f800000);
-    __syncthreads();
-    for (uint32_t k = 2; k <= S2; k <<= 1)
-        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-            for (uint32_t i = tid; i < S2; i += 1024) {
-                const uint32_t l = i ^ j;
-                if (l > i) {
-                    const float a = s[i], b = s[l];
-                    const bool up = (i & k) == 0;
-                    if ((a > b) == up) {
-                        s[i] = b;
-                        s[l] = a;
+    constexpr int kPer = kSampleMax / 1024;
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t s_bits, s_rank;
+    const int tid = threadIdx.x, lane = tid & 31;
+    uint32_t v[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const uint32_t i = static_cast<uint32_t>(tid) + 1024u * j;
+        v[j] = i < P.sample ? __float_as_uint(fabsf(P.x[splitmix64(P.seed + i) % P.n])) : 0u;
+    }
+    if (tid == 0) {
+        s_bits = 0;
+        s_rank = P.rank;  // 1-based
+    }
+#pragma unroll 1
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        if (tid < 256) hist[tid] = 0;
+        __syncthreads();
+        const uint32_t hi = shift == 24 ? 0u : ~0u << (shift + 8);
+        const uint32_t want = s_bits & hi;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const uint32_t i = static_cast<uint32_t>(tid) + 1024u * j;
+            if (i < P.sample && (v[j] & hi) == want) atomicAdd(&hist[(v[j] >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (tid < 32) {
+            uint32_t h[8], c = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                h[k] = hist[lane * 8 + k];
+                c += h[k];
+            }
+            uint32_t inc = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += t;
+            }
+            const uint32_t r = s_rank;
+            const uint32_t before = inc - c;
+            if (before < r && r <= inc) {  // the bin holding the rank is in this lane's 8
+                uint32_t acc = before;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (acc < r && r <= acc + h[k]) {
+                        s_bits |= static_cast<uint32_t>(lane * 8 + k) << shift;
+                        s_rank = r - acc;
                     }
+                    acc += h[k];
                 }
             }
-            __syncthreads();
         }
-    if (tid == 0) *P.thr = s[P.rank - 1];
+        __syncthreads();
+    }
+    if (tid == 0) *P.thr = __uint_as_float(s_bits);
 }
 
 // the keeping predicate: |x| >= threshold, zeros never kept
