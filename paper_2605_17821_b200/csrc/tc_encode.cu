@@ -13,8 +13,9 @@
 //   A  encode_mask_kernel   one CTA per scan block of B words (B = 4096 4-byte / 8192 2-byte
 //                           words; 16 KB per operand).  A dynamic ticket orders the blocks.
 //                           ref+cur are staged by two 1-D TMA bulk copies into shared memory;
-//                           lane l of a warp tests word 32q+l so __ballot_sync IS the mask word;
-//                           __popc + warp scans give counts; ref advance is fused.  A sparse
+//                           each lane compares one 128-bit vector (4 fp32 / 8 bf16 words) and a
+//                           shfl_xor OR across the 8 | 4 lanes sharing a mask word assembles it
+//                           (LSB-first); __popc + warp scans give counts; ref advance is fused.  A sparse
 //                           block (<= 8 KB of changed words in mask records, <= 4 KB in index
 //                           records) packs its new words into its spill slot; a dense one leaves
 //                           them for kernel B.  The mask and the
