@@ -571,6 +571,7 @@ def run_ours(args):
         n_ops["stage"] = ck.times["stage"]
         state["rest_version"] = ck.chain.head  # the standby replica (R) and the reference (A)
         state["index"] = ck.next_fmt == "index"  # the format the next record would take
+        state["fmt"] = ck.next_fmt
         timed_done = [d for d in ck_done if d[0] >= v_timed0]
         n_ops["replicate"] = [(a, b, d[1]) for (a, b), d in zip(ck.times["push"], timed_done)]
         state["modes"] = [d[2] for d in timed_done]
@@ -641,11 +642,17 @@ def run_ours(args):
             s_comp.synchronize()
     restore = None
     if args.restore_chain > 0:
-        restore = restore_bench(tc, ctx, X, Y, A, R, recs[0], sizes, wb, seed, p53, T, C, s_comp,
-                                args.restore_chain, args.structure if args.structure != S3_ADAM else 0, peak, dev,
-                                state["index"], comm=comm,
-                                spare=recs[1] if len(recs) > 1 else None,
-                                recovery=args.recovery if args.recovery is not None else workload == "cfg4")
+        try:
+            restore = restore_bench(tc, ctx, X, Y, A, R, recs[0], sizes, wb, seed, p53, T, C, s_comp,
+                                    args.restore_chain, args.structure if args.structure != S3_ADAM else 0, peak,
+                                    dev, state["index"], comm=comm,
+                                    spare=recs[1] if len(recs) > 1 else None,
+                                    recovery=args.recovery if args.recovery is not None else workload == "cfg4",
+                                    full=state.get("fmt") == "full")
+        except (torch.OutOfMemoryError, tc.TcError) as ex:  # an untimed probe must not lose the step's line
+            restore = {"unavailable": f"{type(ex).__name__}: {ex}"[:300]}
+            s_comp.synchronize()
+            torch.cuda.empty_cache()
         # put the step buffers back to the X / Y pair (X intact; Y, A, R were reused)
         if args.structure == S3_ADAM:
             adam_pair(X, Y, seed, s_comp)
@@ -976,7 +983,9 @@ def run_streaming(args, rank, world, local, dev):
             tc.synth_base(R[i], seed, i, stream=s_comp)
     del slots
     big = max(max(16, n) for _, _, n in diffs)
-    stage = [torch.empty(big, dtype=torch.uint8, device=dev) for _ in range(min(5, len(diffs)))]
+    torch.cuda.empty_cache()  # (the timed run's ring slots went above)
+    fit = int(torch.cuda.mem_get_info(dev)[0] * 0.8) // big  # batches of up to N = 5 that fit
+    stage = [torch.empty(big, dtype=torch.uint8, device=dev) for _ in range(max(1, min(5, len(diffs), fit)))]
     tr0, tr1 = ev(), ev()
     tr0.record(s_comp)
     for j in range(0, len(diffs), len(stage)):
@@ -1242,7 +1251,7 @@ def recovery_bench(tc, ctx, comm, X, Z, R, recs, lens, hosts, spare, s, dev):
 
 
 def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nrec, structure, peak, dev,
-                  index_mode=False, comm=None, spare=None, recovery=False):
+                  index_mode=False, comm=None, spare=None, recovery=False, full=False):
     """a7 at N = nrec (SURVEY §8(a), config 4's "chained restore of 8 differentials"): build a real
     chain of `nrec` incremental records (versions 1..nrec, each a fresh f-change set), then
     (1) fold all of them onto a base copy in one tc_diff_apply call (records resident in HBM), and
@@ -1258,6 +1267,10 @@ def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nre
     recs, lens, counts = [], [], []
     with torch.cuda.stream(s):
         for v in range(1, nrec + 1):
+            # dense chains outgrow the HBM the step leaves (f = 30 %: 7 GB per record at cfg2): the
+            # chain stops at the records that fit (reported) instead of failing the run
+            if lens and torch.cuda.mem_get_info(dev)[0] < lens[-1] * 1.05 + (2 << 30):
+                break
             for i, z in enumerate(Z):
                 tc.synth_step(z, seed, i, 1000 + v, p53, structure, stream=s)
             cnt = 0
@@ -1265,11 +1278,15 @@ def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nre
                 for a in range(0, z.numel(), 1 << 27):
                     cnt += int((r_[a: a + (1 << 27)] != z[a: a + (1 << 27)]).sum().item())
             counts.append(cnt)
-            tc.diff_encode(ctx, ref, Z, tmp, ob, v, v - 1, T, C, True, stream=s, index_mode=index_mode)
+            tc.diff_encode(ctx, ref, Z, tmp, ob, v, v - 1, T, C, True, stream=s, index_mode=index_mode, full=full)
             s.synchronize()
             n = int(ob.item())
+            if not recs and torch.cuda.mem_get_info(dev)[0] < n + (1 << 30):
+                return {"unavailable": f"one {n / 1e9:.1f} GB record does not fit beside the step's buffers"}
             recs.append(tmp[:n].clone())
             lens.append(n)
+    cut = len(recs) < nrec
+    nrec = len(recs)
     union, line_bytes = 0, 0
     with torch.cuda.stream(s):
         for x, z, w_ in zip(X, Z, wb):
@@ -1299,7 +1316,7 @@ def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nre
         with torch.cuda.stream(s):
             for r_, x in zip(R, X):
                 r_.copy_(x)
-        staged = [torch.empty(max(n, 16), dtype=torch.uint8, device=dev) for n in lens]
+        staged = recs  # the H2D lands in the device records themselves (same bytes; no 2nd copy of the chain)
         a, b = ev(), ev()
         a.record(s)
         for d, h, n in zip(staged, hosts, lens):
@@ -1317,7 +1334,8 @@ def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nre
     meta = 0
     for n_, w_ in zip(sizes, wb):
         chunks = max(1, -(-n_ // C))
-        meta += nrec * ((0 if index_mode else 4 * -(-n_ // 32)) + 4 * (-(-n_ // T) + chunks) + 64 * chunks)
+        meta += nrec * (64 * chunks if full else
+                        (0 if index_mode else 4 * -(-n_ // 32)) + 4 * (-(-n_ // T) + chunks) + 64 * chunks)
     if index_mode:  # every record's u16 positions: 2 bytes per changed word of each record
         meta += 2 * sum(counts)
     wmean = sum(n_ * w_ for n_, w_ in zip(sizes, wb)) / sum(sizes)
@@ -1337,7 +1355,8 @@ def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nre
     # holding a word of the union written
     fu = union / max(1, words)
     fold_bs = meta + union * wmean + sum(n_ * w_ * (1 - (1 - fu) ** (32 // w_)) for n_, w_ in zip(sizes, wb))
-    return {"records": nrec, "record_format": "index" if index_mode else "mask",
+    return {"records": nrec, **({"chain_cut": "HBM left after the step holds this many records"} if cut else {}),
+            "record_format": "full" if full else "index" if index_mode else "mask",
             "strategy": "stream" if dense else "scatter",
             "record_bytes_total": sum(lens), "union_changed_words": union,
             "fold_ms": round(fm, 4), "state_gbs": round(W / fm / 1e6, 1),

@@ -68,6 +68,25 @@ uint64_t bound_of(uint64_t n, const Opts& o) {
     return kHdr + 16 * chunks + pad16u(2 * n) + pad16u(4 * n);
 }
 
+// programmatic dependent launch (sm_90+): a primary lets its dependents start; a dependent waits for
+// its primary's completion and memory (a no-op when launched without the attribute)
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+template <typename K, typename A>
+cudaError_t launch_pdl(K kernel, unsigned grid, unsigned block, cudaStream_t s, const A& arg) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, arg);
+}
+
 __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
     z += 0x9E3779B97F4A7C15ull;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -147,6 +166,7 @@ __global__ void __launch_bounds__(1024) grad_sample_kernel(const __grid_constant
     __shared__ uint32_t hist[256];
     __shared__ uint32_t s_bits, s_rank;
     const int tid = threadIdx.x, lane = tid & 31;
+    pdl_launch_dependents();  // the counting pass may start loading its tiles now
     uint32_t v[kPer];
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
@@ -238,7 +258,6 @@ __global__ void __launch_bounds__(kGThreads) grad_count_kernel(const __grid_cons
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint64_t b = blockIdx.x;
     const uint64_t i0 = b * kGB + 16ull * tid;
-    const float thr = *P.thr;
     float v[16];
     uint32_t f = 0;
     if (i0 + 16 <= P.n) {
@@ -255,6 +274,10 @@ __global__ void __launch_bounds__(kGThreads) grad_count_kernel(const __grid_cons
 #pragma unroll
         for (int e = 0; e < 16; ++e) v[e] = i0 + e < P.n ? P.x[i0 + e] : 0.0f;
     }
+    // programmatic dependent launch: the first CTAs started while the sample kernel ran, their
+    // tiles in flight; the threshold is read once that kernel has completed
+    pdl_wait();
+    const float thr = *P.thr;
     if (thr > 0.0f) {
 #pragma unroll
         for (int e = 0; e < 16; ++e) f |= fabsf(v[e]) >= thr ? (1u << e) : 0u;
@@ -303,6 +326,7 @@ __global__ void __launch_bounds__(1024) grad_prefix_kernel(const __grid_constant
     __shared__ unsigned long long s_carry;
     __shared__ unsigned long long s_warp[32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    pdl_launch_dependents();  // the emit CTAs may be resident (and load their block counts) now
     if (tid == 0) s_carry = 0;
     __syncthreads();
     for (uint64_t base = 0; base < P.ngroups; base += 1024) {
@@ -363,13 +387,15 @@ __global__ void __launch_bounds__(kGThreads) grad_emit_kernel(const __grid_const
     __shared__ uint32_t s_warp[kGThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const uint64_t g = blockIdx.x;
+    const uint64_t bb = g * kGGroup + tid;
+    const uint32_t info = bb < P.nblocks ? P.bcount[bb] : 0u;  // the counting pass completed before the prefix kernel
+    pdl_wait();  // the prefix kernel's group prefix, chunk starts and header
     const uint64_t kept = P.gpre[P.ngroups];
     const uint64_t voff = kHdr + 16 * P.nchunks, ioff = voff + pad16u(2 * kept);
     if (ioff + pad16u(4 * kept) > P.cap) return;  // CAPACITY was reported by the prefix kernel
     uint16_t* gv = reinterpret_cast<uint16_t*>(P.out + voff);
     int32_t* gi = reinterpret_cast<int32_t*>(P.out + ioff);
-    const uint64_t b = g * kGGroup + tid;
-    const uint32_t info = b < P.nblocks ? P.bcount[b] : 0u;
+    const uint64_t b = bb;
     const uint32_t c = info & ~kDenseBit;
     uint32_t inc = c;
 #pragma unroll
@@ -1155,11 +1181,15 @@ tc_status tc_grad_compress(tc_ctx* ctx, const float* grad, uint64_t n, const tc_
     P.spill = sb + o_sp;
     cudaError_t e0 = cudaMemsetAsync(P.gsum, 0, 8 * P.ngroups, s);
     if (e0 != cudaSuccess) return cuda_fail(e0, "cudaMemsetAsync(group sums)");
+    // sample -> count and prefix -> emit as programmatic dependent launches (the dependent grid
+    // starts while its 1-CTA predecessor runs; griddepcontrol.wait orders the data)
     grad_sample_kernel<<<1, 1024, 0, s>>>(P);
-    grad_count_kernel<<<static_cast<unsigned>(P.nblocks), kGThreads, 0, s>>>(P);
-    grad_prefix_kernel<<<1, 1024, 0, s>>>(P);
-    grad_emit_kernel<<<static_cast<unsigned>(P.ngroups), kGThreads, 0, s>>>(P);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_pdl(grad_count_kernel, static_cast<unsigned>(P.nblocks), kGThreads, s, P);
+    if (e == cudaSuccess) {
+        grad_prefix_kernel<<<1, 1024, 0, s>>>(P);
+        e = launch_pdl(grad_emit_kernel, static_cast<unsigned>(P.ngroups), kGThreads, s, P);
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "grad compress launch");
     tc::ctx_add_launches(ctx, 4);
     return TC_OK;
