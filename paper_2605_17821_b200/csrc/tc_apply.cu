@@ -167,9 +167,10 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
             P.info[3] = 0;
             P.info[4] = 0;
             P.info[5] = 0;
+            P.info[6] = 0;
         } else {
             const unsigned R = s_nrec[0];
-            uint64_t u = 0, ndense = 0, nlist = 0, nentry = 0;
+            uint64_t u = 0, ndense = 0, nlist = 0, nentry = 0, nmlist = 0;
             for (unsigned r = 0; r < R; ++r) {
                 P.unit_first[r] = u;
                 FoldRec& a = P.desc[r];
@@ -187,6 +188,9 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
                 for (int k = 0; k < P.nrec && all_index; ++k) all_index = P.desc[static_cast<size_t>(k) * P.cap + r].idx != nullptr;
                 bool any_full = false;  // chains with a full record are scattered (fold_unit handles them)
                 for (int k = 0; k < P.nrec; ++k) any_full = any_full || P.desc[static_cast<size_t>(k) * P.cap + r].full;
+                // every record a mask-mode one at T = 4096: the mask-list kernel can stream the chain
+                bool all_mask = a.T == kListT && P.nrec <= static_cast<int>(kListMaxRec) && !any_full;
+                for (int k = 0; k < P.nrec && all_mask; ++k) all_mask = P.desc[static_cast<size_t>(k) * P.cap + r].idx == nullptr;
                 const uint64_t mm = a.m;
                 if (any_full) {
                     a.dense = 0u;
@@ -198,16 +202,17 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
                     // 2.3 ms at 1 %; the streaming list fold of 8 records 6.6 / 8.1 ms)
                     a.dense = 3u;
                 } else if (P.dense_permille == 0u) {
-                    a.dense = all_idx ? 2u : 1u;
-                } else if (P.dense_permille == 0xffffffffu || !all_idx) {
+                    a.dense = all_idx ? 2u : all_mask ? 4u : 1u;
+                } else if (P.dense_permille == 0xffffffffu || !(all_idx || all_mask)) {
                     a.dense = 0u;
                 } else {
                     const bool stream = (P.nrec >= 4 && sum * 1000ull >= mm * 5ull) || sum * 1000ull > mm * P.dense_permille;
-                    a.dense = stream ? 2u : 0u;
+                    a.dense = stream ? (all_idx ? 2u : 4u) : 0u;
                 }
                 ndense += a.dense == 1u;
                 nlist += a.dense == 2u;
                 nentry += a.dense == 3u;
+                nmlist += a.dense == 4u;
                 const uint64_t U = fold_unit_words(a.T, a.dense);
                 u += a.m ? cdiv(a.m, U) : 0;
             }
@@ -215,9 +220,10 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
             P.info[0] = R;
             P.info[1] = u;
             P.info[2] = ndense;              // chunks for fold_dense_kernel
-            P.info[3] = R - ndense - nlist - nentry;  // chunks for fold_kernel
+            P.info[3] = R - ndense - nlist - nentry - nmlist;  // chunks for fold_kernel
             P.info[4] = nlist;               // chunks for fold_list_kernel
             P.info[5] = nentry;              // chunks for fold_entries_kernel
+            P.info[6] = nmlist;              // chunks for fold_mlist_kernel
         }
     }
 }
@@ -536,7 +542,7 @@ __global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const __grid_cons
             const uint64_t mid = (lo + hi) >> 1;
             if (P.unit_first[mid] <= u) lo = mid; else hi = mid;
         }
-        if (P.desc[lo].dense == 1u || P.desc[lo].dense == 2u) {  // a streaming kernel's chunk: jump past it
+        if (P.desc[lo].dense == 1u || P.desc[lo].dense == 2u || P.desc[lo].dense == 4u) {  // a streaming kernel's chunk: jump past it
             const uint64_t nxt = P.unit_first[lo + 1];
             u += (nxt - u + nwarps - 1) / nwarps * nwarps - nwarps;
             continue;
@@ -1301,6 +1307,255 @@ __global__ void __launch_bounds__(kListThreads, kListBlocksPerSM) fold_list_kern
     if (bad && tid == 0) tc_set_err(P.err, TC_ERR_CORRUPT);
 }
 
+// ------------------------------------------------------ mask-list fold (strategy 4) -------
+// Chains of mask-mode records at T = 4096 (the adaptive format above ~6 % changed words), streamed
+// like the list kernel: one CTA per 4096-word tile, the tile's state in shared memory by one bulk
+// load, each record's value run for the tile ([tile_off[t], tile_off[t+1]) — contiguous) staged by
+// 16-byte cp.async copies, in rounds of records newest first, as many as the stage holds (one
+// record's whole run always fits).  Thread t owns mask word t of the tile (= 32-word line t): a
+// record's winners on it are the bits no newer record set (cov), their values taken from the stage
+// at the record's running count (a block scan of the mask words' popcounts), so records need no
+// ordering barrier and each word is written once; every line a record touched goes back whole
+// with 16-byte stores (no partial-sector writes).  The scatter fold of such chains pays a gather
+// round trip per record and an L2 fill per partially written sector (cfg4, N = 8, f = 10 %: 39 ms).
+// Checks: a record's popcount over the tile equals its tile_off difference, tile_off monotone,
+// first 0, last = count, positions inside the tile.
+constexpr uint32_t kMListThreads = 128;        // = the mask words of a 4096-word tile
+constexpr uint32_t kMListStage = 16384 + 256;  // bytes: a whole fp32 run of one tile + alignment
+constexpr int kMListBatch = 8;                 // records per round at most (their mask words in registers)
+constexpr uint32_t kMListBlocksPerSM = 6;
+
+struct MListSmem {
+    uint4 tile[kListT * 4 / 16];
+    uint4 stage[kMListStage / 16];
+    const uint32_t* mask[kListMaxRec];
+    const uint8_t* val[kListMaxRec];
+    const uint32_t* toff[kListMaxRec];
+    uint32_t count[kListMaxRec];
+    uint32_t carry[kListMaxRec];   // first entry of the tile, per record
+    uint32_t tend[kListMaxRec];    // end entry of the tile, per record
+    uint32_t wtot[kMListBatch / 2][kMListThreads / 32];  // packed pairs of records
+    uint8_t touched[kListT / 32];
+    uint64_t bar;
+};
+
+template <int W>
+__device__ __forceinline__ void mlist_unit(MListSmem& S, int N, uint32_t nw, uint32_t ku, uint8_t* st,
+                                           uint32_t& phase, int tid, bool& bad) {
+    using word_t = typename Word<W>::T;
+    constexpr uint32_t kVec = 16 / W;
+    word_t* tw = reinterpret_cast<word_t*>(S.tile);
+    word_t* state = reinterpret_cast<word_t*>(st);
+    uint8_t* sb = reinterpret_cast<uint8_t*>(S.stage);
+    const int lane = tid & 31, wid = tid >> 5;
+    const uint32_t nmw = (nw + 31) / 32;
+    // this thread's line: the bits inside the tile
+    const uint32_t lim = 32u * tid >= nw ? 0u : nw - 32u * tid >= 32u ? ~0u : (1u << (nw - 32u * tid)) - 1u;
+    uint32_t cov = 0;  // bits of this thread's line set by a newer record
+    bool tile_ready = false;
+    for (int r = N - 1; r >= 0;) {
+        // the round: records r, r-1, ... whose runs fit the stage together (CTA-uniform)
+        int nb = 0;
+        uint32_t used = 0, soff[kMListBatch];
+#pragma unroll
+        for (int q = 0; q < kMListBatch; ++q) {
+            soff[q] = used;
+            if (q == nb && r - q >= 0) {
+                const uint32_t a = S.carry[r - q], b = S.tend[r - q];
+                const uint32_t sz = b > a ? static_cast<uint32_t>(((static_cast<uint64_t>(b) * W + 15) & ~uint64_t(15)) -
+                                                                  (static_cast<uint64_t>(a) * W & ~uint64_t(15)))
+                                          : 0u;
+                if (used + sz <= kMListStage) {
+                    used += sz;
+                    ++nb;
+                }
+            }
+        }
+        uint32_t mw[kMListBatch];
+#pragma unroll
+        for (int q = 0; q < kMListBatch; ++q)
+            mw[q] = q < nb && tid < static_cast<int>(nmw) ? ldg_u32(S.mask[r - q] + static_cast<size_t>(ku) * 128 + tid) : 0u;
+#pragma unroll
+        for (int q = 0; q < kMListBatch; ++q) {
+            if (q < nb) {
+                const uint32_t a = S.carry[r - q], b = S.tend[r - q];
+                if (b > a) {
+                    const uint64_t lo = static_cast<uint64_t>(a) * W & ~uint64_t(15);
+                    const uint64_t hi = (static_cast<uint64_t>(b) * W + 15) & ~uint64_t(15);
+                    const uint8_t* src = S.val[r - q] + lo;
+                    for (uint32_t o = 16 * tid; o < hi - lo; o += 16 * kMListThreads) cp_async16(sb + soff[q] + o, src + o);
+                }
+            }
+        }
+        // each record's running count before this thread's mask word: warp scans + warp totals
+        // two records per scan: their counts packed in 16-bit halves (a tile's prefix <= 4096)
+        uint32_t pre[kMListBatch];
+#pragma unroll
+        for (int q = 0; q < kMListBatch; q += 2) {
+            const uint32_t c = __popc(mw[q]) | (__popc(mw[q + 1]) << 16);
+            uint32_t inc = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += y;
+            }
+            pre[q] = (inc - c) & 0xffffu;
+            pre[q + 1] = (inc - c) >> 16;
+            if (lane == 31) S.wtot[q / 2][wid] = inc;
+        }
+        cp_async_wait_all();
+        if (!tile_ready) {
+            mbar_wait_parity(&S.bar, phase);
+            phase ^= 1u;
+            tile_ready = true;
+        }
+        __syncthreads();  // the stage, the warp totals and the tile
+#pragma unroll
+        for (int q = 0; q < kMListBatch; ++q) {
+            if (q < nb) {
+                const int rr = r - q;
+                uint32_t before = 0, tot = 0;  // (packed pair q & ~1: this record's half)
+#pragma unroll
+                for (int k = 0; k < static_cast<int>(kMListThreads / 32); ++k) {
+                    const uint32_t x = S.wtot[q / 2][k];
+                    before += k < wid ? x : 0u;
+                    tot += x;
+                }
+                before = (q & 1) ? before >> 16 : before & 0xffffu;
+                tot = (q & 1) ? tot >> 16 : tot & 0xffffu;
+                const uint32_t a = S.carry[rr];
+                // the mask must agree with tile_off, and set no bit past the chunk's last word; then
+                // every rank below is < tot and every position inside the tile (no per-word test)
+                if (tot != S.tend[rr] - a || (mw[q] & ~lim)) {  // (the stage holds tend - a values)
+                    bad = true;
+                    continue;
+                }
+                const word_t* sv = reinterpret_cast<const word_t*>(sb + soff[q] + ((a * W) & 15u)) + before + pre[q];
+                word_t* tl = tw + 32u * tid;
+                const uint32_t mq = mw[q];
+                uint32_t win = mq & ~cov;
+                cov |= mq;
+                while (win) {  // highest bit first (FLO, no bit reversal)
+                    const int b = 31 - __clz(win);
+                    win ^= 1u << b;
+                    tl[b] = sv[__popc(mq & ((1u << b) - 1u))];
+                }
+            }
+        }
+        __syncthreads();  // the stage and the warp totals are reused by the next round
+        r -= nb;
+    }
+    S.touched[tid] = cov != 0u;
+    __syncthreads();
+    // touched lines back, 16 bytes per thread (consecutive threads, consecutive bytes)
+    const uint32_t npieces = (nw + kVec - 1) / kVec;
+    for (uint32_t q = tid; q < npieces; q += kMListThreads) {
+        const uint32_t wi = q * kVec;
+        if (S.touched[wi >> 5]) {
+            if (wi + kVec <= nw)
+                *reinterpret_cast<uint4*>(state + wi) = S.tile[q];
+            else
+                for (uint32_t i = wi; i < nw; ++i) state[i] = tw[i];
+        }
+    }
+    fence_proxy_async_smem();  // these tile reads precede the next bulk load into the tile
+}
+
+__global__ void __launch_bounds__(kMListThreads, kMListBlocksPerSM) fold_mlist_kernel(const __grid_constant__ FoldParams P) {
+    __shared__ MListSmem S;
+    if (*reinterpret_cast<volatile unsigned*>(P.err) != 0) return;  // sticky error pending
+    if (P.info[6] == 0) return;                                       // no mask-list chunk
+    const int tid = threadIdx.x;
+    const int N = P.nrec;
+    const uint64_t R = P.info[0];
+    const uint64_t total = P.info[1];
+    if (blockIdx.x * kDenseRun >= total) return;
+    if (tid == 0) mbar_init(&S.bar, 1);
+    __syncthreads();
+    bool bad = false;
+    uint32_t phase = 0;
+    uint64_t cur = ~uint64_t(0);
+    uint32_t te = 0;  // thread j < N: record j's end entry of the next tile (prefetched)
+    bool te_valid = false;
+    uint64_t lo = 0, u1 = 0;
+    for (uint64_t u = 0;; ++u) {
+        if (u >= u1) {  // the next run of consecutive units
+            const uint64_t run = u1 == 0 ? blockIdx.x : u1 / kDenseRun + gridDim.x - 1;
+            if (run * kDenseRun >= total) break;
+            u = run * kDenseRun;
+            u1 = u + kDenseRun < total ? u + kDenseRun : total;
+            uint64_t hi = R;
+            lo = 0;
+            while (hi - lo > 1) {
+                const uint64_t mid = (lo + hi) >> 1;
+                if (P.unit_first[mid] <= u) lo = mid; else hi = mid;
+            }
+            te_valid = false;
+        }
+        while (u >= P.unit_first[lo + 1]) ++lo;
+        const FoldRec& L = P.desc[lo];
+        if (L.dense != 4u) {  // folded by another kernel: skip the chunk
+            u = (P.unit_first[lo + 1] < u1 ? P.unit_first[lo + 1] : u1) - 1;
+            te_valid = false;
+            continue;
+        }
+        if (lo != cur) {
+            if (tid < N) {
+                const FoldRec& F = P.desc[static_cast<size_t>(tid) * P.cap + lo];
+                S.mask[tid] = reinterpret_cast<const uint32_t*>(F.mask);
+                S.val[tid] = F.values;
+                S.toff[tid] = reinterpret_cast<const uint32_t*>(F.toff);
+                S.count[tid] = static_cast<uint32_t>(F.count);
+            }
+            cur = lo;
+            te_valid = false;
+        }
+        const uint32_t ku = static_cast<uint32_t>(u - P.unit_first[lo]);
+        const uint32_t m = L.m, w = L.w;
+        const uint32_t nw = m - ku * kListT < kListT ? m - ku * kListT : kListT;
+        uint8_t* st = P.state[L.seg] + (L.chunk_off + static_cast<uint64_t>(ku) * kListT) * w;
+        // the tile (its previous contents were read by every thread before the last barrier)
+        if (tid == 0) {
+            const uint32_t bytes = nw * w, bulk = bytes & ~15u;
+            mbar_arrive_expect_tx(&S.bar, bulk);
+            if (bulk) bulk_g2s(S.tile, st, bulk, &S.bar);
+            for (uint32_t i = bulk; i < bytes; ++i) reinterpret_cast<uint8_t*>(S.tile)[i] = st[i];
+        }
+        const bool next = u + 1 < u1 && u + 1 < P.unit_first[lo + 1];
+        __syncthreads();  // the record table is in place
+        if (tid < N) {  // this tile's entry range per record; the next tile's end, one unit ahead
+            if (te_valid) {
+                S.carry[tid] = S.tend[tid];
+                S.tend[tid] = te;
+            } else {
+                S.carry[tid] = ldg_u32(S.toff[tid] + ku);
+                S.tend[tid] = ldg_u32(S.toff[tid] + ku + 1);
+            }
+            const uint32_t k0 = S.carry[tid], k1 = S.tend[tid];
+            if (k1 < k0 || k1 - k0 > nw || k1 > S.count[tid] || (ku == 0 && k0 != 0) ||
+                ((ku + 1) * kListT >= m && k1 != S.count[tid]))
+                bad = true;
+        }
+        if (next && tid < N) te = ldg_u32(S.toff[tid] + ku + 2);
+        te_valid = next;
+        if (__syncthreads_or(bad)) {  // a corrupt tile_off: drain the tile load, write nothing
+            mbar_wait_parity(&S.bar, phase);
+            phase ^= 1u;
+            bad = true;
+            break;
+        }
+        if (w == 4)
+            mlist_unit<4>(S, N, nw, ku, st, phase, tid, bad);
+        else
+            mlist_unit<2>(S, N, nw, ku, st, phase, tid, bad);
+        if (__syncthreads_or(bad)) {  // also: every thread is done with the tile
+            bad = true;
+            break;
+        }
+    }
+    if (bad && tid == 0) tc_set_err(P.err, TC_ERR_CORRUPT);
+}
+
 }  // namespace
 
 cudaError_t launch_fold(const FoldParams& p, cudaStream_t s, int num_sms, uint64_t* launches) {
@@ -1339,12 +1594,21 @@ cudaError_t launch_fold(const FoldParams& p, cudaStream_t s, int num_sms, uint64
             occ_e < 1)
             occ_e = 4;
     }
+    static int occ_m = 0;
+    if (!occ_m) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_m, fold_mlist_kernel, kMListThreads, 0) != cudaSuccess ||
+            occ_m < 1)
+            occ_m = 1;
+    }
+    fold_mlist_kernel<<<num_sms * occ_m, kMListThreads, 0, s>>>(p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
     for (int j = 0; j < p.nrec; ++j) {  // each returns at once when no chunk takes strategy 3
         fold_entries_kernel<<<num_sms * occ_e, kFoldThreads, 0, s>>>(p, j);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    *launches += 4 + static_cast<uint64_t>(p.nrec);
+    *launches += 5 + static_cast<uint64_t>(p.nrec);
     return cudaGetLastError();
 }
 
