@@ -22,7 +22,7 @@ PROF = os.path.join(ROOT, "profiles")
 
 def short(name):
     for k in ("encode_mask_kernel", "encode_prefix_kernel", "encode_emit_kernel", "encode_full_kernel",
-              "fold_walk_kernel", "fold_dense_kernel", "fold_list_kernel", "fold_entries_kernel", "fold_kernel", "synth_base_kernel", "synth_step_kernel", "stage_sizes_kernel"):
+              "fold_walk_kernel", "fold_dense_kernel", "fold_list_kernel", "fold_mlist_kernel", "fold_entries_kernel", "fold_kernel", "synth_base_kernel", "synth_step_kernel", "stage_sizes_kernel"):
         if k in name:
             return k
     return name.split("(")[0][-60:]
