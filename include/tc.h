@@ -135,10 +135,10 @@ tc_status tc_ctx_check(tc_ctx* ctx, tc_stream stream);
 uint64_t tc_ctx_launches(const tc_ctx* ctx);
 /* Restore strategy.  tc_diff_apply folds a chunk either by scattering the
  * winning words in place or by streaming the chunk's tiles through shared memory (whole-line
- * writes).  Chains of index-mode records, and chains of mask-mode records, at T = 4096 (at most
- * 32 records, one format per chain) are streamed when they are long (>= 4 records changing
- * >= 0.5 % of the words in total) or dense (> permille/1000 of the words in total); all other
- * chunks are scattered.  Default 60 (6 %).  0 = stream every chunk; UINT32_MAX = scatter every
+ * writes).  Chains of index-mode records at T = 4096 are streamed when they are long (>= 4
+ * records changing >= 0.5 % of the words in total) or dense (> permille/1000 of the words in
+ * total), chains of mask-mode records at T = 4096 when dense (at most 32 records, one format per
+ * chain); all other chunks are scattered.  Default 60 (6 %).  0 = stream every chunk; UINT32_MAX = scatter every
  * chunk.  Every strategy produces the same state.
  * Takes effect for later tc_diff_apply calls.  Errors: TC_ERR_INVALID (NULL ctx). */
 tc_status tc_ctx_set_fold_dense_permille(tc_ctx* ctx, uint32_t permille);

@@ -205,9 +205,14 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
                     a.dense = all_idx ? 2u : all_mask ? 4u : 1u;
                 } else if (P.dense_permille == 0xffffffffu || !(all_idx || all_mask)) {
                     a.dense = 0u;
-                } else {
+                } else if (all_idx) {
                     const bool stream = (P.nrec >= 4 && sum * 1000ull >= mm * 5ull) || sum * 1000ull > mm * P.dense_permille;
-                    a.dense = stream ? (all_idx ? 2u : 4u) : 0u;
+                    a.dense = stream ? 2u : 0u;
+                } else {
+                    // mask chains (cfg2 sweep, profiles/rd5q_mask_fold_sweep.txt): streaming wins once the
+                    // records change more than ~6 % of the words in total, whatever N (N = 4 at 1 % each:
+                    // scatter 8.4 vs 9.5 ms; N = 2 at 3 %: 9.0 vs 8.7; N = 8 at 1 %: 16.5 vs 12.3)
+                    a.dense = sum * 1000ull > mm * P.dense_permille ? 4u : 0u;
                 }
                 ndense += a.dense == 1u;
                 nlist += a.dense == 2u;
