@@ -142,6 +142,14 @@ uint64_t tc_ctx_launches(const tc_ctx* ctx);
  * chunk.  Every strategy produces the same state.
  * Takes effect for later tc_diff_apply calls.  Errors: TC_ERR_INVALID (NULL ctx). */
 tc_status tc_ctx_set_fold_dense_permille(tc_ctx* ctx, uint32_t permille);
+/* Upper bound on the records of one diff that later tc_diff_apply calls on this ctx will fold
+ * (the caller knows it: sum over segments of max(1, ceil(n_words / chunk_words))).  Without it the
+ * fold's descriptor scratch is sized from the record bytes (>= 80 bytes per record, at most
+ * TC_MAX_RECORDS_PER_DIFF): ~38 MB for a chain of 8 cfg2-sized records, ~300 MB for 64; with it,
+ * records x 72 bytes per diff.  A diff holding more
+ * records fails with TC_ERR_CAPACITY (nothing folded).  0 (default) = no bound.
+ * Errors: TC_ERR_INVALID (NULL ctx). */
+tc_status tc_ctx_set_fold_max_records(tc_ctx* ctx, uint64_t records);
 /* CTAs of tc_push_peer's NVLink copy on this ctx (0 = default 32).  More CTAs = more stores in
  * flight (a 1 GiB push: ~530 GB/s at 16, ~600 at 32, ~700 at 296 per direction) but more
  * interference with kernels running beside it.  Errors: TC_ERR_INVALID. */

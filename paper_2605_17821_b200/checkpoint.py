@@ -245,6 +245,11 @@ class Checkpointer:
         if overlap_standby and self.standby is not None:
             self.s_stby = torch.cuda.Stream(self.device, priority=-1)
             self.sctx = tc.Ctx(dev)
+        # every diff of this layout holds sum_s max(1, ceil(n_s / C)) records: the folds' descriptor
+        # scratch is sized for that, not for the worst case the record bytes allow
+        self.records_per_diff = sum(max(1, -(-n // chunk_words)) for n in self.sizes)
+        for c in {id(self.ctx): self.ctx, id(self.sctx): self.sctx}.values():
+            c.set_fold_max_records(self.records_per_diff)
         self.ahead = ahead
         self.timing = timing
         self.times = {"encode": [], "stage": [], "push": [], "fold": []}

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
                     break;
                 }
                 if (r >= P.cap) {  // below the ABI limit the table is sized by the shortest diff:
-                    err = P.cap < TC_MAX_RECORDS_PER_DIFF ? TC_ERR_INVALID : TC_ERR_CAPACITY;  // layouts differ
+                    err = P.cap_hinted || P.cap >= TC_MAX_RECORDS_PER_DIFF ? TC_ERR_CAPACITY : TC_ERR_INVALID;  // layouts differ
                     break;
                 }
                 if (imode && T > kIndexMaxT) { err = TC_ERR_INVALID; break; }  // unsupported here

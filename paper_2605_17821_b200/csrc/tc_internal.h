@@ -143,6 +143,7 @@ struct FoldParams {
     int nseg;
     int nrec;               // diffs folded
     uint32_t cap;           // descriptor capacity per diff
+    uint32_t cap_hinted;    // cap comes from tc_ctx_set_fold_max_records: more records -> TC_ERR_CAPACITY
     uint64_t state_version;
     uint32_t dense_permille;  // chunk r is dense when sum_j count_j * 1000 > m * dense_permille
     FoldRec* desc;          // [nrec][cap]

@@ -28,6 +28,7 @@ struct tc_ctx {
     unsigned int* err = nullptr;  // [0] sticky device error word, [1] tc_push_peer block counter
     uint64_t launches = 0;
     uint32_t fold_dense_permille = 60;  // tc_ctx_set_fold_dense_permille
+    uint64_t fold_max_records = 0;      // tc_ctx_set_fold_max_records (0: bound by the record bytes)
     uint32_t push_ctas = 0;              // tc_ctx_set_push_ctas (0: default)
     void* grad = nullptr;                // gradient codec / replay scratch (tc_grad.cu)
     size_t grad_bytes = 0;
@@ -160,6 +161,12 @@ tc_status tc_ctx_set_push_ctas(tc_ctx* c, uint32_t ctas) {
     if (!c) return fail(TC_ERR_INVALID, "ctx is NULL");
     if (ctas > 65535) return fail(TC_ERR_INVALID, "ctas must be <= 65535");
     c->push_ctas = ctas;
+    return TC_OK;
+}
+
+tc_status tc_ctx_set_fold_max_records(tc_ctx* c, uint64_t records) {
+    if (!c) return fail(TC_ERR_INVALID, "ctx is NULL");
+    c->fold_max_records = records;
     return TC_OK;
 }
 
@@ -443,6 +450,13 @@ tc_status tc_diff_apply(tc_ctx* ctx, void* const* state, const uint64_t* n_words
         // with more records than that fails the walker's layout check anyway)
         const uint64_t by_bytes = record_bytes_[j] / 80 + 1;
         if (by_bytes < cap) cap = by_bytes;
+    }
+    // the caller's bound on records per diff (its layout and chunk size fix it): the descriptor
+    // table shrinks from min(record_bytes / 80, 65536) entries per diff (~38 MB for a
+    // chain of 8 cfg2-sized records, ~300 MB for 64) to what the layout needs
+    if (ctx->fold_max_records && ctx->fold_max_records < cap) {
+        cap = ctx->fold_max_records;
+        P.cap_hinted = 1;
     }
     P.nseg = nseg;
     P.nrec = n_records;

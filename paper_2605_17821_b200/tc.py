@@ -76,6 +76,7 @@ def _load():
     L.tc_ctx_launches.argtypes = [vp]
     L.tc_ctx_set_fold_dense_permille.argtypes = [vp, u32]
     L.tc_ctx_set_push_ctas.argtypes = [vp, u32]
+    L.tc_ctx_set_fold_max_records.argtypes = [vp, u64]
     L.tc_diff_bound.argtypes = [ctypes.POINTER(Segment), cint, ctypes.POINTER(EncodeOpts),
                                 ctypes.POINTER(u64)]
     L.tc_diff_encode.argtypes = [vp, ctypes.POINTER(Segment), cint, ctypes.POINTER(EncodeOpts), u64, u64,
@@ -220,6 +221,10 @@ class Ctx:
     def set_push_ctas(self, ctas: int):
         """CTAs of tc_push_peer on this ctx (include/tc.h); 0 = default."""
         _check(LIB.tc_ctx_set_push_ctas(self.h, int(ctas)), "tc_ctx_set_push_ctas")
+
+    def set_fold_max_records(self, records: int):
+        """tc_ctx_set_fold_max_records: records per diff the later folds hold at most (0 = no bound)."""
+        _check(LIB.tc_ctx_set_fold_max_records(self.h, int(records)), "tc_ctx_set_fold_max_records")
 
     def set_fold_dense_permille(self, permille: int):
         """Restore strategy threshold (include/tc.h): 0 = always stream, 2**32-1 = always scatter."""

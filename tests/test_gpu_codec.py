@@ -651,3 +651,25 @@ def test_sparse_index_chain_entry_passes(fctx, tco, N, T):
     assert tco.fold([a.copy() for a in states[0]], 0, chain)[0] == tc.ERR_CORRUPT
     rc, _ = gpu_fold(fctx, states[0], 0, chain)
     assert rc == tc.ERR_CORRUPT
+
+
+def test_fold_max_records_hint(tco):
+    """tc_ctx_set_fold_max_records: the exact records-per-diff bound folds exactly (descriptor
+    scratch sized by it); a bound below the diff's record count is refused (CAPACITY), state kept."""
+    sizes, wb, T, C = [20000, 9000, 0], [4, 2, 4], 256, 4096
+    states, diffs = make_chain(tco, sizes, wb, 3, 0.1, T, C, seed=41)
+    per_diff = sum(max(1, -(-n // C)) for n in sizes)  # 5 + 3 + 1 (an empty segment is one record)
+    c = tc.Ctx(0)
+    try:
+        c.set_fold_max_records(per_diff)
+        rc, st_g = gpu_fold(c, states[0], 0, diffs)
+        assert rc == tc.OK and all(np.array_equal(a, b) for a, b in zip(st_g, states[3]))
+        c.set_fold_max_records(per_diff - 1)
+        rc, st_g = gpu_fold(c, states[0], 0, diffs)
+        assert rc == tc.ERR_CAPACITY
+        assert all(np.array_equal(a, b) for a, b in zip(st_g, states[0]))
+        c.set_fold_max_records(0)
+        rc, st_g = gpu_fold(c, states[0], 0, diffs)
+        assert rc == tc.OK and all(np.array_equal(a, b) for a, b in zip(st_g, states[3]))
+    finally:
+        c.close()
