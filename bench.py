@@ -307,7 +307,8 @@ def run_ours(args):
                           expected_f=1.0 if args.structure == S3_ADAM else args.f,
                           record_format=args.format if allow_index else "mask", dev_slots=args.dev_slots,
                           t1_bytes=(args.dev_slots + 1) * est,
-                          t2_slots=2, standby=R, tile_words=T, chunk_words=C, ahead=world == 1,
+                          t2_slots=2, standby=R, tile_words=T, chunk_words=C,
+                          ahead=(world == 1 or bool(args.t2_fused)) if args.ahead is None else bool(args.ahead),
                           stage_base=False, ref=A, stream=s_comp, push_ctas=args.push_ctas, timing=True,
                           fused_t2=bool(args.t2_fused), overlap_standby=bool(args.overlap_standby))
         rec_cap = ck.rec_cap
@@ -1888,6 +1889,9 @@ def main():
                     help="simulated-failure recovery probe (Tier-1 and, N > 1, Tier-2); default: on for cfg4")
     ap.add_argument("--fold-dense-permille", type=int, default=None,
                     help="restore strategy threshold (tc_ctx_set_fold_dense_permille); default: libtc's")
+    ap.add_argument("--ahead", type=int, default=None,
+                    help="Checkpointer runs the host one step ahead of the device (default: at N = 1 and with "
+                         "the fused Tier-2 emit; N = 2: 6.08 vs 6.27 ms per step, profiles/rd5u_*)")
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--numa-bind", type=int, default=1,
                     help="N > 1: bind each rank to its GPU's NUMA node before the pinned buffers are allocated")
