@@ -1350,7 +1350,13 @@ def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nre
     # the default strategy of tc_diff_apply (include/tc.h): index-mode chains at T = 4096 stream
     # when long (N >= 4, >= 0.5 % in total) or dense (> 6 %)
     tot, words = sum(counts), sum(sizes)
-    dense = index_mode and T == 4096 and ((nrec >= 4 and tot * 1000 >= words * 5) or tot * 1000 > words * 60)
+    # (mask chains at T = 4096: the mask-list kernel when > 6 % in total)
+    if full:
+        dense = False
+    elif index_mode:
+        dense = T == 4096 and ((nrec >= 4 and tot * 1000 >= words * 5) or tot * 1000 > words * 60)
+    else:
+        dense = T == 4096 and nrec <= 32 and tot * 1000 > words * 60
     stream_b = W + line_bytes + sum(lens)
     # SURVEY §8(d) sector-granular: the records' metadata, the winning values, every 32-byte sector
     # holding a word of the union written
@@ -1358,7 +1364,7 @@ def restore_bench(tc, ctx, X, Z, ref, R, tmp, sizes, wb, seed, p53, T, C, s, nre
     fold_bs = meta + union * wmean + sum(n_ * w_ * (1 - (1 - fu) ** (32 // w_)) for n_, w_ in zip(sizes, wb))
     return {"records": nrec, **({"chain_cut": "HBM left after the step holds this many records"} if cut else {}),
             "record_format": "full" if full else "index" if index_mode else "mask",
-            "strategy": "stream" if dense else "scatter",
+            "strategy": ("stream (mask-list)" if not index_mode else "stream (list)") if dense else "scatter",
             "record_bytes_total": sum(lens), "union_changed_words": union,
             "fold_ms": round(fm, 4), "state_gbs": round(W / fm / 1e6, 1),
             "hbm_gbs_word": round(fold_b / fm / 1e6, 1), "frac_hbm_word": round(fold_b / fm / 1e6 / peak, 4),
