@@ -289,8 +289,9 @@ tc_status tc_peer_wait(tc_ctx* ctx, const void* mailbox, uint64_t version, uint6
  *   chain: records[0].ref_version == state_version, records[j].ref_version ==
  *   records[j-1].version, version > ref_version -> TC_ERR_PROTOCOL;
  *   all records must share tile_words and chunk layout -> TC_ERR_INVALID;
+ *   more records per diff than tc_ctx_set_fold_max_records allows -> TC_ERR_CAPACITY;
  *   per tile: mask popcount == tile_off difference, tail bits zero -> TC_ERR_CORRUPT.
- * After CORRUPT/PROTOCOL/INVALID found before the fold starts, the state is untouched; after
+ * After CORRUPT/PROTOCOL/INVALID/CAPACITY found before the fold starts, the state is untouched; after
  * a per-tile CORRUPT its contents are unspecified and the caller must refetch.
  * 1 <= n_records <= TC_MAX_FOLD. */
 tc_status tc_diff_apply(tc_ctx* ctx, void* const* state, const uint64_t* n_words,
