@@ -657,6 +657,7 @@ __global__ void grad_tile_start_kernel(const Payload* RP, uint64_t n, uint64_t t
 // ------------------------------------------------------------------- Adam ----------
 struct AdamC {
     float b1, b2, eps;
+    float omb1, omb2;  // 1 - b1, 1 - b2 rounded to fp32 (host IEEE subtraction = __fsub_rn), once per call
 };
 
 __device__ __forceinline__ void adam_update(float& master, float& m, float& v, float g, const AdamC& a, float ss,
@@ -664,9 +665,8 @@ __device__ __forceinline__ void adam_update(float& master, float& m, float& v, f
     // oracle/tco_grad.c order: m, v; denom = sqrt(v) * inv_c2s + eps; master -= step_size * (m / denom).
     // Zero operands take the IEEE result directly (sqrt(+0) = +0, 0 / d = 0 with 0's sign for d > 0):
     // the same values without the slow paths that zeros trigger (most of a sparse gradient is zero)
-    const float omb1 = __fsub_rn(1.0f, a.b1), omb2 = __fsub_rn(1.0f, a.b2);
-    m = __fadd_rn(__fmul_rn(a.b1, m), __fmul_rn(omb1, g));
-    v = __fadd_rn(__fmul_rn(a.b2, v), __fmul_rn(omb2, __fmul_rn(g, g)));
+    m = __fadd_rn(__fmul_rn(a.b1, m), __fmul_rn(a.omb1, g));
+    v = __fadd_rn(__fmul_rn(a.b2, v), __fmul_rn(a.omb2, __fmul_rn(g, g)));
     // Selects, not branches (re-entry; ncu rd6k: branch bookkeeping was 24 % of the replay's
     // instructions): a zero operand is replaced by 1 (the fast path) and the result by the zero
     // itself.  Fused replay of 5 payloads: 24.65 -> 23.42 ms (mid-training moments), 23.73 -> 23.35
@@ -1105,6 +1105,8 @@ AdamC adam_consts(const tc_adam_hp* hp) {
     a.b1 = static_cast<float>(hp ? hp->beta1 : 0.9);
     a.b2 = static_cast<float>(hp ? hp->beta2 : 0.999);
     a.eps = static_cast<float>(hp ? hp->eps : 1e-8);
+    a.omb1 = 1.0f - a.b1;  // one IEEE binary32 subtraction each (exact for beta in [0.5, 1], Sterbenz)
+    a.omb2 = 1.0f - a.b2;
     return a;
 }
 // step_size = lr / (1 - beta1^t), inv_c2s = 1 / sqrt(1 - beta2^t): in double, rounded to fp32
