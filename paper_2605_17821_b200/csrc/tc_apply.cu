@@ -168,9 +168,10 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
             P.info[4] = 0;
             P.info[5] = 0;
             P.info[6] = 0;
+            P.info[7] = 0;
         } else {
             const unsigned R = s_nrec[0];
-            uint64_t u = 0, ndense = 0, nlist = 0, nentry = 0, nmlist = 0;
+            uint64_t u = 0, ndense = 0, nlist = 0, nentry = 0, nmlist = 0, nmlist_s = 0;
             for (unsigned r = 0; r < R; ++r) {
                 P.unit_first[r] = u;
                 FoldRec& a = P.desc[r];
@@ -189,7 +190,7 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
                 bool any_full = false;  // chains with a full record are scattered (fold_unit handles them)
                 for (int k = 0; k < P.nrec; ++k) any_full = any_full || P.desc[static_cast<size_t>(k) * P.cap + r].full;
                 // every record a mask-mode one at T = 4096: the mask-list kernel can stream the chain
-                bool all_mask = a.T == kListT && P.nrec <= static_cast<int>(kListMaxRec) && !any_full;
+                bool all_mask = a.T <= kListT && P.nrec <= static_cast<int>(kListMaxRec) && !any_full;
                 for (int k = 0; k < P.nrec && all_mask; ++k) all_mask = P.desc[static_cast<size_t>(k) * P.cap + r].idx == nullptr;
                 const uint64_t mm = a.m;
                 if (any_full) {
@@ -202,7 +203,7 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
                     // 2.3 ms at 1 %; the streaming list fold of 8 records 6.6 / 8.1 ms)
                     a.dense = 3u;
                 } else if (P.dense_permille == 0u) {
-                    a.dense = all_idx ? 2u : all_mask ? 4u : 1u;
+                    a.dense = all_idx ? 2u : all_mask ? (a.T == kListT ? 4u : 5u) : 1u;
                 } else if (P.dense_permille == 0xffffffffu || !(all_idx || all_mask)) {
                     a.dense = 0u;
                 } else if (all_idx) {
@@ -212,12 +213,13 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
                     // mask chains (cfg2 sweep, profiles/rd5q_mask_fold_sweep.txt): streaming wins once the
                     // records change more than ~6 % of the words in total, whatever N (N = 4 at 1 % each:
                     // scatter 8.4 vs 9.5 ms; N = 2 at 3 %: 9.0 vs 8.7; N = 8 at 1 %: 16.5 vs 12.3)
-                    a.dense = sum * 1000ull > mm * P.dense_permille ? 4u : 0u;
+                    a.dense = sum * 1000ull > mm * P.dense_permille ? (a.T == kListT ? 4u : 5u) : 0u;
                 }
                 ndense += a.dense == 1u;
                 nlist += a.dense == 2u;
                 nentry += a.dense == 3u;
                 nmlist += a.dense == 4u;
+                nmlist_s += a.dense == 5u;
                 const uint64_t U = fold_unit_words(a.T, a.dense);
                 u += a.m ? cdiv(a.m, U) : 0;
             }
@@ -225,10 +227,11 @@ __global__ void __launch_bounds__(TC_MAX_FOLD) fold_walk_kernel(const __grid_con
             P.info[0] = R;
             P.info[1] = u;
             P.info[2] = ndense;              // chunks for fold_dense_kernel
-            P.info[3] = R - ndense - nlist - nentry - nmlist;  // chunks for fold_kernel
+            P.info[3] = R - ndense - nlist - nentry - nmlist - nmlist_s;  // chunks for fold_kernel
             P.info[4] = nlist;               // chunks for fold_list_kernel
             P.info[5] = nentry;              // chunks for fold_entries_kernel
-            P.info[6] = nmlist;              // chunks for fold_mlist_kernel
+            P.info[6] = nmlist;              // chunks for fold_mlist_kernel<false> (T = 4096)
+            P.info[7] = nmlist_s;            // chunks for fold_mlist_kernel<true> (T < 4096)
         }
     }
 }
@@ -547,7 +550,7 @@ __global__ void __launch_bounds__(kFoldThreads, 4) fold_kernel(const __grid_cons
             const uint64_t mid = (lo + hi) >> 1;
             if (P.unit_first[mid] <= u) lo = mid; else hi = mid;
         }
-        if (P.desc[lo].dense == 1u || P.desc[lo].dense == 2u || P.desc[lo].dense == 4u) {  // a streaming kernel's chunk: jump past it
+        if (P.desc[lo].dense == 1u || P.desc[lo].dense == 2u || P.desc[lo].dense >= 4u) {  // a streaming kernel's chunk: jump past it
             const uint64_t nxt = P.unit_first[lo + 1];
             u += (nxt - u + nwarps - 1) / nwarps * nwarps - nwarps;
             continue;
@@ -1344,8 +1347,8 @@ struct MListSmem {
     uint64_t bar;
 };
 
-template <int W>
-__device__ __forceinline__ void mlist_unit(MListSmem& S, int N, uint32_t nw, uint32_t ku, uint8_t* st,
+template <int W, bool SMALLT>  // SMALLT: T < kListT (inner tile_off entries to check)
+__device__ __forceinline__ void mlist_unit(MListSmem& S, int N, uint32_t nw, uint32_t ku, uint32_t T, uint8_t* st,
                                            uint32_t& phase, int tid, bool& bad) {
     using word_t = typename Word<W>::T;
     constexpr uint32_t kVec = 16 / W;
@@ -1435,6 +1438,12 @@ __device__ __forceinline__ void mlist_unit(MListSmem& S, int N, uint32_t nw, uin
                     bad = true;
                     continue;
                 }
+                // T < kListT: the tile_off entries inside the unit must equal the running count at
+                // their tile's first mask word (the unit's ends were checked by the caller)
+                const uint32_t wpt = T / 32;  // mask words per tile
+                if (SMALLT && tid > 0 && tid % wpt == 0 && tid < static_cast<int>(nmw) &&
+                    ldg_u32(S.toff[rr] + ku * (kListT / T) + tid / wpt) != a + before + pre[q])
+                    bad = true;
                 const word_t* sv = reinterpret_cast<const word_t*>(sb + soff[q] + ((a * W) & 15u)) + before + pre[q];
                 word_t* tl = tw + 32u * tid;
                 const uint32_t mq = mw[q];
@@ -1480,10 +1489,13 @@ __device__ __forceinline__ void mlist_unit(MListSmem& S, int N, uint32_t nw, uin
     fence_proxy_async_smem();  // these tile reads precede the next bulk load into the tile
 }
 
+// SMALLT: the chains at T < kListT (walker strategy 5; their fold unit holds several tiles) — a
+// separate instantiation, so the default tile's kernel carries none of that code (2 % on cfg2)
+template <bool SMALLT>
 __global__ void __launch_bounds__(kMListThreads, kMListBlocksPerSM) fold_mlist_kernel(const __grid_constant__ FoldParams P) {
     __shared__ MListSmem S;
     if (*reinterpret_cast<volatile unsigned*>(P.err) != 0) return;  // sticky error pending
-    if (P.info[6] == 0) return;                                       // no mask-list chunk
+    if (P.info[SMALLT ? 7 : 6] == 0) return;                          // no mask-list chunk of this kind
     const int tid = threadIdx.x;
     const int N = P.nrec;
     const uint64_t R = P.info[0];
@@ -1513,7 +1525,7 @@ __global__ void __launch_bounds__(kMListThreads, kMListBlocksPerSM) fold_mlist_k
         }
         while (u >= P.unit_first[lo + 1]) ++lo;
         const FoldRec& L = P.desc[lo];
-        if (L.dense != 4u) {  // folded by another kernel: skip the chunk
+        if (L.dense != (SMALLT ? 5u : 4u)) {  // folded by another kernel: skip the chunk
             u = (P.unit_first[lo + 1] < u1 ? P.unit_first[lo + 1] : u1) - 1;
             te_valid = false;
             continue;
@@ -1542,20 +1554,29 @@ __global__ void __launch_bounds__(kMListThreads, kMListBlocksPerSM) fold_mlist_k
         }
         const bool next = u + 1 < u1 && u + 1 < P.unit_first[lo + 1];
         __syncthreads();  // the record table is in place
-        if (tid < N) {  // this tile's entry range per record; the next tile's end, one unit ahead
+        // the unit's tile_off entries: a unit of kListT words holds tpu = kListT / T tiles (T <= kListT)
+        uint32_t t0 = ku, t1 = ku + 1, t2 = ku + 2;
+        if (SMALLT) {
+            const uint32_t lt = __ffs(L.T) - 1;  // T is a power of two: shifts, not divisions
+            const uint32_t tpu = kListT >> lt, n_tiles = (m + L.T - 1) >> lt;
+            t0 = ku * tpu;
+            t1 = t0 + tpu < n_tiles ? t0 + tpu : n_tiles;
+            t2 = t1 + tpu < n_tiles ? t1 + tpu : n_tiles;
+        }
+        if (tid < N) {  // this unit's entry range per record; the next unit's end, one unit ahead
             if (te_valid) {
                 S.carry[tid] = S.tend[tid];
                 S.tend[tid] = te;
             } else {
-                S.carry[tid] = ldg_u32(S.toff[tid] + ku);
-                S.tend[tid] = ldg_u32(S.toff[tid] + ku + 1);
+                S.carry[tid] = ldg_u32(S.toff[tid] + t0);
+                S.tend[tid] = ldg_u32(S.toff[tid] + t1);
             }
             const uint32_t k0 = S.carry[tid], k1 = S.tend[tid];
             if (k1 < k0 || k1 - k0 > nw || k1 > S.count[tid] || (ku == 0 && k0 != 0) ||
                 ((ku + 1) * kListT >= m && k1 != S.count[tid]))
                 bad = true;
         }
-        if (next && tid < N) te = ldg_u32(S.toff[tid] + ku + 2);
+        if (next && tid < N) te = ldg_u32(S.toff[tid] + t2);
         te_valid = next;
         if (__syncthreads_or(bad)) {  // a corrupt tile_off: drain the tile load, write nothing
             mbar_wait_parity(&S.bar, phase);
@@ -1564,9 +1585,9 @@ __global__ void __launch_bounds__(kMListThreads, kMListBlocksPerSM) fold_mlist_k
             break;
         }
         if (w == 4)
-            mlist_unit<4>(S, N, nw, ku, st, phase, tid, bad);
+            mlist_unit<4, SMALLT>(S, N, nw, ku, L.T, st, phase, tid, bad);
         else
-            mlist_unit<2>(S, N, nw, ku, st, phase, tid, bad);
+            mlist_unit<2, SMALLT>(S, N, nw, ku, L.T, st, phase, tid, bad);
         if (__syncthreads_or(bad)) {  // also: every thread is done with the tile
             bad = true;
             break;
@@ -1615,11 +1636,15 @@ cudaError_t launch_fold(const FoldParams& p, cudaStream_t s, int num_sms, uint64
     }
     static int occ_m = 0;
     if (!occ_m) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_m, fold_mlist_kernel, kMListThreads, 0) != cudaSuccess ||
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_m, fold_mlist_kernel<false>, kMListThreads, 0) !=
+                cudaSuccess ||
             occ_m < 1)
             occ_m = 1;
     }
-    fold_mlist_kernel<<<num_sms * occ_m, kMListThreads, 0, s>>>(p);
+    fold_mlist_kernel<false><<<num_sms * occ_m, kMListThreads, 0, s>>>(p);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    fold_mlist_kernel<true><<<num_sms * occ_m, kMListThreads, 0, s>>>(p);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     for (int j = 0; j < p.nrec; ++j) {  // each returns at once when no chunk takes strategy 3
@@ -1627,7 +1652,7 @@ cudaError_t launch_fold(const FoldParams& p, cudaStream_t s, int num_sms, uint64
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    *launches += 5 + static_cast<uint64_t>(p.nrec);
+    *launches += 6 + static_cast<uint64_t>(p.nrec);
     return cudaGetLastError();
 }
 

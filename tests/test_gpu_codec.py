@@ -321,7 +321,7 @@ def test_launch_counter(ctx):
     tc.diff_encode(ctx, [ref], [ref.clone()], out, ob, 1, 0)
     tc.diff_apply(ctx, [ref], 0, [out], [int(ob.item())])
     ctx.check()
-    assert ctx.launches == before + 9  # encode (mask, prefix, emit) + fold (walker, scatter, stream, list, mask-list, entries)
+    assert ctx.launches == before + 10  # encode (mask, prefix, emit) + fold (walker, scatter, stream, list, mask-list x2, entries)
 
 
 @pytest.mark.parametrize("advance", [True, False])

@@ -29,12 +29,12 @@ def fctx(request):
     c.close()
 
 
-def chain(tco, sizes, wb, N, f, C, seed, index_of=lambda v: False, structure=synth.S1_IID):
+def chain(tco, sizes, wb, N, f, C, seed, index_of=lambda v: False, structure=synth.S1_IID, T=4096):
     states = [synth.state(sizes, wb, seed, v, f, structure) for v in range(N + 1)]
     ref = [a.copy() for a in states[0]]
     diffs = []
     for v in range(1, N + 1):
-        rc, d = tco.encode(ref, states[v], tile_words=4096, chunk_words=C, version=v, ref_version=v - 1,
+        rc, d = tco.encode(ref, states[v], tile_words=T, chunk_words=C, version=v, ref_version=v - 1,
                            index_mode=index_of(v))
         assert rc == 0
         diffs.append(d)
@@ -125,6 +125,28 @@ def test_mlist_tamper_padding_bit(fctx, tco):
     bad = [d.copy() for d in diffs]
     last = 64 + 4 * (m // 32)  # the mask word holding words m-18 .. m+13
     bad[3][last + 3] |= 0x80   # bit 31 of it: word 32 * (m // 32) + 31 >= m
+    rc_o = tco.fold([a.copy() for a in states[0]], 0, bad)[0]
+    rc, _ = gpu_fold(fctx, states[0], 0, bad)
+    assert rc == tc.ERR_CORRUPT == rc_o
+
+
+@pytest.mark.parametrize("T,C", [(32, 1 << 28), (256, 4096 * 3), (1024, 1024 * 5), (2048, 1 << 28)])
+@pytest.mark.parametrize("f", [0.05, 0.5])
+def test_mask_chain_small_tiles(fctx, tco, T, C, f):
+    """T < 4096: a fold unit of 4096 words holds several tiles; their inner tile_off entries are
+    checked against the running count; chunks need not be a multiple of 4096 words."""
+    states, diffs = chain(tco, [4096 * 3 + 777, 9000 + 31], [4, 2], 4, f, C, seed=19, T=T)
+    check(fctx, tco, states, diffs)
+
+
+@pytest.mark.parametrize("T", [256, 1024])
+def test_mlist_tamper_inner_tile_off(fctx, tco, T):
+    """A tile_off entry inside a 4096-word unit (T < 4096) that disagrees with the mask: CORRUPT."""
+    m = 4096 * 3 + 50
+    states, diffs = chain(tco, [m], [4], 4, 0.2, 1 << 28, seed=23, T=T)
+    toff = 64 + ((4 * -(-m // 32) + 15) // 16) * 16
+    bad = [d.copy() for d in diffs]
+    bad[2][toff + 4 * 5] ^= 4  # tile_off[5]: inside unit 0 (T = 256) / unit 1 (T = 1024)
     rc_o = tco.fold([a.copy() for a in states[0]], 0, bad)[0]
     rc, _ = gpu_fold(fctx, states[0], 0, bad)
     assert rc == tc.ERR_CORRUPT == rc_o
