@@ -137,7 +137,7 @@ uint64_t tc_ctx_launches(const tc_ctx* ctx);
  * winning words in place or by streaming the chunk's tiles through shared memory (whole-line
  * writes).  Chains of index-mode records at T = 4096 are streamed when they are long (>= 4
  * records changing >= 0.5 % of the words in total) or dense (> permille/1000 of the words in
- * total), chains of mask-mode records at T = 4096 when dense (at most 32 records, one format per
+ * total), chains of mask-mode records at T <= 4096 when dense (at most 32 records, one format per
  * chain); all other chunks are scattered.  Default 60 (6 %).  0 = stream every chunk; UINT32_MAX = scatter every
  * chunk.  Every strategy produces the same state.
  * Takes effect for later tc_diff_apply calls.  Errors: TC_ERR_INVALID (NULL ctx). */
