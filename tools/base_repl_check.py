@@ -46,6 +46,7 @@ for it in range(1, 11):
         fails.append(f"replica visible before completion (iteration {it})")
     if it >= plan.iters and seen != 10:
         fails.append(f"replica not committed after {it} iterations: {seen}")
+    dist.barrier()  # no rank pushes the next chunk (or the commit) before every rank has looked
 if not torch.equal(rep.received(), flat(shard(prv, 1))):
     fails.append("base 1 replica differs from the neighbour's shard")
 if not torch.equal(rep.host.tensor[:n], flat(shard(rank, 1)).cpu()):
