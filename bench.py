@@ -308,7 +308,7 @@ def run_ours(args):
                           record_format=args.format if allow_index else "mask", dev_slots=args.dev_slots,
                           t1_bytes=(args.dev_slots + 1) * est,
                           t2_slots=2, standby=R, tile_words=T, chunk_words=C,
-                          ahead=(world == 1 or bool(args.t2_fused)) if args.ahead is None else bool(args.ahead),
+                          ahead=True if args.ahead is None else bool(args.ahead),
                           stage_base=False, ref=A, stream=s_comp, push_ctas=args.push_ctas, timing=True,
                           fused_t2=bool(args.t2_fused), overlap_standby=bool(args.overlap_standby))
         rec_cap = ck.rec_cap
@@ -1886,9 +1886,11 @@ def main():
                     help="CTAs of the Tier-2 NVLink push inside the step (fewer = less interference)")
     ap.add_argument("--dev-slots", type=int, default=3,
                     help="device record slots of the Checkpointer (a slot is reused once its Tier-1 copy is done)")
-    ap.add_argument("--t2-fused", type=int, default=1,
+    ap.add_argument("--t2-fused", type=int, default=0,
                     help="push mode: 1 = the encoder writes the record into the neighbour's slot (fused), "
-                         "0 = a separate push kernel after the encode")
+                         "0 = a separate push kernel on the Tier-2 stream, beside the fold and the next encode "
+                         "(default: with the host one step ahead it is the faster step, N = 2: 5.92 vs 6.18 ms, "
+                         "profiles/rd7a_t2_fused_ab.txt)")
     ap.add_argument("--tier2", default="push", choices=["push", "nccl"],
                     help="Tier-2 replication: NVLink stores into the neighbour's IPC slot, or NCCL send/recv")
     ap.add_argument("--recovery", type=int, default=None,
@@ -1896,8 +1898,9 @@ def main():
     ap.add_argument("--fold-dense-permille", type=int, default=None,
                     help="restore strategy threshold (tc_ctx_set_fold_dense_permille); default: libtc's")
     ap.add_argument("--ahead", type=int, default=None,
-                    help="Checkpointer runs the host one step ahead of the device (default: at N = 1 and with "
-                         "the fused Tier-2 emit; N = 2: 6.08 vs 6.27 ms per step, profiles/rd5u_*)")
+                    help="Checkpointer runs the host one step ahead of the device (default on; N = 2: 6.08 vs "
+                         "6.27 ms per step with the fused emit, 5.92 vs 6.19 with the push kernel, profiles/rd5u_*, "
+                         "rd7a_*)")
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--numa-bind", type=int, default=1,
                     help="N > 1: bind each rank to its GPU's NUMA node before the pinned buffers are allocated")
